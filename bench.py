@@ -1,0 +1,369 @@
+"""ν-LPA throughput bench: |E|/runtime on R-MAT (BASELINE.json north star).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--scale 27] [--impl nulpa|reference]
+
+A step is one full lpa() run (identity labels -> convergence, ParallelAsync, the
+reference defaults: tolerance 0.05, <= 20 iterations, Pick-Less every 4, QD probing,
+fp32 values, pruning) over the resident R-MAT graph (scale 27, edgefactor 16 by
+default: n = 2^27, m2 ~ 4.19e9 directed CSR entries after symmetrise + dedup).
+
+value   = K * m2 / (sum of the device iteration-loop times), CUDA events inside the
+          library (the reference's RunStats.elapsed_seconds, lpa.cpp:269,311).
+e2e     = the same metric through the host-buffer C ABI (nulpa_run): every step copies
+          the CSR from pinned host memory to the device, runs, and copies labels back.
+roofline: the dominant tier's algorithmic bytes / its event-timed duration.
+cpu_baseline: the reference library itself (oracle/_ref, multithreaded ParallelAsync,
+          switch_degree = UINT32_MAX per SURVEY F5) on a bounded R-MAT sample.
+
+Multi-GPU (N > 1, torchrun): every rank holds a full replica of the graph and runs the
+same workload ("replicas"); timing is max over ranks. The partitioned label exchange of
+SURVEY §8e is not part of this bench yet.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "edges/s (|E|/runtime) on 2B-edge R-MAT at 1/2/4/8 B200; modularity"
+UNIT = "edges/s"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def hbm_peak():
+    try:
+        p = json.loads(PEAKS.read_text())
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        busy = [x for x in sm if x > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def reference_sample(scale: int, edgefactor: int, seed: int, device: int):
+    """The bounded CPU sample: an R-MAT graph of the same generator at a smaller scale."""
+    from paper_2411_11468_b200 import labelprop as lp
+    dg = lp.DeviceGraph.rmat(scale, edgefactor, seed, device)
+    g = dg.download()
+    dg.free()
+    return g
+
+
+def run_reference_cpu(g, reps: int):
+    """oracle/_ref: the unmodified reference lpa(), ParallelAsync, all host threads."""
+    import oracle as O
+    rg = O.RefGraph.from_csr(g.offsets, g.targets, None)
+    workers = os.cpu_count() or 1
+    out = []
+    for _ in range(reps):
+        labels, st = O.ref_lpa(rg, exec_mode=0, workers=workers, switch_degree=0xFFFFFFFF)
+        out.append((labels, st))
+    return rg, out, workers
+
+
+def bench_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libnulpa_ref.so not built (needs /root/reference at build)"}))
+        return 0
+    g = reference_sample(args.ref_scale, 16, args.seed, 0)
+    m2 = g.directed_size()
+    rg, runs, workers = run_reference_cpu(g, args.warmup + args.steps)
+    timed = runs[args.warmup:]
+    secs = sum(st["elapsed_seconds"] for _, st in timed)
+    value = m2 * len(timed) / secs
+    q = O.ref_modularity(rg, timed[-1][0])
+    sample = (f"R-MAT scale-{args.ref_scale} ef16 (n=2^{args.ref_scale}, m2={m2}), reference "
+              f"ParallelAsync, switch_degree=UINT32_MAX (SURVEY F5), workers={workers}")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / len(timed), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"rmat{args.ref_scale}-ef16 (bounded CPU sample of rmat"
+                                   f"{args.scale}-ef16)", "n": g.order(), "m2": m2,
+                       "iterations": timed[-1][1]["iterations"], "modularity": q},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def bench_nulpa(args):
+    rank, world, local = dist_env()
+    dev = local
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(dev)
+        dist.init_process_group("nccl")
+    from paper_2411_11468_b200 import _capi
+    from paper_2411_11468_b200 import labelprop as lp
+
+    def barrier_max(x: float) -> float:
+        if world == 1:
+            return x
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    t0 = time.time()
+    dg = lp.DeviceGraph.rmat(args.scale, args.edgefactor, args.seed, dev)
+    gen_s = time.time() - t0
+    n, m2 = dg.n, dg.m2
+    cfg = lp.LpaConfig()
+    tuning = lp.Tuning(thread_max_degree=args.thread_max, warp_max_degree=args.warp_max,
+                       block_max_degree=args.block_max)
+    prof_tuning = lp.Tuning(thread_max_degree=args.thread_max, warp_max_degree=args.warp_max,
+                            block_max_degree=args.block_max)
+
+    # warm-up (also builds and caches the tier plan / hub tables)
+    for _ in range(args.warmup):
+        dg.lpa(cfg, tuning, want_host=False)
+
+    # timed region: K device-resident runs, per-tier CUDA-event profile inside the library
+    t = prof_tuning.to_c()
+    t.profile = 1
+    stats = []
+    with ClockSampler(dev) as clk:
+        barrier()
+        w0 = time.time()
+        for _ in range(args.steps):
+            o = lp._opts(cfg, dev)
+            dn = np.zeros(cfg.max_iterations, np.uint64)
+            st = _capi.nulpa_stats()
+            st.delta_n = dn.ctypes.data_as(C.POINTER(C.c_uint64))
+            _capi.check(_capi.lib().nulpa_run_graph(dg._h, C.byref(o), C.byref(t), None, None,
+                                                    C.byref(st)))
+            stats.append((st, dn[:st.iterations].tolist()))
+        barrier()
+        wall = time.time() - w0
+    loop_s = sum(s.elapsed_seconds for s, _ in stats)
+    loop_s = barrier_max(loop_s)
+    wall = barrier_max(wall)
+    value = world * args.steps * m2 / loop_s
+
+    # per-tier roofline (dominant tier by device time)
+    peak, peak_src = hbm_peak()
+    tier_ms = np.sum([[s.tier_ms[i] for i in range(5)] for s, _ in stats], axis=0)
+    tier_bytes = np.sum([[s.tier_bytes[i] for i in range(5)] for s, _ in stats], axis=0)
+    tier_passes = np.sum([[s.tier_passes[i] for i in range(5)] for s, _ in stats], axis=0)
+    top = int(np.argmax(tier_ms))
+    achieved = tier_bytes[top] / (tier_ms[top] * 1e-3) / 1e9
+    total_alg = sum(s.algorithmic_bytes for s, _ in stats)
+    launches = sum(s.kernel_launches for s, _ in stats)
+
+    # quality of the final labels (device modularity)
+    import torch
+    lab = torch.empty(n, dtype=torch.int32, device=f"cuda:{dev}")
+    last = dg.lpa(cfg, tuning, labels_device_ptr=lab.data_ptr(), want_host=False)
+    q = dg.modularity_device(lab.data_ptr())
+    comms = dg.community_count_device(lab.data_ptr())
+    del lab
+
+    # e2e through the host-buffer C ABI (pinned host CSR, H2D + run + D2H every step)
+    e2e = None
+    if args.e2e_steps > 0:
+        off_h = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+        tgt_h = torch.empty(m2, dtype=torch.int32, pin_memory=True)
+        lab_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        _capi.check(_capi.lib().nulpa_graph_download(dg._h, off_h.data_ptr(), tgt_h.data_ptr(),
+                                                     None))
+        csr = _capi.nulpa_csr()
+        csr.n, csr.m2 = n, m2
+        csr.offsets, csr.targets, csr.weights = off_h.data_ptr(), tgt_h.data_ptr(), None
+        dg.free()  # the e2e path owns its own device copy
+        o = lp._opts(cfg, dev)
+        barrier()
+        e0 = time.time()
+        for _ in range(args.e2e_steps):
+            st = _capi.nulpa_stats()
+            _capi.check(_capi.lib().nulpa_run(C.byref(csr), C.byref(o), None, lab_h.data_ptr(),
+                                              C.byref(st)))
+        barrier()
+        e_wall = barrier_max(time.time() - e0)
+        e2e = {"value": world * args.e2e_steps * m2 / e_wall, "unit": UNIT,
+               "h2d_bytes_per_step": int((n + 1) * 8 + m2 * 4),
+               "d2h_bytes_per_step": int(n * 4), "steps": args.e2e_steps,
+               "seconds_per_step": e_wall / args.e2e_steps, "host_memory": "pinned"}
+        del off_h, tgt_h, lab_h
+    else:
+        dg.free()
+
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_baseline:
+        try:
+            import oracle as O
+            if O.ref_available():
+                g = reference_sample(args.ref_scale, 16, args.seed, dev)
+                _, runs, workers = run_reference_cpu(g, 1)
+                stc = runs[-1][1]
+                cpu = {"value": g.directed_size() / stc["elapsed_seconds"], "unit": UNIT,
+                       "cores": workers, "kind": "reference",
+                       "sample": f"R-MAT scale-{args.ref_scale} ef16 (m2={g.directed_size()}), "
+                                 f"reference lpa() ParallelAsync, switch_degree=UINT32_MAX "
+                                 f"(SURVEY F5), {stc['iterations']} iterations, "
+                                 f"{stc['elapsed_seconds']:.2f} s"}
+            else:
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                       "sample": "oracle/_ref not built on this box"}
+        except Exception as e:  # the baseline must never sink the GPU line
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        s0 = stats[-1][0]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {
+                "workload": f"rmat{args.scale}-ef{args.edgefactor}", "n": n, "m2": m2,
+                "E_definition": "m2 = directed CSR entries after symmetrise + dedup",
+                "undirected_draws": (1 << args.scale) * args.edgefactor,
+                "parallelism": "replicas" if world > 1 else "single",
+                "exec": "ParallelAsync", "pl_period": 4, "tolerance": 0.05,
+                "iterations": s0.iterations, "delta_n": stats[-1][1],
+                "converged": bool(s0.converged), "modularity": q, "communities": comms,
+                "final_run_iterations": last.stats.iterations,
+                "loop_seconds_per_step": loop_s / args.steps,
+                "m2_iters_per_s": world * sum(m2 * s.iterations for s, _ in stats) / loop_s,
+                "l2": "inputs (>= 17 GB) far exceed the 126 MB L2; no flush needed",
+                "generate_seconds": gen_s,
+                "tier_ms_per_step": [x / args.steps for x in tier_ms.tolist()],
+                "tier_bytes_per_step": [x / args.steps for x in tier_bytes.tolist()],
+                "tier_names": _capi.TIER_NAMES,
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": f"tier:{_capi.TIER_NAMES[top]}",
+                         "peak_source": peak_src,
+                         "alg_bytes_per_launch": tier_bytes[top] / max(1, tier_passes[top]),
+                         "avg_launch_ms": tier_ms[top] / max(1, tier_passes[top]),
+                         "whole_loop_gbs": total_alg / loop_s / 1e9},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="nulpa", choices=["nulpa", "reference"])
+    ap.add_argument("--scale", type=int, default=27)
+    ap.add_argument("--edgefactor", type=int, default=16)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--ref-scale", type=int, default=22)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--thread-max", type=int, default=0)
+    ap.add_argument("--warp-max", type=int, default=0)
+    ap.add_argument("--block-max", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return bench_reference(args)
+    return bench_nulpa(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

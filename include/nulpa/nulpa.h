@@ -1,0 +1,195 @@
+/* nulpa — B200-native ν-LPA label propagation: the C-ABI boundary.
+ *
+ * Plain pointers and sizes only; no torch or C++ types cross this boundary.
+ * Every entry point replaces one reference interface (paths relative to
+ * /root/reference/proj) and keeps its argument meaning and error behaviour:
+ *
+ *   nulpa_run              labelprop::lpa(const CsrGraph&, const LpaConfig&)
+ *                            include/labelprop/lpa.hpp:84, src/lpa.cpp:362-366
+ *   nulpa_sync_step        one sync_move label-choice step from arbitrary labels
+ *                            (detail::scan_candidate lpa.hpp:92-111 + lpa.cpp:87-88)
+ *   nulpa_modularity       labelprop::modularity  quality.hpp:19, quality.cpp:21-49
+ *   nulpa_community_count  labelprop::community_stats(...).count  quality.cpp:56-78
+ *   nulpa_cross_check      labelprop::cross_check  lpa.hpp:72-73, lpa.cpp:338-360
+ *   nulpa_partition_by_degree  labelprop::partition_by_degree  lpa.hpp:63, lpa.cpp:330-336
+ *
+ * Error codes (the C++ drop-in in paper_2411_11468_b200/csrc/dropin.cpp maps
+ * them back to the reference exceptions, graph.hpp:17-31):
+ *   0 ok, 1 invalid argument (ValidationError), 2 out of memory (std::bad_alloc),
+ *   3 internal invariant / hashtable failure (InternalError), 4 CUDA error,
+ *   5 other. nulpa_last_error() returns the thread-local message.
+ *
+ * There is no CPU fallback: every compute entry point runs CUDA kernels for
+ * sm_100a and fails with code 4 when no CUDA device is usable.
+ */
+#ifndef NULPA_NULPA_H
+#define NULPA_NULPA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NULPA_OK 0
+#define NULPA_EINVAL 1
+#define NULPA_ENOMEM 2
+#define NULPA_EINTERNAL 3
+#define NULPA_ECUDA 4
+#define NULPA_EOTHER 5
+
+/* Probe strategies: labelprop::ProbeStrategy, hashtable.hpp:25 (same values). */
+#define NULPA_PROBE_LINEAR 0
+#define NULPA_PROBE_QUADRATIC 1
+#define NULPA_PROBE_DOUBLE 2
+#define NULPA_PROBE_QUADRATIC_DOUBLE 3
+
+/* Exec modes: labelprop::ExecMode, lpa.hpp:20 (same values). */
+#define NULPA_EXEC_PARALLEL_ASYNC 0
+#define NULPA_EXEC_SEQUENTIAL 1
+#define NULPA_EXEC_SYNCHRONOUS 2
+
+/* CSR graph (labelprop::CsrGraph, graph.hpp:53-84): offsets u64[n+1],
+ * targets u32[m2], weights f32[m2] or NULL meaning every weight is 1.0f.
+ * Rows sorted by target, both directions stored, self-loops stored once.
+ * Borrowed: never freed or modified by the library. */
+typedef struct nulpa_csr {
+  uint32_t n;
+  uint32_t reserved;
+  uint64_t m2;
+  const uint64_t* offsets;
+  const uint32_t* targets;
+  const float* weights;
+} nulpa_csr;
+
+/* labelprop::LpaConfig (lpa.hpp:25-37), field for field, same defaults. */
+typedef struct nulpa_opts {
+  double tolerance;       /* 0.05 */
+  int32_t max_iterations; /* 20 */
+  int32_t pl_period;      /* 4; 0 disables pick-less */
+  int32_t cc_period;      /* 0; 0 disables cross-check */
+  int32_t strategy;       /* NULPA_PROBE_QUADRATIC_DOUBLE */
+  uint32_t switch_degree; /* 32: thread-per-vertex below, cooperative at and above */
+  int32_t precision;      /* 32 or 64 (hashtable value width) */
+  int32_t exec;           /* NULPA_EXEC_PARALLEL_ASYNC */
+  int32_t workers;        /* echoed only (no meaning on a GPU) */
+  uint64_t seed;          /* echoed only (the reference never uses it either) */
+  int32_t prune;          /* 1 */
+  int32_t device;         /* CUDA device ordinal (not an LpaConfig field) */
+} nulpa_opts;
+
+/* Kernel-tier tuning (not part of LpaConfig). Zero fields take defaults. */
+typedef struct nulpa_tuning {
+  uint32_t thread_max_degree; /* thread-per-vertex tier upper bound (<= 16) */
+  uint32_t warp_max_degree;   /* warp-per-vertex tier upper bound (<= 512) */
+  uint32_t block_max_degree;  /* CTA-per-vertex smem-table tier upper bound (<= 4096) */
+  uint32_t hub_chunk;         /* edges per CTA work item in the global-table hub tier */
+  uint32_t use_graphs;        /* reserved */
+  uint32_t profile;           /* 1: time each tier with CUDA events (stats.tier_*) */
+  uint32_t reserved[2];
+} nulpa_tuning;
+
+#define NULPA_TIERS 5 /* 0 thread, 1 warp, 2 block, 3 hub, 4 other (deferred wake, cross-check) */
+
+/* labelprop::RunStats (lpa.hpp:39-46) plus device counters for roofline
+ * accounting. delta_n must point at >= max_iterations u64 (or be NULL). */
+typedef struct nulpa_stats {
+  int32_t iterations;
+  int32_t converged;
+  int32_t pl_iterations;
+  int32_t reserved;
+  uint64_t cc_reverts;
+  double elapsed_seconds; /* iteration loop only, CUDA events (lpa.cpp:269,311) */
+  uint64_t* delta_n;      /* caller buffer, delta_n_per_iter */
+  /* totals over all passes (SURVEY §8d algorithmic-byte model) */
+  uint64_t processed_vertices;
+  uint64_t processed_edges;
+  uint64_t wake_edges;
+  uint64_t algorithmic_bytes;
+  double setup_seconds; /* tiering + table allocation before the loop */
+  uint64_t kernel_launches;            /* nulpa kernels launched inside the loop */
+  double tier_ms[NULPA_TIERS];         /* device time per tier (tuning.profile) */
+  double tier_bytes[NULPA_TIERS];      /* algorithmic bytes per tier */
+  uint64_t tier_edges[NULPA_TIERS];    /* edges scanned per tier */
+  uint32_t tier_passes[NULPA_TIERS];   /* passes in which the tier launched */
+  uint32_t reserved2;
+} nulpa_stats;
+
+typedef struct nulpa_graph nulpa_graph; /* device-resident CSR */
+
+const char* nulpa_last_error(void);
+int nulpa_version(void);
+void nulpa_default_opts(nulpa_opts* opts);
+int nulpa_device_count(int* count);
+
+/* ---- host-buffer entry points (the drop-in boundary) ---------------------- */
+
+/* labelprop::lpa: upload the graph, run, download labels[n]. */
+int nulpa_run(const nulpa_csr* csr, const nulpa_opts* opts, const nulpa_tuning* tuning,
+              uint32_t* labels_out, nulpa_stats* stats);
+
+/* One synchronous label-choice step over every vertex of degree >= 1 (no
+ * pruning flags): out[i] = c* if (pick_less ? c* < in[i] : c* != in[i]) else in[i]. */
+int nulpa_sync_step(const nulpa_csr* csr, const uint32_t* labels_in, int pick_less,
+                    int strategy, int precision, uint32_t* labels_out, uint64_t* changed);
+
+int nulpa_modularity(const nulpa_csr* csr, const uint32_t* labels, double* q);
+int nulpa_community_count(const nulpa_csr* csr, const uint32_t* labels, uint64_t* count);
+
+/* labelprop::cross_check on host arrays (labels and flags updated in place). */
+int nulpa_cross_check(const nulpa_csr* csr, uint32_t* labels, const uint32_t* prev,
+                      uint8_t* flags, uint64_t* reverted);
+
+/* labelprop::partition_by_degree: low/high must hold n entries each. */
+int nulpa_partition_by_degree(const nulpa_csr* csr, uint32_t switch_degree, uint32_t* low,
+                              uint64_t* n_low, uint32_t* high, uint64_t* n_high);
+
+/* ---- device-resident graph ------------------------------------------------ */
+
+/* Copy a host CSR to the device (weights that are all 1.0f are elided). */
+int nulpa_graph_upload(const nulpa_csr* host_csr, int device, nulpa_graph** out);
+/* Borrow device arrays (e.g. from a generator or torch); not freed by us. */
+int nulpa_graph_wrap_device(const nulpa_csr* device_csr, int device, nulpa_graph** out);
+int nulpa_graph_free(nulpa_graph* g);
+int nulpa_graph_info(const nulpa_graph* g, uint32_t* n, uint64_t* m2, uint32_t* max_degree,
+                     int* weighted);
+/* Device pointers of the resident arrays (weights NULL when unit). */
+int nulpa_graph_device_csr(const nulpa_graph* g, nulpa_csr* out);
+/* Download the resident CSR into host buffers (weights may be NULL). */
+int nulpa_graph_download(const nulpa_graph* g, uint64_t* offsets, uint32_t* targets,
+                         float* weights);
+
+/* lpa() on a resident graph; labels to host and/or device buffers (NULL = skip). */
+int nulpa_run_graph(nulpa_graph* g, const nulpa_opts* opts, const nulpa_tuning* tuning,
+                    uint32_t* labels_host, uint32_t* labels_device, nulpa_stats* stats);
+/* Sync step on a resident graph; labels are DEVICE pointers. */
+int nulpa_sync_step_graph(nulpa_graph* g, const uint32_t* labels_in_dev, int pick_less,
+                          int strategy, int precision, uint32_t* labels_out_dev,
+                          uint64_t* changed);
+/* Modularity on a resident graph; labels is a DEVICE pointer. */
+int nulpa_modularity_graph(nulpa_graph* g, const uint32_t* labels_dev, double* q);
+int nulpa_community_count_graph(nulpa_graph* g, const uint32_t* labels_dev, uint64_t* count);
+
+/* ---- synthetic inputs built on the device (bench / tests) ----------------- */
+
+/* Graph500-style R-MAT (A=.57,B=.19,C=.19,D=.05), edgefactor*2^scale draws,
+ * seeded vertex permutation, self-loops dropped, symmetrised, deduplicated,
+ * unit weights, rows sorted. */
+int nulpa_gen_rmat(uint32_t scale, uint32_t edgefactor, uint64_t seed, int device,
+                   nulpa_graph** out);
+/* rows x cols 4-neighbour lattice, id = r*cols + c, unit weights. */
+int nulpa_gen_grid(uint32_t rows, uint32_t cols, int device, nulpa_graph** out);
+/* Chung-Lu power-law graph: n vertices, ~edges undirected draws, exponent
+ * gamma, the top `hubs` vertices forced to degree ~hub_degree; dedup'd. */
+int nulpa_gen_web(uint32_t n, uint64_t edges, double gamma, uint32_t hubs,
+                  uint32_t hub_degree, uint64_t seed, int device, nulpa_graph** out);
+/* Build a symmetric, deduplicated, sorted CSR from a host edge list on the
+ * device (duplicate pairs dropped, unit weights) — for SBM-style inputs. */
+int nulpa_graph_from_edges(const uint32_t* u, const uint32_t* v, uint64_t ne, uint32_t n,
+                           int device, nulpa_graph** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

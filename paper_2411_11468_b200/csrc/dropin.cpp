@@ -1,0 +1,135 @@
+// C++ drop-in for the reference engine entry points, over the nulpa C ABI.
+//
+// Replaces (paths relative to /root/reference/proj):
+//   labelprop::lpa                  include/labelprop/lpa.hpp:84, src/lpa.cpp:362-366
+//   labelprop::partition_by_degree  include/labelprop/lpa.hpp:63, src/lpa.cpp:330-336
+//   labelprop::cross_check          include/labelprop/lpa.hpp:72-73, src/lpa.cpp:338-360
+//   labelprop::modularity           include/labelprop/quality.hpp:19, src/quality.cpp:21-49
+//   CsrGraph::CsrGraph / weighted_degree   src/graph.cpp:165-178
+// Error codes from the C ABI map back onto the reference exceptions:
+// 1 → ValidationError, 2 → std::bad_alloc, 3 → InternalError, else runtime_error.
+#include <cstdlib>
+#include <new>
+#include <string>
+
+#include "labelprop/graph.hpp"
+#include "labelprop/lpa.hpp"
+#include "labelprop/quality.hpp"
+#include "nulpa/nulpa.h"
+
+namespace labelprop {
+
+namespace {
+
+[[noreturn]] void raise(int rc) {
+  const std::string msg = nulpa_last_error();
+  switch (rc) {
+    case NULPA_EINVAL: throw ValidationError(msg);
+    case NULPA_ENOMEM: throw std::bad_alloc();
+    case NULPA_EINTERNAL: throw InternalError(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+nulpa_csr view(const CsrGraph& g) {
+  nulpa_csr c;
+  c.n = g.order();
+  c.reserved = 0;
+  c.m2 = g.directed_size();
+  c.offsets = g.offsets().data();
+  c.targets = g.targets().data();
+  c.weights = g.weights().empty() ? nullptr : g.weights().data();
+  return c;
+}
+
+int device_from_env() {
+  const char* d = std::getenv("NULPA_DEVICE");
+  return d ? std::atoi(d) : 0;
+}
+
+}  // namespace
+
+CsrGraph::CsrGraph(std::vector<std::uint64_t> offsets, std::vector<VertexId> targets,
+                   std::vector<float> weights)
+    : offsets_(std::move(offsets)), targets_(std::move(targets)), weights_(std::move(weights)) {
+  if (offsets_.empty() || offsets_.back() != targets_.size() || targets_.size() != weights_.size())
+    throw ValidationError("inconsistent CSR arrays");
+  total_weight_2m_ = 0.0;
+  for (float w : weights_) total_weight_2m_ += static_cast<double>(w);
+}
+
+double CsrGraph::weighted_degree(VertexId i) const {
+  double k = 0.0;
+  for (float w : edge_weights(i)) k += static_cast<double>(w);
+  return k;
+}
+
+LpaResult lpa(const CsrGraph& g, const LpaConfig& cfg) {
+  nulpa_opts o;
+  nulpa_default_opts(&o);
+  o.tolerance = cfg.tolerance;
+  o.max_iterations = cfg.max_iterations;
+  o.pl_period = cfg.pl_period;
+  o.cc_period = cfg.cc_period;
+  o.strategy = static_cast<int32_t>(cfg.strategy);
+  o.switch_degree = cfg.switch_degree;
+  o.precision = static_cast<int32_t>(cfg.precision);
+  o.exec = static_cast<int32_t>(cfg.exec);
+  o.workers = cfg.workers;
+  o.seed = cfg.seed;
+  o.prune = cfg.prune ? 1 : 0;
+  o.device = device_from_env();
+
+  LpaResult r;
+  r.labels.resize(g.order());
+  std::vector<std::uint64_t> dn(cfg.max_iterations > 0 ? cfg.max_iterations : 1);
+  nulpa_stats st{};
+  st.delta_n = dn.data();
+  const nulpa_csr c = view(g);
+  const int rc = nulpa_run(&c, &o, nullptr, r.labels.data(), &st);
+  if (rc != NULPA_OK) raise(rc);
+  r.stats.iterations = st.iterations;
+  r.stats.delta_n_per_iter.assign(dn.begin(), dn.begin() + st.iterations);
+  r.stats.converged = st.converged != 0;
+  r.stats.pl_iterations = st.pl_iterations;
+  r.stats.cc_reverts = st.cc_reverts;
+  r.stats.elapsed_seconds = st.elapsed_seconds;
+  return r;
+}
+
+DegreePartition partition_by_degree(const CsrGraph& g, std::uint32_t switch_degree) {
+  DegreePartition p;
+  p.low.resize(g.order());
+  p.high.resize(g.order());
+  std::uint64_t nl = 0, nh = 0;
+  const nulpa_csr c = view(g);
+  const int rc = nulpa_partition_by_degree(&c, switch_degree, p.low.data(), &nl, p.high.data(), &nh);
+  if (rc != NULPA_OK) raise(rc);
+  p.low.resize(nl);
+  p.high.resize(nh);
+  return p;
+}
+
+std::uint64_t cross_check(const CsrGraph& g, std::span<VertexId> labels,
+                          std::span<const VertexId> prev, std::span<std::uint8_t> flags) {
+  if (labels.size() != g.order() || prev.size() != g.order() || flags.size() != g.order())
+    throw ValidationError("cross-check label arrays must cover every vertex");
+  std::uint64_t reverted = 0;
+  const nulpa_csr c = view(g);
+  const int rc = nulpa_cross_check(&c, labels.data(), prev.data(), flags.data(), &reverted);
+  if (rc != NULPA_OK) raise(rc);
+  return reverted;
+}
+
+double modularity(const CsrGraph& g, std::span<const VertexId> labels) {
+  if (labels.size() != g.order())
+    throw ValidationError("labeling has " + std::to_string(labels.size()) + " entries for " +
+                          std::to_string(g.order()) + " vertices");
+  double q = 0.0;
+  const nulpa_csr c = view(g);
+  const int rc = nulpa_modularity(&c, labels.data(), &q);
+  if (rc != NULPA_OK) raise(rc);
+  return q;
+}
+
+}  // namespace labelprop

@@ -1,0 +1,467 @@
+// Device CSR residency and the per-graph execution plan (degree tiers).
+//
+// CsrGraph (graph.hpp:53-84, graph.cpp:165-178) becomes a device-resident
+// structure: offsets u64[n+1], targets u32[m2], weights f32[m2] — weights are
+// elided when every weight is 1.0f, so unit-weight graphs move 8 bytes per
+// scanned edge instead of 12. partition_by_degree (lpa.cpp:330-336) becomes a
+// four-way device tiering built once per graph (K1 in SURVEY §2.2).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+#include "plan.hpp"
+
+namespace nulpa {
+
+namespace {
+thread_local std::string g_last_error;
+
+struct DegreeOf {
+  const uint64_t* off;
+  __host__ __device__ uint32_t operator()(uint32_t i) const {
+    return static_cast<uint32_t>(off[i + 1] - off[i]);
+  }
+};
+
+struct DegInRange {
+  const uint64_t* off;
+  uint64_t lo, hi;
+  __host__ __device__ bool operator()(uint32_t i) const {
+    const uint64_t d = off[i + 1] - off[i];
+    return d >= lo && d <= hi;
+  }
+};
+
+struct IsUnit {
+  __host__ __device__ uint32_t operator()(float w) const { return w == 1.0f ? 0u : 1u; }
+};
+
+struct ToDouble {
+  __host__ __device__ double operator()(float w) const { return static_cast<double>(w); }
+};
+
+__global__ void k_gather_degrees(const uint32_t* list, const uint64_t* off, uint32_t count,
+                                 uint32_t* deg) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x)
+    deg[t] = static_cast<uint32_t>(off[list[t] + 1] - off[list[t]]);
+}
+
+__global__ void k_check_offsets(const uint64_t* off, uint32_t n, uint64_t m2, unsigned* bad) {
+  for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (off[i + 1] < off[i]) atomicOr(bad, 1u);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (off[0] != 0 || off[n] != m2)) atomicOr(bad, 2u);
+}
+
+__global__ void k_check_targets(const uint32_t* tgt, uint64_t m2, uint32_t n, unsigned* bad) {
+  for (uint64_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m2;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    if (tgt[e] >= n) atomicOr(bad, 4u);
+}
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+const std::string& last_error() { return g_last_error; }
+
+void use_device(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    (void)cudaGetLastError();
+    throw Error(NULPA_ECUDA, std::string("no CUDA device available (nulpa has no CPU fallback): ") +
+                                 cudaGetErrorString(e));
+  }
+  if (device < 0 || device >= count)
+    throw Error(NULPA_EINVAL, "CUDA device " + std::to_string(device) + " out of range");
+  NULPA_CUDA(cudaSetDevice(device));
+}
+
+void* dmalloc(size_t bytes) {
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    throw Error(e == cudaErrorMemoryAllocation ? NULPA_ENOMEM : NULPA_ECUDA,
+                "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
+  }
+  return p;
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+void check_host_csr(const nulpa_csr* csr) {
+  if (!csr) throw Error(NULPA_EINVAL, "null CSR");
+  if (!csr->offsets) throw Error(NULPA_EINVAL, "inconsistent CSR arrays");
+  if (csr->offsets[0] != 0 || csr->offsets[csr->n] != csr->m2)
+    throw Error(NULPA_EINVAL, "inconsistent CSR arrays");
+  if (csr->m2 > 0 && !csr->targets) throw Error(NULPA_EINVAL, "inconsistent CSR arrays");
+}
+
+// Reductions over the resident arrays: max degree, 2m, unit-weight detection,
+// structural validation (offsets monotone, targets < n).
+void finalize_graph(nulpa_graph* g, cudaStream_t s) {
+  const uint32_t n = g->n;
+  unsigned* d_bad = dalloc<unsigned>(1);
+  uint32_t* d_max = dalloc<uint32_t>(1);
+  double* d_sum = dalloc<double>(1);
+  uint32_t* d_nonunit = dalloc<uint32_t>(1);
+  NULPA_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), s));
+  k_check_offsets<<<256, 256, 0, s>>>(g->offsets, n, g->m2, d_bad);
+  if (g->m2) k_check_targets<<<1024, 256, 0, s>>>(g->targets, g->m2, n, d_bad);
+  NULPA_CUDA(cudaGetLastError());
+  unsigned bad = 0;
+  NULPA_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, s));
+  NULPA_CUDA(cudaStreamSynchronize(s));
+  if (bad) {
+    dfree(d_bad);
+    dfree(d_max);
+    dfree(d_sum);
+    dfree(d_nonunit);
+    throw Error(NULPA_EINVAL, bad & 4u ? "CSR target id out of range" : "inconsistent CSR arrays");
+  }
+  uint32_t maxd = 0;
+  if (n > 0) {
+    auto degs = cub::TransformInputIterator<uint32_t, DegreeOf, cub::CountingInputIterator<uint32_t>>(
+        cub::CountingInputIterator<uint32_t>(0), DegreeOf{g->offsets});
+    size_t tb = 0;
+    cub::DeviceReduce::Max(nullptr, tb, degs, d_max, n, s);
+    void* tmp = dmalloc(tb);
+    cub::DeviceReduce::Max(tmp, tb, degs, d_max, n, s);
+    NULPA_CUDA(cudaMemcpyAsync(&maxd, d_max, sizeof maxd, cudaMemcpyDeviceToHost, s));
+    NULPA_CUDA(cudaStreamSynchronize(s));
+    dfree(tmp);
+  }
+  g->max_degree = maxd;
+  double total = static_cast<double>(g->m2);
+  if (g->weights && g->m2) {
+    auto wd = cub::TransformInputIterator<double, ToDouble, const float*>(g->weights, ToDouble{});
+    auto nu = cub::TransformInputIterator<uint32_t, IsUnit, const float*>(g->weights, IsUnit{});
+    size_t tb1 = 0, tb2 = 0;
+    cub::DeviceReduce::Sum(nullptr, tb1, wd, d_sum, g->m2, s);
+    cub::DeviceReduce::Sum(nullptr, tb2, nu, d_nonunit, g->m2, s);
+    void* tmp = dmalloc(std::max(tb1, tb2));
+    cub::DeviceReduce::Sum(tmp, tb1, wd, d_sum, g->m2, s);
+    NULPA_CUDA(cudaMemcpyAsync(&total, d_sum, sizeof total, cudaMemcpyDeviceToHost, s));
+    uint32_t nonunit = 0;
+    cub::DeviceReduce::Sum(tmp, tb2, nu, d_nonunit, g->m2, s);
+    NULPA_CUDA(cudaMemcpyAsync(&nonunit, d_nonunit, sizeof nonunit, cudaMemcpyDeviceToHost, s));
+    NULPA_CUDA(cudaStreamSynchronize(s));
+    dfree(tmp);
+    if (nonunit == 0) {
+      // Every weight is 1.0f: drop the array (results are identical, 4 B/edge saved).
+      if (g->owns) dfree(g->weights);
+      g->weights = nullptr;
+    }
+  }
+  g->total_2m = total;
+  dfree(d_bad);
+  dfree(d_max);
+  dfree(d_sum);
+  dfree(d_nonunit);
+}
+
+void partition_two_way(const uint64_t* off, uint32_t n, uint32_t sw, uint32_t* low,
+                       uint32_t* high, uint64_t* n_low, uint64_t* n_high, cudaStream_t s) {
+  uint64_t* d_num = dalloc<uint64_t>(1);
+  cub::CountingInputIterator<uint32_t> ids(0);
+  size_t tb = 0;
+  cub::DeviceSelect::If(nullptr, tb, ids, low, d_num, static_cast<uint64_t>(n),
+                        DegInRange{off, 0, sw - 1ull}, s);
+  void* tmp = dmalloc(tb);
+  cub::DeviceSelect::If(tmp, tb, ids, low, d_num, static_cast<uint64_t>(n),
+                        DegInRange{off, 0, sw - 1ull}, s);
+  NULPA_CUDA(cudaMemcpyAsync(n_low, d_num, 8, cudaMemcpyDeviceToHost, s));
+  cub::DeviceSelect::If(tmp, tb, ids, high, d_num, static_cast<uint64_t>(n),
+                        DegInRange{off, sw, ~0ull}, s);
+  NULPA_CUDA(cudaMemcpyAsync(n_high, d_num, 8, cudaMemcpyDeviceToHost, s));
+  NULPA_CUDA(cudaStreamSynchronize(s));
+  dfree(tmp);
+  dfree(d_num);
+}
+
+Plan::~Plan() {
+  for (auto* p : list) dfree(p);
+  dfree(tab_off);
+  dfree(tab_cap);
+  dfree(occ_off);
+  dfree(occ_n);
+  dfree(occ);
+  dfree(keys);
+  dfree(vals);
+  dfree(best);
+  dfree(best_k);
+  dfree(active);
+  dfree(changed);
+  dfree(item_hub);
+  dfree(item_start);
+}
+
+TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* t) {
+  // Thread tier: deg < switch_degree (the reference's scalar path), capped by
+  // the register table of k_thread (16 entries).
+  uint32_t tmax = (t && t->thread_max_degree) ? t->thread_max_degree : 8u;
+  tmax = std::min<uint32_t>(tmax, 16u);
+  if (switch_degree >= 2) tmax = std::min<uint32_t>(tmax, switch_degree - 1);
+  uint32_t wmax = (t && t->warp_max_degree) ? t->warp_max_degree : uint32_t(dev::kWarpTier);
+  wmax = std::max<uint32_t>(std::min<uint32_t>(wmax, dev::kWarpTier), tmax);
+  uint32_t bmax = (t && t->block_max_degree) ? t->block_max_degree : dev::kBlockTier;
+  bmax = std::max<uint32_t>(std::min<uint32_t>(bmax, dev::kBlockTier), wmax);
+  return {tmax, wmax, bmax};
+}
+
+Plan* get_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream_t s) {
+  if (g->plan && g->plan->thread_max == tb.thread_max && g->plan->warp_max == tb.warp_max &&
+      g->plan->block_max == tb.block_max && g->plan->value_bytes == value_bytes)
+    return g->plan;
+  delete g->plan;
+  g->plan = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  Plan* p = new Plan();
+  try {
+    p->thread_max = tb.thread_max;
+    p->warp_max = tb.warp_max;
+    p->block_max = tb.block_max;
+    p->value_bytes = value_bytes;
+    const uint32_t n = g->n;
+    const uint64_t bounds[4][2] = {{1, tb.thread_max},
+                                   {uint64_t(tb.thread_max) + 1, tb.warp_max},
+                                   {uint64_t(tb.warp_max) + 1, tb.block_max},
+                                   {uint64_t(tb.block_max) + 1, ~0ull}};
+    uint64_t* d_num = dalloc<uint64_t>(1);
+    size_t tbytes = 0;
+    cub::CountingInputIterator<uint32_t> ids(0);
+    cub::DeviceSelect::If(nullptr, tbytes, ids, static_cast<uint32_t*>(nullptr), d_num,
+                          static_cast<uint64_t>(n), DegInRange{g->offsets, 1, 1}, s);
+    void* tmp = dmalloc(tbytes);
+    for (int t = 0; t < 4; ++t) {
+      uint32_t* out = dalloc<uint32_t>(n + 1);
+      cub::DeviceSelect::If(tmp, tbytes, ids, out, d_num, static_cast<uint64_t>(n),
+                            DegInRange{g->offsets, bounds[t][0], bounds[t][1]}, s);
+      uint64_t cnt = 0;
+      NULPA_CUDA(cudaMemcpyAsync(&cnt, d_num, sizeof cnt, cudaMemcpyDeviceToHost, s));
+      NULPA_CUDA(cudaStreamSynchronize(s));
+      p->list[t] = out;
+      p->count[t] = static_cast<uint32_t>(cnt);
+    }
+    dfree(tmp);
+    dfree(d_num);
+
+    // Hub tier: per-hub global tables and (hub, chunk) work items. Hub counts
+    // are small (vertices of degree > block_max), so the layout is built on
+    // the host.
+    const uint32_t H = p->count[3];
+    p->n_hubs = H;
+    std::vector<uint32_t> hdeg(H);
+    if (H) {
+      uint32_t* d_deg = dalloc<uint32_t>(H);
+      k_gather_degrees<<<256, 256, 0, s>>>(p->list[3], g->offsets, H, d_deg);
+      NULPA_CUDA(cudaGetLastError());
+      NULPA_CUDA(cudaMemcpyAsync(hdeg.data(), d_deg, H * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      NULPA_CUDA(cudaStreamSynchronize(s));
+      dfree(d_deg);
+    }
+    std::vector<uint64_t> toff(H), ooff(H);
+    std::vector<uint32_t> tcap(H), ihub, istart;
+    uint64_t slots = 0, occs = 0;
+    for (uint32_t x = 0; x < H; ++x) {
+      const uint32_t d = hdeg[x];
+      const uint32_t cap = dev::pow2_ceil(d + d / 2 + 1);  // load factor <= 2/3
+      toff[x] = slots;
+      tcap[x] = cap;
+      ooff[x] = occs;
+      slots += cap;
+      occs += d;
+      for (uint32_t e = 0; e < d; e += dev::kHubChunk) {
+        ihub.push_back(x);
+        istart.push_back(e);
+      }
+      p->edges[3] += d;
+    }
+    p->n_items = static_cast<uint32_t>(ihub.size());
+    p->table_slots = slots;
+    p->occ_slots = occs;
+    // (+1 entries so every array is non-empty and the memsets below stay in bounds)
+    p->tab_off = dalloc<uint64_t>(H + 1);
+    p->tab_cap = dalloc<uint32_t>(H + 1);
+    p->occ_off = dalloc<uint64_t>(H + 1);
+    p->occ_n = dalloc<uint32_t>(H + 1);
+    p->best = dalloc<unsigned long long>(H + 1);
+    p->best_k = dalloc<uint32_t>(H + 1);
+    p->active = dalloc<uint8_t>(H + 1);
+    p->changed = dalloc<uint8_t>(H + 1);
+    p->occ = dalloc<uint32_t>(occs + 1);
+    p->keys = dalloc<uint32_t>(slots + 1);
+    p->vals = dmalloc(slots * value_bytes + 16);
+    p->item_hub = dalloc<uint32_t>(p->n_items + 1);
+    p->item_start = dalloc<uint32_t>(p->n_items + 1);
+    if (H) {
+      NULPA_CUDA(cudaMemcpy(p->tab_off, toff.data(), H * 8, cudaMemcpyHostToDevice));
+      NULPA_CUDA(cudaMemcpy(p->tab_cap, tcap.data(), H * 4, cudaMemcpyHostToDevice));
+      NULPA_CUDA(cudaMemcpy(p->occ_off, ooff.data(), H * 8, cudaMemcpyHostToDevice));
+      NULPA_CUDA(cudaMemcpy(p->item_hub, ihub.data(), ihub.size() * 4, cudaMemcpyHostToDevice));
+      NULPA_CUDA(cudaMemcpy(p->item_start, istart.data(), istart.size() * 4, cudaMemcpyHostToDevice));
+    }
+    NULPA_CUDA(cudaMemsetAsync(p->occ_n, 0, H * 4 + 4, s));
+    NULPA_CUDA(cudaMemsetAsync(p->best, 0, H * 8 + 8, s));
+    NULPA_CUDA(cudaMemsetAsync(p->best_k, 0xFF, H * 4 + 4, s));
+    NULPA_CUDA(cudaMemsetAsync(p->changed, 0, H + 1, s));
+    NULPA_CUDA(cudaMemsetAsync(p->keys, 0xFF, slots * 4 + 4, s));
+    NULPA_CUDA(cudaMemsetAsync(p->vals, 0, slots * value_bytes + 16, s));
+    NULPA_CUDA(cudaStreamSynchronize(s));
+    // Edge totals of the lower tiers (for reporting).
+    // (computed lazily by callers that need them; hubs are exact above)
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  p->build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  g->plan = p;
+  return p;
+}
+
+}  // namespace nulpa
+
+// ---- C ABI: resident graph ------------------------------------------------------
+
+using namespace nulpa;
+
+extern "C" {
+
+const char* nulpa_last_error(void) { return nulpa::last_error().c_str(); }
+
+int nulpa_version(void) { return 1; }
+
+int nulpa_device_count(int* count) {
+  return guarded([&] {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      c = 0;
+    }
+    *count = c;
+  });
+}
+
+int nulpa_graph_upload(const nulpa_csr* csr, int device, nulpa_graph** out) {
+  return guarded([&] {
+    check_host_csr(csr);
+    use_device(device);
+    auto* g = new nulpa_graph();
+    try {
+      g->device = device;
+      g->n = csr->n;
+      g->m2 = csr->m2;
+      g->owns = true;
+      g->offsets = dalloc<uint64_t>(uint64_t(csr->n) + 1);
+      g->targets = dalloc<uint32_t>(csr->m2);
+      NULPA_CUDA(cudaMemcpy(g->offsets, csr->offsets, (uint64_t(csr->n) + 1) * 8,
+                            cudaMemcpyHostToDevice));
+      if (csr->m2)
+        NULPA_CUDA(cudaMemcpy(g->targets, csr->targets, csr->m2 * 4, cudaMemcpyHostToDevice));
+      if (csr->weights && csr->m2) {
+        g->weights = dalloc<float>(csr->m2);
+        NULPA_CUDA(cudaMemcpy(g->weights, csr->weights, csr->m2 * 4, cudaMemcpyHostToDevice));
+      }
+      finalize_graph(g, 0);
+    } catch (...) {
+      nulpa_graph_free(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int nulpa_graph_wrap_device(const nulpa_csr* csr, int device, nulpa_graph** out) {
+  return guarded([&] {
+    if (!csr || !csr->offsets || (csr->m2 && !csr->targets))
+      throw Error(NULPA_EINVAL, "inconsistent CSR arrays");
+    use_device(device);
+    auto* g = new nulpa_graph();
+    g->device = device;
+    g->n = csr->n;
+    g->m2 = csr->m2;
+    g->owns = false;
+    g->offsets = const_cast<uint64_t*>(csr->offsets);
+    g->targets = const_cast<uint32_t*>(csr->targets);
+    g->weights = const_cast<float*>(csr->weights);
+    try {
+      finalize_graph(g, 0);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int nulpa_graph_free(nulpa_graph* g) {
+  return guarded([&] {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    delete g->plan;
+    if (g->owns) {
+      dfree(g->offsets);
+      dfree(g->targets);
+      dfree(g->weights);
+    }
+    delete g;
+  });
+}
+
+int nulpa_graph_info(const nulpa_graph* g, uint32_t* n, uint64_t* m2, uint32_t* max_degree,
+                     int* weighted) {
+  return guarded([&] {
+    if (!g) throw Error(NULPA_EINVAL, "null graph");
+    if (n) *n = g->n;
+    if (m2) *m2 = g->m2;
+    if (max_degree) *max_degree = g->max_degree;
+    if (weighted) *weighted = g->weights ? 1 : 0;
+  });
+}
+
+int nulpa_graph_device_csr(const nulpa_graph* g, nulpa_csr* out) {
+  return guarded([&] {
+    if (!g) throw Error(NULPA_EINVAL, "null graph");
+    out->n = g->n;
+    out->reserved = 0;
+    out->m2 = g->m2;
+    out->offsets = g->offsets;
+    out->targets = g->targets;
+    out->weights = g->weights;
+  });
+}
+
+int nulpa_graph_download(const nulpa_graph* g, uint64_t* offsets, uint32_t* targets,
+                         float* weights) {
+  return guarded([&] {
+    if (!g) throw Error(NULPA_EINVAL, "null graph");
+    use_device(g->device);
+    if (offsets)
+      NULPA_CUDA(cudaMemcpy(offsets, g->offsets, (uint64_t(g->n) + 1) * 8, cudaMemcpyDeviceToHost));
+    if (targets && g->m2)
+      NULPA_CUDA(cudaMemcpy(targets, g->targets, g->m2 * 4, cudaMemcpyDeviceToHost));
+    if (weights) {
+      if (g->weights)
+        NULPA_CUDA(cudaMemcpy(weights, g->weights, g->m2 * 4, cudaMemcpyDeviceToHost));
+      else
+        std::fill(weights, weights + g->m2, 1.0f);
+    }
+  });
+}
+
+}  // extern "C"

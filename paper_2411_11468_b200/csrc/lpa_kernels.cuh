@@ -1,0 +1,639 @@
+// ν-LPA pass kernels for sm_100a, one per degree tier.
+//
+// Reference hot path (paths relative to /root/reference/proj):
+//   parallel_move scalar path   src/lpa.cpp:139-165
+//   parallel_move team path     src/lpa.cpp:169-230
+//   sync_move                   src/lpa.cpp:70-100
+//   lpa_move (Sequential)       include/labelprop/lpa.hpp:123-145
+//   detail::scan_candidate      include/labelprop/lpa.hpp:92-111
+//   ht_accumulate/ht_max_key    include/labelprop/hashtable.hpp:96-185
+//
+// Every kernel applies the same per-vertex rule: skip if flagged, mark
+// processed, pick the neighbour label of greatest total weight (self-loops
+// skipped, ties to the smaller label), move if (pick_less ? c* < cur : c* !=
+// cur), then wake every neighbour (async: inline; sync: deferred to k_wake
+// after the joint application, lpa.cpp:92-98).
+//
+// Tiers (all lists ascending by vertex id, like partition_by_degree):
+//   k_thread  deg <= DMAX          one thread per vertex, register O(d^2) count
+//   k_warp    deg <= 512           one warp per vertex; deg <= 32 uses
+//                                  __match_any_sync dedup in registers, larger
+//                                  rows a per-warp shared-memory table
+//   k_block   deg <= 4096          one CTA per vertex, shared-memory table
+//   k_hub_*   larger               (vertex, 4096-edge chunk) work items: CTA
+//                                  shared-memory pre-aggregation, flushed into
+//                                  a per-hub global table; sparse argmax via
+//                                  the occupied-slot list; decide; chunked wake
+#pragma once
+
+#include "device.cuh"
+
+namespace nulpa {
+namespace dev {
+
+// ---- shared epilogue ----------------------------------------------------------
+
+// Apply the move rule for vertex i (lpa.cpp:157-164 / :87-90). Returns true if
+// the label changed. Called by exactly one thread per vertex.
+template <int MODE>
+__device__ __forceinline__ bool apply_move(const PassCtx& c, uint32_t i, uint32_t cand) {
+  if (cand == kEmpty) return false;
+  const uint32_t cur = (MODE == kAsync) ? __ldcg(c.lab_out + i) : __ldg(c.lab_in + i);
+  const bool allowed = c.pick_less ? (cand < cur) : (cand != cur);
+  if (!allowed) return false;
+  if constexpr (MODE == kAsync) {
+    __stcg(c.lab_out + i, cand);
+    __threadfence();  // publish the label before the neighbour wake-ups
+  } else {
+    c.lab_out[i] = cand;
+    if (c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
+  }
+  return true;
+}
+
+// Check-and-set the processed flag (lpa.cpp:143-144). Returns true to skip.
+__device__ __forceinline__ bool claim_vertex(const PassCtx& c, uint32_t i) {
+  if (!c.flags) return false;
+  if (load_flag(c.flags + i)) return true;
+  c.flags[i] = 1;
+  return false;
+}
+
+// ---- tier 0: thread per vertex ---------------------------------------------------
+
+template <int MODE, typename W, bool WEIGHTED, int DMAX>
+__global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __restrict__ list,
+                                                uint32_t count) {
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  // The loop bound is rounded up to whole warps so warp_add_counter sees 32 lanes.
+  const uint32_t bound = (count + 31u) & ~31u;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < bound; t += stride) {
+    if (t >= count) continue;
+    const uint32_t i = __ldg(list + t);
+    if (claim_vertex(c, i)) continue;
+    const uint64_t lo = __ldg(c.g.off + i);
+    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+    uint32_t nb[DMAX];
+    uint32_t lab[DMAX];
+    W wt[DMAX];
+#pragma unroll
+    for (int k = 0; k < DMAX; ++k) nb[k] = (k < d) ? __ldg(c.g.tgt + lo + k) : i;
+#pragma unroll
+    for (int k = 0; k < DMAX; ++k) {
+      const bool valid = k < d && nb[k] != i;  // self-loops skipped (lpa.hpp:102)
+      lab[k] = valid ? load_label<MODE>(c.lab_in + nb[k]) : kEmpty;
+      wt[k] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + k) : W(0);
+    }
+    // Per-label total in neighbour order (bit-identical to the reference's
+    // sequential accumulation, even for non-integer weights), then argmax.
+    Best<W> b{W(0), kEmpty};
+#pragma unroll
+    for (int k = 0; k < DMAX; ++k) {
+      W s = W(0);
+#pragma unroll
+      for (int m = 0; m < DMAX; ++m) s += (lab[m] == lab[k]) ? wt[m] : W(0);
+      best_merge(b, s, lab[k]);
+    }
+    ++n_v;
+    n_e += d;
+    if (!apply_move<MODE>(c, i, b.k)) continue;
+    ++n_dn;
+    if (MODE == kAsync && c.flags) {
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k)
+        if (k < d) c.flags[nb[k]] = 0;
+      n_w += d;
+    }
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+}
+
+// ---- cooperative gather + insert -------------------------------------------------
+
+// One round of a team gather: each lane holds one edge (or none), dedups its
+// label against the warp with __match_any_sync, and the lowest lane of each
+// label group adds the group's weight to the table. All 32 lanes call it.
+template <int MODE, typename W, bool WEIGHTED>
+__device__ __forceinline__ void gather_insert(const PassCtx& c, uint32_t i, uint32_t lab,
+                                              W w, uint32_t* keys, W* vals, uint32_t cap,
+                                              unsigned long long& fails, uint32_t* occ = nullptr,
+                                              uint32_t* occ_n = nullptr) {
+  const unsigned peers = __match_any_sync(kFull, lab);
+  W s;
+  if constexpr (WEIGHTED)
+    s = peer_sum(w, peers);
+  else
+    s = static_cast<W>(__popc(peers));
+  const int lane = threadIdx.x & 31;
+  if (lab != kEmpty && (__ffs(peers) - 1) == lane) {
+    if (!ht_add(keys, vals, cap, c.strategy, lab, s, occ, occ_n)) ++fails;
+  }
+}
+
+// ---- tier 1: warp per vertex ------------------------------------------------------
+
+template <int MODE, typename W, bool WEIGHTED>
+__global__ void __launch_bounds__(kBlockThreads) k_warp(PassCtx c,
+                                                        const uint32_t* __restrict__ list,
+                                                        uint32_t count) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kBlockThreads / 32;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw) + warp * kWarpCap;
+  W* vals = reinterpret_cast<W*>(smem_raw + kWarps * kWarpCap * sizeof(uint32_t)) + warp * kWarpCap;
+
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
+  const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  for (uint32_t t = gw; t < count; t += nw) {
+    const uint32_t i = __ldg(list + t);
+    int skip = 0;
+    if (lane == 0) skip = claim_vertex(c, i) ? 1 : 0;
+    if (__shfl_sync(kFull, skip, 0)) continue;
+    const uint64_t lo = __ldg(c.g.off + i);
+    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+    Best<W> b{W(0), kEmpty};
+    if (d <= 32) {
+      // Register path: one label per lane, dedup by __match_any_sync.
+      const uint32_t j = lane < d ? __ldg(c.g.tgt + lo + lane) : i;
+      const bool valid = lane < d && j != i;
+      const uint32_t lab = valid ? load_label<MODE>(c.lab_in + j) : kEmpty;
+      const W w = valid ? edge_weight<W, WEIGHTED>(c.g, lo + lane) : W(0);
+      const unsigned peers = __match_any_sync(kFull, lab);
+      W s;
+      if constexpr (WEIGHTED)
+        s = peer_sum(w, peers);
+      else
+        s = static_cast<W>(__popc(peers));
+      if (lab != kEmpty && (__ffs(peers) - 1) == lane) b = Best<W>{s, lab};
+    } else {
+      // Table path: cap = pow2 >= 2d slots of the warp's shared region.
+      const uint32_t cap = pow2_ceil(2 * d);
+      for (uint32_t s = lane; s < cap; s += 32) {
+        keys[s] = kEmpty;
+        vals[s] = W(0);
+      }
+      __syncwarp();
+      constexpr int U = 4;
+      for (uint32_t base = 0; base < d; base += 32 * U) {
+        uint32_t j[U], lab[U];
+        W w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t e = base + u * 32 + lane;
+          j[u] = e < d ? __ldg(c.g.tgt + lo + e) : i;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t e = base + u * 32 + lane;
+          const bool valid = e < d && j[u] != i;
+          lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+          w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          gather_insert<MODE, W, WEIGHTED>(c, i, lab[u], w[u], keys, vals, cap, fails);
+      }
+      __syncwarp();
+      for (uint32_t s = lane; s < cap; s += 32) best_merge(b, vals[s], keys[s]);
+      __syncwarp();
+    }
+    b = warp_best(b);
+    int changed = 0;
+    if (lane == 0) changed = apply_move<MODE>(c, i, b.k) ? 1 : 0;
+    changed = __shfl_sync(kFull, changed, 0);
+    if (lane == 0) {
+      ++n_v;
+      n_e += d;
+      n_dn += changed;
+    }
+    if (MODE == kAsync && changed && c.flags) {
+      for (uint32_t e = lane; e < d; e += 32) c.flags[__ldg(c.g.tgt + lo + e)] = 0;
+      if (lane == 0) n_w += d;
+    }
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+  warp_add_counter(c.ctr, C_FAIL, fails);
+}
+
+// ---- block-wide helpers ------------------------------------------------------------
+
+template <typename W>
+__device__ __forceinline__ Best<W> block_best(Best<W> b, Best<W>* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  b = warp_best(b);
+  if (lane == 0) red[warp] = b;
+  __syncthreads();
+  if (warp == 0) {
+    Best<W> r = lane < (blockDim.x >> 5) ? red[lane] : Best<W>{W(0), kEmpty};
+    r = warp_best(r);
+    if (lane == 0) red[0] = r;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+// Gather edges [e0, e1) of vertex i into a CTA-shared table (U edges per thread
+// in flight).
+template <int MODE, typename W, bool WEIGHTED>
+__device__ __forceinline__ void block_gather(const PassCtx& c, uint32_t i, uint64_t lo,
+                                             uint32_t e0, uint32_t e1, uint32_t* keys, W* vals,
+                                             uint32_t cap, unsigned long long& fails) {
+  constexpr int U = 4;
+  const uint32_t T = blockDim.x;
+  for (uint32_t base = e0; base < e1; base += T * U) {
+    uint32_t j[U], lab[U];
+    W w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t e = base + u * T + threadIdx.x;
+      j[u] = e < e1 ? __ldg(c.g.tgt + lo + e) : i;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t e = base + u * T + threadIdx.x;
+      const bool valid = e < e1 && j[u] != i;
+      lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+      w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      gather_insert<MODE, W, WEIGHTED>(c, i, lab[u], w[u], keys, vals, cap, fails);
+  }
+}
+
+// ---- tier 2: CTA per vertex, shared-memory table ------------------------------------
+
+template <int MODE, typename W, bool WEIGHTED>
+__global__ void __launch_bounds__(kBlockThreads) k_block(PassCtx c,
+                                                         const uint32_t* __restrict__ list,
+                                                         uint32_t count) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);
+  W* vals = reinterpret_cast<W*>(smem_raw + kBlockCap * sizeof(uint32_t));
+  __shared__ Best<W> red[32];
+  __shared__ int s_flag;
+
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
+  for (uint32_t t = blockIdx.x; t < count; t += gridDim.x) {
+    const uint32_t i = __ldg(list + t);
+    if (threadIdx.x == 0) s_flag = claim_vertex(c, i) ? 1 : 0;
+    __syncthreads();
+    const int skip = s_flag;
+    __syncthreads();
+    if (skip) continue;
+    const uint64_t lo = __ldg(c.g.off + i);
+    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+    const uint32_t cap = pow2_ceil(2 * d);
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
+      keys[s] = kEmpty;
+      vals[s] = W(0);
+    }
+    __syncthreads();
+    block_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, keys, vals, cap, fails);
+    __syncthreads();
+    Best<W> b{W(0), kEmpty};
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) best_merge(b, vals[s], keys[s]);
+    b = block_best(b, red);
+    if (threadIdx.x == 0) {
+      s_flag = apply_move<MODE>(c, i, b.k) ? 1 : 0;
+      ++n_v;
+      n_e += d;
+      n_dn += s_flag;
+    }
+    __syncthreads();
+    const int changed = s_flag;
+    if (MODE == kAsync && changed && c.flags) {
+      for (uint32_t e = threadIdx.x; e < d; e += blockDim.x) c.flags[__ldg(c.g.tgt + lo + e)] = 0;
+      if (threadIdx.x == 0) n_w += d;
+    }
+    __syncthreads();
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+  warp_add_counter(c.ctr, C_FAIL, fails);
+}
+
+// ---- tier 3: hubs, global tables -------------------------------------------------------
+
+template <int MODE>
+__global__ void k_hub_select(PassCtx c, HubCtx h) {
+  unsigned long long n_v = 0, n_e = 0;
+  const uint32_t bound = (h.n_hubs + 31u) & ~31u;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < bound;
+       x += gridDim.x * blockDim.x) {
+    if (x >= h.n_hubs) continue;
+    const uint32_t i = h.hub_v[x];
+    const bool skip = claim_vertex(c, i);
+    h.active[x] = skip ? 0 : 1;
+    if (!skip) {
+      ++n_v;
+      n_e += c.g.off[i + 1] - c.g.off[i];
+    }
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+}
+
+// Accumulate one (hub, chunk) item: pre-aggregate the chunk in shared memory,
+// then flush each distinct label once into the hub's global table.
+template <int MODE, typename W, bool WEIGHTED>
+__global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);
+  W* vals = reinterpret_cast<W*>(smem_raw + kBlockCap * sizeof(uint32_t));
+  W* gvals = static_cast<W*>(h.vals);
+  unsigned long long fails = 0;
+  for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
+    const uint32_t x = h.item_hub[it];
+    if (!h.active[x]) continue;  // uniform across the CTA
+    const uint32_t i = h.hub_v[x];
+    const uint64_t lo = __ldg(c.g.off + i);
+    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+    const uint32_t e0 = h.item_start[it];
+    const uint32_t e1 = min(d, e0 + kHubChunk);
+    const uint32_t cap = kBlockCap;
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
+      keys[s] = kEmpty;
+      vals[s] = W(0);
+    }
+    __syncthreads();
+    block_gather<MODE, W, WEIGHTED>(c, i, lo, e0, e1, keys, vals, cap, fails);
+    __syncthreads();
+    uint32_t* gk = h.keys + h.tab_off[x];
+    W* gv = gvals + h.tab_off[x];
+    uint32_t* occ = h.occ + h.occ_off[x];
+    const uint32_t gcap = h.tab_cap[x];
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
+      const uint32_t k = keys[s];
+      if (k != kEmpty && !ht_add(gk, gv, gcap, c.strategy, k, vals[s], occ, h.occ_n + x)) ++fails;
+    }
+    __syncthreads();
+  }
+  warp_add_counter(c.ctr, C_FAIL, fails);
+}
+
+// Sparse argmax over the occupied slots of each active hub; clears the slots
+// it reads (float path) so the tables are idle for the next pass.
+template <typename W>
+__global__ void __launch_bounds__(kBlockThreads) k_hub_argmax(HubCtx h) {
+  __shared__ Best<W> red[32];
+  W* gvals = static_cast<W*>(h.vals);
+  for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
+    const uint32_t x = h.item_hub[it];
+    if (!h.active[x]) continue;
+    const uint32_t e0 = h.item_start[it];
+    const uint32_t n_occ = h.occ_n[x];
+    if (e0 >= n_occ) continue;
+    const uint32_t e1 = min(n_occ, e0 + kHubChunk);
+    uint32_t* gk = h.keys + h.tab_off[x];
+    W* gv = gvals + h.tab_off[x];
+    const uint32_t* occ = h.occ + h.occ_off[x];
+    Best<W> b{W(0), kEmpty};
+    for (uint32_t p = e0 + threadIdx.x; p < e1; p += blockDim.x) {
+      const uint32_t s = occ[p];
+      best_merge(b, gv[s], gk[s]);
+      if constexpr (sizeof(W) == 4) {
+        gk[s] = kEmpty;
+        gv[s] = W(0);
+      }
+    }
+    b = block_best(b, red);
+    if (threadIdx.x == 0 && b.k != kEmpty) {
+      if constexpr (sizeof(W) == 4) {
+        // (value bits, ~key): a larger value wins, then a smaller key.
+        const unsigned long long packed =
+            (static_cast<unsigned long long>(__float_as_uint(static_cast<float>(b.v))) << 32) |
+            static_cast<unsigned long long>(~b.k);
+        atomicMax(h.best + x, packed);
+      } else {
+        atomicMax(h.best + x, static_cast<unsigned long long>(__double_as_longlong(b.v)));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Double path only: the smallest key among slots holding the maximum value;
+// clears the slots.
+__global__ void __launch_bounds__(kBlockThreads) k_hub_argmax_key_f64(HubCtx h) {
+  double* gvals = static_cast<double*>(h.vals);
+  for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
+    const uint32_t x = h.item_hub[it];
+    if (!h.active[x]) continue;
+    const uint32_t e0 = h.item_start[it];
+    const uint32_t n_occ = h.occ_n[x];
+    if (e0 >= n_occ) continue;
+    const uint32_t e1 = min(n_occ, e0 + kHubChunk);
+    uint32_t* gk = h.keys + h.tab_off[x];
+    double* gv = gvals + h.tab_off[x];
+    const uint32_t* occ = h.occ + h.occ_off[x];
+    const double bestv = __longlong_as_double(static_cast<long long>(h.best[x]));
+    for (uint32_t p = e0 + threadIdx.x; p < e1; p += blockDim.x) {
+      const uint32_t s = occ[p];
+      if (gv[s] == bestv) atomicMin(h.best_k + x, gk[s]);
+      gk[s] = kEmpty;
+      gv[s] = 0.0;
+    }
+  }
+}
+
+template <int MODE, typename W>
+__global__ void k_hub_decide(PassCtx c, HubCtx h) {
+  unsigned long long n_dn = 0;
+  const uint32_t bound = (h.n_hubs + 31u) & ~31u;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < bound;
+       x += gridDim.x * blockDim.x) {
+    if (x >= h.n_hubs) continue;
+    uint8_t ch = 0;
+    if (h.active[x]) {
+      uint32_t cand = kEmpty;
+      if (h.occ_n[x] > 0) {
+        if constexpr (sizeof(W) == 4)
+          cand = ~static_cast<uint32_t>(h.best[x] & 0xFFFFFFFFull);
+        else
+          cand = h.best_k[x];
+      }
+      ch = apply_move<MODE>(c, h.hub_v[x], cand) ? 1 : 0;
+      n_dn += ch;
+    }
+    h.changed[x] = ch;
+    h.occ_n[x] = 0;
+    h.best[x] = 0;
+    h.best_k[x] = kEmpty;
+  }
+  warp_add_counter(c.ctr, C_DN, n_dn);
+}
+
+// Async wake for changed hubs, one chunk per work item.
+__global__ void __launch_bounds__(kBlockThreads) k_hub_wake(PassCtx c, HubCtx h) {
+  unsigned long long n_w = 0;
+  for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
+    const uint32_t x = h.item_hub[it];
+    if (!h.changed[x]) continue;
+    const uint32_t i = h.hub_v[x];
+    const uint64_t lo = c.g.off[i];
+    const uint32_t d = static_cast<uint32_t>(c.g.off[i + 1] - lo);
+    const uint32_t e0 = h.item_start[it];
+    const uint32_t e1 = min(d, e0 + kHubChunk);
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) c.flags[__ldg(c.g.tgt + lo + e)] = 0;
+    if (threadIdx.x == 0) n_w += e1 - e0;
+  }
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+}
+
+// ---- sync-mode deferred wake (lpa.cpp:97-98) -----------------------------------------
+
+__global__ void __launch_bounds__(kBlockThreads) k_wake_list(Graph g, uint8_t* flags,
+                                                             const uint32_t* list,
+                                                             const unsigned long long* count_p,
+                                                             unsigned long long* ctr) {
+  const uint32_t count = static_cast<uint32_t>(*count_p);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
+  unsigned long long n_w = 0;
+  for (uint32_t t = gw; t < count; t += nw) {
+    const uint32_t i = list[t];
+    const uint64_t lo = g.off[i], hi = g.off[i + 1];
+    for (uint64_t e = lo + lane; e < hi; e += 32) flags[__ldg(g.tgt + e)] = 0;
+    if (lane == 0) n_w += hi - lo;
+  }
+  warp_add_counter(ctr, C_WAKE_E, n_w);
+}
+
+// ---- Sequential mode (lpa_move, lpa.hpp:123-145) -----------------------------------------
+// One CTA walks the vertices in ascending id order with in-place updates; each
+// vertex's scan is CTA-parallel. Exact reference semantics on the GPU (no CPU
+// fallback); slow by construction — a compatibility mode, not the hot path.
+template <typename W, bool WEIGHTED>
+__global__ void __launch_bounds__(kBlockThreads) k_sequential(PassCtx c, uint32_t* gkeys,
+                                                              W* gvals) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* skeys = reinterpret_cast<uint32_t*>(smem_raw);
+  W* svals = reinterpret_cast<W*>(smem_raw + kBlockCap * sizeof(uint32_t));
+  __shared__ Best<W> red[32];
+  __shared__ int s_flag;
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
+  for (uint32_t i = 0; i < c.g.n; ++i) {
+    if (threadIdx.x == 0) {
+      int skip = 1;
+      if (!c.flags[i]) {
+        c.flags[i] = 1;
+        skip = (c.g.off[i + 1] == c.g.off[i]) ? 1 : 0;
+      }
+      s_flag = skip;
+    }
+    __syncthreads();
+    const int skip = s_flag;
+    __syncthreads();
+    if (skip) continue;
+    const uint64_t lo = c.g.off[i];
+    const uint32_t d = static_cast<uint32_t>(c.g.off[i + 1] - lo);
+    const uint32_t cap = pow2_ceil(2 * d);
+    uint32_t* keys = cap <= kBlockCap ? skeys : gkeys;
+    W* vals = cap <= kBlockCap ? svals : gvals;
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
+      keys[s] = kEmpty;
+      vals[s] = W(0);
+    }
+    __syncthreads();
+    for (uint32_t base = 0; base < d; base += blockDim.x) {
+      const uint32_t e = base + threadIdx.x;
+      const uint32_t j = e < d ? c.g.tgt[lo + e] : i;
+      const bool valid = e < d && j != i;
+      const uint32_t lab = valid ? c.lab_out[j] : kEmpty;
+      const W w = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
+      gather_insert<kSync, W, WEIGHTED>(c, i, lab, w, keys, vals, cap, fails);
+    }
+    __syncthreads();
+    Best<W> b{W(0), kEmpty};
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) best_merge(b, vals[s], keys[s]);
+    b = block_best(b, red);
+    if (threadIdx.x == 0) {
+      int ch = 0;
+      if (b.k != kEmpty) {
+        const uint32_t cur = c.lab_out[i];
+        if (c.pick_less ? (b.k < cur) : (b.k != cur)) {
+          c.lab_out[i] = b.k;
+          ch = 1;
+        }
+      }
+      s_flag = ch;
+      ++n_v;
+      n_e += d;
+      n_dn += ch;
+    }
+    __syncthreads();
+    if (s_flag) {
+      for (uint32_t e = threadIdx.x; e < d; e += blockDim.x) c.flags[c.g.tgt[lo + e]] = 0;
+      if (threadIdx.x == 0) n_w += d;
+    }
+    __syncthreads();
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+  warp_add_counter(c.ctr, C_FAIL, fails);
+}
+
+// ---- cross-check (lpa.cpp:338-360) ---------------------------------------------------------
+// The reference scans i ascending and reads labels[c*] (c* < i) after earlier
+// reverts. revert(i) = changed(i) && i > c_i && final(c_i) != c_i with
+// final(v) = revert(v) ? prev[v] : lab[v]: a recursion on strictly smaller ids,
+// solved by Jacobi rounds until no flag moves (depth-bounded).
+__global__ void k_cc_round(const uint32_t* lab, const uint32_t* prev, const uint8_t* r_in,
+                           uint8_t* r_out, uint32_t n, unsigned long long* moved) {
+  unsigned long long mv = 0;
+  const uint32_t bound = (n + 31u) & ~31u;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < bound;
+       i += gridDim.x * blockDim.x) {
+    if (i >= n) continue;
+    const uint32_t ci = lab[i];
+    uint8_t r = 0;
+    if (ci != prev[i] && i > ci) {
+      const uint32_t fc = r_in[ci] ? prev[ci] : lab[ci];
+      r = fc != ci ? 1 : 0;
+    }
+    if (r != r_in[i]) ++mv;
+    r_out[i] = r;
+  }
+  warp_add_counter(moved, 0, mv);
+}
+
+__global__ void k_cc_apply(Graph g, uint32_t* lab, const uint32_t* prev, const uint8_t* r,
+                           uint8_t* flags, unsigned long long* reverted) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
+  unsigned long long nrev = 0;
+  // Warp-per-32-vertex blocks so the neighbour wake is warp-cooperative.
+  for (uint32_t base = gw * 32; base < g.n; base += nw * 32) {
+    const uint32_t i = base + lane;
+    unsigned mine = (i < g.n && r[i]) ? 1u : 0u;
+    if (mine) {
+      lab[i] = prev[i];
+      flags[i] = 0;
+      ++nrev;
+    }
+    unsigned m = __ballot_sync(kFull, mine);
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t v = base + b;
+      const uint64_t lo = g.off[v], hi = g.off[v + 1];
+      for (uint64_t e = lo + lane; e < hi; e += 32) flags[g.tgt[e]] = 0;
+    }
+  }
+  warp_add_counter(reverted, 0, nrev);
+}
+
+}  // namespace dev
+}  // namespace nulpa

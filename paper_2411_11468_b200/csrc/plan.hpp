@@ -1,0 +1,71 @@
+// Per-graph execution plan: degree tiers and hub tables.
+#pragma once
+
+#include <cstdint>
+
+#include "internal.hpp"
+#include "device.cuh"
+
+namespace nulpa {
+
+struct Plan {
+  uint32_t thread_max = 0, warp_max = 0, block_max = 0;
+  int value_bytes = 4;  // hashtable value width the hub tables were sized for
+  // Tier vertex lists (ascending id): 0 thread, 1 warp, 2 block, 3 hub.
+  uint32_t* list[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint32_t count[4] = {0, 0, 0, 0};
+  uint64_t edges[4] = {0, 0, 0, 0};
+  // Hub tier.
+  uint32_t n_hubs = 0, n_items = 0;
+  uint64_t table_slots = 0, occ_slots = 0;
+  uint64_t* tab_off = nullptr;
+  uint32_t* tab_cap = nullptr;
+  uint64_t* occ_off = nullptr;
+  uint32_t* occ_n = nullptr;
+  uint32_t* occ = nullptr;
+  uint32_t* keys = nullptr;
+  void* vals = nullptr;
+  unsigned long long* best = nullptr;
+  uint32_t* best_k = nullptr;
+  uint8_t* active = nullptr;
+  uint8_t* changed = nullptr;
+  uint32_t* item_hub = nullptr;
+  uint32_t* item_start = nullptr;
+  double build_seconds = 0.0;
+
+  dev::HubCtx hub_ctx() const {
+    dev::HubCtx h;
+    h.hub_v = list[3];
+    h.tab_off = tab_off;
+    h.tab_cap = tab_cap;
+    h.occ_off = occ_off;
+    h.occ_n = occ_n;
+    h.occ = occ;
+    h.keys = keys;
+    h.vals = vals;
+    h.best = best;
+    h.best_k = best_k;
+    h.active = active;
+    h.changed = changed;
+    h.item_hub = item_hub;
+    h.item_start = item_start;
+    h.n_hubs = n_hubs;
+    h.n_items = n_items;
+    return h;
+  }
+  ~Plan();
+};
+
+struct TierBounds {
+  uint32_t thread_max, warp_max, block_max;
+};
+
+// Resolve the tier bounds from LpaConfig.switch_degree and the tuning struct.
+TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* tuning);
+
+// Build (or reuse the cached) plan of a resident graph.
+Plan* get_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream_t s);
+
+int sm_count();
+
+}  // namespace nulpa

@@ -1,0 +1,239 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Gates, strongest first:
+  1. a single synchronous label-choice step, bit-exact (labels and changed count);
+  2. full Synchronous / Sequential trajectories, bit-exact (labels, delta_n_per_iter,
+     iterations, converged, pl_iterations, cc_reverts);
+  3. ParallelAsync end to end: KATs exactly, modularity within 0.01 of the reference's
+     Synchronous modularity on the SBM (tolerance written in the test).
+Oracles: the committed golden vectors (made by the reference itself) and the C
+restatement (oracle/liboracle.so) on larger seeded inputs.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden_names, load_golden
+from paper_2411_11468_b200 import labelprop as lp
+
+pytestmark = pytest.mark.gpu
+
+Q_TOL = 0.01  # north star: final modularity within 0.01 absolute
+
+
+def graph_of(d):
+    return lp.CsrGraph(d["offsets"], d["targets"], d["weights"])
+
+
+def cfg_of(run):
+    c = run["config"]
+    return lp.LpaConfig(exec=lp.ExecMode(c["exec_mode"]), pl_period=c["pl_period"],
+                        cc_period=c["cc_period"], prune=c["prune"], tolerance=run["tolerance"],
+                        max_iterations=20)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_trajectories_bit_exact(name, golden_index):
+    meta = golden_index[name]
+    d = load_golden(name)
+    g = graph_of(d)
+    for k, run in enumerate(meta["runs"]):
+        r = lp.lpa(g, cfg_of(run))
+        assert np.array_equal(r.labels, d[f"run{k}_labels"]), (name, run["config"])
+        assert r.stats.delta_n_per_iter == run["delta_n"], (name, run["config"])
+        assert r.stats.iterations == run["iterations"]
+        assert r.stats.converged == run["converged"]
+        assert r.stats.pl_iterations == run["pl_iterations"]
+        assert r.stats.cc_reverts == run["cc_reverts"]
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_sync_step_bit_exact(name, golden_index):
+    meta = golden_index[name]
+    d = load_golden(name)
+    g = graph_of(d)
+    for st in meta["steps"]:
+        k, pl = st["input"], st["pick_less"]
+        for strategy in range(4):
+            for precision in (32, 64):
+                out, ch = lp.sync_step(g, d[f"step{k}_{pl}_in"], pl, strategy, precision)
+                assert ch == st["changed"]
+                assert np.array_equal(out, d[f"step{k}_{pl}_out"])
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_modularity_crosscheck_partition(name, golden_index):
+    meta = golden_index[name]
+    d = load_golden(name)
+    g = graph_of(d)
+    for k, q in enumerate(meta["modularity"]):
+        assert abs(lp.modularity(g, d[f"mod{k}_labels"]) - q) < 1e-12
+    if meta["cc_reverts"] is not None:
+        lab = d["cc_labels_in"].copy()
+        flags = np.ones(g.order(), np.uint8)
+        assert lp.cross_check(g, lab, d["cc_prev"], flags) == meta["cc_reverts"]
+        assert np.array_equal(lab, d["cc_labels_out"])
+        assert np.array_equal(flags, d["cc_flags_out"])
+    part = lp.partition_by_degree(g, 3)
+    assert np.array_equal(part.low, d["part3_low"]) and np.array_equal(part.high, d["part3_high"])
+
+
+# ---- ParallelAsync KATs (test_lpa.cpp:242-267) -------------------------------------
+
+
+def test_async_two_triangles():
+    d = load_golden("kat_two_triangles")
+    r = lp.lpa(graph_of(d), lp.LpaConfig(pl_period=4))
+    assert r.labels.tolist() == [0, 0, 0, 3, 3, 3] and r.stats.converged
+
+
+def test_async_team_hub():
+    d = load_golden("kat_star40")
+    for sw in (2, 8, 32):
+        r = lp.lpa(graph_of(d), lp.LpaConfig(pl_period=0, switch_degree=sw))
+        assert r.labels.tolist() == [0] * 41
+        assert r.stats.delta_n_per_iter == [40, 0] and r.stats.converged
+
+
+def test_async_disjoint_blocks_recover_planted():
+    # test_lpa.cpp:269-297: six disjoint dense blocks -> exactly six communities.
+    if not O.ref_available():
+        pytest.skip("needs oracle/_ref for planted_partition")
+    g0 = O.RefGraph.planted(600, 6, 0.2, 0.0, 17)
+    off, tgt, w = g0.arrays()
+    g = lp.CsrGraph(off, tgt, w)
+    r = lp.lpa(g)
+    assert r.stats.converged
+    assert lp.community_count(g, r.labels) == 6
+    assert lp.modularity(g, r.labels) > 0.8
+
+
+# ---- larger seeded inputs vs the C restatement ----------------------------------------
+
+
+def _device_graph(kind, size, seed=7):
+    if kind == "rmat":
+        dg = lp.DeviceGraph.rmat(size, 16, seed)
+    elif kind == "grid":
+        dg = lp.DeviceGraph.grid(size, size)
+    else:
+        dg = lp.DeviceGraph.web(size, 8 * size, 2.1, 4, size // 4, seed)
+    return dg, dg.download()
+
+
+@pytest.mark.parametrize("kind,size", [("rmat", 14), ("rmat", 18), ("grid", 300), ("web", 50000)])
+def test_sync_step_vs_port(kind, size):
+    dg, g = _device_graph(kind, size)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    rng = np.random.default_rng(size)
+    inputs = [np.arange(g.order(), dtype=np.uint32),
+              rng.integers(0, g.order(), g.order()).astype(np.uint32),
+              (rng.integers(0, 64, g.order()) * (g.order() // 64)).astype(np.uint32)]
+    for lab in inputs:
+        for pl in (0, 1):
+            want, wc = O.port_sync_step(pg, lab, pl)
+            got, gc = lp.sync_step(g, lab, pl)
+            assert gc == wc and np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("kind,size", [("rmat", 13), ("grid", 128), ("web", 20000)])
+def test_sync_trajectory_vs_port(kind, size):
+    dg, g = _device_graph(kind, size)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    for pl, cc in ((4, 0), (0, 1), (4, 2)):
+        want, ws = O.port_lpa(pg, exec_mode=2, pl_period=pl, cc_period=cc)
+        r = dg.lpa(lp.LpaConfig(exec=lp.ExecMode.Synchronous, pl_period=pl, cc_period=cc))
+        assert np.array_equal(r.labels, want), (kind, pl, cc)
+        assert r.stats.delta_n_per_iter == ws["delta_n"]
+        assert r.stats.converged == ws["converged"]
+        assert r.stats.cc_reverts == ws["cc_reverts"]
+
+
+def test_sequential_vs_port_small_rmat():
+    dg, g = _device_graph("rmat", 10)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    want, ws = O.port_lpa(pg, exec_mode=1, pl_period=4)
+    r = lp.lpa(g, lp.LpaConfig(exec=lp.ExecMode.Sequential, pl_period=4))
+    assert np.array_equal(r.labels, want) and r.stats.delta_n_per_iter == ws["delta_n"]
+
+
+def test_modularity_vs_port_large():
+    dg, g = _device_graph("rmat", 16)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    rng = np.random.default_rng(3)
+    lab = (rng.integers(0, 100, g.order()) * 7).astype(np.uint32)
+    assert abs(lp.modularity(g, lab) - O.port_modularity(pg, lab)) < 1e-9
+
+
+# ---- end-to-end async quality (gate 3) -------------------------------------------------
+
+
+def _sbm(n, seed):
+    if O.ref_available():
+        g0 = O.RefGraph.planted(n, 100, 14 / 999 if n == 100000 else 0.15,
+                                2 / 99000 if n == 100000 else (20 - 0.15 * 99) / 9900, seed)
+        off, tgt, w = g0.arrays()
+        return lp.CsrGraph(off, tgt, w)
+    d = load_golden("sbm10k_seed101")
+    return graph_of(d)
+
+
+def test_async_modularity_within_tolerance_of_reference_sync():
+    g = _sbm(100000, 1)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    ref_labels, rs = O.port_lpa(pg, exec_mode=2)  # == reference Synchronous (pinned)
+    q_ref = O.port_modularity(pg, ref_labels)
+    qs = []
+    for _ in range(3):
+        r = lp.lpa(g)
+        qs.append(lp.modularity(g, r.labels))
+        assert 1 <= r.stats.iterations <= 20
+    assert max(abs(q - q_ref) for q in qs) <= Q_TOL, (qs, q_ref)
+
+
+def test_precision_and_strategy_invariance_async_kat():
+    d = load_golden("kat_ring_of_cliques")
+    g = graph_of(d)
+    base = lp.lpa(g, lp.LpaConfig(exec=lp.ExecMode.Synchronous)).labels
+    for s in lp.ProbeStrategy:
+        for p in lp.ValuePrecision:
+            r = lp.lpa(g, lp.LpaConfig(exec=lp.ExecMode.Synchronous, strategy=s, precision=p))
+            assert np.array_equal(r.labels, base)
+
+
+# ---- generators -----------------------------------------------------------------------
+
+
+def test_generated_csr_is_simple_symmetric_sorted():
+    for kind, size in (("rmat", 12), ("web", 5000), ("grid", 37)):
+        _, g = _device_graph(kind, size)
+        n = g.order()
+        off = g.offsets.astype(np.int64)
+        src = np.repeat(np.arange(n), np.diff(off))
+        tgt = g.targets.astype(np.int64)
+        assert (src != tgt).all()  # no self-loops
+        key = src * n + tgt
+        assert (np.diff(key) > 0).all()  # rows sorted, no duplicates
+        rev = np.sort(tgt * n + src)
+        assert np.array_equal(rev, key)  # symmetric
+
+
+def test_grid_matches_numpy():
+    R, C = 13, 7
+    _, g = _device_graph("grid", 0) if False else (None, lp.DeviceGraph.grid(R, C).download())
+    rows = []
+    for r in range(R):
+        for c in range(C):
+            v = r * C + c
+            nb = []
+            if r > 0:
+                nb.append(v - C)
+            if c > 0:
+                nb.append(v - 1)
+            if c + 1 < C:
+                nb.append(v + 1)
+            if r + 1 < R:
+                nb.append(v + C)
+            rows.append(nb)
+    assert g.targets.tolist() == [x for row in rows for x in row]
+    assert np.array_equal(np.diff(g.offsets.astype(np.int64)), [len(r) for r in rows])
