@@ -233,9 +233,9 @@ def bench_nulpa(args):
 
     # per-tier roofline (dominant tier by device time)
     peak, peak_src = hbm_peak()
-    tier_ms = np.sum([[s.tier_ms[i] for i in range(5)] for s, _ in stats], axis=0)
-    tier_bytes = np.sum([[s.tier_bytes[i] for i in range(5)] for s, _ in stats], axis=0)
-    tier_passes = np.sum([[s.tier_passes[i] for i in range(5)] for s, _ in stats], axis=0)
+    tier_ms = np.sum([[s.tier_ms[i] for i in range(_capi.NULPA_TIERS)] for s, _ in stats], axis=0)
+    tier_bytes = np.sum([[s.tier_bytes[i] for i in range(_capi.NULPA_TIERS)] for s, _ in stats], axis=0)
+    tier_passes = np.sum([[s.tier_passes[i] for i in range(_capi.NULPA_TIERS)] for s, _ in stats], axis=0)
     top = int(np.argmax(tier_ms))
     achieved = tier_bytes[top] / (tier_ms[top] * 1e-3) / 1e9
     total_alg = sum(s.algorithmic_bytes for s, _ in stats)

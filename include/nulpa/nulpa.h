@@ -87,10 +87,14 @@ typedef struct nulpa_tuning {
   uint32_t hub_chunk;         /* edges per CTA work item in the global-table hub tier */
   uint32_t use_graphs;        /* reserved */
   uint32_t profile;           /* 1: time each tier with CUDA events (stats.tier_*) */
-  uint32_t reserved[2];
+  uint32_t schedule;          /* ParallelAsync visit order inside each tier:
+                                 0 default, 1 ascending id (partition_by_degree order),
+                                 2 scrambled (hashed) order */
+  uint32_t reserved[1];
 } nulpa_tuning;
 
-#define NULPA_TIERS 5 /* 0 thread, 1 warp, 2 block, 3 hub, 4 other (deferred wake, cross-check) */
+#define NULPA_TIERS 7 /* 0 thread, 1 half-warp, 2 warp, 3 warp+smem table, 4 CTA, 5 hub,
+                         6 other (deferred wake, cross-check, sequential) */
 
 /* labelprop::RunStats (lpa.hpp:39-46) plus device counters for roofline
  * accounting. delta_n must point at >= max_iterations u64 (or be NULL). */
@@ -188,6 +192,35 @@ int nulpa_gen_web(uint32_t n, uint64_t edges, double gamma, uint32_t hubs,
  * device (duplicate pairs dropped, unit weights) — for SBM-style inputs. */
 int nulpa_graph_from_edges(const uint32_t* u, const uint32_t* v, uint64_t ne, uint32_t n,
                            int device, nulpa_graph** out);
+
+/* ---- pass-level sessions: the partitioned multi-GPU path --------
+ * A session runs single passes over the vertex range [v_begin, v_end) of a
+ * resident graph, on caller-owned DEVICE arrays labels[n] / flags[n] that are
+ * replicated across ranks; the caller exchanges the owned label ranges and the
+ * wake flags between passes (torch.distributed / NCCL) and drives the
+ * run_engine schedule (paper_2411_11468_b200/dist.py). ParallelAsync updates
+ * labels in place inside the range; Synchronous stages decisions and applies
+ * them to the range after the pass, then wakes neighbours (remote ones too). */
+typedef struct nulpa_session nulpa_session;
+
+typedef struct nulpa_pass_info {
+  uint64_t changed;            /* label changes in the range */
+  uint64_t processed_vertices;
+  uint64_t processed_edges;
+  uint64_t wake_edges;
+  double device_ms;            /* CUDA-event time of the pass */
+  uint64_t kernel_launches;
+} nulpa_pass_info;
+
+/* Edge-balanced 1-D split: bounds[0..parts] with offsets[bounds[p]] ~ p*m2/parts. */
+int nulpa_graph_edge_ranges(nulpa_graph* g, uint32_t parts, uint32_t* bounds);
+int nulpa_session_create(nulpa_graph* g, const nulpa_opts* opts, const nulpa_tuning* tuning,
+                         uint32_t v_begin, uint32_t v_end, uint32_t* labels_dev,
+                         uint8_t* flags_dev, nulpa_session** out);
+/* labels[i] = i and flags[i] = (degree(i) == 0) over ALL n vertices. */
+int nulpa_session_init(nulpa_session* s);
+int nulpa_session_pass(nulpa_session* s, int pick_less, nulpa_pass_info* info);
+int nulpa_session_free(nulpa_session* s);
 
 #ifdef __cplusplus
 }

@@ -32,10 +32,10 @@ class nulpa_tuning(C.Structure):
     _fields_ = [("thread_max_degree", C.c_uint32), ("warp_max_degree", C.c_uint32),
                 ("block_max_degree", C.c_uint32), ("hub_chunk", C.c_uint32),
                 ("use_graphs", C.c_uint32), ("profile", C.c_uint32),
-                ("reserved", C.c_uint32 * 2)]
+                ("schedule", C.c_uint32), ("reserved", C.c_uint32 * 1)]
 
-NULPA_TIERS = 5
-TIER_NAMES = ["thread", "warp", "block", "hub", "other"]
+NULPA_TIERS = 7
+TIER_NAMES = ["thread", "half_warp", "warp", "warp_table", "block", "hub", "other"]
 
 
 class nulpa_stats(C.Structure):
@@ -45,9 +45,15 @@ class nulpa_stats(C.Structure):
                 ("delta_n", C.POINTER(C.c_uint64)), ("processed_vertices", C.c_uint64),
                 ("processed_edges", C.c_uint64), ("wake_edges", C.c_uint64),
                 ("algorithmic_bytes", C.c_uint64), ("setup_seconds", C.c_double),
-                ("kernel_launches", C.c_uint64), ("tier_ms", C.c_double * 5),
-                ("tier_bytes", C.c_double * 5), ("tier_edges", C.c_uint64 * 5),
-                ("tier_passes", C.c_uint32 * 5), ("reserved2", C.c_uint32)]
+                ("kernel_launches", C.c_uint64), ("tier_ms", C.c_double * 7),
+                ("tier_bytes", C.c_double * 7), ("tier_edges", C.c_uint64 * 7),
+                ("tier_passes", C.c_uint32 * 7), ("reserved2", C.c_uint32)]
+
+
+class nulpa_pass_info(C.Structure):
+    _fields_ = [("changed", C.c_uint64), ("processed_vertices", C.c_uint64),
+                ("processed_edges", C.c_uint64), ("wake_edges", C.c_uint64),
+                ("device_ms", C.c_double), ("kernel_launches", C.c_uint64)]
 
 
 class NulpaError(RuntimeError):
@@ -95,6 +101,13 @@ _SIGS = {
                                 C.c_uint64, C.c_int, C.POINTER(C.c_void_p)]),
     "nulpa_graph_from_edges": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_int,
                                          C.POINTER(C.c_void_p)]),
+    "nulpa_graph_edge_ranges": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "nulpa_session_create": (C.c_int, [C.c_void_p, C.POINTER(nulpa_opts),
+                                       C.POINTER(nulpa_tuning), C.c_uint32, C.c_uint32,
+                                       C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "nulpa_session_init": (C.c_int, [C.c_void_p]),
+    "nulpa_session_pass": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(nulpa_pass_info)]),
+    "nulpa_session_free": (C.c_int, [C.c_void_p]),
 }
 
 

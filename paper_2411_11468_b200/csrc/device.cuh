@@ -1,42 +1,67 @@
 // Device primitives shared by the nulpa kernels (sm_100a).
 //
 // The per-vertex open-addressing hashtable (reference: hashtable.hpp:16-185)
-// is re-designed for the GPU: power-of-two capacity so the slot index is a
-// mask instead of a 64-bit `%`, Fibonacci start slot, and the reference's
-// hybrid quadratic-double advance (idx += step; step = 2*step + h2(key)) for
-// the first `cap` probes followed by a +1 completeness sweep — the same
-// "strategy budget, then sweep" structure as hashtable.hpp:126-147. Keys are
-// claimed with atomicCAS and values accumulated with atomicAdd (the
-// reference's `shared` branch, hashtable.hpp:110-118) because every table is
-// filled by a whole warp or CTA. Placement is never observable in results:
-// the argmax (hashtable.hpp:163-185) is order-independent.
+// is re-designed for the GPU:
+//  * power-of-two capacity, so the slot index is a mask instead of the
+//    reference's 64-bit `idx % p1`;
+//  * Fibonacci start slot and the reference's hybrid quadratic-double advance
+//    (idx += step; step = 2*step + h2(key)) for the first `cap` probes, then a
+//    +1 completeness sweep — the "strategy budget, then sweep" structure of
+//    hashtable.hpp:126-147 (all four ProbeStrategy advances are selectable);
+//  * unit-weight graphs (the common case) use ONE 64-bit word per slot,
+//    (key << 32) | count: a new key is claimed and counted by a single 64-bit
+//    CAS, an existing key is counted by a single 64-bit atomicAdd, and a slot
+//    is read with one load. Weighted graphs use split key / value arrays with
+//    CAS + atomicAdd (the reference's `shared` branch, hashtable.hpp:110-118).
+// Placement is never observable in results: the argmax (higher value, ties to
+// the smaller key; hashtable.hpp:163-185) is order-independent. Warp argmax
+// uses two redux.sync instructions on order-preserving value bits.
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 namespace nulpa {
 namespace dev {
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr unsigned long long kEmptyWord = 0xFFFFFFFF00000000ull;  // packed slot: key EMPTY, count 0
 
 enum Mode : int { kAsync = 0, kSync = 1 };
 
-// Device counters (u64), zeroed per pass.
+// Device counters (u64), zeroed per pass. One C_COUNT block per tier.
 enum Counter : int {
   C_DN = 0,        // label changes
   C_PROC_V = 1,    // processed (examined) vertices
   C_PROC_E = 2,    // edges scanned by processed vertices
   C_WAKE_E = 3,    // neighbour wake stores
   C_FAIL = 4,      // hashtable insert failures (must stay 0)
-  C_NCHANGED = 5,  // length of the changed-vertex list (sync mode; "other" slot)
-  C_AUX = 6,       // cross-check scratch ("other" slot)
+  C_NCHANGED = 5,  // length of the changed-vertex list (sync mode; "other" block)
+  C_AUX = 6,       // cross-check scratch ("other" block)
   C_COUNT = 8
 };
-// One C_COUNT block of counters per tier: 0 thread, 1 warp, 2 block, 3 hub, 4 other.
-constexpr int kTiers = 5;
+
+// Degree tiers.
+enum Tier : int {
+  T_THREAD = 0,  // deg <= thread_max (<= 16): one thread per vertex
+  T_HALF = 1,    // deg <= 16: half a warp per vertex, register dedup
+  T_WARP = 2,    // deg <= 32: one warp per vertex, register dedup
+  T_WTAB = 3,    // deg <= 256: one warp per vertex, per-warp shared-memory table
+  T_BLOCK = 4,   // deg <= 2048: one CTA per vertex, shared-memory table
+  T_HUB = 5,     // larger: (hub, chunk) items, shared pre-aggregation + global table
+  T_OTHER = 6,   // deferred wake, cross-check, sequential
+  kTiers = 7
+};
+
+constexpr int kBlockThreads = 256;
+constexpr int kWarpTabMax = 256;   // T_WTAB degree bound
+constexpr int kWarpTabCap = 512;   // per-warp slots (load <= 1/2)
+constexpr int kBlockMax = 2048;    // T_BLOCK degree bound
+constexpr int kBlockCap = 4096;    // per-CTA slots (load <= 1/2)
+constexpr int kHubChunk = 2048;    // edges per hub work item (<= kBlockCap / 2)
 
 struct Graph {
   const uint64_t* __restrict__ off;
@@ -47,36 +72,27 @@ struct Graph {
 
 struct PassCtx {
   Graph g;
-  const uint32_t* lab_in;   // neighbour labels are read here (async: == lab_out)
-  uint32_t* lab_out;        // decisions are written here
-  uint8_t* flags;           // pruning flags; nullptr = examine everything, no flags
-  unsigned long long* ctr;  // Counter array
-  uint32_t* changed;        // sync mode: changed-vertex list for the deferred wake
+  const uint32_t* lab_in;         // neighbour labels are read here (async: == lab_out)
+  uint32_t* lab_out;              // decisions are written here
+  uint8_t* flags;                 // pruning flags; nullptr = examine everything
+  unsigned long long* ctr;        // this tier's Counter block
+  uint32_t* changed;              // sync mode: changed-vertex list for the deferred wake
   unsigned long long* changed_n;  // its length
   int pick_less;
   int strategy;
 };
 
-// Tier geometry.
-constexpr int kWarpCap = 1024;    // per-warp table slots (deg <= 512 at load <= 1/2)
-constexpr int kWarpTier = 512;
-constexpr int kBlockCap = 8192;   // per-CTA table slots (deg <= 4096 at load <= 1/2)
-constexpr int kBlockTier = 4096;
-constexpr int kHubChunk = 4096;   // edges per hub work item (<= kBlockCap / 2)
-constexpr int kBlockThreads = 256;
-
-
 // Hub-tier tables and work items (k_hub_* in lpa_kernels.cuh).
 struct HubCtx {
   const uint32_t* hub_v;      // [H] vertex ids
-  const uint64_t* tab_off;    // [H] slot offset into keys/vals
+  const uint64_t* tab_off;    // [H] slot offset into the global table
   const uint32_t* tab_cap;    // [H] power-of-two capacity
   const uint64_t* occ_off;    // [H] offset into occ
   uint32_t* occ_n;            // [H] occupied-slot counts
   uint32_t* occ;              // occupied-slot lists
-  uint32_t* keys;             // global table keys (kEmpty when idle)
-  void* vals;                 // global table values (W)
-  unsigned long long* best;   // [H] packed argmax (float) / value bits (double)
+  void* tab;                  // packed words (unit weights) or keys (split)
+  void* tab_vals;             // split tables: values
+  unsigned long long* best;   // [H] packed argmax (value bits << 32 | ~key), or double bits
   uint32_t* best_k;           // [H] min key among maxima (double path)
   uint8_t* active;            // [H]
   uint8_t* changed;           // [H]
@@ -87,6 +103,20 @@ struct HubCtx {
 };
 
 // ---- memory access helpers -------------------------------------------------
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Adjacency is streamed once per pass: bypass L1 and evict first from L2 so it
+// does not push the re-read label array out of the 126 MB L2.
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
 
 // Async mode reads neighbour labels that other SMs may be writing in place:
 // load through L2 (ld.global.cg) so a stale L1 line is never reused within a
@@ -109,16 +139,28 @@ __device__ __forceinline__ W edge_weight(const Graph& g, uint64_t e) {
     return W(1);
 }
 
-// ---- (value, key) argmax with ties to the smaller key -----------------------
-// ht_better, hashtable.hpp:163-169. kEmpty marks "no candidate".
+// ---- (value, key) argmax, ties to the smaller key (ht_better, hashtable.hpp:163-169) ----
+// Candidate values travel as order-preserving u32 bits (integer counts, or the
+// bits of non-negative fp32 sums); fp64 sums travel as doubles.
 template <typename W>
-struct Best {
-  W v;
-  uint32_t k;
-};
+using VBits = std::conditional_t<sizeof(W) == 8, double, uint32_t>;
 
 template <typename W>
-__device__ __forceinline__ void best_merge(Best<W>& a, W v, uint32_t k) {
+__device__ __forceinline__ VBits<W> to_vbits(W v) {
+  if constexpr (sizeof(W) == 8)
+    return v;
+  else
+    return __float_as_uint(static_cast<float>(v));
+}
+
+template <typename V>
+struct Best {
+  V v;
+  uint32_t k;  // kEmpty = no candidate
+};
+
+template <typename V>
+__device__ __forceinline__ void best_merge(Best<V>& a, V v, uint32_t k) {
   if (k == kEmpty) return;
   if (a.k == kEmpty || v > a.v || (v == a.v && k < a.k)) {
     a.v = v;
@@ -126,12 +168,20 @@ __device__ __forceinline__ void best_merge(Best<W>& a, W v, uint32_t k) {
   }
 }
 
-template <typename W, int WIDTH = 32>
-__device__ __forceinline__ Best<W> warp_best(Best<W> b) {
+// Argmax over the lanes in `mask` (every lane in `mask` calls it with the same mask).
+__device__ __forceinline__ Best<uint32_t> warp_best(Best<uint32_t> b, unsigned mask = kFull) {
+  // values are < 2^31 for counts and non-negative floats; +1 makes "none" the minimum
+  const uint32_t v = b.k == kEmpty ? 0u : b.v + 1u;
+  const uint32_t mv = __reduce_max_sync(mask, v);
+  const uint32_t mk = __reduce_min_sync(mask, (v == mv && b.k != kEmpty) ? b.k : kEmpty);
+  return Best<uint32_t>{mv ? mv - 1u : 0u, mk};
+}
+
+__device__ __forceinline__ Best<double> warp_best(Best<double> b, unsigned = kFull) {
 #pragma unroll
-  for (int o = WIDTH / 2; o > 0; o >>= 1) {
-    const W ov = __shfl_xor_sync(kFull, b.v, o, WIDTH);
-    const uint32_t ok = __shfl_xor_sync(kFull, b.k, o, WIDTH);
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(kFull, b.v, o);
+    const uint32_t ok = __shfl_xor_sync(kFull, b.k, o);
     best_merge(b, ov, ok);
   }
   return b;
@@ -150,17 +200,18 @@ __device__ __forceinline__ W peer_sum(W w, unsigned peers) {
   return s;
 }
 
-// ---- open-addressing table ----------------------------------------------------
+// ---- probing ------------------------------------------------------------------
 
-__device__ __forceinline__ uint32_t hash_start(uint32_t key) { return key * 0x9E3779B1u; }
+__device__ __forceinline__ uint32_t hash_start(uint32_t key, uint32_t cap) {
+  return cap == 1 ? 0u : (key * 0x9E3779B1u) >> (__clz(cap) + 1);  // top log2(cap) bits
+}
 __device__ __forceinline__ uint32_t hash_step(uint32_t key) {
   uint32_t h = key ^ (key >> 15);
   h *= 0x85EBCA6Bu;
   return (h ^ (h >> 13)) | 1u;
 }
 
-// Advance the probe index (hashtable.hpp:134-147 advance rules) — strategy
-// numbering matches labelprop::ProbeStrategy.
+// Advance rules of hashtable.hpp:134-147 (strategy numbering = labelprop::ProbeStrategy).
 __device__ __forceinline__ void probe_advance(int strategy, uint32_t& idx, uint32_t& step,
                                               uint32_t h2) {
   switch (strategy) {
@@ -171,41 +222,116 @@ __device__ __forceinline__ void probe_advance(int strategy, uint32_t& idx, uint3
   }
 }
 
-// Accumulate (key, v) into a table of `cap` (power of two) slots that several
-// threads fill concurrently. `occ`/`occ_n` (optional) record each newly
-// claimed slot so the table can be swept and cleared sparsely.
-// Returns false only if every slot is taken by other keys.
+// Insert results: 0 = failed (table full), 1 = counted into an existing key,
+// 2 = claimed a new slot. The slot index is returned through *slot.
+template <bool PACKED, typename W>
+struct Table;
+
+// Unit weights: one 64-bit word per slot, (key << 32) | count.
 template <typename W>
-__device__ __forceinline__ bool ht_add(uint32_t* keys, W* vals, uint32_t cap, int strategy,
-                                       uint32_t key, W v, uint32_t* occ = nullptr,
-                                       uint32_t* occ_n = nullptr) {
-  const uint32_t mask = cap - 1;
-  const uint32_t h2 = hash_step(key);
-  uint32_t idx = hash_start(key) >> (__clz(cap) + 1);  // top log2(cap) bits
-  if (cap == 1) idx = 0;
-  uint32_t step = 1;
-  for (uint32_t t = 0; t < 2 * cap; ++t) {
-    const uint32_t s = idx & mask;
-    uint32_t cur = *((volatile uint32_t*)(keys + s));
-    if (cur == kEmpty) {
-      cur = atomicCAS(keys + s, kEmpty, key);
-      if (cur == kEmpty) {
-        atomicAdd(vals + s, v);
-        if (occ) occ[atomicAdd(occ_n, 1u)] = s;
-        return true;
-      }
-    }
-    if (cur == key) {
-      atomicAdd(vals + s, v);
-      return true;
-    }
-    if (t + 1 >= cap)
-      idx += 1;  // completeness sweep
-    else
-      probe_advance(strategy, idx, step, h2);
+struct Table<true, W> {
+  unsigned long long* w;
+  static constexpr size_t kSlotBytes = 8;
+  __device__ __forceinline__ void bind(void* base, uint32_t) {
+    w = static_cast<unsigned long long*>(base);
   }
-  return false;
-}
+  __device__ __forceinline__ void bind_split(void* base, void*) {
+    w = static_cast<unsigned long long*>(base);
+  }
+  __device__ __forceinline__ void clear_slot(uint32_t s) { w[s] = kEmptyWord; }
+  __device__ __forceinline__ int add(uint32_t cap, int strategy, uint32_t key, W v,
+                                     uint32_t* slot) {
+    const uint32_t cnt = static_cast<uint32_t>(v);
+    const unsigned long long mine = (static_cast<unsigned long long>(key) << 32) | cnt;
+    const uint32_t mask = cap - 1, h2 = hash_step(key);
+    uint32_t idx = hash_start(key, cap), step = 1;
+    for (uint32_t t = 0; t < 2 * cap; ++t) {
+      const uint32_t s = idx & mask;
+      unsigned long long cur = *((volatile unsigned long long*)(w + s));
+      if (cur == kEmptyWord) {
+        cur = atomicCAS(w + s, kEmptyWord, mine);
+        if (cur == kEmptyWord) {
+          *slot = s;
+          return 2;
+        }
+      }
+      if (static_cast<uint32_t>(cur >> 32) == key) {
+        atomicAdd(w + s, static_cast<unsigned long long>(cnt));
+        *slot = s;
+        return 1;
+      }
+      if (t + 1 >= cap)
+        idx += 1;  // completeness sweep
+      else
+        probe_advance(strategy, idx, step, h2);
+    }
+    return 0;
+  }
+  __device__ __forceinline__ void read(uint32_t s, uint32_t& key, VBits<W>& v) const {
+    const unsigned long long x = w[s];
+    key = static_cast<uint32_t>(x >> 32);
+    if constexpr (sizeof(W) == 8)
+      v = static_cast<double>(static_cast<uint32_t>(x));
+    else
+      v = static_cast<uint32_t>(x);  // integer counts compare like their float bits
+  }
+  __device__ __forceinline__ W value(uint32_t s) const {
+    return static_cast<W>(static_cast<uint32_t>(w[s]));
+  }
+};
+
+// Weighted: split key / value arrays, CAS on the key then atomicAdd on the value.
+template <typename W>
+struct Table<false, W> {
+  uint32_t* k;
+  W* v;
+  static constexpr size_t kSlotBytes = 4 + sizeof(W);
+  // base holds `cap_slots` keys followed by `cap_slots` values
+  __device__ __forceinline__ void bind(void* base, uint32_t cap_slots) {
+    k = static_cast<uint32_t*>(base);
+    v = reinterpret_cast<W*>(static_cast<unsigned char*>(base) + cap_slots * sizeof(uint32_t));
+  }
+  __device__ __forceinline__ void bind_split(void* keys, void* vals) {
+    k = static_cast<uint32_t*>(keys);
+    v = static_cast<W*>(vals);
+  }
+  __device__ __forceinline__ void clear_slot(uint32_t s) {
+    k[s] = kEmpty;
+    v[s] = W(0);
+  }
+  __device__ __forceinline__ int add(uint32_t cap, int strategy, uint32_t key, W val,
+                                     uint32_t* slot) {
+    const uint32_t mask = cap - 1, h2 = hash_step(key);
+    uint32_t idx = hash_start(key, cap), step = 1;
+    for (uint32_t t = 0; t < 2 * cap; ++t) {
+      const uint32_t s = idx & mask;
+      uint32_t cur = *((volatile uint32_t*)(k + s));
+      if (cur == kEmpty) {
+        cur = atomicCAS(k + s, kEmpty, key);
+        if (cur == kEmpty) {
+          atomicAdd(v + s, val);
+          *slot = s;
+          return 2;
+        }
+      }
+      if (cur == key) {
+        atomicAdd(v + s, val);
+        *slot = s;
+        return 1;
+      }
+      if (t + 1 >= cap)
+        idx += 1;
+      else
+        probe_advance(strategy, idx, step, h2);
+    }
+    return 0;
+  }
+  __device__ __forceinline__ void read(uint32_t s, uint32_t& key, VBits<W>& val) const {
+    key = k[s];
+    val = to_vbits<W>(v[s]);
+  }
+  __device__ __forceinline__ W value(uint32_t s) const { return v[s]; }
+};
 
 // Smallest power of two >= x (x >= 1).
 __host__ __device__ __forceinline__ uint32_t pow2_ceil(uint32_t x) {

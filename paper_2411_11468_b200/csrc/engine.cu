@@ -61,64 +61,80 @@ struct Prof {
 template <int MODE, typename W, bool WEIGHTED>
 int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t s, int sms,
                 Prof& prof) {
-  constexpr size_t warp_smem = (kBlockThreads / 32) * kWarpCap * (sizeof(uint32_t) + sizeof(W));
-  constexpr size_t block_smem = kBlockCap * (sizeof(uint32_t) + sizeof(W));
+  using Tab = Table<kPacked<WEIGHTED>, W>;
+  constexpr size_t wtab_smem = (kBlockThreads / 32) * kWarpTabCap * Tab::kSlotBytes;
+  constexpr size_t block_smem = kBlockCap * Tab::kSlotBytes;
   static bool init = false;
   if (!init) {
-    allow_smem(k_warp<MODE, W, WEIGHTED>, warp_smem);
+    allow_smem(k_wtab<MODE, W, WEIGHTED>, wtab_smem);
     allow_smem(k_block<MODE, W, WEIGHTED>, block_smem);
     allow_smem(k_hub_accum<MODE, W, WEIGHTED>, block_smem);
     init = true;
   }
   int launches = 0;
-  if (p.count[0]) {
-    c.ctr = ctr + 0 * C_COUNT;
-    prof.begin(0, s);
-    const unsigned gb = grid_for(p.count[0], 256, sms * 8);
+  auto tier = [&](int t) {
+    c.ctr = ctr + t * C_COUNT;
+    prof.begin(t, s);
+  };
+  if (p.count[T_THREAD]) {
+    tier(T_THREAD);
+    const unsigned gb = grid_for(p.count[T_THREAD], 256, sms * 8);
     if (p.thread_max <= 8)
-      k_thread<MODE, W, WEIGHTED, 8><<<gb, 256, 0, s>>>(c, p.list[0], p.count[0]);
+      k_thread<MODE, W, WEIGHTED, 8><<<gb, 256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
     else
-      k_thread<MODE, W, WEIGHTED, 16><<<gb, 256, 0, s>>>(c, p.list[0], p.count[0]);
-    prof.end(0, s);
+      k_thread<MODE, W, WEIGHTED, 16><<<gb, 256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+    prof.end(T_THREAD, s);
     ++launches;
   }
-  if (p.count[1]) {
-    c.ctr = ctr + 1 * C_COUNT;
-    prof.begin(1, s);
-    k_warp<MODE, W, WEIGHTED><<<grid_for(p.count[1], kBlockThreads / 32, sms * 3), kBlockThreads,
-                                warp_smem, s>>>(c, p.list[1], p.count[1]);
-    prof.end(1, s);
+  if (p.count[T_HALF]) {
+    tier(T_HALF);
+    k_group<MODE, W, WEIGHTED, 16><<<grid_for(p.count[T_HALF], 16, sms * 8), 256, 0, s>>>(
+        c, p.list[T_HALF], p.count[T_HALF]);
+    prof.end(T_HALF, s);
     ++launches;
   }
-  if (p.count[2]) {
-    c.ctr = ctr + 2 * C_COUNT;
-    prof.begin(2, s);
-    k_block<MODE, W, WEIGHTED><<<grid_for(p.count[2], 1, sms * 3), kBlockThreads, block_smem, s>>>(
-        c, p.list[2], p.count[2]);
-    prof.end(2, s);
+  if (p.count[T_WARP]) {
+    tier(T_WARP);
+    k_group<MODE, W, WEIGHTED, 32><<<grid_for(p.count[T_WARP], 8, sms * 8), 256, 0, s>>>(
+        c, p.list[T_WARP], p.count[T_WARP]);
+    prof.end(T_WARP, s);
+    ++launches;
+  }
+  if (p.count[T_WTAB]) {
+    tier(T_WTAB);
+    k_wtab<MODE, W, WEIGHTED><<<grid_for(p.count[T_WTAB], kBlockThreads / 32, sms * 6),
+                                kBlockThreads, wtab_smem, s>>>(c, p.list[T_WTAB],
+                                                               p.count[T_WTAB]);
+    prof.end(T_WTAB, s);
+    ++launches;
+  }
+  if (p.count[T_BLOCK]) {
+    tier(T_BLOCK);
+    k_block<MODE, W, WEIGHTED><<<grid_for(p.count[T_BLOCK], 1, sms * 6), kBlockThreads,
+                                 block_smem, s>>>(c, p.list[T_BLOCK], p.count[T_BLOCK]);
+    prof.end(T_BLOCK, s);
     ++launches;
   }
   if (p.n_hubs) {
-    c.ctr = ctr + 3 * C_COUNT;
-    prof.begin(3, s);
+    tier(T_HUB);
     const HubCtx h = p.hub_ctx();
-    const unsigned gi = grid_for(p.n_items, 1, sms * 3);
+    const unsigned gi = grid_for(p.n_items, 1, sms * 6);
     const unsigned gh = grid_for(p.n_hubs, 256, 1024);
     k_hub_select<MODE><<<gh, 256, 0, s>>>(c, h);
     k_hub_accum<MODE, W, WEIGHTED><<<gi, kBlockThreads, block_smem, s>>>(c, h);
-    k_hub_argmax<W><<<gi, kBlockThreads, 0, s>>>(h);
+    k_hub_argmax<W, WEIGHTED><<<gi, kBlockThreads, 0, s>>>(h);
     launches += 3;
-    if constexpr (sizeof(W) == 8) {
+    if constexpr (sizeof(VBits<W>) == 8) {
       k_hub_argmax_key_f64<<<gi, kBlockThreads, 0, s>>>(h);
       ++launches;
     }
-    k_hub_decide<MODE, W><<<gh, 256, 0, s>>>(c, h);
+    k_hub_decide<MODE, W, WEIGHTED><<<gh, 256, 0, s>>>(c, h);
     ++launches;
     if (MODE == kAsync && c.flags) {
       k_hub_wake<<<gi, kBlockThreads, 0, s>>>(c, h);
       ++launches;
     }
-    prof.end(3, s);
+    prof.end(T_HUB, s);
   }
   NULPA_CUDA(cudaGetLastError());
   return launches;
@@ -136,14 +152,14 @@ int dispatch_pass(const Plan& p, const PassCtx& c, unsigned long long* ctr, int 
 }
 
 template <typename W, bool WEIGHTED>
-void launch_sequential(const PassCtx& c, uint32_t* gkeys, void* gvals, cudaStream_t s) {
-  constexpr size_t smem = kBlockCap * (sizeof(uint32_t) + sizeof(W));
+void launch_sequential(const PassCtx& c, void* gtab, cudaStream_t s) {
+  constexpr size_t smem = kBlockCap * Table<kPacked<WEIGHTED>, W>::kSlotBytes;
   static bool init = false;
   if (!init) {
     allow_smem(k_sequential<W, WEIGHTED>, smem);
     init = true;
   }
-  k_sequential<W, WEIGHTED><<<1, kBlockThreads, smem, s>>>(c, gkeys, static_cast<W*>(gvals));
+  k_sequential<W, WEIGHTED><<<1, kBlockThreads, smem, s>>>(c, gtab);
   NULPA_CUDA(cudaGetLastError());
 }
 
@@ -240,21 +256,17 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
   DBuf<uint8_t> flags(n);
   constexpr int kCtr = kTiers * C_COUNT;
   DBuf<unsigned long long> ctr(kCtr);
-  unsigned long long* ctr_other = ctr.p + 4 * C_COUNT;
+  unsigned long long* ctr_other = ctr.p + T_OTHER * C_COUNT;
   Pinned hc(kCtr);
   if (o.exec == NULPA_EXEC_SYNCHRONOUS) {
     lab1 = DBuf<uint32_t>(n);
     changed = DBuf<uint32_t>(n);
   }
   if (o.cc_period > 0) prev = DBuf<uint32_t>(n);
-  DBuf<uint32_t> seq_keys;
-  DBuf<unsigned char> seq_vals;
+  DBuf<unsigned char> seq_tab;  // global table for Sequential rows beyond shared memory
   if (o.exec == NULPA_EXEC_SEQUENTIAL) {
     const uint64_t cap = pow2_ceil(2 * std::max<uint32_t>(g->max_degree, 1));
-    if (cap > static_cast<uint64_t>(kBlockCap)) {
-      seq_keys = DBuf<uint32_t>(cap);
-      seq_vals = DBuf<unsigned char>(cap * vbytes);
-    }
+    if (cap > static_cast<uint64_t>(kBlockCap)) seq_tab = DBuf<unsigned char>(cap * (4 + 8));
   }
   Prof prof;
   prof.on = tuning && tuning->profile;
@@ -314,10 +326,10 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       c.lab_out = nxt;
       c.changed = changed.p;
       launches += dispatch_pass<kSync>(*p, c, ctr.p, vbytes, s, sms, prof);
-      prof.begin(4, s);
+      prof.begin(T_OTHER, s);
       k_wake_list<<<grid_for(n, kBlockThreads / 32, sms * 8), kBlockThreads, 0, s>>>(
           dg, flags.p, changed.p, ctr_other + C_NCHANGED, ctr_other);
-      prof.end(4, s);
+      prof.end(T_OTHER, s);
       ++launches;
       NULPA_CUDA(cudaGetLastError());
       std::swap(cur, nxt);
@@ -325,24 +337,24 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       c.lab_in = cur;
       c.lab_out = cur;
       c.ctr = ctr_other;
-      prof.begin(4, s);
+      prof.begin(T_OTHER, s);
       if (vbytes == 8) {
         if (dg.w)
-          launch_sequential<double, true>(c, seq_keys.p, seq_vals.p, s);
+          launch_sequential<double, true>(c, seq_tab.p, s);
         else
-          launch_sequential<double, false>(c, seq_keys.p, seq_vals.p, s);
+          launch_sequential<double, false>(c, seq_tab.p, s);
       } else {
         if (dg.w)
-          launch_sequential<float, true>(c, seq_keys.p, seq_vals.p, s);
+          launch_sequential<float, true>(c, seq_tab.p, s);
         else
-          launch_sequential<float, false>(c, seq_keys.p, seq_vals.p, s);
+          launch_sequential<float, false>(c, seq_tab.p, s);
       }
-      prof.end(4, s);
+      prof.end(T_OTHER, s);
       ++launches;
     }
     uint64_t reverted = 0;
     if (check)
-      reverted = device_cross_check(g, cur, prev.p, flags.p, ctr_other + C_AUX, hc.p + 4 * C_COUNT + C_AUX,
+      reverted = device_cross_check(g, cur, prev.p, flags.p, ctr_other + C_AUX, hc.p + T_OTHER * C_COUNT + C_AUX,
                                     s, sms, &launches);
     NULPA_CUDA(cudaMemcpyAsync(hc.p, ctr.p, kCtr * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s));
@@ -361,7 +373,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       // + own label of processed vertices (12 B), target + neighbour label
       // (+ weight) per scanned edge, label write per change, wake store per
       // neighbour of a changed vertex.
-      const double list_len = t < 4 ? (t < 3 ? p->count[t] : p->n_hubs) : 0.0;
+      const double list_len = t < Plan::kLists ? p->count[t] : 0.0;
       tier_bytes[t] += list_len + 12.0 * k[C_PROC_V] + edge_bytes * k[C_PROC_E] +
                        4.0 * k[C_DN] + double(k[C_WAKE_E]);
       if (prof.used[t]) {
@@ -445,7 +457,7 @@ uint64_t run_sync_step(nulpa_graph* g, const uint32_t* lab_in_dev, int pick_less
   c.flags = nullptr;
   c.ctr = ctr.p;
   c.changed = nullptr;
-  c.changed_n = ctr.p + 4 * C_COUNT + C_NCHANGED;
+  c.changed_n = ctr.p + T_OTHER * C_COUNT + C_NCHANGED;
   c.pick_less = pick_less ? 1 : 0;
   c.strategy = strategy;
   Prof prof;
@@ -469,6 +481,120 @@ uint64_t run_cross_check(nulpa_graph* g, uint32_t* lab_dev, const uint32_t* prev
   DBuf<unsigned long long> aux(1);
   Pinned hc;
   return device_cross_check(g, lab_dev, prev_dev, flags_dev, aux.p, hc.p, stream.s, sm_count());
+}
+
+}  // namespace nulpa
+
+// ---- pass-level session over a vertex range (multi-GPU partition) ------------
+
+struct nulpa_session {
+  nulpa_graph* g = nullptr;
+  nulpa_opts o{};
+  nulpa::Plan* plan = nullptr;
+  uint32_t lo = 0, hi = 0;
+  uint32_t* labels = nullptr;  // caller device array [n] (replicated)
+  uint8_t* flags = nullptr;    // caller device array [n]
+  nulpa::DBuf<uint32_t> staging, changed;
+  nulpa::DBuf<unsigned long long> ctr;
+  nulpa::Pinned hc{nulpa::dev::kTiers * nulpa::dev::C_COUNT};
+  nulpa::Stream stream;
+  int sms = 148, vbytes = 4;
+  ~nulpa_session() { delete plan; }
+};
+
+namespace nulpa {
+namespace {
+__global__ void k_copy_range(const uint32_t* src, uint32_t* dst, uint32_t lo, uint32_t hi) {
+  for (uint32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+__global__ void k_edge_bounds(const uint64_t* off, uint32_t n, uint32_t parts, uint32_t* bounds) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > parts) return;
+  if (p == 0) {
+    bounds[0] = 0;
+    return;
+  }
+  if (p == parts) {
+    bounds[parts] = n;
+    return;
+  }
+  // smallest v with off[v] >= p * m2 / parts (edge-balanced 1-D split)
+  const uint64_t target = (off[n] * p) / parts;
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if (off[mid] >= target)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  bounds[p] = lo;
+}
+}  // namespace
+
+void session_pass(nulpa_session* ss, int pick_less, nulpa_pass_info* info) {
+  using namespace dev;
+  nulpa_graph* g = ss->g;
+  cudaStream_t s = ss->stream.s;
+  constexpr int kCtr = kTiers * C_COUNT;
+  NULPA_CUDA(cudaMemsetAsync(ss->ctr.p, 0, kCtr * sizeof(unsigned long long), s));
+  PassCtx c;
+  c.g = Graph{g->offsets, g->targets, g->weights, g->n};
+  c.flags = ss->flags;
+  c.ctr = ss->ctr.p;
+  c.pick_less = pick_less ? 1 : 0;
+  c.strategy = ss->o.strategy;
+  c.changed = nullptr;
+  unsigned long long* other = ss->ctr.p + T_OTHER * C_COUNT;
+  c.changed_n = other + C_NCHANGED;
+  Prof prof;
+  cudaEvent_t e0, e1;
+  NULPA_CUDA(cudaEventCreate(&e0));
+  NULPA_CUDA(cudaEventCreate(&e1));
+  NULPA_CUDA(cudaEventRecord(e0, s));
+  uint64_t launches = 0;
+  if (ss->o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
+    c.lab_in = ss->labels;
+    c.lab_out = ss->labels;
+    launches += dispatch_pass<kAsync>(*ss->plan, c, ss->ctr.p, ss->vbytes, s, ss->sms, prof);
+  } else {
+    // Synchronous: decisions from the replicated snapshot into `staging`, applied to
+    // the owned range after the pass, then the deferred wake (lpa.cpp:92-98).
+    NULPA_CUDA(cudaMemcpyAsync(ss->staging.p, ss->labels, g->n * 4ull, cudaMemcpyDeviceToDevice, s));
+    c.lab_in = ss->labels;
+    c.lab_out = ss->staging.p;
+    c.changed = ss->changed.p;
+    launches += dispatch_pass<kSync>(*ss->plan, c, ss->ctr.p, ss->vbytes, s, ss->sms, prof);
+    k_copy_range<<<grid_for(ss->hi - ss->lo, 256, ss->sms * 8), 256, 0, s>>>(
+        ss->staging.p, ss->labels, ss->lo, ss->hi);
+    k_wake_list<<<grid_for(ss->hi - ss->lo, kBlockThreads / 32, ss->sms * 8), kBlockThreads, 0,
+                  s>>>(c.g, ss->flags, ss->changed.p, other + C_NCHANGED, other);
+    launches += 2;
+    NULPA_CUDA(cudaGetLastError());
+  }
+  NULPA_CUDA(cudaEventRecord(e1, s));
+  NULPA_CUDA(cudaMemcpyAsync(ss->hc.p, ss->ctr.p, kCtr * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s));
+  NULPA_CUDA(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  NULPA_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  nulpa_pass_info r{};
+  for (int t = 0; t < kTiers; ++t) {
+    const unsigned long long* k = ss->hc.p + t * C_COUNT;
+    if (k[C_FAIL])
+      throw Error(NULPA_EINTERNAL, "hashtable insertion failed (capacity invariant violated)");
+    r.changed += k[C_DN];
+    r.processed_vertices += k[C_PROC_V];
+    r.processed_edges += k[C_PROC_E];
+    r.wake_edges += k[C_WAKE_E];
+  }
+  r.device_ms = ms;
+  r.kernel_launches = launches;
+  if (info) *info = r;
 }
 
 }  // namespace nulpa
@@ -600,6 +726,84 @@ int nulpa_partition_by_degree(const nulpa_csr* csr, uint32_t switch_degree, uint
     if (nh) NULPA_CUDA(cudaMemcpy(high, d_high.p, nh * 4, cudaMemcpyDeviceToHost));
     *n_low = nl;
     *n_high = nh;
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int nulpa_graph_edge_ranges(nulpa_graph* g, uint32_t parts, uint32_t* bounds) {
+  return guarded([&] {
+    if (!g || parts == 0) throw Error(NULPA_EINVAL, "bad partition request");
+    use_device(g->device);
+    DBuf<uint32_t> d(parts + 1);
+    k_edge_bounds<<<(parts + 256) / 256, 256>>>(g->offsets, g->n, parts, d.p);
+    NULPA_CUDA(cudaGetLastError());
+    NULPA_CUDA(cudaMemcpy(bounds, d.p, (parts + 1) * 4ull, cudaMemcpyDeviceToHost));
+  });
+}
+
+int nulpa_session_create(nulpa_graph* g, const nulpa_opts* opts, const nulpa_tuning* tuning,
+                         uint32_t v_begin, uint32_t v_end, uint32_t* labels_dev,
+                         uint8_t* flags_dev, nulpa_session** out) {
+  return guarded([&] {
+    if (!g || !opts || !labels_dev || !flags_dev) throw Error(NULPA_EINVAL, "null argument");
+    validate_opts(g, *opts);
+    if (opts->exec == NULPA_EXEC_SEQUENTIAL)
+      throw Error(NULPA_EINVAL, "sequential mode cannot be partitioned across devices");
+    if (v_begin > v_end || v_end > g->n) throw Error(NULPA_EINVAL, "vertex range out of bounds");
+    use_device(g->device);
+    auto* ss = new nulpa_session();
+    try {
+      ss->g = g;
+      ss->o = *opts;
+      ss->lo = v_begin;
+      ss->hi = v_end;
+      ss->labels = labels_dev;
+      ss->flags = flags_dev;
+      ss->sms = sm_count();
+      ss->vbytes = opts->precision == 64 ? 8 : 4;
+      ss->plan = build_plan(g, resolve_tiers(opts->switch_degree, tuning), ss->vbytes,
+                            ss->stream.s, v_begin, v_end);
+      ss->ctr = DBuf<unsigned long long>(dev::kTiers * dev::C_COUNT);
+      if (opts->exec == NULPA_EXEC_SYNCHRONOUS) {
+        ss->staging = DBuf<uint32_t>(g->n);
+        ss->changed = DBuf<uint32_t>(uint64_t(v_end - v_begin) + 1);
+      }
+    } catch (...) {
+      delete ss;
+      throw;
+    }
+    *out = ss;
+  });
+}
+
+int nulpa_session_init(nulpa_session* ss) {
+  return guarded([&] {
+    if (!ss) throw Error(NULPA_EINVAL, "null session");
+    use_device(ss->g->device);
+    k_init<<<grid_for(ss->g->n, 256, ss->sms * 8), 256, 0, ss->stream.s>>>(
+        ss->labels, ss->flags, ss->g->offsets, ss->g->n);
+    NULPA_CUDA(cudaGetLastError());
+    NULPA_CUDA(cudaStreamSynchronize(ss->stream.s));
+  });
+}
+
+int nulpa_session_pass(nulpa_session* ss, int pick_less, nulpa_pass_info* info) {
+  return guarded([&] {
+    if (!ss) throw Error(NULPA_EINVAL, "null session");
+    use_device(ss->g->device);
+    session_pass(ss, pick_less, info);
+  });
+}
+
+int nulpa_session_free(nulpa_session* ss) {
+  return guarded([&] {
+    if (ss) {
+      cudaSetDevice(ss->g->device);
+      delete ss;
+    }
   });
 }
 

@@ -52,6 +52,12 @@ __global__ void k_gather_degrees(const uint32_t* list, const uint64_t* off, uint
     deg[t] = static_cast<uint32_t>(off[list[t] + 1] - off[list[t]]);
 }
 
+__global__ void k_fill_u64(unsigned long long* p, uint64_t count, unsigned long long v) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < count;
+       t += (uint64_t)gridDim.x * blockDim.x)
+    p[t] = v;
+}
+
 __global__ void k_check_offsets(const uint64_t* off, uint32_t n, uint64_t m2, unsigned* bad) {
   for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     if (off[i + 1] < off[i]) atomicOr(bad, 1u);
@@ -193,6 +199,37 @@ void partition_two_way(const uint64_t* off, uint32_t n, uint32_t sw, uint32_t* l
   dfree(d_num);
 }
 
+__global__ void k_hash_keys(const uint32_t* ids, uint32_t count, uint32_t* keys) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
+    uint32_t x = ids[t] * 0x9E3779B1u;
+    x ^= x >> 16;
+    x *= 0x85EBCA6Bu;
+    x ^= x >> 13;
+    keys[t] = x;
+  }
+}
+
+// Reorder a vertex list by a hash of the id (a fixed pseudo-random permutation).
+void scramble_list(uint32_t* list, uint32_t count, cudaStream_t s) {
+  if (count < 2) return;
+  uint32_t* k0 = dalloc<uint32_t>(count);
+  uint32_t* k1 = dalloc<uint32_t>(count);
+  uint32_t* v1 = dalloc<uint32_t>(count);
+  k_hash_keys<<<256, 256, 0, s>>>(list, count, k0);
+  cub::DoubleBuffer<uint32_t> keys(k0, k1), vals(list, v1);
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, count, 0, 32, s);
+  void* tmp = dmalloc(tb);
+  cub::DeviceRadixSort::SortPairs(tmp, tb, keys, vals, count, 0, 32, s);
+  if (vals.Current() != list)
+    NULPA_CUDA(cudaMemcpyAsync(list, vals.Current(), count * 4ull, cudaMemcpyDeviceToDevice, s));
+  NULPA_CUDA(cudaStreamSynchronize(s));
+  dfree(tmp);
+  dfree(k0);
+  dfree(k1);
+  dfree(v1);
+}
+
 Plan::~Plan() {
   for (auto* p : list) dfree(p);
   dfree(tab_off);
@@ -200,8 +237,8 @@ Plan::~Plan() {
   dfree(occ_off);
   dfree(occ_n);
   dfree(occ);
-  dfree(keys);
-  dfree(vals);
+  dfree(tab);
+  dfree(tab_vals);
   dfree(best);
   dfree(best_k);
   dfree(active);
@@ -212,63 +249,90 @@ Plan::~Plan() {
 
 TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* t) {
   // Thread tier: deg < switch_degree (the reference's scalar path), capped by
-  // the register table of k_thread (16 entries).
+  // the register table of k_thread (16 entries). The half-warp and warp
+  // register tiers cover the rest up to 32; then the per-warp table tier
+  // (<= 256), the per-CTA table tier (<= 2048) and the hub tier.
   uint32_t tmax = (t && t->thread_max_degree) ? t->thread_max_degree : 8u;
   tmax = std::min<uint32_t>(tmax, 16u);
   if (switch_degree >= 2) tmax = std::min<uint32_t>(tmax, switch_degree - 1);
-  uint32_t wmax = (t && t->warp_max_degree) ? t->warp_max_degree : uint32_t(dev::kWarpTier);
-  wmax = std::max<uint32_t>(std::min<uint32_t>(wmax, dev::kWarpTier), tmax);
-  uint32_t bmax = (t && t->block_max_degree) ? t->block_max_degree : dev::kBlockTier;
-  bmax = std::max<uint32_t>(std::min<uint32_t>(bmax, dev::kBlockTier), wmax);
-  return {tmax, wmax, bmax};
+  uint32_t wmax = (t && t->warp_max_degree) ? t->warp_max_degree : uint32_t(dev::kWarpTabMax);
+  wmax = std::max<uint32_t>(std::min<uint32_t>(wmax, dev::kWarpTabMax), 32u);
+  uint32_t bmax = (t && t->block_max_degree) ? t->block_max_degree : uint32_t(dev::kBlockMax);
+  bmax = std::max<uint32_t>(std::min<uint32_t>(bmax, dev::kBlockMax), wmax);
+  const uint32_t sched = (t && t->schedule) ? t->schedule : 1u;
+  return {tmax, wmax, bmax, sched};
 }
 
 Plan* get_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream_t s) {
   if (g->plan && g->plan->thread_max == tb.thread_max && g->plan->warp_max == tb.warp_max &&
-      g->plan->block_max == tb.block_max && g->plan->value_bytes == value_bytes)
+      g->plan->block_max == tb.block_max && g->plan->schedule == tb.schedule &&
+      g->plan->value_bytes == value_bytes && g->plan->v_lo == 0 && g->plan->v_hi == g->n)
     return g->plan;
   delete g->plan;
   g->plan = nullptr;
+  g->plan = build_plan(g, tb, value_bytes, s, 0, g->n);
+  return g->plan;
+}
+
+Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream_t s,
+                 uint32_t v_lo, uint32_t v_hi) {
   const auto t0 = std::chrono::steady_clock::now();
   Plan* p = new Plan();
   try {
     p->thread_max = tb.thread_max;
     p->warp_max = tb.warp_max;
     p->block_max = tb.block_max;
+    p->schedule = tb.schedule;
     p->value_bytes = value_bytes;
-    const uint32_t n = g->n;
-    const uint64_t bounds[4][2] = {{1, tb.thread_max},
-                                   {uint64_t(tb.thread_max) + 1, tb.warp_max},
-                                   {uint64_t(tb.warp_max) + 1, tb.block_max},
-                                   {uint64_t(tb.block_max) + 1, ~0ull}};
+    p->v_lo = v_lo;
+    p->v_hi = v_hi;
+    const uint32_t span = v_hi - v_lo;
+    p->weighted = g->weights != nullptr;
+    const uint64_t tm = tb.thread_max;
+    const uint64_t bounds[Plan::kLists][2] = {
+        {1, tm},                                        // T_THREAD
+        {tm + 1, 16},                                   // T_HALF (empty if tm >= 16)
+        {std::max<uint64_t>(tm, 16) + 1, 32},           // T_WARP
+        {33, tb.warp_max},                              // T_WTAB
+        {uint64_t(tb.warp_max) + 1, tb.block_max},      // T_BLOCK
+        {uint64_t(tb.block_max) + 1, ~0ull}};           // T_HUB
     uint64_t* d_num = dalloc<uint64_t>(1);
+    uint32_t* scratch = dalloc<uint32_t>(uint64_t(span) + 1);
     size_t tbytes = 0;
-    cub::CountingInputIterator<uint32_t> ids(0);
-    cub::DeviceSelect::If(nullptr, tbytes, ids, static_cast<uint32_t*>(nullptr), d_num,
-                          static_cast<uint64_t>(n), DegInRange{g->offsets, 1, 1}, s);
+    cub::CountingInputIterator<uint32_t> ids(v_lo);
+    cub::DeviceSelect::If(nullptr, tbytes, ids, scratch, d_num, static_cast<uint64_t>(span),
+                          DegInRange{g->offsets, 1, 1}, s);
     void* tmp = dmalloc(tbytes);
-    for (int t = 0; t < 4; ++t) {
-      uint32_t* out = dalloc<uint32_t>(n + 1);
-      cub::DeviceSelect::If(tmp, tbytes, ids, out, d_num, static_cast<uint64_t>(n),
+    for (int t = 0; t < Plan::kLists; ++t) {
+      cub::DeviceSelect::If(tmp, tbytes, ids, scratch, d_num, static_cast<uint64_t>(span),
                             DegInRange{g->offsets, bounds[t][0], bounds[t][1]}, s);
       uint64_t cnt = 0;
       NULPA_CUDA(cudaMemcpyAsync(&cnt, d_num, sizeof cnt, cudaMemcpyDeviceToHost, s));
       NULPA_CUDA(cudaStreamSynchronize(s));
-      p->list[t] = out;
+      p->list[t] = dalloc<uint32_t>(cnt + 1);
       p->count[t] = static_cast<uint32_t>(cnt);
+      if (cnt)
+        NULPA_CUDA(cudaMemcpyAsync(p->list[t], scratch, cnt * 4, cudaMemcpyDeviceToDevice, s));
     }
+    NULPA_CUDA(cudaStreamSynchronize(s));
     dfree(tmp);
     dfree(d_num);
+    dfree(scratch);
+    // Scrambled visit order (ParallelAsync only: any interleaving is a valid
+    // asynchronous schedule; Synchronous/Sequential results do not depend on it).
+    // The hub tier keeps ascending order (its decisions land after the tier).
+    if (tb.schedule == 2)
+      for (int t = 0; t < dev::T_HUB; ++t) scramble_list(p->list[t], p->count[t], s);
 
     // Hub tier: per-hub global tables and (hub, chunk) work items. Hub counts
     // are small (vertices of degree > block_max), so the layout is built on
     // the host.
-    const uint32_t H = p->count[3];
+    const uint32_t H = p->count[dev::T_HUB];
     p->n_hubs = H;
     std::vector<uint32_t> hdeg(H);
     if (H) {
       uint32_t* d_deg = dalloc<uint32_t>(H);
-      k_gather_degrees<<<256, 256, 0, s>>>(p->list[3], g->offsets, H, d_deg);
+      k_gather_degrees<<<256, 256, 0, s>>>(p->list[dev::T_HUB], g->offsets, H, d_deg);
       NULPA_CUDA(cudaGetLastError());
       NULPA_CUDA(cudaMemcpyAsync(hdeg.data(), d_deg, H * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
       NULPA_CUDA(cudaStreamSynchronize(s));
@@ -289,7 +353,6 @@ Plan* get_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream
         ihub.push_back(x);
         istart.push_back(e);
       }
-      p->edges[3] += d;
     }
     p->n_items = static_cast<uint32_t>(ihub.size());
     p->table_slots = slots;
@@ -304,8 +367,12 @@ Plan* get_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream
     p->active = dalloc<uint8_t>(H + 1);
     p->changed = dalloc<uint8_t>(H + 1);
     p->occ = dalloc<uint32_t>(occs + 1);
-    p->keys = dalloc<uint32_t>(slots + 1);
-    p->vals = dmalloc(slots * value_bytes + 16);
+    if (p->weighted) {
+      p->tab = dalloc<uint32_t>(slots + 1);
+      p->tab_vals = dmalloc(slots * value_bytes + 16);
+    } else {
+      p->tab = dalloc<unsigned long long>(slots + 1);
+    }
     p->item_hub = dalloc<uint32_t>(p->n_items + 1);
     p->item_start = dalloc<uint32_t>(p->n_items + 1);
     if (H) {
@@ -319,8 +386,14 @@ Plan* get_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream
     NULPA_CUDA(cudaMemsetAsync(p->best, 0, H * 8 + 8, s));
     NULPA_CUDA(cudaMemsetAsync(p->best_k, 0xFF, H * 4 + 4, s));
     NULPA_CUDA(cudaMemsetAsync(p->changed, 0, H + 1, s));
-    NULPA_CUDA(cudaMemsetAsync(p->keys, 0xFF, slots * 4 + 4, s));
-    NULPA_CUDA(cudaMemsetAsync(p->vals, 0, slots * value_bytes + 16, s));
+    if (p->weighted) {
+      NULPA_CUDA(cudaMemsetAsync(p->tab, 0xFF, slots * 4 + 4, s));
+      NULPA_CUDA(cudaMemsetAsync(p->tab_vals, 0, slots * value_bytes + 16, s));
+    } else {
+      k_fill_u64<<<1024, 256, 0, s>>>(static_cast<unsigned long long*>(p->tab), slots + 1,
+                                      dev::kEmptyWord);
+      NULPA_CUDA(cudaGetLastError());
+    }
     NULPA_CUDA(cudaStreamSynchronize(s));
     // Edge totals of the lower tiers (for reporting).
     // (computed lazily by callers that need them; hubs are exact above)
@@ -329,7 +402,6 @@ Plan* get_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream
     throw;
   }
   p->build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  g->plan = p;
   return p;
 }
 

@@ -11,19 +11,20 @@
 // Every kernel applies the same per-vertex rule: skip if flagged, mark
 // processed, pick the neighbour label of greatest total weight (self-loops
 // skipped, ties to the smaller label), move if (pick_less ? c* < cur : c* !=
-// cur), then wake every neighbour (async: inline; sync: deferred to k_wake
-// after the joint application, lpa.cpp:92-98).
+// cur), then wake every neighbour (async: inline; sync: deferred to
+// k_wake_list after the joint application, lpa.cpp:92-98).
 //
-// Tiers (all lists ascending by vertex id, like partition_by_degree):
-//   k_thread  deg <= DMAX          one thread per vertex, register O(d^2) count
-//   k_warp    deg <= 512           one warp per vertex; deg <= 32 uses
-//                                  __match_any_sync dedup in registers, larger
-//                                  rows a per-warp shared-memory table
-//   k_block   deg <= 4096          one CTA per vertex, shared-memory table
-//   k_hub_*   larger               (vertex, 4096-edge chunk) work items: CTA
-//                                  shared-memory pre-aggregation, flushed into
-//                                  a per-hub global table; sparse argmax via
-//                                  the occupied-slot list; decide; chunked wake
+// Tiers (device.cuh), each list ascending by vertex id like partition_by_degree
+// (or hashed, tuning.schedule = 2):
+//   k_thread    deg <= 8/16   one thread per vertex, labels in registers, O(d^2) count
+//                             in neighbour order (bit-identical to the reference sums)
+//   k_group<16> deg <= 16     half a warp per vertex, __match_any_sync dedup, redux argmax
+//   k_group<32> deg <= 32     one warp per vertex, same
+//   k_wtab      deg <= 256    one warp per vertex, per-warp shared-memory table
+//   k_block     deg <= 2048   one CTA per vertex, shared-memory table
+//   k_hub_*     larger        (hub, 2048-edge chunk) items: shared-memory pre-aggregation,
+//                             flush into a per-hub global table, sparse argmax over the
+//                             occupied-slot list (packed 64-bit atomicMax), decide, wake
 #pragma once
 
 #include "device.cuh"
@@ -43,7 +44,6 @@ __device__ __forceinline__ bool apply_move(const PassCtx& c, uint32_t i, uint32_
   if (!allowed) return false;
   if constexpr (MODE == kAsync) {
     __stcg(c.lab_out + i, cand);
-    __threadfence();  // publish the label before the neighbour wake-ups
   } else {
     c.lab_out[i] = cand;
     if (c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
@@ -59,17 +59,18 @@ __device__ __forceinline__ bool claim_vertex(const PassCtx& c, uint32_t i) {
   return false;
 }
 
-// ---- tier 0: thread per vertex ---------------------------------------------------
+template <bool WEIGHTED>
+constexpr bool kPacked = !WEIGHTED;  // unit weights -> packed 64-bit slots
+
+// ---- tier: thread per vertex ---------------------------------------------------
 
 template <int MODE, typename W, bool WEIGHTED, int DMAX>
 __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __restrict__ list,
                                                 uint32_t count) {
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
+  const uint64_t pol = policy_evict_first();
   const uint32_t stride = gridDim.x * blockDim.x;
-  // The loop bound is rounded up to whole warps so warp_add_counter sees 32 lanes.
-  const uint32_t bound = (count + 31u) & ~31u;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < bound; t += stride) {
-    if (t >= count) continue;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
     const uint32_t i = __ldg(list + t);
     if (claim_vertex(c, i)) continue;
     const uint64_t lo = __ldg(c.g.off + i);
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
     uint32_t lab[DMAX];
     W wt[DMAX];
 #pragma unroll
-    for (int k = 0; k < DMAX; ++k) nb[k] = (k < d) ? __ldg(c.g.tgt + lo + k) : i;
+    for (int k = 0; k < DMAX; ++k) nb[k] = (k < d) ? ld_stream(c.g.tgt + lo + k, pol) : i;
 #pragma unroll
     for (int k = 0; k < DMAX; ++k) {
       const bool valid = k < d && nb[k] != i;  // self-loops skipped (lpa.hpp:102)
@@ -87,13 +88,13 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
     }
     // Per-label total in neighbour order (bit-identical to the reference's
     // sequential accumulation, even for non-integer weights), then argmax.
-    Best<W> b{W(0), kEmpty};
+    Best<VBits<W>> b{VBits<W>(0), kEmpty};
 #pragma unroll
     for (int k = 0; k < DMAX; ++k) {
       W s = W(0);
 #pragma unroll
       for (int m = 0; m < DMAX; ++m) s += (lab[m] == lab[k]) ? wt[m] : W(0);
-      best_merge(b, s, lab[k]);
+      best_merge(b, to_vbits<W>(s), lab[k]);
     }
     ++n_v;
     n_e += d;
@@ -112,16 +113,85 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
   warp_add_counter(c.ctr, C_WAKE_E, n_w);
 }
 
+// ---- tier: G lanes per vertex, register dedup -------------------------------------
+
+template <typename V, int G>
+__device__ __forceinline__ Best<V> group_best(Best<V> b, unsigned gmask) {
+  if constexpr (std::is_same_v<V, uint32_t>) {
+    return warp_best(b, gmask);
+  } else {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, b.v, o, G);
+      const uint32_t ok = __shfl_xor_sync(kFull, b.k, o, G);
+      best_merge(b, ov, ok);
+    }
+    return b;
+  }
+}
+
+template <int MODE, typename W, bool WEIGHTED, int G>
+__global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __restrict__ list,
+                                               uint32_t count) {
+  constexpr int kPer = 32 / G;  // vertices per warp
+  const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+  const unsigned gmask = (G == 32) ? kFull : (((1u << G) - 1u) << (sub * G));
+  const uint64_t pol = policy_evict_first();
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t base = gw * kPer; base < count; base += nw * kPer) {
+    const uint32_t t = base + sub;
+    bool active = t < count;
+    const uint32_t i = active ? __ldg(list + t) : 0u;
+    int skip = 0;
+    if (active && gl == 0) skip = claim_vertex(c, i) ? 1 : 0;
+    skip = __shfl_sync(kFull, skip, sub * G);
+    active = active && !skip;
+    uint64_t lo = 0;
+    uint32_t d = 0;
+    if (active) {
+      lo = __ldg(c.g.off + i);
+      d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+    }
+    const uint32_t j = (gl < d) ? ld_stream(c.g.tgt + lo + gl, pol) : i;
+    const bool valid = gl < d && j != i;
+    const uint32_t lab = valid ? load_label<MODE>(c.lab_in + j) : kEmpty;
+    const W w = valid ? edge_weight<W, WEIGHTED>(c.g, lo + gl) : W(0);
+    const unsigned peers = __match_any_sync(kFull, lab) & gmask;
+    W s;
+    if constexpr (WEIGHTED)
+      s = peer_sum(w, peers);
+    else
+      s = static_cast<W>(__popc(peers));
+    Best<VBits<W>> b{VBits<W>(0), kEmpty};
+    if (lab != kEmpty && (__ffs(peers) - 1) == lane) b = Best<VBits<W>>{to_vbits<W>(s), lab};
+    b = group_best<VBits<W>, G>(b, gmask);
+    int ch = 0;
+    if (active && gl == 0) {
+      ch = apply_move<MODE>(c, i, b.k) ? 1 : 0;
+      ++n_v;
+      n_e += d;
+      n_dn += ch;
+      if (MODE == kAsync && ch && c.flags) n_w += d;
+    }
+    ch = __shfl_sync(kFull, ch, sub * G);
+    if (MODE == kAsync && ch && c.flags && gl < d) c.flags[j] = 0;
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+}
+
 // ---- cooperative gather + insert -------------------------------------------------
 
 // One round of a team gather: each lane holds one edge (or none), dedups its
 // label against the warp with __match_any_sync, and the lowest lane of each
 // label group adds the group's weight to the table. All 32 lanes call it.
-template <int MODE, typename W, bool WEIGHTED>
-__device__ __forceinline__ void gather_insert(const PassCtx& c, uint32_t i, uint32_t lab,
-                                              W w, uint32_t* keys, W* vals, uint32_t cap,
-                                              unsigned long long& fails, uint32_t* occ = nullptr,
-                                              uint32_t* occ_n = nullptr) {
+template <typename W, bool WEIGHTED, typename Tab>
+__device__ __forceinline__ void gather_insert(const PassCtx& c, uint32_t lab, W w, Tab& tab,
+                                              uint32_t cap, unsigned long long& fails) {
   const unsigned peers = __match_any_sync(kFull, lab);
   W s;
   if constexpr (WEIGHTED)
@@ -130,22 +200,51 @@ __device__ __forceinline__ void gather_insert(const PassCtx& c, uint32_t i, uint
     s = static_cast<W>(__popc(peers));
   const int lane = threadIdx.x & 31;
   if (lab != kEmpty && (__ffs(peers) - 1) == lane) {
-    if (!ht_add(keys, vals, cap, c.strategy, lab, s, occ, occ_n)) ++fails;
+    uint32_t slot;
+    if (!tab.add(cap, c.strategy, lab, s, &slot)) ++fails;
   }
 }
 
-// ---- tier 1: warp per vertex ------------------------------------------------------
+// Gather edges [e0, e1) of vertex i (U edges per thread in flight) into `tab`.
+// `T` threads cooperate; all of them call it with the same bounds.
+template <int MODE, typename W, bool WEIGHTED, typename Tab, int U = 4>
+__device__ __forceinline__ void team_gather(const PassCtx& c, uint32_t i, uint64_t lo,
+                                            uint32_t e0, uint32_t e1, Tab& tab, uint32_t cap,
+                                            uint32_t tid, uint32_t T, uint64_t pol,
+                                            unsigned long long& fails) {
+  for (uint32_t base = e0; base < e1; base += T * U) {
+    uint32_t j[U], lab[U];
+    W w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t e = base + u * T + tid;
+      j[u] = e < e1 ? ld_stream(c.g.tgt + lo + e, pol) : i;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t e = base + u * T + tid;
+      const bool valid = e < e1 && j[u] != i;
+      lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+      w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) gather_insert<W, WEIGHTED>(c, lab[u], w[u], tab, cap, fails);
+  }
+}
+
+// ---- tier: warp per vertex, per-warp shared-memory table -----------------------------
 
 template <int MODE, typename W, bool WEIGHTED>
-__global__ void __launch_bounds__(kBlockThreads) k_warp(PassCtx c,
+__global__ void __launch_bounds__(kBlockThreads) k_wtab(PassCtx c,
                                                         const uint32_t* __restrict__ list,
                                                         uint32_t count) {
+  using Tab = Table<kPacked<WEIGHTED>, W>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kWarps = kBlockThreads / 32;
-  uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw) + warp * kWarpCap;
-  W* vals = reinterpret_cast<W*>(smem_raw + kWarps * kWarpCap * sizeof(uint32_t)) + warp * kWarpCap;
-
+  Tab tab;
+  tab.bind(smem_raw + size_t(warp) * kWarpTabCap * Tab::kSlotBytes, kWarpTabCap);
+  const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
   const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   for (uint32_t t = gw; t < count; t += nw) {
@@ -155,65 +254,31 @@ __global__ void __launch_bounds__(kBlockThreads) k_warp(PassCtx c,
     if (__shfl_sync(kFull, skip, 0)) continue;
     const uint64_t lo = __ldg(c.g.off + i);
     const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
-    Best<W> b{W(0), kEmpty};
-    if (d <= 32) {
-      // Register path: one label per lane, dedup by __match_any_sync.
-      const uint32_t j = lane < d ? __ldg(c.g.tgt + lo + lane) : i;
-      const bool valid = lane < d && j != i;
-      const uint32_t lab = valid ? load_label<MODE>(c.lab_in + j) : kEmpty;
-      const W w = valid ? edge_weight<W, WEIGHTED>(c.g, lo + lane) : W(0);
-      const unsigned peers = __match_any_sync(kFull, lab);
-      W s;
-      if constexpr (WEIGHTED)
-        s = peer_sum(w, peers);
-      else
-        s = static_cast<W>(__popc(peers));
-      if (lab != kEmpty && (__ffs(peers) - 1) == lane) b = Best<W>{s, lab};
-    } else {
-      // Table path: cap = pow2 >= 2d slots of the warp's shared region.
-      const uint32_t cap = pow2_ceil(2 * d);
-      for (uint32_t s = lane; s < cap; s += 32) {
-        keys[s] = kEmpty;
-        vals[s] = W(0);
-      }
-      __syncwarp();
-      constexpr int U = 4;
-      for (uint32_t base = 0; base < d; base += 32 * U) {
-        uint32_t j[U], lab[U];
-        W w[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t e = base + u * 32 + lane;
-          j[u] = e < d ? __ldg(c.g.tgt + lo + e) : i;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t e = base + u * 32 + lane;
-          const bool valid = e < d && j[u] != i;
-          lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
-          w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          gather_insert<MODE, W, WEIGHTED>(c, i, lab[u], w[u], keys, vals, cap, fails);
-      }
-      __syncwarp();
-      for (uint32_t s = lane; s < cap; s += 32) best_merge(b, vals[s], keys[s]);
-      __syncwarp();
+    const uint32_t cap = pow2_ceil(2 * d);
+    for (uint32_t s = lane; s < cap; s += 32) tab.clear_slot(s);
+    __syncwarp();
+    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, lane, 32, pol, fails);
+    __syncwarp();
+    Best<VBits<W>> b{VBits<W>(0), kEmpty};
+    for (uint32_t s = lane; s < cap; s += 32) {
+      uint32_t k;
+      VBits<W> v;
+      tab.read(s, k, v);
+      best_merge(b, v, k);
     }
     b = warp_best(b);
+    __syncwarp();
     int changed = 0;
-    if (lane == 0) changed = apply_move<MODE>(c, i, b.k) ? 1 : 0;
-    changed = __shfl_sync(kFull, changed, 0);
     if (lane == 0) {
+      changed = apply_move<MODE>(c, i, b.k) ? 1 : 0;
       ++n_v;
       n_e += d;
       n_dn += changed;
+      if (MODE == kAsync && changed && c.flags) n_w += d;
     }
-    if (MODE == kAsync && changed && c.flags) {
-      for (uint32_t e = lane; e < d; e += 32) c.flags[__ldg(c.g.tgt + lo + e)] = 0;
-      if (lane == 0) n_w += d;
-    }
+    changed = __shfl_sync(kFull, changed, 0);
+    if (MODE == kAsync && changed && c.flags)
+      for (uint32_t e = lane; e < d; e += 32) c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
   warp_add_counter(c.ctr, C_PROC_E, n_e);
@@ -224,14 +289,14 @@ __global__ void __launch_bounds__(kBlockThreads) k_warp(PassCtx c,
 
 // ---- block-wide helpers ------------------------------------------------------------
 
-template <typename W>
-__device__ __forceinline__ Best<W> block_best(Best<W> b, Best<W>* red) {
+template <typename V>
+__device__ __forceinline__ Best<V> block_best(Best<V> b, Best<V>* red) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   b = warp_best(b);
   if (lane == 0) red[warp] = b;
   __syncthreads();
   if (warp == 0) {
-    Best<W> r = lane < (blockDim.x >> 5) ? red[lane] : Best<W>{W(0), kEmpty};
+    Best<V> r = lane < static_cast<int>(blockDim.x >> 5) ? red[lane] : Best<V>{V(0), kEmpty};
     r = warp_best(r);
     if (lane == 0) red[0] = r;
   }
@@ -239,80 +304,54 @@ __device__ __forceinline__ Best<W> block_best(Best<W> b, Best<W>* red) {
   return red[0];
 }
 
-// Gather edges [e0, e1) of vertex i into a CTA-shared table (U edges per thread
-// in flight).
-template <int MODE, typename W, bool WEIGHTED>
-__device__ __forceinline__ void block_gather(const PassCtx& c, uint32_t i, uint64_t lo,
-                                             uint32_t e0, uint32_t e1, uint32_t* keys, W* vals,
-                                             uint32_t cap, unsigned long long& fails) {
-  constexpr int U = 4;
-  const uint32_t T = blockDim.x;
-  for (uint32_t base = e0; base < e1; base += T * U) {
-    uint32_t j[U], lab[U];
-    W w[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t e = base + u * T + threadIdx.x;
-      j[u] = e < e1 ? __ldg(c.g.tgt + lo + e) : i;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t e = base + u * T + threadIdx.x;
-      const bool valid = e < e1 && j[u] != i;
-      lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
-      w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      gather_insert<MODE, W, WEIGHTED>(c, i, lab[u], w[u], keys, vals, cap, fails);
-  }
-}
-
-// ---- tier 2: CTA per vertex, shared-memory table ------------------------------------
+// ---- tier: CTA per vertex, shared-memory table --------------------------------------
 
 template <int MODE, typename W, bool WEIGHTED>
 __global__ void __launch_bounds__(kBlockThreads) k_block(PassCtx c,
                                                          const uint32_t* __restrict__ list,
                                                          uint32_t count) {
+  using Tab = Table<kPacked<WEIGHTED>, W>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);
-  W* vals = reinterpret_cast<W*>(smem_raw + kBlockCap * sizeof(uint32_t));
-  __shared__ Best<W> red[32];
+  Tab tab;
+  tab.bind(smem_raw, kBlockCap);
+  __shared__ Best<VBits<W>> red[32];
   __shared__ int s_flag;
-
+  const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
   for (uint32_t t = blockIdx.x; t < count; t += gridDim.x) {
     const uint32_t i = __ldg(list + t);
     if (threadIdx.x == 0) s_flag = claim_vertex(c, i) ? 1 : 0;
-    __syncthreads();
-    const int skip = s_flag;
-    __syncthreads();
-    if (skip) continue;
     const uint64_t lo = __ldg(c.g.off + i);
     const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
     const uint32_t cap = pow2_ceil(2 * d);
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-      keys[s] = kEmpty;
-      vals[s] = W(0);
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) tab.clear_slot(s);
+    __syncthreads();
+    if (s_flag) {
+      __syncthreads();  // s_flag is rewritten by the next iteration
+      continue;
     }
+    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, threadIdx.x, blockDim.x, pol, fails);
     __syncthreads();
-    block_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, keys, vals, cap, fails);
-    __syncthreads();
-    Best<W> b{W(0), kEmpty};
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) best_merge(b, vals[s], keys[s]);
+    Best<VBits<W>> b{VBits<W>(0), kEmpty};
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
+      uint32_t k;
+      VBits<W> v;
+      tab.read(s, k, v);
+      best_merge(b, v, k);
+    }
     b = block_best(b, red);
     if (threadIdx.x == 0) {
       s_flag = apply_move<MODE>(c, i, b.k) ? 1 : 0;
       ++n_v;
       n_e += d;
       n_dn += s_flag;
+      if (MODE == kAsync && s_flag && c.flags) n_w += d;
     }
     __syncthreads();
     const int changed = s_flag;
-    if (MODE == kAsync && changed && c.flags) {
-      for (uint32_t e = threadIdx.x; e < d; e += blockDim.x) c.flags[__ldg(c.g.tgt + lo + e)] = 0;
-      if (threadIdx.x == 0) n_w += d;
-    }
+    if (MODE == kAsync && changed && c.flags)
+      for (uint32_t e = threadIdx.x; e < d; e += blockDim.x)
+        c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
     __syncthreads();
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
@@ -322,7 +361,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_block(PassCtx c,
   warp_add_counter(c.ctr, C_FAIL, fails);
 }
 
-// ---- tier 3: hubs, global tables -------------------------------------------------------
+// ---- tier: hubs, global tables -------------------------------------------------------
 
 template <int MODE>
 __global__ void k_hub_select(PassCtx c, HubCtx h) {
@@ -343,14 +382,27 @@ __global__ void k_hub_select(PassCtx c, HubCtx h) {
   warp_add_counter(c.ctr, C_PROC_E, n_e);
 }
 
+template <typename Tab, typename W, bool PACKED>
+__device__ __forceinline__ void bind_hub_table(Tab& g, const HubCtx& h, uint32_t x) {
+  if constexpr (PACKED)
+    g.bind_split(static_cast<unsigned long long*>(h.tab) + h.tab_off[x], nullptr);
+  else
+    g.bind_split(static_cast<uint32_t*>(h.tab) + h.tab_off[x],
+                 static_cast<W*>(h.tab_vals) + h.tab_off[x]);
+}
+
 // Accumulate one (hub, chunk) item: pre-aggregate the chunk in shared memory,
-// then flush each distinct label once into the hub's global table.
+// then flush each distinct label once into the hub's global table; newly
+// claimed global slots are appended to the hub's occupied list (one atomic per
+// warp).
 template <int MODE, typename W, bool WEIGHTED>
 __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h) {
+  using Tab = Table<kPacked<WEIGHTED>, W>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);
-  W* vals = reinterpret_cast<W*>(smem_raw + kBlockCap * sizeof(uint32_t));
-  W* gvals = static_cast<W*>(h.vals);
+  Tab tab;
+  tab.bind(smem_raw, kBlockCap);
+  const uint64_t pol = policy_evict_first();
+  const int lane = threadIdx.x & 31;
   unsigned long long fails = 0;
   for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
     const uint32_t x = h.item_hub[it];
@@ -361,32 +413,45 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h
     const uint32_t e0 = h.item_start[it];
     const uint32_t e1 = min(d, e0 + kHubChunk);
     const uint32_t cap = kBlockCap;
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-      keys[s] = kEmpty;
-      vals[s] = W(0);
-    }
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) tab.clear_slot(s);
     __syncthreads();
-    block_gather<MODE, W, WEIGHTED>(c, i, lo, e0, e1, keys, vals, cap, fails);
+    team_gather<MODE, W, WEIGHTED>(c, i, lo, e0, e1, tab, cap, threadIdx.x, blockDim.x, pol,
+                                   fails);
     __syncthreads();
-    uint32_t* gk = h.keys + h.tab_off[x];
-    W* gv = gvals + h.tab_off[x];
+    Tab g;
+    bind_hub_table<Tab, W, kPacked<WEIGHTED>>(g, h, x);
     uint32_t* occ = h.occ + h.occ_off[x];
     const uint32_t gcap = h.tab_cap[x];
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-      const uint32_t k = keys[s];
-      if (k != kEmpty && !ht_add(gk, gv, gcap, c.strategy, k, vals[s], occ, h.occ_n + x)) ++fails;
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {  // uniform trip count
+      uint32_t k;
+      VBits<W> vb;
+      tab.read(s, k, vb);
+      int r = -1;
+      uint32_t gslot = 0;
+      if (k != kEmpty) {
+        r = g.add(gcap, c.strategy, k, tab.value(s), &gslot);
+        if (r == 0) ++fails;
+      }
+      const unsigned claimed = __ballot_sync(kFull, r == 2);
+      if (claimed) {
+        const int leader = __ffs(claimed) - 1;
+        uint32_t basepos = 0;
+        if (lane == leader) basepos = atomicAdd(h.occ_n + x, static_cast<uint32_t>(__popc(claimed)));
+        basepos = __shfl_sync(kFull, basepos, leader);
+        if (r == 2) occ[basepos + __popc(claimed & ((1u << lane) - 1u))] = gslot;
+      }
     }
     __syncthreads();
   }
   warp_add_counter(c.ctr, C_FAIL, fails);
 }
 
-// Sparse argmax over the occupied slots of each active hub; clears the slots
-// it reads (float path) so the tables are idle for the next pass.
-template <typename W>
+// Sparse argmax over the occupied slots of each active hub; the slots it reads
+// are reset (u32-bits path) so the tables are idle for the next pass.
+template <typename W, bool WEIGHTED>
 __global__ void __launch_bounds__(kBlockThreads) k_hub_argmax(HubCtx h) {
-  __shared__ Best<W> red[32];
-  W* gvals = static_cast<W*>(h.vals);
+  using Tab = Table<kPacked<WEIGHTED>, W>;
+  __shared__ Best<VBits<W>> red[32];
   for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
     const uint32_t x = h.item_hub[it];
     if (!h.active[x]) continue;
@@ -394,26 +459,24 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_argmax(HubCtx h) {
     const uint32_t n_occ = h.occ_n[x];
     if (e0 >= n_occ) continue;
     const uint32_t e1 = min(n_occ, e0 + kHubChunk);
-    uint32_t* gk = h.keys + h.tab_off[x];
-    W* gv = gvals + h.tab_off[x];
+    Tab g;
+    bind_hub_table<Tab, W, kPacked<WEIGHTED>>(g, h, x);
     const uint32_t* occ = h.occ + h.occ_off[x];
-    Best<W> b{W(0), kEmpty};
+    Best<VBits<W>> b{VBits<W>(0), kEmpty};
     for (uint32_t p = e0 + threadIdx.x; p < e1; p += blockDim.x) {
       const uint32_t s = occ[p];
-      best_merge(b, gv[s], gk[s]);
-      if constexpr (sizeof(W) == 4) {
-        gk[s] = kEmpty;
-        gv[s] = W(0);
-      }
+      uint32_t k;
+      VBits<W> v;
+      g.read(s, k, v);
+      best_merge(b, v, k);
+      if constexpr (sizeof(VBits<W>) == 4) g.clear_slot(s);
     }
     b = block_best(b, red);
     if (threadIdx.x == 0 && b.k != kEmpty) {
-      if constexpr (sizeof(W) == 4) {
+      if constexpr (sizeof(VBits<W>) == 4) {
         // (value bits, ~key): a larger value wins, then a smaller key.
-        const unsigned long long packed =
-            (static_cast<unsigned long long>(__float_as_uint(static_cast<float>(b.v))) << 32) |
-            static_cast<unsigned long long>(~b.k);
-        atomicMax(h.best + x, packed);
+        atomicMax(h.best + x, (static_cast<unsigned long long>(b.v) << 32) |
+                                  static_cast<unsigned long long>(~b.k));
       } else {
         atomicMax(h.best + x, static_cast<unsigned long long>(__double_as_longlong(b.v)));
       }
@@ -422,10 +485,10 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_argmax(HubCtx h) {
   }
 }
 
-// Double path only: the smallest key among slots holding the maximum value;
-// clears the slots.
+// fp64 weighted path only: the smallest key among slots holding the maximum
+// value; resets the slots.
 __global__ void __launch_bounds__(kBlockThreads) k_hub_argmax_key_f64(HubCtx h) {
-  double* gvals = static_cast<double*>(h.vals);
+  Table<false, double> g;
   for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
     const uint32_t x = h.item_hub[it];
     if (!h.active[x]) continue;
@@ -433,20 +496,19 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_argmax_key_f64(HubCtx h) 
     const uint32_t n_occ = h.occ_n[x];
     if (e0 >= n_occ) continue;
     const uint32_t e1 = min(n_occ, e0 + kHubChunk);
-    uint32_t* gk = h.keys + h.tab_off[x];
-    double* gv = gvals + h.tab_off[x];
+    g.bind_split(static_cast<uint32_t*>(h.tab) + h.tab_off[x],
+                 static_cast<double*>(h.tab_vals) + h.tab_off[x]);
     const uint32_t* occ = h.occ + h.occ_off[x];
     const double bestv = __longlong_as_double(static_cast<long long>(h.best[x]));
     for (uint32_t p = e0 + threadIdx.x; p < e1; p += blockDim.x) {
       const uint32_t s = occ[p];
-      if (gv[s] == bestv) atomicMin(h.best_k + x, gk[s]);
-      gk[s] = kEmpty;
-      gv[s] = 0.0;
+      if (g.v[s] == bestv) atomicMin(h.best_k + x, g.k[s]);
+      g.clear_slot(s);
     }
   }
 }
 
-template <int MODE, typename W>
+template <int MODE, typename W, bool WEIGHTED>
 __global__ void k_hub_decide(PassCtx c, HubCtx h) {
   unsigned long long n_dn = 0;
   const uint32_t bound = (h.n_hubs + 31u) & ~31u;
@@ -457,7 +519,7 @@ __global__ void k_hub_decide(PassCtx c, HubCtx h) {
     if (h.active[x]) {
       uint32_t cand = kEmpty;
       if (h.occ_n[x] > 0) {
-        if constexpr (sizeof(W) == 4)
+        if constexpr (sizeof(VBits<W>) == 4)
           cand = ~static_cast<uint32_t>(h.best[x] & 0xFFFFFFFFull);
         else
           cand = h.best_k[x];
@@ -476,6 +538,7 @@ __global__ void k_hub_decide(PassCtx c, HubCtx h) {
 // Async wake for changed hubs, one chunk per work item.
 __global__ void __launch_bounds__(kBlockThreads) k_hub_wake(PassCtx c, HubCtx h) {
   unsigned long long n_w = 0;
+  const uint64_t pol = policy_evict_first();
   for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
     const uint32_t x = h.item_hub[it];
     if (!h.changed[x]) continue;
@@ -484,7 +547,8 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_wake(PassCtx c, HubCtx h)
     const uint32_t d = static_cast<uint32_t>(c.g.off[i + 1] - lo);
     const uint32_t e0 = h.item_start[it];
     const uint32_t e1 = min(d, e0 + kHubChunk);
-    for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) c.flags[__ldg(c.g.tgt + lo + e)] = 0;
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+      c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
     if (threadIdx.x == 0) n_w += e1 - e0;
   }
   warp_add_counter(c.ctr, C_WAKE_E, n_w);
@@ -514,12 +578,10 @@ __global__ void __launch_bounds__(kBlockThreads) k_wake_list(Graph g, uint8_t* f
 // vertex's scan is CTA-parallel. Exact reference semantics on the GPU (no CPU
 // fallback); slow by construction — a compatibility mode, not the hot path.
 template <typename W, bool WEIGHTED>
-__global__ void __launch_bounds__(kBlockThreads) k_sequential(PassCtx c, uint32_t* gkeys,
-                                                              W* gvals) {
+__global__ void __launch_bounds__(kBlockThreads) k_sequential(PassCtx c, void* gtab) {
+  using Tab = Table<kPacked<WEIGHTED>, W>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* skeys = reinterpret_cast<uint32_t*>(smem_raw);
-  W* svals = reinterpret_cast<W*>(smem_raw + kBlockCap * sizeof(uint32_t));
-  __shared__ Best<W> red[32];
+  __shared__ Best<VBits<W>> red[32];
   __shared__ int s_flag;
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
   for (uint32_t i = 0; i < c.g.n; ++i) {
@@ -538,12 +600,12 @@ __global__ void __launch_bounds__(kBlockThreads) k_sequential(PassCtx c, uint32_
     const uint64_t lo = c.g.off[i];
     const uint32_t d = static_cast<uint32_t>(c.g.off[i + 1] - lo);
     const uint32_t cap = pow2_ceil(2 * d);
-    uint32_t* keys = cap <= kBlockCap ? skeys : gkeys;
-    W* vals = cap <= kBlockCap ? svals : gvals;
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-      keys[s] = kEmpty;
-      vals[s] = W(0);
-    }
+    Tab tab;
+    if (cap <= static_cast<uint32_t>(kBlockCap))
+      tab.bind(smem_raw, kBlockCap);
+    else
+      tab.bind(gtab, cap);
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) tab.clear_slot(s);
     __syncthreads();
     for (uint32_t base = 0; base < d; base += blockDim.x) {
       const uint32_t e = base + threadIdx.x;
@@ -551,11 +613,16 @@ __global__ void __launch_bounds__(kBlockThreads) k_sequential(PassCtx c, uint32_
       const bool valid = e < d && j != i;
       const uint32_t lab = valid ? c.lab_out[j] : kEmpty;
       const W w = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
-      gather_insert<kSync, W, WEIGHTED>(c, i, lab, w, keys, vals, cap, fails);
+      gather_insert<W, WEIGHTED>(c, lab, w, tab, cap, fails);
     }
     __syncthreads();
-    Best<W> b{W(0), kEmpty};
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) best_merge(b, vals[s], keys[s]);
+    Best<VBits<W>> b{VBits<W>(0), kEmpty};
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
+      uint32_t k;
+      VBits<W> v;
+      tab.read(s, k, v);
+      best_merge(b, v, k);
+    }
     b = block_best(b, red);
     if (threadIdx.x == 0) {
       int ch = 0;

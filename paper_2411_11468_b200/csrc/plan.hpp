@@ -9,12 +9,15 @@
 namespace nulpa {
 
 struct Plan {
-  uint32_t thread_max = 0, warp_max = 0, block_max = 0;
+  uint32_t thread_max = 0, warp_max = 0, block_max = 0, schedule = 1;
+  uint32_t v_lo = 0, v_hi = 0;  // vertex range the tiers cover
   int value_bytes = 4;  // hashtable value width the hub tables were sized for
-  // Tier vertex lists (ascending id): 0 thread, 1 warp, 2 block, 3 hub.
-  uint32_t* list[4] = {nullptr, nullptr, nullptr, nullptr};
-  uint32_t count[4] = {0, 0, 0, 0};
-  uint64_t edges[4] = {0, 0, 0, 0};
+  // Tier vertex lists (ascending id unless scrambled), indexed by dev::Tier;
+  // list[T_HUB] holds the hubs.
+  static constexpr int kLists = dev::T_HUB + 1;
+  uint32_t* list[kLists] = {};
+  uint32_t count[kLists] = {};
+  bool weighted = false;  // hub tables: packed 64-bit words (unit weights) or split
   // Hub tier.
   uint32_t n_hubs = 0, n_items = 0;
   uint64_t table_slots = 0, occ_slots = 0;
@@ -23,8 +26,8 @@ struct Plan {
   uint64_t* occ_off = nullptr;
   uint32_t* occ_n = nullptr;
   uint32_t* occ = nullptr;
-  uint32_t* keys = nullptr;
-  void* vals = nullptr;
+  void* tab = nullptr;       // packed words, or keys (weighted)
+  void* tab_vals = nullptr;  // weighted: values
   unsigned long long* best = nullptr;
   uint32_t* best_k = nullptr;
   uint8_t* active = nullptr;
@@ -35,14 +38,14 @@ struct Plan {
 
   dev::HubCtx hub_ctx() const {
     dev::HubCtx h;
-    h.hub_v = list[3];
+    h.hub_v = list[dev::T_HUB];
     h.tab_off = tab_off;
     h.tab_cap = tab_cap;
     h.occ_off = occ_off;
     h.occ_n = occ_n;
     h.occ = occ;
-    h.keys = keys;
-    h.vals = vals;
+    h.tab = tab;
+    h.tab_vals = tab_vals;
     h.best = best;
     h.best_k = best_k;
     h.active = active;
@@ -58,13 +61,17 @@ struct Plan {
 
 struct TierBounds {
   uint32_t thread_max, warp_max, block_max;
+  uint32_t schedule;  // 1 ascending id, 2 scrambled
 };
 
 // Resolve the tier bounds from LpaConfig.switch_degree and the tuning struct.
 TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* tuning);
 
-// Build (or reuse the cached) plan of a resident graph.
+// Build (or reuse the cached) plan of a resident graph over all vertices.
 Plan* get_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream_t s);
+// Build an uncached plan over the vertex range [v_lo, v_hi) (caller owns it).
+Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream_t s,
+                 uint32_t v_lo, uint32_t v_hi);
 
 int sm_count();
 

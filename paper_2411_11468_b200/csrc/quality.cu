@@ -170,10 +170,10 @@ double modularity_device(nulpa_graph* g, const uint32_t* lab, cudaStream_t s) {
   NULPA_CUDA(cudaMemsetAsync(sigma, 0, (2ull * n + 1) * sizeof(double), s));
   const Graph dg{g->offsets, g->targets, g->weights, n};
   const int sms = sm_count();
-  if (p->count[0])
-    k_mod_thread<<<std::min<uint32_t>((p->count[0] + 255) / 256, sms * 8), 256, 0, s>>>(
-        dg, lab, p->list[0], p->count[0], sigma, big);
-  for (int t = 1; t <= 2; ++t)
+  if (p->count[T_THREAD])
+    k_mod_thread<<<std::min<uint32_t>((p->count[T_THREAD] + 255) / 256, sms * 8), 256, 0, s>>>(
+        dg, lab, p->list[T_THREAD], p->count[T_THREAD], sigma, big);
+  for (int t = T_HALF; t <= T_BLOCK; ++t)
     if (p->count[t])
       k_mod_warp<<<std::min<uint32_t>((p->count[t] + 7) / 8, sms * 8), 256, 0, s>>>(
           dg, lab, p->list[t], p->count[t], sigma, big);

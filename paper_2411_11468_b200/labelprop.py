@@ -100,12 +100,16 @@ class Tuning:
     thread_max_degree: int = 0
     warp_max_degree: int = 0
     block_max_degree: int = 0
+    schedule: int = 0  # 0 default, 1 ascending id, 2 scrambled
+    profile: bool = False
 
     def to_c(self) -> _capi.nulpa_tuning:
         t = _capi.nulpa_tuning()
         t.thread_max_degree = self.thread_max_degree
         t.warp_max_degree = self.warp_max_degree
         t.block_max_degree = self.block_max_degree
+        t.schedule = self.schedule
+        t.profile = 1 if self.profile else 0
         return t
 
 

@@ -47,7 +47,8 @@ def test_abi_struct_layouts(tmp_path):
     """The ctypes mirrors agree with the C header, field by field (compiled probe)."""
     import ctypes as C
     structs = {"nulpa_csr": _capi.nulpa_csr, "nulpa_opts": _capi.nulpa_opts,
-               "nulpa_tuning": _capi.nulpa_tuning, "nulpa_stats": _capi.nulpa_stats}
+               "nulpa_tuning": _capi.nulpa_tuning, "nulpa_stats": _capi.nulpa_stats,
+               "nulpa_pass_info": _capi.nulpa_pass_info}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "nulpa/nulpa.h"',
              'int main(void) {']
     for sname, cls in structs.items():

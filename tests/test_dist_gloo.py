@@ -1,0 +1,109 @@
+"""The partitioned multi-GPU driver (paper_2411_11468_b200/dist.py) on CPU: world_size 2, gloo.
+
+Each rank's pass is the C restatement (oracle) restricted to its edge-balanced range — a
+CPU stand-in for nulpa_session_pass — so this checks the host logic of SURVEY §8e: the
+partition, the all-gather-v of labels, the MIN-reduce of wake flags, the counter
+all-reduce and the run_engine schedule. A partitioned Synchronous run must equal the
+single-process Synchronous run bit for bit.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from conftest import load_golden
+from paper_2411_11468_b200.dist import Exchange, edge_balanced_bounds, run_partitioned
+from paper_2411_11468_b200.labelprop import ExecMode, LpaConfig
+
+
+class PortRangeEngine:
+    """CPU stand-in for one rank's nulpa_session (Synchronous semantics, lpa.cpp:70-100)."""
+
+    def __init__(self, off, tgt, lo, hi):
+        self.off, self.tgt = off, tgt
+        self.pg = O.PortGraph(off, tgt, None)
+        self.n = off.size - 1
+        self.lo, self.hi = lo, hi
+        self.labels = torch.zeros(self.n, dtype=torch.int32)
+        self.flags = torch.zeros(self.n, dtype=torch.uint8)
+
+    def init(self):
+        self.labels.copy_(torch.arange(self.n, dtype=torch.int32))
+        deg = np.diff(self.off.astype(np.int64))
+        self.flags.copy_(torch.from_numpy((deg == 0).astype(np.uint8)))
+
+    def pass_(self, pick_less):
+        lab = self.labels.numpy().view(np.uint32)
+        flg = self.flags.numpy()
+        cand, _ = O.port_sync_step(self.pg, lab, pick_less)  # from the frozen snapshot
+        own = np.zeros(self.n, bool)
+        own[self.lo:self.hi] = True
+        processed = own & (flg == 0)
+        flg[processed] = 1
+        changed = np.flatnonzero(processed & (cand != lab))
+        lab[changed] = cand[changed]
+        for v in changed:  # wake after the joint application
+            flg[self.tgt[self.off[v]:self.off[v + 1]]] = 0
+        return {"changed": int(changed.size), "processed_vertices": int(processed.sum()),
+                "processed_edges": 0, "wake_edges": 0, "device_ms": 0.0, "kernel_launches": 0}
+
+    def sync(self):
+        pass
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, cfg_kw, out):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    d = load_golden(name)
+    off, tgt = d["offsets"], d["targets"]
+    bounds = edge_balanced_bounds(off, world)
+    eng = PortRangeEngine(off, tgt, bounds[rank], bounds[rank + 1])
+    cfg = LpaConfig(exec=ExecMode.Synchronous, **cfg_kw)
+    st = run_partitioned(eng, cfg, rank, world, Exchange(bounds, staged=True), eng.n)
+    out[rank] = (eng.labels.numpy().view(np.uint32).copy(), st.delta_n_per_iter, st.converged,
+                 st.pl_iterations)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["sbm10k_seed101", "random05", "kat_ring_of_cliques"])
+@pytest.mark.parametrize("cfg_kw", [{"pl_period": 4}, {"pl_period": 0}, {"pl_period": 1,
+                                                                        "prune": False}])
+def test_partitioned_sync_equals_single_process(name, cfg_kw):
+    world = 2
+    d = load_golden(name)
+    pg = O.PortGraph(d["offsets"], d["targets"], None)
+    want, ws = O.port_lpa(pg, exec_mode=2, pl_period=cfg_kw["pl_period"],
+                          prune=cfg_kw.get("prune", True))
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_worker, args=(world, _free_port(), name, cfg_kw, out), nprocs=world, join=True)
+    for r in range(world):
+        labels, dn, conv, pli = out[r]
+        assert np.array_equal(labels, want), (name, cfg_kw, r)
+        assert dn == ws["delta_n"] and conv == ws["converged"]
+        assert pli == ws["pl_iterations"]
+
+
+def test_edge_balanced_bounds():
+    d = load_golden("sbm10k_seed101")
+    off = d["offsets"]
+    for P in (1, 2, 3, 4, 8):
+        b = edge_balanced_bounds(off, P)
+        assert b[0] == 0 and b[-1] == off.size - 1 and all(x <= y for x, y in zip(b, b[1:]))
+        m2 = int(off[-1])
+        for p in range(1, P):
+            assert int(off[b[p]]) >= m2 * p // P
+            assert b[p] == 0 or int(off[b[p] - 1]) < m2 * p // P
