@@ -88,13 +88,16 @@ typedef struct nulpa_tuning {
   uint32_t use_graphs;        /* reserved */
   uint32_t profile;           /* 1: time each tier with CUDA events (stats.tier_*) */
   uint32_t schedule;          /* ParallelAsync visit order inside each tier:
-                                 0 default, 1 ascending id (partition_by_degree order),
-                                 2 scrambled (hashed) order */
+                                 0 default (= 2), 1 ascending id (partition_by_degree
+                                 order), 2 scrambled (hashed) order. Any order is a valid
+                                 asynchronous schedule; Synchronous/Sequential results do
+                                 not depend on it. */
   uint32_t reserved[1];
 } nulpa_tuning;
 
-#define NULPA_TIERS 7 /* 0 thread, 1 half-warp, 2 warp, 3 warp+smem table, 4 CTA, 5 hub,
-                         6 other (deferred wake, cross-check, sequential) */
+#define NULPA_TIERS 9 /* 0 thread, 1 half-warp, 2 warp, 3 warp+smem table, 4 CTA, 5 1024-thread CTA,
+                         6 8-CTA cluster (DSMEM table), 7 hub (global table),
+                         8 other (deferred wake, cross-check, sequential) */
 
 /* labelprop::RunStats (lpa.hpp:39-46) plus device counters for roofline
  * accounting. delta_n must point at >= max_iterations u64 (or be NULL). */
@@ -219,7 +222,9 @@ int nulpa_session_create(nulpa_graph* g, const nulpa_opts* opts, const nulpa_tun
                          uint8_t* flags_dev, nulpa_session** out);
 /* labels[i] = i and flags[i] = (degree(i) == 0) over ALL n vertices. */
 int nulpa_session_init(nulpa_session* s);
-int nulpa_session_pass(nulpa_session* s, int pick_less, nulpa_pass_info* info);
+/* wake = 0 skips the neighbour wake-up stores (legal when the caller's schedule
+ * resets every flag before the next pass, see engine.cu run_lpa). */
+int nulpa_session_pass(nulpa_session* s, int pick_less, int wake, nulpa_pass_info* info);
 int nulpa_session_free(nulpa_session* s);
 
 #ifdef __cplusplus

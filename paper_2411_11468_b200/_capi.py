@@ -34,8 +34,9 @@ class nulpa_tuning(C.Structure):
                 ("use_graphs", C.c_uint32), ("profile", C.c_uint32),
                 ("schedule", C.c_uint32), ("reserved", C.c_uint32 * 1)]
 
-NULPA_TIERS = 7
-TIER_NAMES = ["thread", "half_warp", "warp", "warp_table", "block", "hub", "other"]
+NULPA_TIERS = 9
+TIER_NAMES = ["thread", "half_warp", "warp", "warp_table", "block", "big_block", "cluster",
+              "hub", "other"]
 
 
 class nulpa_stats(C.Structure):
@@ -45,9 +46,9 @@ class nulpa_stats(C.Structure):
                 ("delta_n", C.POINTER(C.c_uint64)), ("processed_vertices", C.c_uint64),
                 ("processed_edges", C.c_uint64), ("wake_edges", C.c_uint64),
                 ("algorithmic_bytes", C.c_uint64), ("setup_seconds", C.c_double),
-                ("kernel_launches", C.c_uint64), ("tier_ms", C.c_double * 7),
-                ("tier_bytes", C.c_double * 7), ("tier_edges", C.c_uint64 * 7),
-                ("tier_passes", C.c_uint32 * 7), ("reserved2", C.c_uint32)]
+                ("kernel_launches", C.c_uint64), ("tier_ms", C.c_double * 9),
+                ("tier_bytes", C.c_double * 9), ("tier_edges", C.c_uint64 * 9),
+                ("tier_passes", C.c_uint32 * 9), ("reserved2", C.c_uint32)]
 
 
 class nulpa_pass_info(C.Structure):
@@ -106,7 +107,7 @@ _SIGS = {
                                        C.POINTER(nulpa_tuning), C.c_uint32, C.c_uint32,
                                        C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     "nulpa_session_init": (C.c_int, [C.c_void_p]),
-    "nulpa_session_pass": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(nulpa_pass_info)]),
+    "nulpa_session_pass": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(nulpa_pass_info)]),
     "nulpa_session_free": (C.c_int, [C.c_void_p]),
 }
 

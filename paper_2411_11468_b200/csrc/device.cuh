@@ -46,22 +46,30 @@ enum Counter : int {
 
 // Degree tiers.
 enum Tier : int {
-  T_THREAD = 0,  // deg <= thread_max (<= 16): one thread per vertex
-  T_HALF = 1,    // deg <= 16: half a warp per vertex, register dedup
-  T_WARP = 2,    // deg <= 32: one warp per vertex, register dedup
-  T_WTAB = 3,    // deg <= 256: one warp per vertex, per-warp shared-memory table
-  T_BLOCK = 4,   // deg <= 2048: one CTA per vertex, shared-memory table
-  T_HUB = 5,     // larger: (hub, chunk) items, shared pre-aggregation + global table
-  T_OTHER = 6,   // deferred wake, cross-check, sequential
-  kTiers = 7
+  T_THREAD = 0,   // deg <= thread_max (<= 16): one thread per vertex
+  T_HALF = 1,     // deg <= 16: half a warp per vertex, register dedup
+  T_WARP = 2,     // deg <= 32: one warp per vertex, register dedup
+  T_WTAB = 3,     // deg <= 256: one warp per vertex, per-warp shared-memory table
+  T_BLOCK = 4,    // deg <= 2048: one 256-thread CTA per vertex, shared-memory table
+  T_BIG = 5,      // deg <= 12288: one 1024-thread CTA per vertex, 128 KB shared table
+  T_CLUSTER = 6,  // deg <= 98304: one 8-CTA cluster per vertex, table distributed over DSMEM
+  T_HUB = 7,      // larger: (hub, chunk) items, shared pre-aggregation + global table
+  T_OTHER = 8,    // deferred wake, cross-check, sequential
+  kTiers = 9
 };
 
 constexpr int kBlockThreads = 256;
-constexpr int kWarpTabMax = 256;   // T_WTAB degree bound
-constexpr int kWarpTabCap = 512;   // per-warp slots (load <= 1/2)
-constexpr int kBlockMax = 2048;    // T_BLOCK degree bound
-constexpr int kBlockCap = 4096;    // per-CTA slots (load <= 1/2)
-constexpr int kHubChunk = 2048;    // edges per hub work item (<= kBlockCap / 2)
+constexpr int kWarpTabMax = 256;    // T_WTAB degree bound
+constexpr int kWarpTabCap = 512;    // per-warp slots (load <= 1/2)
+constexpr int kBlockMax = 2048;     // T_BLOCK degree bound
+constexpr int kBlockCap = 4096;     // per-CTA slots (load <= 1/2)
+constexpr int kBigThreads = 1024;
+constexpr int kBigCap = 16384;      // 128 KB packed
+constexpr int kBigMax = 12288;      // load <= 3/4
+constexpr int kClusterSize = 8;     // portable cluster size
+constexpr int kClusterCap = 16384;  // slots per CTA of the cluster
+constexpr int kClusterMax = kClusterSize * kClusterCap * 3 / 4;  // 98304, load <= 3/4
+constexpr int kHubChunk = 2048;     // edges per hub work item (<= kBlockCap / 2)
 
 struct Graph {
   const uint64_t* __restrict__ off;
@@ -80,6 +88,8 @@ struct PassCtx {
   unsigned long long* changed_n;  // its length
   int pick_less;
   int strategy;
+  int wake;                       // store neighbour wake-ups (0 when provably dead, see engine.cu)
+  unsigned int* work;             // dynamic work counter (cluster tier)
 };
 
 // Hub-tier tables and work items (k_hub_* in lpa_kernels.cuh).

@@ -64,10 +64,14 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   using Tab = Table<kPacked<WEIGHTED>, W>;
   constexpr size_t wtab_smem = (kBlockThreads / 32) * kWarpTabCap * Tab::kSlotBytes;
   constexpr size_t block_smem = kBlockCap * Tab::kSlotBytes;
+  constexpr size_t big_smem = kBigCap * Tab::kSlotBytes;
+  constexpr size_t cluster_smem = kClusterCap * Tab::kSlotBytes;
   static bool init = false;
   if (!init) {
     allow_smem(k_wtab<MODE, W, WEIGHTED>, wtab_smem);
-    allow_smem(k_block<MODE, W, WEIGHTED>, block_smem);
+    allow_smem(k_block<MODE, W, WEIGHTED, kBlockThreads, kBlockCap>, block_smem);
+    allow_smem(k_block<MODE, W, WEIGHTED, kBigThreads, kBigCap>, big_smem);
+    allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
     allow_smem(k_hub_accum<MODE, W, WEIGHTED>, block_smem);
     init = true;
   }
@@ -110,9 +114,28 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   }
   if (p.count[T_BLOCK]) {
     tier(T_BLOCK);
-    k_block<MODE, W, WEIGHTED><<<grid_for(p.count[T_BLOCK], 1, sms * 6), kBlockThreads,
-                                 block_smem, s>>>(c, p.list[T_BLOCK], p.count[T_BLOCK]);
+    k_block<MODE, W, WEIGHTED, kBlockThreads, kBlockCap>
+        <<<grid_for(p.count[T_BLOCK], 1, sms * 6), kBlockThreads, block_smem, s>>>(
+            c, p.list[T_BLOCK], p.count[T_BLOCK]);
     prof.end(T_BLOCK, s);
+    ++launches;
+  }
+  if (p.count[T_BIG]) {
+    tier(T_BIG);
+    k_block<MODE, W, WEIGHTED, kBigThreads, kBigCap>
+        <<<grid_for(p.count[T_BIG], 1, sms), kBigThreads, big_smem, s>>>(c, p.list[T_BIG],
+                                                                          p.count[T_BIG]);
+    prof.end(T_BIG, s);
+    ++launches;
+  }
+  if (p.count[T_CLUSTER]) {
+    tier(T_CLUSTER);
+    NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
+    // persistent clusters pull vertices from c.work; grid a multiple of the cluster size
+    const unsigned gc = std::max<unsigned>(kClusterSize, (sms / kClusterSize) * kClusterSize);
+    k_cluster<MODE, W, WEIGHTED><<<gc, kBigThreads, cluster_smem, s>>>(c, p.list[T_CLUSTER],
+                                                                      p.count[T_CLUSTER]);
+    prof.end(T_CLUSTER, s);
     ++launches;
   }
   if (p.n_hubs) {
@@ -130,7 +153,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     }
     k_hub_decide<MODE, W, WEIGHTED><<<gh, 256, 0, s>>>(c, h);
     ++launches;
-    if (MODE == kAsync && c.flags) {
+    if (MODE == kAsync && c.wake) {
       k_hub_wake<<<gi, kBlockThreads, 0, s>>>(c, h);
       ++launches;
     }
@@ -256,6 +279,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
   DBuf<uint8_t> flags(n);
   constexpr int kCtr = kTiers * C_COUNT;
   DBuf<unsigned long long> ctr(kCtr);
+  DBuf<unsigned int> work(2);  // cluster-tier work counter
   unsigned long long* ctr_other = ctr.p + T_OTHER * C_COUNT;
   Pinned hc(kCtr);
   if (o.exec == NULPA_EXEC_SYNCHRONOUS) {
@@ -306,6 +330,16 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     NULPA_CUDA(cudaMemsetAsync(ctr.p, 0, kCtr * sizeof(unsigned long long), s));
     for (bool& u : prof.used) u = false;
 
+    // Neighbour wake-ups are dead stores when the next pass resets every flag
+    // (or there is no next pass) and no reader inside this pass can see them
+    // (Synchronous wakes after the pass; an async pass that started from
+    // all-zero flags only wakes vertices whose flag is already 0 or that were
+    // already examined). Skipping them leaves every result unchanged.
+    const bool this_reset = iter == 0 || !o.prune || (was_pl && !pick_less);
+    const bool next_pl = o.pl_period > 0 && (iter + 1) % o.pl_period == 0;
+    const bool next_reset = iter + 1 >= o.max_iterations || !o.prune || (pick_less && !next_pl);
+    const bool wake = !(next_reset && (this_reset || o.exec == NULPA_EXEC_SYNCHRONOUS));
+
     PassCtx c;
     c.g = dg;
     c.flags = flags.p;
@@ -314,6 +348,8 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     c.strategy = o.strategy;
     c.changed = nullptr;
     c.changed_n = ctr_other + C_NCHANGED;
+    c.wake = wake ? 1 : 0;
+    c.work = work.p;
     if (o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
       c.lab_in = cur;
       c.lab_out = cur;
@@ -324,14 +360,16 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       NULPA_CUDA(cudaMemcpyAsync(nxt, cur, n * 4ull, cudaMemcpyDeviceToDevice, s));
       c.lab_in = cur;
       c.lab_out = nxt;
-      c.changed = changed.p;
+      c.changed = wake ? changed.p : nullptr;
       launches += dispatch_pass<kSync>(*p, c, ctr.p, vbytes, s, sms, prof);
-      prof.begin(T_OTHER, s);
-      k_wake_list<<<grid_for(n, kBlockThreads / 32, sms * 8), kBlockThreads, 0, s>>>(
-          dg, flags.p, changed.p, ctr_other + C_NCHANGED, ctr_other);
-      prof.end(T_OTHER, s);
-      ++launches;
-      NULPA_CUDA(cudaGetLastError());
+      if (wake) {
+        prof.begin(T_OTHER, s);
+        k_wake_list<<<grid_for(n, kBlockThreads / 32, sms * 8), kBlockThreads, 0, s>>>(
+            dg, flags.p, changed.p, ctr_other + C_NCHANGED, ctr_other);
+        prof.end(T_OTHER, s);
+        ++launches;
+        NULPA_CUDA(cudaGetLastError());
+      }
       std::swap(cur, nxt);
     } else {
       c.lab_in = cur;
@@ -460,6 +498,9 @@ uint64_t run_sync_step(nulpa_graph* g, const uint32_t* lab_in_dev, int pick_less
   c.changed_n = ctr.p + T_OTHER * C_COUNT + C_NCHANGED;
   c.pick_less = pick_less ? 1 : 0;
   c.strategy = strategy;
+  c.wake = 0;
+  DBuf<unsigned int> work(2);
+  c.work = work.p;
   Prof prof;
   dispatch_pass<kSync>(*p, c, ctr.p, vbytes, s, sms, prof);
   NULPA_CUDA(cudaMemcpyAsync(hc.p, ctr.p, kCtr * sizeof(unsigned long long),
@@ -496,6 +537,7 @@ struct nulpa_session {
   uint8_t* flags = nullptr;    // caller device array [n]
   nulpa::DBuf<uint32_t> staging, changed;
   nulpa::DBuf<unsigned long long> ctr;
+  nulpa::DBuf<unsigned int> work{2};
   nulpa::Pinned hc{nulpa::dev::kTiers * nulpa::dev::C_COUNT};
   nulpa::Stream stream;
   int sms = 148, vbytes = 4;
@@ -534,7 +576,7 @@ __global__ void k_edge_bounds(const uint64_t* off, uint32_t n, uint32_t parts, u
 }
 }  // namespace
 
-void session_pass(nulpa_session* ss, int pick_less, nulpa_pass_info* info) {
+void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* info) {
   using namespace dev;
   nulpa_graph* g = ss->g;
   cudaStream_t s = ss->stream.s;
@@ -549,6 +591,8 @@ void session_pass(nulpa_session* ss, int pick_less, nulpa_pass_info* info) {
   c.changed = nullptr;
   unsigned long long* other = ss->ctr.p + T_OTHER * C_COUNT;
   c.changed_n = other + C_NCHANGED;
+  c.wake = wake ? 1 : 0;
+  c.work = ss->work.p;
   Prof prof;
   cudaEvent_t e0, e1;
   NULPA_CUDA(cudaEventCreate(&e0));
@@ -565,13 +609,16 @@ void session_pass(nulpa_session* ss, int pick_less, nulpa_pass_info* info) {
     NULPA_CUDA(cudaMemcpyAsync(ss->staging.p, ss->labels, g->n * 4ull, cudaMemcpyDeviceToDevice, s));
     c.lab_in = ss->labels;
     c.lab_out = ss->staging.p;
-    c.changed = ss->changed.p;
+    c.changed = wake ? ss->changed.p : nullptr;
     launches += dispatch_pass<kSync>(*ss->plan, c, ss->ctr.p, ss->vbytes, s, ss->sms, prof);
     k_copy_range<<<grid_for(ss->hi - ss->lo, 256, ss->sms * 8), 256, 0, s>>>(
         ss->staging.p, ss->labels, ss->lo, ss->hi);
-    k_wake_list<<<grid_for(ss->hi - ss->lo, kBlockThreads / 32, ss->sms * 8), kBlockThreads, 0,
-                  s>>>(c.g, ss->flags, ss->changed.p, other + C_NCHANGED, other);
-    launches += 2;
+    ++launches;
+    if (wake) {
+      k_wake_list<<<grid_for(ss->hi - ss->lo, kBlockThreads / 32, ss->sms * 8), kBlockThreads,
+                    0, s>>>(c.g, ss->flags, ss->changed.p, other + C_NCHANGED, other);
+      ++launches;
+    }
     NULPA_CUDA(cudaGetLastError());
   }
   NULPA_CUDA(cudaEventRecord(e1, s));
@@ -790,11 +837,11 @@ int nulpa_session_init(nulpa_session* ss) {
   });
 }
 
-int nulpa_session_pass(nulpa_session* ss, int pick_less, nulpa_pass_info* info) {
+int nulpa_session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* info) {
   return guarded([&] {
     if (!ss) throw Error(NULPA_EINVAL, "null session");
     use_device(ss->g->device);
-    session_pass(ss, pick_less, info);
+    session_pass(ss, pick_less, wake, info);
   });
 }
 

@@ -259,7 +259,7 @@ TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* t) {
   wmax = std::max<uint32_t>(std::min<uint32_t>(wmax, dev::kWarpTabMax), 32u);
   uint32_t bmax = (t && t->block_max_degree) ? t->block_max_degree : uint32_t(dev::kBlockMax);
   bmax = std::max<uint32_t>(std::min<uint32_t>(bmax, dev::kBlockMax), wmax);
-  const uint32_t sched = (t && t->schedule) ? t->schedule : 1u;
+  const uint32_t sched = (t && t->schedule) ? t->schedule : 2u;  // default: scrambled
   return {tmax, wmax, bmax, sched};
 }
 
@@ -295,7 +295,9 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
         {std::max<uint64_t>(tm, 16) + 1, 32},           // T_WARP
         {33, tb.warp_max},                              // T_WTAB
         {uint64_t(tb.warp_max) + 1, tb.block_max},      // T_BLOCK
-        {uint64_t(tb.block_max) + 1, ~0ull}};           // T_HUB
+        {uint64_t(tb.block_max) + 1, dev::kBigMax},      // T_BIG
+        {uint64_t(dev::kBigMax) + 1, dev::kClusterMax},  // T_CLUSTER
+        {uint64_t(dev::kClusterMax) + 1, ~0ull}};        // T_HUB
     uint64_t* d_num = dalloc<uint64_t>(1);
     uint32_t* scratch = dalloc<uint32_t>(uint64_t(span) + 1);
     size_t tbytes = 0;

@@ -27,6 +27,8 @@
 //                             occupied-slot list (packed 64-bit atomicMax), decide, wake
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "device.cuh"
 
 namespace nulpa {
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
     n_e += d;
     if (!apply_move<MODE>(c, i, b.k)) continue;
     ++n_dn;
-    if (MODE == kAsync && c.flags) {
+    if (MODE == kAsync && c.wake) {
 #pragma unroll
       for (int k = 0; k < DMAX; ++k)
         if (k < d) c.flags[nb[k]] = 0;
@@ -173,10 +175,10 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
       ++n_v;
       n_e += d;
       n_dn += ch;
-      if (MODE == kAsync && ch && c.flags) n_w += d;
+      if (MODE == kAsync && ch && c.wake) n_w += d;
     }
     ch = __shfl_sync(kFull, ch, sub * G);
-    if (MODE == kAsync && ch && c.flags && gl < d) c.flags[j] = 0;
+    if (MODE == kAsync && ch && c.wake && gl < d) c.flags[j] = 0;
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
   warp_add_counter(c.ctr, C_PROC_E, n_e);
@@ -274,10 +276,10 @@ __global__ void __launch_bounds__(kBlockThreads) k_wtab(PassCtx c,
       ++n_v;
       n_e += d;
       n_dn += changed;
-      if (MODE == kAsync && changed && c.flags) n_w += d;
+      if (MODE == kAsync && changed && c.wake) n_w += d;
     }
     changed = __shfl_sync(kFull, changed, 0);
-    if (MODE == kAsync && changed && c.flags)
+    if (MODE == kAsync && changed && c.wake)
       for (uint32_t e = lane; e < d; e += 32) c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
@@ -306,14 +308,20 @@ __device__ __forceinline__ Best<V> block_best(Best<V> b, Best<V>* red) {
 
 // ---- tier: CTA per vertex, shared-memory table --------------------------------------
 
-template <int MODE, typename W, bool WEIGHTED>
-__global__ void __launch_bounds__(kBlockThreads) k_block(PassCtx c,
-                                                         const uint32_t* __restrict__ list,
-                                                         uint32_t count) {
+// Table capacity for a row of degree d: load <= 1/2 for the 256-thread tier,
+// <= 3/4 for the 128 KB tiers (always a power of two).
+template <int CAP>
+__device__ __forceinline__ uint32_t table_cap(uint32_t d) {
+  return CAP <= kBlockCap ? pow2_ceil(2 * d) : pow2_ceil(d + d / 3 + 1);
+}
+
+template <int MODE, typename W, bool WEIGHTED, int THREADS, int CAP>
+__global__ void __launch_bounds__(THREADS) k_block(PassCtx c, const uint32_t* __restrict__ list,
+                                                   uint32_t count) {
   using Tab = Table<kPacked<WEIGHTED>, W>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tab tab;
-  tab.bind(smem_raw, kBlockCap);
+  tab.bind(smem_raw, CAP);
   __shared__ Best<VBits<W>> red[32];
   __shared__ int s_flag;
   const uint64_t pol = policy_evict_first();
@@ -323,7 +331,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_block(PassCtx c,
     if (threadIdx.x == 0) s_flag = claim_vertex(c, i) ? 1 : 0;
     const uint64_t lo = __ldg(c.g.off + i);
     const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
-    const uint32_t cap = pow2_ceil(2 * d);
+    const uint32_t cap = table_cap<CAP>(d);
     for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) tab.clear_slot(s);
     __syncthreads();
     if (s_flag) {
@@ -345,15 +353,128 @@ __global__ void __launch_bounds__(kBlockThreads) k_block(PassCtx c,
       ++n_v;
       n_e += d;
       n_dn += s_flag;
-      if (MODE == kAsync && s_flag && c.flags) n_w += d;
+      if (MODE == kAsync && s_flag && c.wake) n_w += d;
     }
     __syncthreads();
     const int changed = s_flag;
-    if (MODE == kAsync && changed && c.flags)
+    if (MODE == kAsync && changed && c.wake)
       for (uint32_t e = threadIdx.x; e < d; e += blockDim.x)
         c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
     __syncthreads();
   }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+  warp_add_counter(c.ctr, C_FAIL, fails);
+}
+
+// ---- tier: 8-CTA cluster per vertex, table distributed over DSMEM --------------------
+// A thread-block cluster owns one hub at a time (vertices are pulled from a
+// work counter). The hub's table is split over the cluster's shared memories:
+// slot owner = a second hash of the label, so every label lives in exactly one
+// CTA; inserts go to the owner's shared memory through DSMEM atomics. Each CTA
+// streams 1/8 of the row, scans its own partition, and rank 0 merges the eight
+// partial argmaxes. No global-memory table, no DRAM traffic for aggregation.
+__device__ __forceinline__ uint32_t owner_of(uint32_t key) {
+  return ((key ^ (key >> 16)) * 0x7FEB352Du) >> (32 - 3);  // 3 = log2(kClusterSize)
+}
+
+template <int MODE, typename W, bool WEIGHTED>
+__global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThreads)
+    k_cluster(PassCtx c,
+                                                         const uint32_t* __restrict__ list,
+                                                         uint32_t count) {
+  namespace cg = cooperative_groups;
+  static_assert(kClusterSize == 8, "owner_of assumes 8 ranks");
+  using Tab = Table<kPacked<WEIGHTED>, W>;
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank = cl.block_rank();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Tab local;
+  local.bind(smem_raw, kClusterCap);
+  __shared__ uint32_t s_item;
+  __shared__ int s_flag, s_changed;
+  __shared__ Best<VBits<W>> red[32];
+  __shared__ Best<VBits<W>> part[kClusterSize];
+  const uint64_t pol = policy_evict_first();
+  const int lane = threadIdx.x & 31;
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
+  for (;;) {
+    if (rank == 0 && threadIdx.x == 0) s_item = atomicAdd(c.work, 1u);
+    cl.sync();                                                   // (A) item published
+    const uint32_t t = *cl.map_shared_rank(&s_item, 0);
+    if (t >= count) break;  // uniform over the cluster; the final sync below keeps rank 0's
+                            // shared memory alive until every rank has read s_item
+    const uint32_t i = __ldg(list + t);
+    if (rank == 0 && threadIdx.x == 0) s_flag = claim_vertex(c, i) ? 1 : 0;
+    const uint64_t lo = __ldg(c.g.off + i);
+    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+    const uint32_t cap = pow2_ceil(d + d / 3 + 1) / kClusterSize;  // per-rank partition
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) local.clear_slot(s);
+    cl.sync();                                                   // (B) flag + clean tables
+    if (*cl.map_shared_rank(&s_flag, 0)) continue;
+    // Stream this rank's slice of the row; warp dedup; insert at the owner rank.
+    const uint32_t e0 = static_cast<uint32_t>((uint64_t(d) * rank) / kClusterSize);
+    const uint32_t e1 = static_cast<uint32_t>((uint64_t(d) * (rank + 1)) / kClusterSize);
+    constexpr int U = 4;
+    for (uint32_t base = e0; base < e1; base += blockDim.x * U) {
+      uint32_t j[U], lab[U];
+      W w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t e = base + u * blockDim.x + threadIdx.x;
+        j[u] = e < e1 ? ld_stream(c.g.tgt + lo + e, pol) : i;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t e = base + u * blockDim.x + threadIdx.x;
+        const bool valid = e < e1 && j[u] != i;
+        lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+        w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned peers = __match_any_sync(kFull, lab[u]);
+        W s;
+        if constexpr (WEIGHTED)
+          s = peer_sum(w[u], peers);
+        else
+          s = static_cast<W>(__popc(peers));
+        if (lab[u] != kEmpty && (__ffs(peers) - 1) == lane) {
+          Tab remote;
+          remote.bind(cl.map_shared_rank(smem_raw, owner_of(lab[u])), kClusterCap);
+          uint32_t slot;
+          if (!remote.add(cap, c.strategy, lab[u], s, &slot)) ++fails;
+        }
+      }
+    }
+    cl.sync();                                                   // (C) all inserts landed
+    Best<VBits<W>> b{VBits<W>(0), kEmpty};
+    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
+      uint32_t k;
+      VBits<W> v;
+      local.read(s, k, v);
+      best_merge(b, v, k);
+    }
+    b = block_best(b, red);
+    if (threadIdx.x == 0) *cl.map_shared_rank(&part[rank], 0) = b;
+    cl.sync();                                                   // (D) partial argmaxes at rank 0
+    if (rank == 0 && threadIdx.x == 0) {
+      Best<VBits<W>> f{VBits<W>(0), kEmpty};
+      for (int r = 0; r < kClusterSize; ++r) best_merge(f, part[r].v, part[r].k);
+      s_changed = apply_move<MODE>(c, i, f.k) ? 1 : 0;
+      ++n_v;
+      n_e += d;
+      n_dn += s_changed;
+      if (MODE == kAsync && s_changed && c.wake) n_w += d;
+    }
+    cl.sync();                                                   // (E) decision visible
+    if (MODE == kAsync && c.wake && *cl.map_shared_rank(&s_changed, 0))
+      for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+        c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
+  }
+  cl.sync();
   warp_add_counter(c.ctr, C_PROC_V, n_v);
   warp_add_counter(c.ctr, C_PROC_E, n_e);
   warp_add_counter(c.ctr, C_DN, n_dn);

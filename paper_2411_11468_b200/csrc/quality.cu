@@ -173,7 +173,7 @@ double modularity_device(nulpa_graph* g, const uint32_t* lab, cudaStream_t s) {
   if (p->count[T_THREAD])
     k_mod_thread<<<std::min<uint32_t>((p->count[T_THREAD] + 255) / 256, sms * 8), 256, 0, s>>>(
         dg, lab, p->list[T_THREAD], p->count[T_THREAD], sigma, big);
-  for (int t = T_HALF; t <= T_BLOCK; ++t)
+  for (int t = T_HALF; t <= T_CLUSTER; ++t)
     if (p->count[t])
       k_mod_warp<<<std::min<uint32_t>((p->count[t] + 7) / 8, sms * 8), 256, 0, s>>>(
           dg, lab, p->list[t], p->count[t], sigma, big);

@@ -74,9 +74,10 @@ class DeviceRangeEngine:
     def init(self):
         _capi.check(_capi.lib().nulpa_session_init(self._h))
 
-    def pass_(self, pick_less: bool) -> dict:
+    def pass_(self, pick_less: bool, wake: bool = True) -> dict:
         info = _capi.nulpa_pass_info()
-        _capi.check(_capi.lib().nulpa_session_pass(self._h, int(pick_less), C.byref(info)))
+        _capi.check(_capi.lib().nulpa_session_pass(self._h, int(pick_less), int(wake),
+                                                   C.byref(info)))
         return {"changed": info.changed, "processed_vertices": info.processed_vertices,
                 "processed_edges": info.processed_edges, "wake_edges": info.wake_edges,
                 "device_ms": info.device_ms, "kernel_launches": info.kernel_launches}
@@ -147,13 +148,19 @@ def run_partitioned(engine, cfg: LpaConfig, rank: int, world: int, exchange: Exc
     for it in range(cfg.max_iterations):
         pick_less = cfg.pl_period > 0 and it % cfg.pl_period == 0
         was_pl = it > 0 and cfg.pl_period > 0 and (it - 1) % cfg.pl_period == 0
+        this_reset = it == 0 or not cfg.prune or (was_pl and not pick_less)
         if not cfg.prune or (was_pl and not pick_less):
             engine.flags.zero_()
+        # wake-ups are dead stores when the next pass resets every flag and nothing in
+        # this pass can observe them (same rule as run_lpa in engine.cu)
+        next_pl = cfg.pl_period > 0 and (it + 1) % cfg.pl_period == 0
+        next_reset = it + 1 >= cfg.max_iterations or not cfg.prune or (pick_less and not next_pl)
+        wake = not (next_reset and (this_reset or cfg.exec == ExecMode.Synchronous))
         # remote entries: "processed", so only real wake-ups survive the MIN-reduce
         engine.flags[:lo] = 1
         engine.flags[hi:] = 1
         engine.sync()
-        info = engine.pass_(pick_less)
+        info = engine.pass_(pick_less, wake)
         t0 = time.perf_counter()
         exchange.labels_and_flags(engine.labels, engine.flags)
         dn, pe, kl = exchange.sum([info["changed"], info["processed_edges"],

@@ -37,7 +37,7 @@ class PortRangeEngine:
         deg = np.diff(self.off.astype(np.int64))
         self.flags.copy_(torch.from_numpy((deg == 0).astype(np.uint8)))
 
-    def pass_(self, pick_less):
+    def pass_(self, pick_less, wake=True):
         lab = self.labels.numpy().view(np.uint32)
         flg = self.flags.numpy()
         cand, _ = O.port_sync_step(self.pg, lab, pick_less)  # from the frozen snapshot
@@ -47,7 +47,7 @@ class PortRangeEngine:
         flg[processed] = 1
         changed = np.flatnonzero(processed & (cand != lab))
         lab[changed] = cand[changed]
-        for v in changed:  # wake after the joint application
+        for v in changed if wake else ():  # wake after the joint application
             flg[self.tgt[self.off[v]:self.off[v + 1]]] = 0
         return {"changed": int(changed.size), "processed_vertices": int(processed.sum()),
                 "processed_edges": 0, "wake_edges": 0, "device_ms": 0.0, "kernel_launches": 0}
@@ -107,3 +107,42 @@ def test_edge_balanced_bounds():
         for p in range(1, P):
             assert int(off[b[p]]) >= m2 * p // P
             assert b[p] == 0 or int(off[b[p] - 1]) < m2 * p // P
+
+
+# ---- the same driver over the real CUDA session (2 processes sharing one GPU) ------------
+
+
+def _gpu_worker(rank, world, port, scale, out):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    from paper_2411_11468_b200 import _capi
+    from paper_2411_11468_b200 import labelprop as lp
+    from paper_2411_11468_b200.dist import DeviceRangeEngine
+    import ctypes as C
+    dg = lp.DeviceGraph.rmat(scale, 16, 5)
+    b = (C.c_uint32 * (world + 1))()
+    _capi.check(_capi.lib().nulpa_graph_edge_ranges(dg._h, world, b))
+    bounds = list(b)
+    cfg = LpaConfig(exec=ExecMode.Synchronous)
+    eng = DeviceRangeEngine(dg, cfg, bounds[rank], bounds[rank + 1])
+    st = run_partitioned(eng, cfg, rank, world, Exchange(bounds, staged=True), dg.n)
+    out[rank] = (eng.labels.cpu().numpy().view(np.uint32).copy(), st.delta_n_per_iter, bounds)
+    eng.free()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_partitioned_cuda_sessions_equal_single_gpu_sync():
+    from paper_2411_11468_b200 import labelprop as lp
+    world, scale = 2, 14
+    dg = lp.DeviceGraph.rmat(scale, 16, 5)
+    want = dg.lpa(LpaConfig(exec=ExecMode.Synchronous))
+    dg.free()
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_gpu_worker, args=(world, _free_port(), scale, out), nprocs=world, join=True)
+    for r in range(world):
+        labels, dn, bounds = out[r]
+        assert 0 < bounds[1] < bounds[2]
+        assert np.array_equal(labels, want.labels)
+        assert dn == want.stats.delta_n_per_iter
