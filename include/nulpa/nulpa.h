@@ -92,7 +92,7 @@ typedef struct nulpa_tuning {
                                  order), 2 scrambled (hashed) order. Any order is a valid
                                  asynchronous schedule; Synchronous/Sequential results do
                                  not depend on it. */
-  uint32_t reserved[1];
+  uint32_t no_identity_first; /* 1: disable the table-free first pass from identity labels */
 } nulpa_tuning;
 
 #define NULPA_TIERS 9 /* 0 thread, 1 half-warp, 2 warp, 3 warp+smem table, 4 CTA, 5 1024-thread CTA,

@@ -311,6 +311,10 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
   NULPA_CUDA(cudaEventRecord(ev0, s));
 
   const Graph dg{g->offsets, g->targets, g->weights, n};
+  // Table-free first pass from identity labels (k_first_pass): unit weights and
+  // strictly ascending rows make every neighbour label unique.
+  const bool identity_first =
+      g->rows_simple && g->weights == nullptr && !(tuning && tuning->no_identity_first);
   int iterations = 0, pl_iterations = 0;
   bool converged = false;
   uint64_t cc_reverts = 0, tot_v = 0, tot_e = 0, tot_w = 0, launches = 0;
@@ -350,7 +354,31 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     c.changed_n = ctr_other + C_NCHANGED;
     c.wake = wake ? 1 : 0;
     c.work = work.p;
-    if (o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
+    if (iter == 0 && identity_first && o.exec != NULPA_EXEC_SEQUENTIAL) {
+      // Labels are still the identity: the table-free first pass (k_first_pass).
+      c.lab_in = cur;
+      c.lab_out = o.exec == NULPA_EXEC_SYNCHRONOUS ? nxt : cur;
+      c.ctr = ctr.p + T_THREAD * C_COUNT;
+      c.changed = (o.exec == NULPA_EXEC_SYNCHRONOUS && wake) ? changed.p : nullptr;
+      if (o.exec == NULPA_EXEC_SYNCHRONOUS)
+        NULPA_CUDA(cudaMemcpyAsync(nxt, cur, n * 4ull, cudaMemcpyDeviceToDevice, s));
+      prof.begin(T_THREAD, s);
+      if (o.exec == NULPA_EXEC_SYNCHRONOUS)
+        k_first_pass<kSync><<<grid_for(n, 256, sms * 8), 256, 0, s>>>(c, 0, n);
+      else
+        k_first_pass<kAsync><<<grid_for(n, 256, sms * 8), 256, 0, s>>>(c, 0, n);
+      prof.end(T_THREAD, s);
+      ++launches;
+      NULPA_CUDA(cudaGetLastError());
+      if (o.exec == NULPA_EXEC_SYNCHRONOUS) {
+        if (wake) {
+          k_wake_list<<<grid_for(n, kBlockThreads / 32, sms * 8), kBlockThreads, 0, s>>>(
+              dg, flags.p, changed.p, ctr_other + C_NCHANGED, ctr_other);
+          ++launches;
+        }
+        std::swap(cur, nxt);
+      }
+    } else if (o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
       c.lab_in = cur;
       c.lab_out = cur;
       launches += dispatch_pass<kAsync>(*p, c, ctr.p, vbytes, s, sms, prof);
@@ -541,6 +569,8 @@ struct nulpa_session {
   nulpa::Pinned hc{nulpa::dev::kTiers * nulpa::dev::C_COUNT};
   nulpa::Stream stream;
   int sms = 148, vbytes = 4;
+  bool fresh = false;           // labels are the identity (after nulpa_session_init)
+  bool identity_first = false;  // graph allows the table-free first pass
   ~nulpa_session() { delete plan; }
 };
 
@@ -599,7 +629,16 @@ void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* i
   NULPA_CUDA(cudaEventCreate(&e1));
   NULPA_CUDA(cudaEventRecord(e0, s));
   uint64_t launches = 0;
-  if (ss->o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
+  const bool first = ss->fresh && ss->identity_first;
+  ss->fresh = false;
+  if (first && ss->o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
+    c.lab_in = ss->labels;
+    c.lab_out = ss->labels;
+    c.ctr = ss->ctr.p + T_THREAD * C_COUNT;
+    k_first_pass<kAsync><<<grid_for(ss->hi - ss->lo, 256, ss->sms * 8), 256, 0, s>>>(c, ss->lo,
+                                                                                   ss->hi);
+    ++launches;
+  } else if (ss->o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
     c.lab_in = ss->labels;
     c.lab_out = ss->labels;
     launches += dispatch_pass<kAsync>(*ss->plan, c, ss->ctr.p, ss->vbytes, s, ss->sms, prof);
@@ -610,7 +649,14 @@ void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* i
     c.lab_in = ss->labels;
     c.lab_out = ss->staging.p;
     c.changed = wake ? ss->changed.p : nullptr;
-    launches += dispatch_pass<kSync>(*ss->plan, c, ss->ctr.p, ss->vbytes, s, ss->sms, prof);
+    if (first) {
+      c.ctr = ss->ctr.p + T_THREAD * C_COUNT;
+      k_first_pass<kSync><<<grid_for(ss->hi - ss->lo, 256, ss->sms * 8), 256, 0, s>>>(c, ss->lo,
+                                                                                    ss->hi);
+      ++launches;
+    } else {
+      launches += dispatch_pass<kSync>(*ss->plan, c, ss->ctr.p, ss->vbytes, s, ss->sms, prof);
+    }
     k_copy_range<<<grid_for(ss->hi - ss->lo, 256, ss->sms * 8), 256, 0, s>>>(
         ss->staging.p, ss->labels, ss->lo, ss->hi);
     ++launches;
@@ -811,6 +857,8 @@ int nulpa_session_create(nulpa_graph* g, const nulpa_opts* opts, const nulpa_tun
       ss->flags = flags_dev;
       ss->sms = sm_count();
       ss->vbytes = opts->precision == 64 ? 8 : 4;
+      ss->identity_first =
+          g->rows_simple && g->weights == nullptr && !(tuning && tuning->no_identity_first);
       ss->plan = build_plan(g, resolve_tiers(opts->switch_degree, tuning), ss->vbytes,
                             ss->stream.s, v_begin, v_end);
       ss->ctr = DBuf<unsigned long long>(dev::kTiers * dev::C_COUNT);
@@ -834,6 +882,7 @@ int nulpa_session_init(nulpa_session* ss) {
         ss->labels, ss->flags, ss->g->offsets, ss->g->n);
     NULPA_CUDA(cudaGetLastError());
     NULPA_CUDA(cudaStreamSynchronize(ss->stream.s));
+    ss->fresh = true;
   });
 }
 

@@ -64,6 +64,26 @@ __global__ void k_check_offsets(const uint64_t* off, uint32_t n, uint64_t m2, un
   if (blockIdx.x == 0 && threadIdx.x == 0 && (off[0] != 0 || off[n] != m2)) atomicOr(bad, 2u);
 }
 
+// Rows are "simple" when targets strictly ascend inside every row: count all
+// descents tgt[e] >= tgt[e+1] and the ones that sit exactly at a row start.
+__global__ void k_count_descents(const uint32_t* tgt, uint64_t m2, unsigned long long* cnt) {
+  unsigned long long c = 0;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e + 1 < m2;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    c += tgt[e] >= tgt[e + 1];
+  if (c) atomicAdd(cnt, c);
+}
+
+__global__ void k_count_boundary_descents(const uint64_t* off, const uint32_t* tgt, uint32_t n,
+                                          unsigned long long* cnt) {
+  unsigned long long c = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t lo = off[i];
+    if (lo > 0 && off[i + 1] > lo) c += tgt[lo - 1] >= tgt[lo];
+  }
+  if (c) atomicAdd(cnt, c);
+}
+
 __global__ void k_check_targets(const uint32_t* tgt, uint64_t m2, uint32_t n, unsigned* bad) {
   for (uint64_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m2;
        e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -174,6 +194,20 @@ void finalize_graph(nulpa_graph* g, cudaStream_t s) {
     }
   }
   g->total_2m = total;
+  // Strictly ascending rows (no duplicate targets) enable the identity first pass.
+  g->rows_simple = true;
+  if (g->m2 > 1) {
+    unsigned long long* d_c = dalloc<unsigned long long>(2);
+    NULPA_CUDA(cudaMemsetAsync(d_c, 0, 16, s));
+    k_count_descents<<<2048, 256, 0, s>>>(g->targets, g->m2, d_c);
+    k_count_boundary_descents<<<1024, 256, 0, s>>>(g->offsets, g->targets, n, d_c + 1);
+    NULPA_CUDA(cudaGetLastError());
+    unsigned long long h[2] = {0, 0};
+    NULPA_CUDA(cudaMemcpyAsync(h, d_c, 16, cudaMemcpyDeviceToHost, s));
+    NULPA_CUDA(cudaStreamSynchronize(s));
+    dfree(d_c);
+    g->rows_simple = h[0] == h[1];
+  }
   dfree(d_bad);
   dfree(d_max);
   dfree(d_sum);

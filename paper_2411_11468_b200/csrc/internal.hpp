@@ -74,6 +74,7 @@ struct nulpa_graph {
   bool owns = false;
   uint32_t max_degree = 0;
   double total_2m = 0.0;  // sum of stored weights (graph.cpp:170-171)
+  bool rows_simple = false;  // every row strictly ascending (no duplicate targets)
   nulpa::Plan* plan = nullptr;  // cached tiering (plan.hpp)
 };
 

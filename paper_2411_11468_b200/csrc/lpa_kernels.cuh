@@ -482,6 +482,45 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
   warp_add_counter(c.ctr, C_FAIL, fails);
 }
 
+// ---- first pass from identity labels -------------------------------------------------
+// run_engine starts from labels[i] = i (lpa.cpp:250). On a graph whose rows hold
+// distinct, ascending targets with unit weights, every neighbour label then
+// occurs exactly once, so scan_candidate's argmax (all counts 1, ties to the
+// smaller key) is simply the smallest neighbour id other than i: the first or
+// second entry of the sorted row. The pass needs no table at all. Synchronous
+// mode gets the reference's exact first pass; ParallelAsync gets the legal
+// schedule in which every first-pass read precedes every write.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_first_pass(PassCtx c, uint32_t v_lo, uint32_t v_hi) {
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
+  const uint32_t bound = v_lo + ((v_hi - v_lo + 31u) & ~31u);
+  for (uint32_t i = v_lo + blockIdx.x * blockDim.x + threadIdx.x; i < bound;
+       i += gridDim.x * blockDim.x) {
+    if (i >= v_hi) continue;
+    if (claim_vertex(c, i)) continue;
+    const uint64_t lo = __ldg(c.g.off + i);
+    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+    if (d == 0) continue;
+    uint32_t cand = __ldg(c.g.tgt + lo);
+    if (cand == i) cand = d > 1 ? __ldg(c.g.tgt + lo + 1) : kEmpty;  // self-loop skipped
+    ++n_v;
+    n_e += d > 1 ? 2 : 1;
+    const bool allowed = cand != kEmpty && (c.pick_less ? cand < i : cand != i);
+    if (!allowed) continue;
+    c.lab_out[i] = cand;
+    ++n_dn;
+    if (MODE == kSync && c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
+    if (MODE == kAsync && c.wake) {
+      for (uint32_t e = 0; e < d; ++e) c.flags[__ldg(c.g.tgt + lo + e)] = 0;
+      n_w += d;
+    }
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+}
+
 // ---- tier: hubs, global tables -------------------------------------------------------
 
 template <int MODE>

@@ -102,6 +102,7 @@ class Tuning:
     block_max_degree: int = 0
     schedule: int = 0  # 0 default, 1 ascending id, 2 scrambled
     profile: bool = False
+    identity_first: bool = True  # table-free first pass from identity labels
 
     def to_c(self) -> _capi.nulpa_tuning:
         t = _capi.nulpa_tuning()
@@ -110,6 +111,7 @@ class Tuning:
         t.block_max_degree = self.block_max_degree
         t.schedule = self.schedule
         t.profile = 1 if self.profile else 0
+        t.no_identity_first = 0 if self.identity_first else 1
         return t
 
 
