@@ -354,7 +354,11 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     c.changed_n = ctr_other + C_NCHANGED;
     c.wake = wake ? 1 : 0;
     c.work = work.p;
-    if (iter == 0 && identity_first && o.exec != NULPA_EXEC_SEQUENTIAL) {
+    // Synchronous only: there the identity first pass is exactly the reference's.
+    // (Under ParallelAsync it is a legal schedule too, but it replaces the in-place
+    // first pass, whose early label flooding converges R-MAT one pass sooner and
+    // which the reference's low-tier-first KATs rely on, test_lpa.cpp:256-267.)
+    if (iter == 0 && identity_first && o.exec == NULPA_EXEC_SYNCHRONOUS) {
       // Labels are still the identity: the table-free first pass (k_first_pass).
       c.lab_in = cur;
       c.lab_out = o.exec == NULPA_EXEC_SYNCHRONOUS ? nxt : cur;
@@ -629,7 +633,8 @@ void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* i
   NULPA_CUDA(cudaEventCreate(&e1));
   NULPA_CUDA(cudaEventRecord(e0, s));
   uint64_t launches = 0;
-  const bool first = ss->fresh && ss->identity_first;
+  const bool first =
+      ss->fresh && ss->identity_first && ss->o.exec == NULPA_EXEC_SYNCHRONOUS;  // see run_lpa
   ss->fresh = false;
   if (first && ss->o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
     c.lab_in = ss->labels;
