@@ -62,17 +62,18 @@ template <int MODE, typename W, bool WEIGHTED>
 int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t s, int sms,
                 Prof& prof) {
   using Tab = Table<kPacked<WEIGHTED>, W>;
-  constexpr size_t wtab_smem = (kBlockThreads / 32) * kWarpTabCap * Tab::kSlotBytes;
-  constexpr size_t block_smem = kBlockCap * Tab::kSlotBytes;
-  constexpr size_t big_smem = kBigCap * Tab::kSlotBytes;
-  constexpr size_t cluster_smem = kClusterCap * Tab::kSlotBytes;
+  constexpr size_t wtab_smem = (kBlockThreads / 32) * wtab_bytes<Tab>();
+  constexpr size_t block_smem = block_bytes<Tab, kBlockCap, kBlockMax>();
+  constexpr size_t big_smem = block_bytes<Tab, kBigCap, kBigMax>();
+  constexpr size_t cluster_smem = cluster_bytes<Tab>();
+  constexpr size_t hub_smem = kBlockCap * Tab::kSlotBytes;
   static bool init = false;
   if (!init) {
     allow_smem(k_wtab<MODE, W, WEIGHTED>, wtab_smem);
-    allow_smem(k_block<MODE, W, WEIGHTED, kBlockThreads, kBlockCap>, block_smem);
-    allow_smem(k_block<MODE, W, WEIGHTED, kBigThreads, kBigCap>, big_smem);
+    allow_smem(k_block<MODE, W, WEIGHTED, kBlockThreads, kBlockCap, kBlockMax>, block_smem);
+    allow_smem(k_block<MODE, W, WEIGHTED, kBigThreads, kBigCap, kBigMax>, big_smem);
     allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
-    allow_smem(k_hub_accum<MODE, W, WEIGHTED>, block_smem);
+    allow_smem(k_hub_accum<MODE, W, WEIGHTED>, hub_smem);
     init = true;
   }
   int launches = 0;
@@ -114,7 +115,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   }
   if (p.count[T_BLOCK]) {
     tier(T_BLOCK);
-    k_block<MODE, W, WEIGHTED, kBlockThreads, kBlockCap>
+    k_block<MODE, W, WEIGHTED, kBlockThreads, kBlockCap, kBlockMax>
         <<<grid_for(p.count[T_BLOCK], 1, sms * 6), kBlockThreads, block_smem, s>>>(
             c, p.list[T_BLOCK], p.count[T_BLOCK]);
     prof.end(T_BLOCK, s);
@@ -122,7 +123,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   }
   if (p.count[T_BIG]) {
     tier(T_BIG);
-    k_block<MODE, W, WEIGHTED, kBigThreads, kBigCap>
+    k_block<MODE, W, WEIGHTED, kBigThreads, kBigCap, kBigMax>
         <<<grid_for(p.count[T_BIG], 1, sms), kBigThreads, big_smem, s>>>(c, p.list[T_BIG],
                                                                           p.count[T_BIG]);
     prof.end(T_BIG, s);
@@ -144,7 +145,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     const unsigned gi = grid_for(p.n_items, 1, sms * 6);
     const unsigned gh = grid_for(p.n_hubs, 256, 1024);
     k_hub_select<MODE><<<gh, 256, 0, s>>>(c, h);
-    k_hub_accum<MODE, W, WEIGHTED><<<gi, kBlockThreads, block_smem, s>>>(c, h);
+    k_hub_accum<MODE, W, WEIGHTED><<<gi, kBlockThreads, hub_smem, s>>>(c, h);
     k_hub_argmax<W, WEIGHTED><<<gi, kBlockThreads, 0, s>>>(h);
     launches += 3;
     if constexpr (sizeof(VBits<W>) == 8) {

@@ -187,13 +187,30 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
 }
 
 // ---- cooperative gather + insert -------------------------------------------------
+// Team tables are kept EMPTY between vertices: every newly claimed slot is
+// appended to an occupancy list (one shared atomic per warp), and the argmax
+// sweep reads and resets only the occupied slots. Per-vertex table work is
+// therefore O(distinct labels), not O(capacity).
+
+// Append the slots claimed in this warp round to the occupancy list.
+__device__ __forceinline__ void occ_append(bool claimed, uint32_t slot, uint16_t* occ,
+                                           unsigned* occ_n) {
+  const unsigned m = __ballot_sync(kFull, claimed);
+  if (!m) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  unsigned base = 0;
+  if (lane == leader) base = atomicAdd(occ_n, static_cast<unsigned>(__popc(m)));
+  base = __shfl_sync(kFull, base, leader);
+  if (claimed) occ[base + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(slot);
+}
 
 // One round of a team gather: each lane holds one edge (or none), dedups its
 // label against the warp with __match_any_sync, and the lowest lane of each
 // label group adds the group's weight to the table. All 32 lanes call it.
 template <typename W, bool WEIGHTED, typename Tab>
 __device__ __forceinline__ void gather_insert(const PassCtx& c, uint32_t lab, W w, Tab& tab,
-                                              uint32_t cap, unsigned long long& fails) {
+                                              uint32_t cap, uint16_t* occ, unsigned* occ_n,
+                                              unsigned long long& fails) {
   const unsigned peers = __match_any_sync(kFull, lab);
   W s;
   if constexpr (WEIGHTED)
@@ -201,10 +218,13 @@ __device__ __forceinline__ void gather_insert(const PassCtx& c, uint32_t lab, W 
   else
     s = static_cast<W>(__popc(peers));
   const int lane = threadIdx.x & 31;
+  int r = -1;
+  uint32_t slot = 0;
   if (lab != kEmpty && (__ffs(peers) - 1) == lane) {
-    uint32_t slot;
-    if (!tab.add(cap, c.strategy, lab, s, &slot)) ++fails;
+    r = tab.add(cap, c.strategy, lab, s, &slot);
+    if (r == 0) ++fails;
   }
+  if (occ) occ_append(r == 2, slot, occ, occ_n);
 }
 
 // Gather edges [e0, e1) of vertex i (U edges per thread in flight) into `tab`.
@@ -213,6 +233,7 @@ template <int MODE, typename W, bool WEIGHTED, typename Tab, int U = 4>
 __device__ __forceinline__ void team_gather(const PassCtx& c, uint32_t i, uint64_t lo,
                                             uint32_t e0, uint32_t e1, Tab& tab, uint32_t cap,
                                             uint32_t tid, uint32_t T, uint64_t pol,
+                                            uint16_t* occ, unsigned* occ_n,
                                             unsigned long long& fails) {
   for (uint32_t base = e0; base < e1; base += T * U) {
     uint32_t j[U], lab[U];
@@ -230,11 +251,34 @@ __device__ __forceinline__ void team_gather(const PassCtx& c, uint32_t i, uint64
       w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) gather_insert<W, WEIGHTED>(c, lab[u], w[u], tab, cap, fails);
+    for (int u = 0; u < U; ++u)
+      gather_insert<W, WEIGHTED>(c, lab[u], w[u], tab, cap, occ, occ_n, fails);
   }
 }
 
+// Argmax over the occupied slots [tid, n_occ) step T; resets them as it goes.
+template <typename W, typename Tab>
+__device__ __forceinline__ Best<VBits<W>> occ_argmax_reset(Tab& tab, const uint16_t* occ,
+                                                          unsigned n_occ, uint32_t tid,
+                                                          uint32_t T) {
+  Best<VBits<W>> b{VBits<W>(0), kEmpty};
+  for (uint32_t p = tid; p < n_occ; p += T) {
+    const uint32_t s = occ[p];
+    uint32_t k;
+    VBits<W> v;
+    tab.read(s, k, v);
+    best_merge(b, v, k);
+    tab.clear_slot(s);
+  }
+  return b;
+}
+
 // ---- tier: warp per vertex, per-warp shared-memory table -----------------------------
+
+template <typename Tab>
+constexpr size_t wtab_bytes() {
+  return size_t(kWarpTabCap) * Tab::kSlotBytes + size_t(kWarpTabMax) * sizeof(uint16_t);
+}
 
 template <int MODE, typename W, bool WEIGHTED>
 __global__ void __launch_bounds__(kBlockThreads) k_wtab(PassCtx c,
@@ -242,32 +286,34 @@ __global__ void __launch_bounds__(kBlockThreads) k_wtab(PassCtx c,
                                                         uint32_t count) {
   using Tab = Table<kPacked<WEIGHTED>, W>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ unsigned s_occ_n[kBlockThreads / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kWarps = kBlockThreads / 32;
+  unsigned char* base = smem_raw + size_t(warp) * wtab_bytes<Tab>();
   Tab tab;
-  tab.bind(smem_raw + size_t(warp) * kWarpTabCap * Tab::kSlotBytes, kWarpTabCap);
+  tab.bind(base, kWarpTabCap);
+  uint16_t* occ = reinterpret_cast<uint16_t*>(base + size_t(kWarpTabCap) * Tab::kSlotBytes);
+  unsigned* occ_n = s_occ_n + warp;
+  for (uint32_t s = lane; s < kWarpTabCap; s += 32) tab.clear_slot(s);  // once per lifetime
+  __syncwarp();
   const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
   const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   for (uint32_t t = gw; t < count; t += nw) {
     const uint32_t i = __ldg(list + t);
     int skip = 0;
-    if (lane == 0) skip = claim_vertex(c, i) ? 1 : 0;
+    if (lane == 0) {
+      skip = claim_vertex(c, i) ? 1 : 0;
+      *occ_n = 0;
+    }
     if (__shfl_sync(kFull, skip, 0)) continue;
     const uint64_t lo = __ldg(c.g.off + i);
     const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
     const uint32_t cap = pow2_ceil(2 * d);
-    for (uint32_t s = lane; s < cap; s += 32) tab.clear_slot(s);
     __syncwarp();
-    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, lane, 32, pol, fails);
+    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, lane, 32, pol, occ, occ_n, fails);
     __syncwarp();
-    Best<VBits<W>> b{VBits<W>(0), kEmpty};
-    for (uint32_t s = lane; s < cap; s += 32) {
-      uint32_t k;
-      VBits<W> v;
-      tab.read(s, k, v);
-      best_merge(b, v, k);
-    }
+    Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, *occ_n, lane, 32);
     b = warp_best(b);
     __syncwarp();
     int changed = 0;
@@ -315,38 +361,43 @@ __device__ __forceinline__ uint32_t table_cap(uint32_t d) {
   return CAP <= kBlockCap ? pow2_ceil(2 * d) : pow2_ceil(d + d / 3 + 1);
 }
 
-template <int MODE, typename W, bool WEIGHTED, int THREADS, int CAP>
+template <typename Tab, int CAP, int MAXD>
+constexpr size_t block_bytes() {
+  return size_t(CAP) * Tab::kSlotBytes + size_t(MAXD) * sizeof(uint16_t);
+}
+
+template <int MODE, typename W, bool WEIGHTED, int THREADS, int CAP, int MAXD>
 __global__ void __launch_bounds__(THREADS) k_block(PassCtx c, const uint32_t* __restrict__ list,
                                                    uint32_t count) {
   using Tab = Table<kPacked<WEIGHTED>, W>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tab tab;
   tab.bind(smem_raw, CAP);
+  uint16_t* occ = reinterpret_cast<uint16_t*>(smem_raw + size_t(CAP) * Tab::kSlotBytes);
   __shared__ Best<VBits<W>> red[32];
   __shared__ int s_flag;
+  __shared__ unsigned s_occ_n;
+  for (uint32_t s = threadIdx.x; s < CAP; s += THREADS) tab.clear_slot(s);  // once
   const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
   for (uint32_t t = blockIdx.x; t < count; t += gridDim.x) {
     const uint32_t i = __ldg(list + t);
-    if (threadIdx.x == 0) s_flag = claim_vertex(c, i) ? 1 : 0;
+    if (threadIdx.x == 0) {
+      s_flag = claim_vertex(c, i) ? 1 : 0;
+      s_occ_n = 0;
+    }
     const uint64_t lo = __ldg(c.g.off + i);
     const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
     const uint32_t cap = table_cap<CAP>(d);
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) tab.clear_slot(s);
     __syncthreads();
     if (s_flag) {
       __syncthreads();  // s_flag is rewritten by the next iteration
       continue;
     }
-    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, threadIdx.x, blockDim.x, pol, fails);
+    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, threadIdx.x, THREADS, pol, occ,
+                                   &s_occ_n, fails);
     __syncthreads();
-    Best<VBits<W>> b{VBits<W>(0), kEmpty};
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-      uint32_t k;
-      VBits<W> v;
-      tab.read(s, k, v);
-      best_merge(b, v, k);
-    }
+    Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n, threadIdx.x, THREADS);
     b = block_best(b, red);
     if (threadIdx.x == 0) {
       s_flag = apply_move<MODE>(c, i, b.k) ? 1 : 0;
@@ -358,7 +409,7 @@ __global__ void __launch_bounds__(THREADS) k_block(PassCtx c, const uint32_t* __
     __syncthreads();
     const int changed = s_flag;
     if (MODE == kAsync && changed && c.wake)
-      for (uint32_t e = threadIdx.x; e < d; e += blockDim.x)
+      for (uint32_t e = threadIdx.x; e < d; e += THREADS)
         c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
     __syncthreads();
   }
@@ -373,18 +424,22 @@ __global__ void __launch_bounds__(THREADS) k_block(PassCtx c, const uint32_t* __
 // A thread-block cluster owns one hub at a time (vertices are pulled from a
 // work counter). The hub's table is split over the cluster's shared memories:
 // slot owner = a second hash of the label, so every label lives in exactly one
-// CTA; inserts go to the owner's shared memory through DSMEM atomics. Each CTA
-// streams 1/8 of the row, scans its own partition, and rank 0 merges the eight
-// partial argmaxes. No global-memory table, no DRAM traffic for aggregation.
+// CTA; inserts (and occupancy-list appends) go to the owner's shared memory
+// through DSMEM atomics. Each CTA streams 1/8 of the row, sweeps its own
+// occupied slots, and rank 0 merges the eight partial argmaxes. No global-memory
+// table, no DRAM traffic for aggregation.
 __device__ __forceinline__ uint32_t owner_of(uint32_t key) {
   return ((key ^ (key >> 16)) * 0x7FEB352Du) >> (32 - 3);  // 3 = log2(kClusterSize)
 }
 
+template <typename Tab>
+constexpr size_t cluster_bytes() {
+  return size_t(kClusterCap) * Tab::kSlotBytes + size_t(kClusterCap) * sizeof(uint16_t);
+}
+
 template <int MODE, typename W, bool WEIGHTED>
 __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThreads)
-    k_cluster(PassCtx c,
-                                                         const uint32_t* __restrict__ list,
-                                                         uint32_t count) {
+    k_cluster(PassCtx c, const uint32_t* __restrict__ list, uint32_t count) {
   namespace cg = cooperative_groups;
   static_assert(kClusterSize == 8, "owner_of assumes 8 ranks");
   using Tab = Table<kPacked<WEIGHTED>, W>;
@@ -393,15 +448,21 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tab local;
   local.bind(smem_raw, kClusterCap);
+  uint16_t* occ = reinterpret_cast<uint16_t*>(smem_raw + size_t(kClusterCap) * Tab::kSlotBytes);
   __shared__ uint32_t s_item;
   __shared__ int s_flag, s_changed;
+  __shared__ unsigned s_occ_n;
   __shared__ Best<VBits<W>> red[32];
   __shared__ Best<VBits<W>> part[kClusterSize];
+  for (uint32_t s = threadIdx.x; s < kClusterCap; s += blockDim.x) local.clear_slot(s);  // once
   const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31;
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
   for (;;) {
-    if (rank == 0 && threadIdx.x == 0) s_item = atomicAdd(c.work, 1u);
+    if (threadIdx.x == 0) {
+      s_occ_n = 0;
+      if (rank == 0) s_item = atomicAdd(c.work, 1u);
+    }
     cl.sync();                                                   // (A) item published
     const uint32_t t = *cl.map_shared_rank(&s_item, 0);
     if (t >= count) break;  // uniform over the cluster; the final sync below keeps rank 0's
@@ -411,8 +472,7 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
     const uint64_t lo = __ldg(c.g.off + i);
     const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
     const uint32_t cap = pow2_ceil(d + d / 3 + 1) / kClusterSize;  // per-rank partition
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) local.clear_slot(s);
-    cl.sync();                                                   // (B) flag + clean tables
+    cl.sync();                                                   // (B) flag visible
     if (*cl.map_shared_rank(&s_flag, 0)) continue;
     // Stream this rank's slice of the row; warp dedup; insert at the owner rank.
     const uint32_t e0 = static_cast<uint32_t>((uint64_t(d) * rank) / kClusterSize);
@@ -442,21 +502,24 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
         else
           s = static_cast<W>(__popc(peers));
         if (lab[u] != kEmpty && (__ffs(peers) - 1) == lane) {
+          const uint32_t own = owner_of(lab[u]);
+          unsigned char* rbase = cl.map_shared_rank(smem_raw, own);
           Tab remote;
-          remote.bind(cl.map_shared_rank(smem_raw, owner_of(lab[u])), kClusterCap);
+          remote.bind(rbase, kClusterCap);
           uint32_t slot;
-          if (!remote.add(cap, c.strategy, lab[u], s, &slot)) ++fails;
+          const int r = remote.add(cap, c.strategy, lab[u], s, &slot);
+          if (r == 0) {
+            ++fails;
+          } else if (r == 2) {
+            const unsigned pos = atomicAdd(cl.map_shared_rank(&s_occ_n, own), 1u);
+            reinterpret_cast<uint16_t*>(rbase + size_t(kClusterCap) * Tab::kSlotBytes)[pos] =
+                static_cast<uint16_t>(slot);
+          }
         }
       }
     }
     cl.sync();                                                   // (C) all inserts landed
-    Best<VBits<W>> b{VBits<W>(0), kEmpty};
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
-      uint32_t k;
-      VBits<W> v;
-      local.read(s, k, v);
-      best_merge(b, v, k);
-    }
+    Best<VBits<W>> b = occ_argmax_reset<W>(local, occ, s_occ_n, threadIdx.x, blockDim.x);
     b = block_best(b, red);
     if (threadIdx.x == 0) *cl.map_shared_rank(&part[rank], 0) = b;
     cl.sync();                                                   // (D) partial argmaxes at rank 0
@@ -576,7 +639,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h
     for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) tab.clear_slot(s);
     __syncthreads();
     team_gather<MODE, W, WEIGHTED>(c, i, lo, e0, e1, tab, cap, threadIdx.x, blockDim.x, pol,
-                                   fails);
+                                   nullptr, nullptr, fails);
     __syncthreads();
     Tab g;
     bind_hub_table<Tab, W, kPacked<WEIGHTED>>(g, h, x);
@@ -773,7 +836,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_sequential(PassCtx c, void* g
       const bool valid = e < d && j != i;
       const uint32_t lab = valid ? c.lab_out[j] : kEmpty;
       const W w = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
-      gather_insert<W, WEIGHTED>(c, lab, w, tab, cap, fails);
+      gather_insert<W, WEIGHTED>(c, lab, w, tab, cap, nullptr, nullptr, fails);
     }
     __syncthreads();
     Best<VBits<W>> b{VBits<W>(0), kEmpty};
