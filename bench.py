@@ -116,23 +116,21 @@ def dist_env():
     return rank, world, local
 
 
-def reference_sample(scale: int, edgefactor: int, seed: int, device: int):
-    """The bounded CPU sample: an R-MAT graph of the same generator at a smaller scale."""
-    from paper_2411_11468_b200 import labelprop as lp
-    dg = lp.DeviceGraph.rmat(scale, edgefactor, seed, device)
-    g = dg.download()
-    dg.free()
-    return g
+def ref_switch_degree(workload: str) -> int:
+    # the team path costs ~210 us per vertex of degree >= 32 per pass, so on
+    # the power-law inputs the reference runs all-scalar (switch_degree = UINT32_MAX, F5).
+    return 0xFFFFFFFF if workload in ("rmat", "web") else 32
 
 
-def run_reference_cpu(g, reps: int):
+def run_reference_cpu(g, reps: int, workload: str = "rmat"):
     """oracle/_ref: the unmodified reference lpa(), ParallelAsync, all host threads."""
     import oracle as O
     rg = O.RefGraph.from_csr(g.offsets, g.targets, None)
     workers = os.cpu_count() or 1
     out = []
     for _ in range(reps):
-        labels, st = O.ref_lpa(rg, exec_mode=0, workers=workers, switch_degree=0xFFFFFFFF)
+        labels, st = O.ref_lpa(rg, exec_mode=0, workers=workers,
+                               switch_degree=ref_switch_degree(workload))
         out.append((labels, st))
     return rg, out, workers
 
@@ -146,21 +144,22 @@ def bench_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libnulpa_ref.so not built (needs /root/reference at build)"}))
         return 0
-    g = reference_sample(args.ref_scale, 16, args.seed, 0)
+    from paper_2411_11468_b200 import workloads
+    g, desc = workloads.cpu_sample(args.workload, args.ref_scale, args.seed, 0)
     m2 = g.directed_size()
-    rg, runs, workers = run_reference_cpu(g, args.warmup + args.steps)
+    rg, runs, workers = run_reference_cpu(g, args.warmup + args.steps, args.workload)
     timed = runs[args.warmup:]
     secs = sum(st["elapsed_seconds"] for _, st in timed)
     value = m2 * len(timed) / secs
     q = O.ref_modularity(rg, timed[-1][0])
-    sample = (f"R-MAT scale-{args.ref_scale} ef16 (n=2^{args.ref_scale}, m2={m2}), reference "
-              f"ParallelAsync, switch_degree=UINT32_MAX (SURVEY F5), workers={workers}")
+    sample = (f"{desc} (n={g.order()}, m2={m2}), reference ParallelAsync, switch_degree="
+              f"{ref_switch_degree(args.workload)}, workers={workers}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / len(timed), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"rmat{args.ref_scale}-ef16 (bounded CPU sample of rmat"
-                                   f"{args.scale}-ef16)", "n": g.order(), "m2": m2,
+            "config": {"workload": f"{desc} (bounded CPU sample of the {args.workload} "
+                                   f"workload)", "n": g.order(), "m2": m2,
                        "iterations": timed[-1][1]["iterations"], "modularity": q},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers,
                              "kind": "reference", "sample": sample},
@@ -195,8 +194,9 @@ def bench_nulpa(args):
             import torch.distributed as dist
             dist.barrier()
 
+    from paper_2411_11468_b200 import workloads
     t0 = time.time()
-    dg = lp.DeviceGraph.rmat(args.scale, args.edgefactor, args.seed, dev)
+    dg, wdesc = workloads.build(args.workload, args.scale, args.seed, dev)
     gen_s = time.time() - t0
     n, m2 = dg.n, dg.m2
     cfg = lp.LpaConfig()
@@ -283,14 +283,15 @@ def bench_nulpa(args):
         try:
             import oracle as O
             if O.ref_available():
-                g = reference_sample(args.ref_scale, 16, args.seed, dev)
-                _, runs, workers = run_reference_cpu(g, 1)
+                g, desc = workloads.cpu_sample(args.workload, args.ref_scale, args.seed, dev)
+                _, runs, workers = run_reference_cpu(g, 1, args.workload)
                 stc = runs[-1][1]
                 cpu = {"value": g.directed_size() / stc["elapsed_seconds"], "unit": UNIT,
                        "cores": workers, "kind": "reference",
-                       "sample": f"R-MAT scale-{args.ref_scale} ef16 (m2={g.directed_size()}), "
-                                 f"reference lpa() ParallelAsync, switch_degree=UINT32_MAX "
-                                 f"(SURVEY F5), {stc['iterations']} iterations, "
+                       "sample": f"{desc} (m2={g.directed_size()}), reference lpa() "
+                                 f"ParallelAsync, switch_degree="
+                                 f"{ref_switch_degree(args.workload)}, "
+                                 f"{stc['iterations']} iterations, "
                                  f"{stc['elapsed_seconds']:.2f} s"}
             else:
                 cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
@@ -307,9 +308,10 @@ def bench_nulpa(args):
             "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {
-                "workload": f"rmat{args.scale}-ef{args.edgefactor}", "n": n, "m2": m2,
+                **wdesc, "n": n, "m2": m2,
                 "E_definition": "m2 = directed CSR entries after symmetrise + dedup",
-                "undirected_draws": (1 << args.scale) * args.edgefactor,
+                "undirected_draws": ((1 << args.scale) * args.edgefactor
+                                     if args.workload == "rmat" else None),
                 "parallelism": "replicas" if world > 1 else "single",
                 "exec": "ParallelAsync", "pl_period": 4, "tolerance": 0.05,
                 "iterations": s0.iterations, "delta_n": stats[-1][1],
@@ -360,8 +362,9 @@ def bench_partitioned(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    from paper_2411_11468_b200 import workloads
     t0 = time.time()
-    dg = lp.DeviceGraph.rmat(args.scale, args.edgefactor, args.seed, local)
+    dg, wdesc = workloads.build(args.workload, args.scale, args.seed, local)
     gen_s = time.time() - t0
     n, m2 = dg.n, dg.m2
     b = (C.c_uint32 * (world + 1))()
@@ -399,7 +402,7 @@ def bench_partitioned(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic",
-            "config": {"workload": f"rmat{args.scale}-ef{args.edgefactor}", "n": n, "m2": m2,
+            "config": {**wdesc, "n": n, "m2": m2,
                        "parallelism": f"edge-balanced 1-D partition x{world}, replicated labels, "
                                       "NCCL all-gather-v + MIN-reduce of wake flags per pass",
                        "bounds": bounds, "exec": "ParallelAsync (Jacobi across ranks)",
@@ -424,6 +427,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nulpa", choices=["nulpa", "reference"])
+    ap.add_argument("--workload", default="rmat", choices=["rmat", "grid", "web", "sbm"])
     ap.add_argument("--scale", type=int, default=27)
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--seed", type=int, default=1)

@@ -356,9 +356,10 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
     dfree(scratch);
     // Scrambled visit order (ParallelAsync only: any interleaving is a valid
     // asynchronous schedule; Synchronous/Sequential results do not depend on it).
-    // The hub tier keeps ascending order (its decisions land after the tier).
+    // The thread tier keeps ascending order (its tiny rows then stream coalesced),
+    // and so does the hub tier (its decisions land after the tier anyway).
     if (tb.schedule == 2)
-      for (int t = 0; t < dev::T_HUB; ++t) scramble_list(p->list[t], p->count[t], s);
+      for (int t = dev::T_HALF; t < dev::T_HUB; ++t) scramble_list(p->list[t], p->count[t], s);
 
     // Hub tier: per-hub global tables and (hub, chunk) work items. Hub counts
     // are small (vertices of degree > block_max), so the layout is built on
