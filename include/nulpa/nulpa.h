@@ -82,8 +82,8 @@ typedef struct nulpa_opts {
 /* Kernel-tier tuning (not part of LpaConfig). Zero fields take defaults. */
 typedef struct nulpa_tuning {
   uint32_t thread_max_degree; /* thread-per-vertex tier upper bound (<= 16) */
-  uint32_t warp_max_degree;   /* warp-per-vertex tier upper bound (<= 512) */
-  uint32_t block_max_degree;  /* CTA-per-vertex smem-table tier upper bound (<= 4096) */
+  uint32_t warp_max_degree;   /* 32-thread team tier upper bound (<= 256) */
+  uint32_t block_max_degree;  /* 128-thread team tier upper bound (<= 1024) */
   uint32_t hub_chunk;         /* edges per CTA work item in the global-table hub tier */
   uint32_t use_graphs;        /* reserved */
   uint32_t profile;           /* 1: time each tier with CUDA events (stats.tier_*) */
@@ -95,9 +95,9 @@ typedef struct nulpa_tuning {
   uint32_t no_identity_first; /* 1: disable the table-free first pass from identity labels */
 } nulpa_tuning;
 
-#define NULPA_TIERS 9 /* 0 thread, 1 half-warp, 2 warp, 3 warp+smem table, 4 CTA, 5 1024-thread CTA,
-                         6 8-CTA cluster (DSMEM table), 7 hub (global table),
-                         8 other (deferred wake, cross-check, sequential) */
+#define NULPA_TIERS 10 /* 0 thread, 1 half-warp, 2 warp, 3/4/5 32/128/256-thread teams with
+                          shared tables, 6 1024-thread CTA, 7 8-CTA cluster (DSMEM table),
+                          8 hub (global table), 9 other (deferred wake, cross-check, sequential) */
 
 /* labelprop::RunStats (lpa.hpp:39-46) plus device counters for roofline
  * accounting. delta_n must point at >= max_iterations u64 (or be NULL). */

@@ -34,9 +34,9 @@ class nulpa_tuning(C.Structure):
                 ("use_graphs", C.c_uint32), ("profile", C.c_uint32),
                 ("schedule", C.c_uint32), ("no_identity_first", C.c_uint32)]
 
-NULPA_TIERS = 9
-TIER_NAMES = ["thread", "half_warp", "warp", "warp_table", "block", "big_block", "cluster",
-              "hub", "other"]
+NULPA_TIERS = 10
+TIER_NAMES = ["thread", "half_warp", "warp", "team32", "team128", "team256", "cta1024",
+              "cluster", "hub", "other"]
 
 
 class nulpa_stats(C.Structure):
@@ -46,9 +46,9 @@ class nulpa_stats(C.Structure):
                 ("delta_n", C.POINTER(C.c_uint64)), ("processed_vertices", C.c_uint64),
                 ("processed_edges", C.c_uint64), ("wake_edges", C.c_uint64),
                 ("algorithmic_bytes", C.c_uint64), ("setup_seconds", C.c_double),
-                ("kernel_launches", C.c_uint64), ("tier_ms", C.c_double * 9),
-                ("tier_bytes", C.c_double * 9), ("tier_edges", C.c_uint64 * 9),
-                ("tier_passes", C.c_uint32 * 9), ("reserved2", C.c_uint32)]
+                ("kernel_launches", C.c_uint64), ("tier_ms", C.c_double * 10),
+                ("tier_bytes", C.c_double * 10), ("tier_edges", C.c_uint64 * 10),
+                ("tier_passes", C.c_uint32 * 10), ("reserved2", C.c_uint32)]
 
 
 class nulpa_pass_info(C.Structure):

@@ -49,20 +49,24 @@ enum Tier : int {
   T_THREAD = 0,   // deg <= thread_max (<= 16): one thread per vertex
   T_HALF = 1,     // deg <= 16: half a warp per vertex, register dedup
   T_WARP = 2,     // deg <= 32: one warp per vertex, register dedup
-  T_WTAB = 3,     // deg <= 256: one warp per vertex, per-warp shared-memory table
-  T_BLOCK = 4,    // deg <= 2048: one 256-thread CTA per vertex, shared-memory table
-  T_BIG = 5,      // deg <= 12288: one 1024-thread CTA per vertex, 128 KB shared table
-  T_CLUSTER = 6,  // deg <= 98304: one 8-CTA cluster per vertex, table distributed over DSMEM
-  T_HUB = 7,      // larger: (hub, chunk) items, shared pre-aggregation + global table
-  T_OTHER = 8,    // deferred wake, cross-check, sequential
-  kTiers = 9
+  T_WTAB = 3,     // deg <= 256: a 32-thread team per vertex, shared-memory table
+  T_BLOCK = 4,    // deg <= 1024: a 128-thread team per vertex
+  T_BLOCK2 = 5,   // deg <= 4096: a 256-thread team per vertex
+  T_BIG = 6,      // deg <= 12288: one 1024-thread CTA per vertex, 128 KB shared table
+  T_CLUSTER = 7,  // deg <= 98304: one 8-CTA cluster per vertex, table distributed over DSMEM
+  T_HUB = 8,      // larger: (hub, chunk) items, shared pre-aggregation + global table
+  T_OTHER = 9,    // deferred wake, cross-check, sequential
+  kTiers = 10
 };
 
 constexpr int kBlockThreads = 256;
 constexpr int kWarpTabMax = 256;    // T_WTAB degree bound
-constexpr int kWarpTabCap = 512;    // per-warp slots (load <= 1/2)
-constexpr int kBlockMax = 2048;     // T_BLOCK degree bound
-constexpr int kBlockCap = 4096;     // per-CTA slots (load <= 1/2)
+constexpr int kWarpTabCap = 512;    // per-team slots (load <= 1/2)
+constexpr int kBlockMax = 1024;     // T_BLOCK degree bound
+constexpr int kBlockCap = 2048;     // per-team slots (load <= 1/2)
+constexpr int kBlock2Max = 4096;    // T_BLOCK2 degree bound
+constexpr int kBlock2Cap = 8192;    // per-team slots (load <= 1/2)
+constexpr int kHubCap = 4096;       // hub pre-aggregation slots per CTA
 constexpr int kBigThreads = 1024;
 constexpr int kBigCap = 16384;      // 128 KB packed
 constexpr int kBigMax = 12288;      // load <= 3/4

@@ -62,16 +62,23 @@ template <int MODE, typename W, bool WEIGHTED>
 int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t s, int sms,
                 Prof& prof) {
   using Tab = Table<kPacked<WEIGHTED>, W>;
-  constexpr size_t wtab_smem = (kBlockThreads / 32) * wtab_bytes<Tab>();
-  constexpr size_t block_smem = block_bytes<Tab, kBlockCap, kBlockMax>();
-  constexpr size_t big_smem = block_bytes<Tab, kBigCap, kBigMax>();
+  // Team kernels: <CTA threads, team threads, table slots, max degree> per tier.
+  constexpr size_t wtab_smem = 8 * team_bytes<Tab, kWarpTabCap, kWarpTabMax>();
+  constexpr size_t block_smem = 2 * team_bytes<Tab, kBlockCap, kBlockMax>();
+  constexpr size_t block2_smem = 1 * team_bytes<Tab, kBlock2Cap, kBlock2Max>();
+  constexpr size_t big_smem = team_bytes<Tab, kBigCap, kBigMax>();
   constexpr size_t cluster_smem = cluster_bytes<Tab>();
-  constexpr size_t hub_smem = kBlockCap * Tab::kSlotBytes;
+  constexpr size_t hub_smem = kHubCap * Tab::kSlotBytes;
+  auto k_wt = k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax>;
+  auto k_b1 = k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax>;
+  auto k_b2 = k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max>;
+  auto k_bg = k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax>;
   static bool init = false;
   if (!init) {
-    allow_smem(k_wtab<MODE, W, WEIGHTED>, wtab_smem);
-    allow_smem(k_block<MODE, W, WEIGHTED, kBlockThreads, kBlockCap, kBlockMax>, block_smem);
-    allow_smem(k_block<MODE, W, WEIGHTED, kBigThreads, kBigCap, kBigMax>, big_smem);
+    allow_smem(k_wt, wtab_smem);
+    allow_smem(k_b1, block_smem);
+    allow_smem(k_b2, block2_smem);
+    allow_smem(k_bg, big_smem);
     allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
     allow_smem(k_hub_accum<MODE, W, WEIGHTED>, hub_smem);
     init = true;
@@ -107,25 +114,29 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   }
   if (p.count[T_WTAB]) {
     tier(T_WTAB);
-    k_wtab<MODE, W, WEIGHTED><<<grid_for(p.count[T_WTAB], kBlockThreads / 32, sms * 6),
-                                kBlockThreads, wtab_smem, s>>>(c, p.list[T_WTAB],
-                                                               p.count[T_WTAB]);
+    k_wt<<<grid_for(p.count[T_WTAB], 8, sms * 6), 256, wtab_smem, s>>>(c, p.list[T_WTAB],
+                                                                      p.count[T_WTAB]);
     prof.end(T_WTAB, s);
     ++launches;
   }
   if (p.count[T_BLOCK]) {
     tier(T_BLOCK);
-    k_block<MODE, W, WEIGHTED, kBlockThreads, kBlockCap, kBlockMax>
-        <<<grid_for(p.count[T_BLOCK], 1, sms * 6), kBlockThreads, block_smem, s>>>(
-            c, p.list[T_BLOCK], p.count[T_BLOCK]);
+    k_b1<<<grid_for(p.count[T_BLOCK], 2, sms * 6), 256, block_smem, s>>>(c, p.list[T_BLOCK],
+                                                                        p.count[T_BLOCK]);
     prof.end(T_BLOCK, s);
+    ++launches;
+  }
+  if (p.count[T_BLOCK2]) {
+    tier(T_BLOCK2);
+    k_b2<<<grid_for(p.count[T_BLOCK2], 1, sms * 3), 256, block2_smem, s>>>(c, p.list[T_BLOCK2],
+                                                                          p.count[T_BLOCK2]);
+    prof.end(T_BLOCK2, s);
     ++launches;
   }
   if (p.count[T_BIG]) {
     tier(T_BIG);
-    k_block<MODE, W, WEIGHTED, kBigThreads, kBigCap, kBigMax>
-        <<<grid_for(p.count[T_BIG], 1, sms), kBigThreads, big_smem, s>>>(c, p.list[T_BIG],
-                                                                          p.count[T_BIG]);
+    k_bg<<<grid_for(p.count[T_BIG], 1, sms), kBigThreads, big_smem, s>>>(c, p.list[T_BIG],
+                                                                        p.count[T_BIG]);
     prof.end(T_BIG, s);
     ++launches;
   }
@@ -177,7 +188,7 @@ int dispatch_pass(const Plan& p, const PassCtx& c, unsigned long long* ctr, int 
 
 template <typename W, bool WEIGHTED>
 void launch_sequential(const PassCtx& c, void* gtab, cudaStream_t s) {
-  constexpr size_t smem = kBlockCap * Table<kPacked<WEIGHTED>, W>::kSlotBytes;
+  constexpr size_t smem = kHubCap * Table<kPacked<WEIGHTED>, W>::kSlotBytes;
   static bool init = false;
   if (!init) {
     allow_smem(k_sequential<W, WEIGHTED>, smem);
@@ -291,7 +302,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
   DBuf<unsigned char> seq_tab;  // global table for Sequential rows beyond shared memory
   if (o.exec == NULPA_EXEC_SEQUENTIAL) {
     const uint64_t cap = pow2_ceil(2 * std::max<uint32_t>(g->max_degree, 1));
-    if (cap > static_cast<uint64_t>(kBlockCap)) seq_tab = DBuf<unsigned char>(cap * (4 + 8));
+    if (cap > static_cast<uint64_t>(kHubCap)) seq_tab = DBuf<unsigned char>(cap * (4 + 8));
   }
   Prof prof;
   prof.on = tuning && tuning->profile;

@@ -358,7 +358,7 @@ __device__ __forceinline__ Best<V> block_best(Best<V> b, Best<V>* red) {
 // <= 3/4 for the 128 KB tiers (always a power of two).
 template <int CAP>
 __device__ __forceinline__ uint32_t table_cap(uint32_t d) {
-  return CAP <= kBlockCap ? pow2_ceil(2 * d) : pow2_ceil(d + d / 3 + 1);
+  return CAP <= kBlock2Cap ? pow2_ceil(2 * d) : pow2_ceil(d + d / 3 + 1);
 }
 
 template <typename Tab, int CAP, int MAXD>
@@ -412,6 +412,107 @@ __global__ void __launch_bounds__(THREADS) k_block(PassCtx c, const uint32_t* __
       for (uint32_t e = threadIdx.x; e < d; e += THREADS)
         c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
     __syncthreads();
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+  warp_add_counter(c.ctr, C_FAIL, fails);
+}
+
+// ---- tier: TEAM threads per vertex, several teams per CTA ---------------------------
+// A CTA of CTA_THREADS threads holds CTA_THREADS / TEAM independent teams; each
+// team owns one vertex at a time and its own shared table + occupancy list, and
+// synchronises on its own named barrier (bar.sync id, TEAM), so teams never wait
+// for each other. The team size is matched to the degree band (about 4-8 edges
+// per thread) so no round of the gather runs mostly-idle lanes.
+__device__ __forceinline__ void team_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int TEAM, typename V>
+__device__ __forceinline__ Best<V> team_best(Best<V> b, Best<V>* red, int team_tid, int bar) {
+  b = warp_best(b);
+  if constexpr (TEAM == 32) {
+    return b;
+  } else {
+    const int w = team_tid >> 5, lane = team_tid & 31;
+    if (lane == 0) red[w] = b;
+    team_sync(bar, TEAM);
+    if (w == 0) {
+      Best<V> r = lane < TEAM / 32 ? red[lane] : Best<V>{V(0), kEmpty};
+      r = warp_best(r);
+      if (lane == 0) red[0] = r;
+    }
+    team_sync(bar, TEAM);
+    return red[0];
+  }
+}
+
+template <typename Tab, int CAP, int MAXD>
+constexpr size_t team_bytes() {
+  return size_t(CAP) * Tab::kSlotBytes + size_t(MAXD) * sizeof(uint16_t);
+}
+
+template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CAP, int MAXD>
+__global__ void __launch_bounds__(CTA_THREADS) k_team(PassCtx c, const uint32_t* __restrict__ list,
+                                                      uint32_t count) {
+  static_assert(CTA_THREADS % TEAM == 0 && TEAM % 32 == 0, "team shape");
+  constexpr int kTeams = CTA_THREADS / TEAM;
+  using Tab = Table<kPacked<WEIGHTED>, W>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Best<VBits<W>> s_red[kTeams][TEAM / 32 > 0 ? TEAM / 32 : 1];
+  __shared__ int s_flag[kTeams];
+  __shared__ unsigned s_occ_n[kTeams];
+  const int team = threadIdx.x / TEAM, ttid = threadIdx.x % TEAM;
+  const int bar = 1 + team;  // named barrier 0 is __syncthreads
+  unsigned char* base = smem_raw + size_t(team) * team_bytes<Tab, CAP, MAXD>();
+  Tab tab;
+  tab.bind(base, CAP);
+  uint16_t* occ = reinterpret_cast<uint16_t*>(base + size_t(CAP) * Tab::kSlotBytes);
+  auto sync = [&]() {
+    if constexpr (TEAM == 32)
+      __syncwarp();
+    else
+      team_sync(bar, TEAM);
+  };
+  for (uint32_t s = ttid; s < CAP; s += TEAM) tab.clear_slot(s);  // once per lifetime
+  const uint64_t pol = policy_evict_first();
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
+  const uint32_t stride = gridDim.x * kTeams;
+  for (uint32_t t = blockIdx.x * kTeams + team; t < count; t += stride) {
+    const uint32_t i = __ldg(list + t);
+    if (ttid == 0) {
+      s_flag[team] = claim_vertex(c, i) ? 1 : 0;
+      s_occ_n[team] = 0;
+    }
+    const uint64_t lo = __ldg(c.g.off + i);
+    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+    const uint32_t cap = table_cap<CAP>(d);
+    sync();
+    if (s_flag[team]) {
+      sync();  // s_flag is rewritten by the next iteration
+      continue;
+    }
+    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, ttid, TEAM, pol, occ,
+                                   &s_occ_n[team], fails);
+    sync();
+    Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n[team], ttid, TEAM);
+    b = team_best<TEAM>(b, s_red[team], ttid, bar);
+    int changed = 0;
+    if (ttid == 0) {
+      changed = apply_move<MODE>(c, i, b.k) ? 1 : 0;
+      s_flag[team] = changed;
+      ++n_v;
+      n_e += d;
+      n_dn += changed;
+      if (MODE == kAsync && changed && c.wake) n_w += d;
+    }
+    sync();
+    changed = s_flag[team];
+    if (MODE == kAsync && changed && c.wake)
+      for (uint32_t e = ttid; e < d; e += TEAM) c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
+    sync();
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
   warp_add_counter(c.ctr, C_PROC_E, n_e);
@@ -623,7 +724,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h
   using Tab = Table<kPacked<WEIGHTED>, W>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tab tab;
-  tab.bind(smem_raw, kBlockCap);
+  tab.bind(smem_raw, kHubCap);
   const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31;
   unsigned long long fails = 0;
@@ -635,7 +736,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h
     const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
     const uint32_t e0 = h.item_start[it];
     const uint32_t e1 = min(d, e0 + kHubChunk);
-    const uint32_t cap = kBlockCap;
+    const uint32_t cap = kHubCap;
     for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) tab.clear_slot(s);
     __syncthreads();
     team_gather<MODE, W, WEIGHTED>(c, i, lo, e0, e1, tab, cap, threadIdx.x, blockDim.x, pol,
@@ -824,8 +925,8 @@ __global__ void __launch_bounds__(kBlockThreads) k_sequential(PassCtx c, void* g
     const uint32_t d = static_cast<uint32_t>(c.g.off[i + 1] - lo);
     const uint32_t cap = pow2_ceil(2 * d);
     Tab tab;
-    if (cap <= static_cast<uint32_t>(kBlockCap))
-      tab.bind(smem_raw, kBlockCap);
+    if (cap <= static_cast<uint32_t>(kHubCap))
+      tab.bind(smem_raw, kHubCap);
     else
       tab.bind(gtab, cap);
     for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) tab.clear_slot(s);
