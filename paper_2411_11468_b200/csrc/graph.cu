@@ -105,21 +105,37 @@ void use_device(int device) {
   if (device < 0 || device >= count)
     throw Error(NULPA_EINVAL, "CUDA device " + std::to_string(device) + " out of range");
   NULPA_CUDA(cudaSetDevice(device));
+  // Device buffers come from the stream-ordered pool; keep up to 64 GB of freed
+  // memory cached so repeated lpa() calls (new graph, plan, labels each time)
+  // do not pay cudaMalloc/cudaFree of multi-GB arrays.
+  static thread_local int configured = -1;
+  if (configured != device) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = 64ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    (void)cudaGetLastError();
+    configured = device;
+  }
 }
 
+// Allocations are stream-ordered on the legacy stream; every buffer is freed only
+// after the work that used it has been synchronised.
 void* dmalloc(size_t bytes) {
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
+  cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     throw Error(e == cudaErrorMemoryAllocation ? NULPA_ENOMEM : NULPA_ECUDA,
-                "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
+                "cudaMallocAsync(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
   }
   return p;
 }
 
 void dfree(void* p) {
-  if (p) cudaFree(p);
+  if (p) cudaFreeAsync(p, 0);
 }
 
 int sm_count() {
@@ -233,9 +249,9 @@ void partition_two_way(const uint64_t* off, uint32_t n, uint32_t sw, uint32_t* l
   dfree(d_num);
 }
 
-__global__ void k_hash_keys(const uint32_t* ids, uint32_t count, uint32_t* keys) {
+__global__ void k_hash_keys(const uint32_t* ids, uint32_t count, uint32_t* keys, int shift) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
-    uint32_t x = ids[t] * 0x9E3779B1u;
+    uint32_t x = (ids[t] >> shift) * 0x9E3779B1u;
     x ^= x >> 16;
     x *= 0x85EBCA6Bu;
     x ^= x >> 13;
@@ -243,13 +259,15 @@ __global__ void k_hash_keys(const uint32_t* ids, uint32_t count, uint32_t* keys)
   }
 }
 
-// Reorder a vertex list by a hash of the id (a fixed pseudo-random permutation).
-void scramble_list(uint32_t* list, uint32_t count, cudaStream_t s) {
+// Reorder a vertex list by a hash of (id >> shift): a fixed pseudo-random
+// permutation of 2^shift-id blocks; the stable sort keeps ascending order inside
+// a block, so shift > 0 keeps the rows of neighbouring ids together.
+void scramble_list(uint32_t* list, uint32_t count, cudaStream_t s, int shift = 0) {
   if (count < 2) return;
   uint32_t* k0 = dalloc<uint32_t>(count);
   uint32_t* k1 = dalloc<uint32_t>(count);
   uint32_t* v1 = dalloc<uint32_t>(count);
-  k_hash_keys<<<256, 256, 0, s>>>(list, count, k0);
+  k_hash_keys<<<256, 256, 0, s>>>(list, count, k0, shift);
   cub::DoubleBuffer<uint32_t> keys(k0, k1), vals(list, v1);
   size_t tb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, count, 0, 32, s);
@@ -357,10 +375,13 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
     dfree(scratch);
     // Scrambled visit order (ParallelAsync only: any interleaving is a valid
     // asynchronous schedule; Synchronous/Sequential results do not depend on it).
-    // The thread tier keeps ascending order (its tiny rows then stream coalesced),
-    // and so does the hub tier (its decisions land after the tier anyway).
-    if (tb.schedule == 2)
+    // The thread tier is scrambled in 32-id blocks (its tiny rows still stream
+    // coalesced within a warp); the hub tier keeps ascending order (its decisions
+    // land after the tier anyway).
+    if (tb.schedule == 2) {
+      scramble_list(p->list[dev::T_THREAD], p->count[dev::T_THREAD], s, 5);
       for (int t = dev::T_HALF; t < dev::T_HUB; ++t) scramble_list(p->list[t], p->count[t], s);
+    }
 
     // Hub tier: per-hub global tables and (hub, chunk) work items. Hub counts
     // are small (vertices of degree > block_max), so the layout is built on
