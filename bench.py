@@ -392,8 +392,9 @@ def bench_partitioned(args):
     secs = dmax(ev0.elapsed_time(ev1) * 1e-3)
     pass_ms = dmax(sum(sum(s.pass_ms) for s in stats))
     exch_ms = dmax(sum(sum(s.exchange_ms) for s in stats))
-    q = dg.modularity_device(eng.labels.data_ptr()) if rank == 0 else None
-    comms = dg.community_count_device(eng.labels.data_ptr()) if rank == 0 else None
+    vl = eng.vertex_labels() if rank == 0 else None
+    q = dg.modularity_device(vl.data_ptr()) if rank == 0 else None
+    comms = dg.community_count_device(vl.data_ptr()) if rank == 0 else None
     launches = int(sum(s.kernel_launches for s in stats))
     if rank == 0:
         s0 = stats[-1]

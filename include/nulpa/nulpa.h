@@ -125,6 +125,16 @@ typedef struct nulpa_stats {
 
 typedef struct nulpa_graph nulpa_graph; /* device-resident CSR */
 
+/* Resident layouts. DEGREE_BUCKETS (the default) stores the rows in POSITION
+ * order: vertices grouped by ceil(log2(degree)), largest first, isolated last,
+ * ascending id inside a group, so the labels of the high-degree vertices that
+ * most edges point at are packed together and stay in L2. Label VALUES are
+ * always vertex ids and every label array that crosses this ABI is in vertex
+ * order (except the session API below, which works on position-order arrays);
+ * results do not depend on the layout. IDENTITY keeps the input numbering. */
+#define NULPA_LAYOUT_IDENTITY 0
+#define NULPA_LAYOUT_DEGREE_BUCKETS 1
+
 const char* nulpa_last_error(void);
 int nulpa_version(void);
 void nulpa_default_opts(nulpa_opts* opts);
@@ -161,9 +171,19 @@ int nulpa_graph_wrap_device(const nulpa_csr* device_csr, int device, nulpa_graph
 int nulpa_graph_free(nulpa_graph* g);
 int nulpa_graph_info(const nulpa_graph* g, uint32_t* n, uint64_t* m2, uint32_t* max_degree,
                      int* weighted);
-/* Device pointers of the resident arrays (weights NULL when unit). */
+/* Layout used by graphs created after this call (process-wide; default
+ * NULPA_LAYOUT_DEGREE_BUCKETS). */
+int nulpa_set_default_layout(int layout);
+int nulpa_graph_layout(const nulpa_graph* g, int* layout);
+/* Permute a DEVICE label array between position order and vertex order
+ * (out-of-place; a plain copy under the identity layout). */
+int nulpa_graph_labels_to_vertex_order(const nulpa_graph* g, const uint32_t* pos_dev,
+                                       uint32_t* vtx_dev);
+int nulpa_graph_labels_to_position_order(const nulpa_graph* g, const uint32_t* vtx_dev,
+                                         uint32_t* pos_dev);
+/* Device pointers of the resident arrays, POSITION order (weights NULL when unit). */
 int nulpa_graph_device_csr(const nulpa_graph* g, nulpa_csr* out);
-/* Download the resident CSR into host buffers (weights may be NULL). */
+/* Download the resident CSR into host buffers in VERTEX order (weights may be NULL). */
 int nulpa_graph_download(const nulpa_graph* g, uint64_t* offsets, uint32_t* targets,
                          float* weights);
 
@@ -197,9 +217,10 @@ int nulpa_graph_from_edges(const uint32_t* u, const uint32_t* v, uint64_t ne, ui
                            int device, nulpa_graph** out);
 
 /* ---- pass-level sessions: the partitioned multi-GPU path --------
- * A session runs single passes over the vertex range [v_begin, v_end) of a
- * resident graph, on caller-owned DEVICE arrays labels[n] / flags[n] that are
- * replicated across ranks; the caller exchanges the owned label ranges and the
+ * A session runs single passes over the POSITION range [v_begin, v_end) of a
+ * resident graph, on caller-owned DEVICE arrays labels[n] / flags[n] in
+ * position order (nulpa_graph_labels_to_vertex_order converts the result) that
+ * are replicated across ranks; the caller exchanges the owned label ranges and the
  * wake flags between passes (torch.distributed / NCCL) and drives the
  * run_engine schedule (paper_2411_11468_b200/dist.py). ParallelAsync updates
  * labels in place inside the range; Synchronous stages decisions and applies
@@ -215,12 +236,13 @@ typedef struct nulpa_pass_info {
   uint64_t kernel_launches;
 } nulpa_pass_info;
 
-/* Edge-balanced 1-D split: bounds[0..parts] with offsets[bounds[p]] ~ p*m2/parts. */
+/* Edge-balanced 1-D split of the position order: bounds[0..parts] with
+ * offsets[bounds[p]] ~ p*m2/parts. */
 int nulpa_graph_edge_ranges(nulpa_graph* g, uint32_t parts, uint32_t* bounds);
 int nulpa_session_create(nulpa_graph* g, const nulpa_opts* opts, const nulpa_tuning* tuning,
                          uint32_t v_begin, uint32_t v_end, uint32_t* labels_dev,
                          uint8_t* flags_dev, nulpa_session** out);
-/* labels[i] = i and flags[i] = (degree(i) == 0) over ALL n vertices. */
+/* labels[p] = vertex id at p and flags[p] = (degree == 0) over ALL n positions. */
 int nulpa_session_init(nulpa_session* s);
 /* wake = 0 skips the neighbour wake-up stores (legal when the caller's schedule
  * resets every flag before the next pass, see engine.cu run_lpa). */

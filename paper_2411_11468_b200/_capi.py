@@ -13,6 +13,7 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "libnulpa.so"
 
 NULPA_OK, NULPA_EINVAL, NULPA_ENOMEM, NULPA_EINTERNAL, NULPA_ECUDA, NULPA_EOTHER = range(6)
+NULPA_LAYOUT_IDENTITY, NULPA_LAYOUT_DEGREE_BUCKETS = 0, 1
 
 
 class nulpa_csr(C.Structure):
@@ -88,6 +89,10 @@ _SIGS = {
     "nulpa_graph_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64),
                                    C.POINTER(C.c_uint32), C.POINTER(C.c_int)]),
     "nulpa_graph_device_csr": (C.c_int, [C.c_void_p, C.POINTER(nulpa_csr)]),
+    "nulpa_set_default_layout": (C.c_int, [C.c_int]),
+    "nulpa_graph_layout": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+    "nulpa_graph_labels_to_vertex_order": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "nulpa_graph_labels_to_position_order": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "nulpa_graph_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "nulpa_run_graph": (C.c_int, [C.c_void_p, C.POINTER(nulpa_opts), C.POINTER(nulpa_tuning),
                                   C.c_void_p, C.c_void_p, C.POINTER(nulpa_stats)]),

@@ -24,7 +24,7 @@ OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libnulpa.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["graph.cu", "engine.cu", "quality.cu", "gen.cu"]
+CU_SOURCES = ["graph.cu", "layout.cu", "engine.cu", "quality.cu", "gen.cu"]
 CXX_SOURCES = ["dropin.cpp"]
 
 

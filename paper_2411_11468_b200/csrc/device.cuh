@@ -94,7 +94,17 @@ struct PassCtx {
   int strategy;
   int wake;                       // store neighbour wake-ups (0 when provably dead, see engine.cu)
   unsigned int* work;             // dynamic work counter (cluster tier)
+  const uint32_t* vid;            // position -> vertex id (layout.cu); nullptr = identity
+  const uint32_t* pos;            // vertex id -> position; nullptr = identity
 };
+
+// Vertex id stored at position p (label values are vertex ids).
+__device__ __forceinline__ uint32_t vertex_id(const uint32_t* vid, uint32_t p) {
+  return vid ? __ldg(vid + p) : p;
+}
+__device__ __forceinline__ uint32_t position_of(const uint32_t* pos, uint32_t v) {
+  return pos ? __ldg(pos + v) : v;
+}
 
 // Hub-tier tables and work items (k_hub_* in lpa_kernels.cuh).
 struct HubCtx {

@@ -15,6 +15,7 @@
 #include <utility>
 
 #include "internal.hpp"
+#include "layout.hpp"
 #include "lpa_kernels.cuh"
 #include "plan.hpp"
 
@@ -24,9 +25,11 @@ using namespace dev;
 
 namespace {
 
-__global__ void k_init(uint32_t* lab, uint8_t* flags, const uint64_t* off, uint32_t n) {
+// labels = identity (lpa.cpp:250): position p holds the vertex id stored there.
+__global__ void k_init(uint32_t* lab, uint8_t* flags, const uint64_t* off, uint32_t n,
+                       const uint32_t* vid) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    lab[i] = i;
+    lab[i] = vid ? vid[i] : i;
     if (flags) flags[i] = (off[i + 1] == off[i]) ? 1 : 0;  // isolated: never examined
   }
 }
@@ -244,6 +247,7 @@ struct Pinned {
 };
 
 // cross_check (lpa.cpp:338-360) on the device; returns the revert count.
+// Arrays in position order.
 uint64_t device_cross_check(nulpa_graph* g, uint32_t* lab, const uint32_t* prev, uint8_t* flags,
                             unsigned long long* d_aux, unsigned long long* h_aux, cudaStream_t s,
                             int sms, uint64_t* launches = nullptr) {
@@ -255,7 +259,7 @@ uint64_t device_cross_check(nulpa_graph* g, uint32_t* lab, const uint32_t* prev,
   const unsigned gb = grid_for(n, 256, sms * 8);
   for (uint32_t round = 0; round <= n; ++round) {
     NULPA_CUDA(cudaMemsetAsync(d_aux, 0, sizeof(unsigned long long), s));
-    k_cc_round<<<gb, 256, 0, s>>>(lab, prev, rin, rout, n, d_aux);
+    k_cc_round<<<gb, 256, 0, s>>>(lab, prev, rin, rout, n, d_aux, g->perm, g->inv);
     NULPA_CUDA(cudaGetLastError());
     if (launches) ++*launches;
     NULPA_CUDA(cudaMemcpyAsync(h_aux, d_aux, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -311,7 +315,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       NULPA_CUDA(cudaEventCreate(&e[0]));
       NULPA_CUDA(cudaEventCreate(&e[1]));
     }
-  k_init<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(lab0.p, flags.p, g->offsets, n);
+  k_init<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(lab0.p, flags.p, g->offsets, n, g->perm);
   NULPA_CUDA(cudaGetLastError());
   NULPA_CUDA(cudaStreamSynchronize(s));
   const double setup_s =
@@ -366,6 +370,8 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     c.changed_n = ctr_other + C_NCHANGED;
     c.wake = wake ? 1 : 0;
     c.work = work.p;
+    c.vid = g->perm;
+    c.pos = g->inv;
     // Synchronous only: there the identity first pass is exactly the reference's.
     // (Under ParallelAsync it is a legal schedule too, but it replaces the in-place
     // first pass, whose early label flooding converges R-MAT one pass sooner and
@@ -489,10 +495,22 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       cudaEventDestroy(e[1]);
     }
 
-  if (labels_host)
-    NULPA_CUDA(cudaMemcpyAsync(labels_host, cur, n * 4ull, cudaMemcpyDeviceToHost, s));
-  if (labels_dev_out)
-    NULPA_CUDA(cudaMemcpyAsync(labels_dev_out, cur, n * 4ull, cudaMemcpyDeviceToDevice, s));
+  // Results leave in vertex order (layout.cu).
+  if (labels_dev_out) to_vertices_u32(g, cur, labels_dev_out, s);
+  if (labels_host) {
+    const uint32_t* src = cur;
+    if (g->perm) {
+      if (labels_dev_out) {
+        src = labels_dev_out;
+      } else {
+        if (!nxt) lab1 = DBuf<uint32_t>(n);
+        uint32_t* tmp = cur == lab0.p ? lab1.p : lab0.p;
+        to_vertices_u32(g, cur, tmp, s);
+        src = tmp;
+      }
+    }
+    NULPA_CUDA(cudaMemcpyAsync(labels_host, src, n * 4ull, cudaMemcpyDeviceToHost, s));
+  }
   NULPA_CUDA(cudaStreamSynchronize(s));
   if (st) {
     st->iterations = iterations;
@@ -531,11 +549,24 @@ uint64_t run_sync_step(nulpa_graph* g, const uint32_t* lab_in_dev, int pick_less
   DBuf<unsigned long long> ctr(kCtr);
   Pinned hc(kCtr);
   NULPA_CUDA(cudaMemsetAsync(ctr.p, 0, kCtr * sizeof(unsigned long long), s));
-  NULPA_CUDA(cudaMemcpyAsync(lab_out_dev, lab_in_dev, g->n * 4ull, cudaMemcpyDeviceToDevice, s));
+  // Labels arrive and leave in vertex order; the pass runs in position order.
+  DBuf<uint32_t> pin, pout;
+  const uint32_t* in_p = lab_in_dev;
+  uint32_t* out_p = lab_out_dev;
+  if (g->perm) {
+    pin = DBuf<uint32_t>(g->n);
+    pout = DBuf<uint32_t>(g->n);
+    to_positions_u32(g, lab_in_dev, pin.p, s);
+    in_p = pin.p;
+    out_p = pout.p;
+  }
+  NULPA_CUDA(cudaMemcpyAsync(out_p, in_p, g->n * 4ull, cudaMemcpyDeviceToDevice, s));
   PassCtx c;
   c.g = Graph{g->offsets, g->targets, g->weights, g->n};
-  c.lab_in = lab_in_dev;
-  c.lab_out = lab_out_dev;
+  c.vid = g->perm;
+  c.pos = g->inv;
+  c.lab_in = in_p;
+  c.lab_out = out_p;
   c.flags = nullptr;
   c.ctr = ctr.p;
   c.changed = nullptr;
@@ -547,6 +578,7 @@ uint64_t run_sync_step(nulpa_graph* g, const uint32_t* lab_in_dev, int pick_less
   c.work = work.p;
   Prof prof;
   dispatch_pass<kSync>(*p, c, ctr.p, vbytes, s, sms, prof);
+  if (g->perm) to_vertices_u32(g, out_p, lab_out_dev, s);
   NULPA_CUDA(cudaMemcpyAsync(hc.p, ctr.p, kCtr * sizeof(unsigned long long),
                              cudaMemcpyDeviceToHost, s));
   NULPA_CUDA(cudaStreamSynchronize(s));
@@ -559,13 +591,27 @@ uint64_t run_sync_step(nulpa_graph* g, const uint32_t* lab_in_dev, int pick_less
   return dn;
 }
 
+// Vertex-order device arrays (labels and flags updated in place).
 uint64_t run_cross_check(nulpa_graph* g, uint32_t* lab_dev, const uint32_t* prev_dev,
                          uint8_t* flags_dev) {
   use_device(g->device);
   Stream stream;
+  cudaStream_t s = stream.s;
   DBuf<unsigned long long> aux(1);
   Pinned hc;
-  return device_cross_check(g, lab_dev, prev_dev, flags_dev, aux.p, hc.p, stream.s, sm_count());
+  if (!g->perm)
+    return device_cross_check(g, lab_dev, prev_dev, flags_dev, aux.p, hc.p, s, sm_count());
+  const uint32_t n = g->n;
+  DBuf<uint32_t> l(n), pv(n);
+  DBuf<uint8_t> f(n);
+  to_positions_u32(g, lab_dev, l.p, s);
+  to_positions_u32(g, prev_dev, pv.p, s);
+  to_positions_u8(g, flags_dev, f.p, s);
+  const uint64_t r = device_cross_check(g, l.p, pv.p, f.p, aux.p, hc.p, s, sm_count());
+  to_vertices_u32(g, l.p, lab_dev, s);
+  to_vertices_u8(g, f.p, flags_dev, s);
+  NULPA_CUDA(cudaStreamSynchronize(s));
+  return r;
 }
 
 }  // namespace nulpa
@@ -639,6 +685,8 @@ void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* i
   c.changed_n = other + C_NCHANGED;
   c.wake = wake ? 1 : 0;
   c.work = ss->work.p;
+  c.vid = g->perm;
+  c.pos = g->inv;
   Prof prof;
   cudaEvent_t e0, e1;
   NULPA_CUDA(cudaEventCreate(&e0));
@@ -823,15 +871,18 @@ int nulpa_cross_check(const nulpa_csr* csr, uint32_t* labels, const uint32_t* pr
 int nulpa_partition_by_degree(const nulpa_csr* csr, uint32_t switch_degree, uint32_t* low,
                               uint64_t* n_low, uint32_t* high, uint64_t* n_high) {
   return guarded([&] {
-    // partition_by_degree, lpa.cpp:330-336 (same message).
+    // partition_by_degree, lpa.cpp:330-336 (same message), over the input's ids:
+    // only the offsets are needed.
     if (switch_degree < 2) throw Error(NULPA_EINVAL, "switch-degree must be >= 2");
     check_host_csr(csr);
-    HostGraph hg(csr, 0);
-    nulpa_graph* g = hg.g;
+    use_device(0);
+    const uint32_t n = csr->n;
     Stream stream;
-    DevArray<uint32_t> d_low(g->n + 1), d_high(g->n + 1);
+    DevArray<uint64_t> off(uint64_t(n) + 1);
+    off.upload(csr->offsets);
+    DevArray<uint32_t> d_low(n + 1), d_high(n + 1);
     uint64_t nl = 0, nh = 0;
-    partition_two_way(g->offsets, g->n, switch_degree, d_low.p, d_high.p, &nl, &nh, stream.s);
+    partition_two_way(off.p, n, switch_degree, d_low.p, d_high.p, &nl, &nh, stream.s);
     if (nl) NULPA_CUDA(cudaMemcpy(low, d_low.p, nl * 4, cudaMemcpyDeviceToHost));
     if (nh) NULPA_CUDA(cudaMemcpy(high, d_high.p, nh * 4, cudaMemcpyDeviceToHost));
     *n_low = nl;
@@ -896,7 +947,7 @@ int nulpa_session_init(nulpa_session* ss) {
     if (!ss) throw Error(NULPA_EINVAL, "null session");
     use_device(ss->g->device);
     k_init<<<grid_for(ss->g->n, 256, ss->sms * 8), 256, 0, ss->stream.s>>>(
-        ss->labels, ss->flags, ss->g->offsets, ss->g->n);
+        ss->labels, ss->flags, ss->g->offsets, ss->g->n, ss->g->perm);
     NULPA_CUDA(cudaGetLastError());
     NULPA_CUDA(cudaStreamSynchronize(ss->stream.s));
     ss->fresh = true;

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "internal.hpp"
+#include "layout.hpp"
 #include "plan.hpp"
 
 namespace nulpa {
@@ -228,6 +229,9 @@ void finalize_graph(nulpa_graph* g, cudaStream_t s) {
   dfree(d_max);
   dfree(d_sum);
   dfree(d_nonunit);
+  // Position-order residency (layout.cu); rows_simple above refers to the input
+  // numbering, in which the in-row order is kept.
+  relayout_graph(g, s);
 }
 
 void partition_two_way(const uint64_t* off, uint32_t n, uint32_t sw, uint32_t* low,
@@ -550,6 +554,8 @@ int nulpa_graph_free(nulpa_graph* g) {
       dfree(g->targets);
       dfree(g->weights);
     }
+    dfree(g->perm);
+    dfree(g->inv);
     delete g;
   });
 }
@@ -582,16 +588,8 @@ int nulpa_graph_download(const nulpa_graph* g, uint64_t* offsets, uint32_t* targ
   return guarded([&] {
     if (!g) throw Error(NULPA_EINVAL, "null graph");
     use_device(g->device);
-    if (offsets)
-      NULPA_CUDA(cudaMemcpy(offsets, g->offsets, (uint64_t(g->n) + 1) * 8, cudaMemcpyDeviceToHost));
-    if (targets && g->m2)
-      NULPA_CUDA(cudaMemcpy(targets, g->targets, g->m2 * 4, cudaMemcpyDeviceToHost));
-    if (weights) {
-      if (g->weights)
-        NULPA_CUDA(cudaMemcpy(weights, g->weights, g->m2 * 4, cudaMemcpyDeviceToHost));
-      else
-        std::fill(weights, weights + g->m2, 1.0f);
-    }
+    download_vertex_order(g, offsets, targets, g->weights ? weights : nullptr);
+    if (weights && !g->weights) std::fill(weights, weights + g->m2, 1.0f);
   });
 }
 

@@ -75,6 +75,12 @@ struct nulpa_graph {
   uint32_t max_degree = 0;
   double total_2m = 0.0;  // sum of stored weights (graph.cpp:170-171)
   bool rows_simple = false;  // every row strictly ascending (no duplicate targets)
+  // Position-order layout (layout.cu): the arrays above are stored by position;
+  // perm[p] = vertex id at position p, inv[v] = position of vertex v. Both are
+  // nullptr under the identity layout (position == vertex id).
+  int layout = NULPA_LAYOUT_IDENTITY;
+  uint32_t* perm = nullptr;  // device
+  uint32_t* inv = nullptr;   // device
   nulpa::Plan* plan = nullptr;  // cached tiering (plan.hpp)
 };
 

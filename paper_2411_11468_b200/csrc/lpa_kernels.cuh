@@ -667,9 +667,11 @@ __global__ void __launch_bounds__(256) k_first_pass(PassCtx c, uint32_t v_lo, ui
     if (d == 0) continue;
     uint32_t cand = __ldg(c.g.tgt + lo);
     if (cand == i) cand = d > 1 ? __ldg(c.g.tgt + lo + 1) : kEmpty;  // self-loop skipped
+    if (cand != kEmpty) cand = vertex_id(c.vid, cand);  // rows keep the input's in-row order
+    const uint32_t own = vertex_id(c.vid, i);           // identity labels: label = vertex id
     ++n_v;
     n_e += d > 1 ? 2 : 1;
-    const bool allowed = cand != kEmpty && (c.pick_less ? cand < i : cand != i);
+    const bool allowed = cand != kEmpty && (c.pick_less ? cand < own : cand != own);
     if (!allowed) continue;
     c.lab_out[i] = cand;
     ++n_dn;
@@ -908,7 +910,8 @@ __global__ void __launch_bounds__(kBlockThreads) k_sequential(PassCtx c, void* g
   __shared__ Best<VBits<W>> red[32];
   __shared__ int s_flag;
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
-  for (uint32_t i = 0; i < c.g.n; ++i) {
+  for (uint32_t v = 0; v < c.g.n; ++v) {
+    const uint32_t i = position_of(c.pos, v);  // ascending vertex id (lpa.hpp:129)
     if (threadIdx.x == 0) {
       int skip = 1;
       if (!c.flags[i]) {
@@ -981,8 +984,10 @@ __global__ void __launch_bounds__(kBlockThreads) k_sequential(PassCtx c, void* g
 // reverts. revert(i) = changed(i) && i > c_i && final(c_i) != c_i with
 // final(v) = revert(v) ? prev[v] : lab[v]: a recursion on strictly smaller ids,
 // solved by Jacobi rounds until no flag moves (depth-bounded).
+// Arrays are in position order; label values (and the i > c* rule) are vertex ids.
 __global__ void k_cc_round(const uint32_t* lab, const uint32_t* prev, const uint8_t* r_in,
-                           uint8_t* r_out, uint32_t n, unsigned long long* moved) {
+                           uint8_t* r_out, uint32_t n, unsigned long long* moved,
+                           const uint32_t* vid, const uint32_t* pos) {
   unsigned long long mv = 0;
   const uint32_t bound = (n + 31u) & ~31u;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < bound;
@@ -990,8 +995,9 @@ __global__ void k_cc_round(const uint32_t* lab, const uint32_t* prev, const uint
     if (i >= n) continue;
     const uint32_t ci = lab[i];
     uint8_t r = 0;
-    if (ci != prev[i] && i > ci) {
-      const uint32_t fc = r_in[ci] ? prev[ci] : lab[ci];
+    if (ci != prev[i] && vertex_id(vid, i) > ci) {
+      const uint32_t pc = position_of(pos, ci);
+      const uint32_t fc = r_in[pc] ? prev[pc] : lab[pc];
       r = fc != ci ? 1 : 0;
     }
     if (r != r_in[i]) ++mv;

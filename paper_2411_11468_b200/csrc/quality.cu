@@ -10,6 +10,7 @@
 #include <cub/cub.cuh>
 
 #include "internal.hpp"
+#include "layout.hpp"
 #include "plan.hpp"
 
 namespace nulpa {
@@ -157,11 +158,20 @@ void check_labels(nulpa_graph* g, const uint32_t* lab, cudaStream_t s) {
 
 }  // namespace
 
-double modularity_device(nulpa_graph* g, const uint32_t* lab, cudaStream_t s) {
-  check_labels(g, lab, s);
+// `labels` in vertex order (community ids are label values, so only the row
+// order changes under the position layout).
+double modularity_device(nulpa_graph* g, const uint32_t* labels, cudaStream_t s) {
+  check_labels(g, labels, s);
   if (!(g->total_2m > 0.0))
     throw Error(NULPA_EINVAL, "modularity is undefined on a graph without edges");
   const uint32_t n = g->n;
+  uint32_t* lab_pos = nullptr;
+  const uint32_t* lab = labels;
+  if (g->perm) {
+    lab_pos = dalloc<uint32_t>(n);
+    to_positions_u32(g, labels, lab_pos, s);
+    lab = lab_pos;
+  }
   // Any tiering covers every row once: reuse the cached plan when there is one.
   Plan* p = g->plan ? g->plan : get_plan(g, resolve_tiers(32, nullptr), 4, s);
   double* sigma = dalloc<double>(2ull * n + 1);
@@ -187,6 +197,7 @@ double modularity_device(nulpa_graph* g, const uint32_t* lab, cudaStream_t s) {
   NULPA_CUDA(cudaMemcpyAsync(&q, d_q, sizeof q, cudaMemcpyDeviceToHost, s));
   NULPA_CUDA(cudaStreamSynchronize(s));
   dfree(sigma);
+  dfree(lab_pos);
   return q;
 }
 

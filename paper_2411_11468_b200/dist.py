@@ -1,8 +1,9 @@
 """Partitioned multi-GPU ν-LPA: one process per GPU, torch.distributed plumbing.
 
-Layout: a 1-D edge-balanced vertex partition (rank p owns [b_p, b_{p+1}) with
-offsets[b_p] ~ p*m2/P, `nulpa_graph_edge_ranges`); labels u32[n] and wake flags u8[n]
-are replicated on every rank. Each pass:
+Layout: a 1-D edge-balanced partition of the resident position order (rank p owns
+positions [b_p, b_{p+1}) with offsets[b_p] ~ p*m2/P, `nulpa_graph_edge_ranges`); labels
+u32[n] and wake flags u8[n] are replicated on every rank, in position order
+(`DeviceRangeEngine.vertex_labels` returns vertex order). Each pass:
 
 1. every rank runs one pass over its own range (`nulpa_session_pass`): ParallelAsync
    in place inside the range, Synchronous into a staging buffer then applied;
@@ -73,6 +74,13 @@ class DeviceRangeEngine:
 
     def init(self):
         _capi.check(_capi.lib().nulpa_session_init(self._h))
+
+    def vertex_labels(self):
+        """The replicated labels (position order inside the session) in vertex order."""
+        import torch
+        out = torch.empty_like(self.labels)
+        self._dg.labels_to_vertex_order(self.labels.data_ptr(), out.data_ptr())
+        return out
 
     def pass_(self, pick_less: bool, wake: bool = True) -> dict:
         info = _capi.nulpa_pass_info()

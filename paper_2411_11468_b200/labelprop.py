@@ -266,8 +266,16 @@ def cross_check(g: CsrGraph, labels: np.ndarray, prev, flags: np.ndarray) -> int
     return int(rev.value)
 
 
+def set_default_layout(layout: int) -> None:
+    """Layout of graphs created afterwards (nulpa_set_default_layout)."""
+    _capi.check(_capi.lib().nulpa_set_default_layout(int(layout)))
+
+
 class DeviceGraph:
-    """A CSR resident in HBM (nulpa_graph). Build by upload or on-device generator."""
+    """A CSR resident in HBM (nulpa_graph). Build by upload or on-device generator.
+
+    Rows are stored in position order (degree buckets, see include/nulpa/nulpa.h); every
+    label array this class takes or returns is in vertex order."""
 
     def __init__(self, handle: int, device: int = 0):
         self._h = C.c_void_p(handle)
@@ -321,7 +329,22 @@ class DeviceGraph:
                                                      _ptr(w) if w is not None else None))
         return CsrGraph(off, tgt, w)
 
+    @property
+    def layout(self) -> int:
+        """NULPA_LAYOUT_IDENTITY or NULPA_LAYOUT_DEGREE_BUCKETS (position-order rows)."""
+        x = C.c_int()
+        _capi.check(_capi.lib().nulpa_graph_layout(self._h, C.byref(x)))
+        return x.value
+
+    def labels_to_vertex_order(self, pos_ptr: int, out_ptr: int) -> None:
+        """Device label array in position order (sessions) -> vertex order."""
+        _capi.check(_capi.lib().nulpa_graph_labels_to_vertex_order(self._h, pos_ptr, out_ptr))
+
+    def labels_to_position_order(self, vtx_ptr: int, out_ptr: int) -> None:
+        _capi.check(_capi.lib().nulpa_graph_labels_to_position_order(self._h, vtx_ptr, out_ptr))
+
     def device_csr(self) -> _capi.nulpa_csr:
+        """Device pointers of the resident arrays (position order, see `layout`)."""
         c = _capi.nulpa_csr()
         _capi.check(_capi.lib().nulpa_graph_device_csr(self._h, C.byref(c)))
         return c

@@ -126,7 +126,8 @@ def _gpu_worker(rank, world, port, scale, out):
     cfg = LpaConfig(exec=ExecMode.Synchronous)
     eng = DeviceRangeEngine(dg, cfg, bounds[rank], bounds[rank + 1])
     st = run_partitioned(eng, cfg, rank, world, Exchange(bounds, staged=True), dg.n)
-    out[rank] = (eng.labels.cpu().numpy().view(np.uint32).copy(), st.delta_n_per_iter, bounds)
+    out[rank] = (eng.vertex_labels().cpu().numpy().view(np.uint32).copy(), st.delta_n_per_iter,
+                 bounds)
     eng.free()
     dist.destroy_process_group()
 

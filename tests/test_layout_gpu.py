@@ -1,0 +1,108 @@
+"""The position-order residency (layout.cu): results must not depend on the layout.
+
+Under NULPA_LAYOUT_DEGREE_BUCKETS (the default) the resident rows are stored grouped by
+degree bucket; label values stay vertex ids and every label array crossing the ABI is in
+vertex order. These tests pin that: the downloaded CSR equals the identity-layout one, the
+bit-exact gates give the same answers under both layouts, and the position/vertex
+conversions invert each other.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2411_11468_b200 import _capi
+from paper_2411_11468_b200 import labelprop as lp
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def identity_layout():
+    lp.set_default_layout(_capi.NULPA_LAYOUT_IDENTITY)
+    yield
+    lp.set_default_layout(_capi.NULPA_LAYOUT_DEGREE_BUCKETS)
+
+
+def _gen(kind):
+    if kind == "rmat":
+        return lp.DeviceGraph.rmat(13, 16, 11)
+    if kind == "web":
+        return lp.DeviceGraph.web(20000, 160000, 2.1, 4, 5000, 3)
+    return lp.DeviceGraph.grid(97, 41)
+
+
+@pytest.mark.parametrize("kind", ["rmat", "web", "grid"])
+def test_download_is_layout_independent(kind):
+    dg = _gen(kind)
+    assert dg.layout == _capi.NULPA_LAYOUT_DEGREE_BUCKETS
+    a = dg.download()
+    lp.set_default_layout(_capi.NULPA_LAYOUT_IDENTITY)
+    try:
+        di = _gen(kind)
+        assert di.layout == _capi.NULPA_LAYOUT_IDENTITY
+        b = di.download()
+    finally:
+        lp.set_default_layout(_capi.NULPA_LAYOUT_DEGREE_BUCKETS)
+    assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.targets, b.targets)
+
+
+def test_position_order_is_degree_bucketed():
+    import torch
+    dg = _gen("rmat")
+    c = dg.device_csr()
+    off = torch.empty(dg.n + 1, dtype=torch.int64, device="cuda:0")
+    import cuda.bindings.runtime as rt
+    err, = rt.cudaMemcpy(off.data_ptr(), c.offsets, (dg.n + 1) * 8,
+                         rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+    assert err == rt.cudaError_t.cudaSuccess
+    deg = (off[1:] - off[:-1]).cpu().numpy()
+    bucket = np.where(deg == 0, -1, np.ceil(np.log2(np.maximum(deg, 1))).astype(int))
+    assert (np.diff(bucket) <= 0).all()  # largest bucket first, isolated last
+    # positions <-> vertices round trip, and vertex order is the input numbering
+    vid = torch.arange(dg.n, dtype=torch.int32, device="cuda:0")
+    pos = torch.empty_like(vid)
+    back = torch.empty_like(vid)
+    dg.labels_to_position_order(vid.data_ptr(), pos.data_ptr())
+    dg.labels_to_vertex_order(pos.data_ptr(), back.data_ptr())
+    assert torch.equal(back, vid)
+    perm = pos.cpu().numpy()
+    assert np.array_equal(np.sort(perm), np.arange(dg.n))
+    g = dg.download()
+    assert np.array_equal(np.diff(g.offsets.astype(np.int64))[perm], deg)
+
+
+@pytest.mark.parametrize("kind", ["rmat", "web", "grid"])
+def test_gates_identical_under_both_layouts(kind, identity_layout):
+    di = _gen(kind)
+    g = di.download()
+    lp.set_default_layout(_capi.NULPA_LAYOUT_DEGREE_BUCKETS)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    rng = np.random.default_rng(5)
+    lab = rng.integers(0, g.order(), g.order()).astype(np.uint32)
+    for pl in (0, 1):
+        want, wc = O.port_sync_step(pg, lab, pl)
+        for layout in (_capi.NULPA_LAYOUT_IDENTITY, _capi.NULPA_LAYOUT_DEGREE_BUCKETS):
+            lp.set_default_layout(layout)
+            got, gc = lp.sync_step(g, lab, pl)
+            assert gc == wc and np.array_equal(got, want), (kind, layout, pl)
+    want, ws = O.port_lpa(pg, exec_mode=2, pl_period=4, cc_period=2)
+    for layout in (_capi.NULPA_LAYOUT_IDENTITY, _capi.NULPA_LAYOUT_DEGREE_BUCKETS):
+        lp.set_default_layout(layout)
+        r = lp.lpa(g, lp.LpaConfig(exec=lp.ExecMode.Synchronous, pl_period=4, cc_period=2))
+        assert np.array_equal(r.labels, want) and r.stats.delta_n_per_iter == ws["delta_n"]
+        assert r.stats.cc_reverts == ws["cc_reverts"]
+
+
+def test_async_labels_are_vertex_ids_in_vertex_order():
+    dg = _gen("rmat")
+    g = dg.download()
+    r = dg.lpa(lp.LpaConfig())
+    lab = r.labels
+    assert lab.max() < g.order()
+    # every vertex's label is the id of a vertex in its closed neighbourhood's label set:
+    # at least, isolated vertices keep their own id (lpa.cpp:250-253)
+    deg = np.diff(g.offsets.astype(np.int64))
+    iso = np.flatnonzero(deg == 0)
+    assert np.array_equal(lab[iso], iso.astype(np.uint32))
+    q = lp.modularity(g, lab)
+    assert abs(q - O.port_modularity(O.PortGraph(g.offsets, g.targets, None), lab)) < 1e-9
