@@ -9,10 +9,11 @@
 //    +1 completeness sweep — the "strategy budget, then sweep" structure of
 //    hashtable.hpp:126-147 (all four ProbeStrategy advances are selectable);
 //  * unit-weight graphs (the common case) use ONE 64-bit word per slot,
-//    (key << 32) | count: a new key is claimed and counted by a single 64-bit
-//    CAS, an existing key is counted by a single 64-bit atomicAdd, and a slot
-//    is read with one load. Weighted graphs use split key / value arrays with
-//    CAS + atomicAdd (the reference's `shared` branch, hashtable.hpp:110-118).
+//    (key << 32) | count, read with one load by the argmax sweep; a key is
+//    claimed by a 32-bit CAS on the key half and counted by a 32-bit atomicAdd
+//    on the count half (both native shared-memory atomics). Weighted graphs use
+//    split key / value arrays with CAS + atomicAdd (the reference's `shared`
+//    branch, hashtable.hpp:110-118).
 // Placement is never observable in results: the argmax (higher value, ties to
 // the smaller key; hashtable.hpp:163-185) is order-independent. Warp argmax
 // uses two redux.sync instructions on order-preserving value bits.
@@ -251,7 +252,10 @@ __device__ __forceinline__ void probe_advance(int strategy, uint32_t& idx, uint3
 template <bool PACKED, typename W>
 struct Table;
 
-// Unit weights: one 64-bit word per slot, (key << 32) | count.
+// Unit weights: one 64-bit word per slot, (key << 32) | count, so the argmax
+// sweep reads a slot with one load. Updates use native 32-bit shared/global
+// atomics on the two halves (a 64-bit atomicAdd on shared memory is a CAS spin
+// loop in SASS): CAS on the key half to claim, atomicAdd on the count half.
 template <typename W>
 struct Table<true, W> {
   unsigned long long* w;
@@ -262,28 +266,35 @@ struct Table<true, W> {
   __device__ __forceinline__ void bind_split(void* base, void*) {
     w = static_cast<unsigned long long*>(base);
   }
+  __device__ __forceinline__ uint32_t* key_word(uint32_t s) const {
+    return reinterpret_cast<uint32_t*>(w + s) + 1;  // little-endian: high half
+  }
+  __device__ __forceinline__ uint32_t* count_word(uint32_t s) const {
+    return reinterpret_cast<uint32_t*>(w + s);
+  }
   __device__ __forceinline__ void clear_slot(uint32_t s) { w[s] = kEmptyWord; }
   __device__ __forceinline__ int add(uint32_t cap, int strategy, uint32_t key, W v,
                                      uint32_t* slot) {
     const uint32_t cnt = static_cast<uint32_t>(v);
-    const unsigned long long mine = (static_cast<unsigned long long>(key) << 32) | cnt;
-    const uint32_t mask = cap - 1, h2 = hash_step(key);
-    uint32_t idx = hash_start(key, cap), step = 1;
+    const uint32_t mask = cap - 1;
+    uint32_t idx = hash_start(key, cap), step = 1, h2 = 0;
     for (uint32_t t = 0; t < 2 * cap; ++t) {
       const uint32_t s = idx & mask;
-      unsigned long long cur = *((volatile unsigned long long*)(w + s));
-      if (cur == kEmptyWord) {
-        cur = atomicCAS(w + s, kEmptyWord, mine);
-        if (cur == kEmptyWord) {
-          *slot = s;
-          return 2;
+      uint32_t cur = *((volatile uint32_t*)key_word(s));
+      int r = 1;
+      if (cur == kEmpty) {
+        cur = atomicCAS(key_word(s), kEmpty, key);
+        if (cur == kEmpty) {
+          cur = key;
+          r = 2;
         }
       }
-      if (static_cast<uint32_t>(cur >> 32) == key) {
-        atomicAdd(w + s, static_cast<unsigned long long>(cnt));
+      if (cur == key) {
+        atomicAdd(count_word(s), cnt);
         *slot = s;
-        return 1;
+        return r;
       }
+      if (t == 0) h2 = hash_step(key);  // second hash only after a collision
       if (t + 1 >= cap)
         idx += 1;  // completeness sweep
       else
@@ -359,9 +370,13 @@ struct Table<false, W> {
 
 // Smallest power of two >= x (x >= 1).
 __host__ __device__ __forceinline__ uint32_t pow2_ceil(uint32_t x) {
+#ifdef __CUDA_ARCH__
+  return x <= 1 ? 1u : 1u << (32 - __clz(x - 1));
+#else
   uint32_t p = 1;
   while (p < x) p <<= 1;
   return p;
+#endif
 }
 
 // ---- counter aggregation ---------------------------------------------------------

@@ -61,9 +61,10 @@ struct RowDegree {
   }
 };
 
-// dst row r <- src row src_row[r], every target t translated to map[t].
-// A warp owns 32 consecutive destination rows: a lane copies its own row when
-// it is short; longer rows are copied by the whole warp, one at a time.
+// dst row r <- src row src_row[r], every target t translated to map[t], for
+// rows [r0, n). A warp owns 32 consecutive destination rows: a lane copies its
+// own row when it is short; longer rows are copied by the whole warp, one at a
+// time (rows here are <= kLongRow, so a warp's share stays bounded).
 __global__ void __launch_bounds__(256) k_permute_rows(const uint64_t* __restrict__ src_off,
                                                       const uint32_t* __restrict__ src_tgt,
                                                       const float* __restrict__ src_w,
@@ -71,12 +72,13 @@ __global__ void __launch_bounds__(256) k_permute_rows(const uint64_t* __restrict
                                                       const uint32_t* __restrict__ map,
                                                       const uint64_t* __restrict__ dst_off,
                                                       uint32_t* __restrict__ dst_tgt,
-                                                      float* __restrict__ dst_w, uint32_t n) {
+                                                      float* __restrict__ dst_w, uint32_t r0,
+                                                      uint32_t n) {
   constexpr uint32_t kShort = 8;
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t base = gw * 32; base < n; base += nw * 32) {
+  for (uint32_t base = r0 + gw * 32; base < n; base += nw * 32) {
     const uint32_t r = base + lane;
     uint64_t slo = 0, dlo = 0;
     uint32_t d = 0;
@@ -107,6 +109,52 @@ __global__ void __launch_bounds__(256) k_permute_rows(const uint64_t* __restrict
   }
 }
 
+// The long-row prefix [0, P) of a bucketed layout (rows of more than kLongRow
+// entries, up to millions): edge-balanced — every warp owns kSpan consecutive
+// destination entries, finds its first row by binary search and walks rows.
+constexpr uint32_t kLongRow = 256;
+constexpr uint64_t kSpan = 4096;
+
+__global__ void __launch_bounds__(256) k_permute_long_rows(
+    const uint64_t* __restrict__ src_off, const uint32_t* __restrict__ src_tgt,
+    const float* __restrict__ src_w, const uint32_t* __restrict__ src_row,
+    const uint32_t* __restrict__ map, const uint64_t* __restrict__ dst_off,
+    uint32_t* __restrict__ dst_tgt, float* __restrict__ dst_w, uint32_t P) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (gridDim.x * uint64_t(blockDim.x)) >> 5;
+  const uint64_t E = dst_off[P];
+  for (uint64_t e0 = gw * kSpan; e0 < E; e0 += nw * kSpan) {
+    const uint64_t e1 = min(E, e0 + kSpan);
+    uint32_t lo = 0, hi = P;  // dst_off[lo] <= e0 < dst_off[hi]
+    while (hi - lo > 1) {
+      const uint32_t mid = lo + (hi - lo) / 2;
+      if (dst_off[mid] <= e0)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    uint32_t r = lo;
+    for (uint64_t e = e0; e < e1; ++r) {
+      const uint64_t row_end = min(dst_off[r + 1], e1);
+      const uint64_t sb = src_off[src_row[r]] + (e - dst_off[r]);
+      const uint32_t len = static_cast<uint32_t>(row_end - e);
+      for (uint32_t k = lane; k < len; k += 32) {
+        dst_tgt[e + k] = map[src_tgt[sb + k]];
+        if (src_w) dst_w[e + k] = src_w[sb + k];
+      }
+      e = row_end;
+    }
+  }
+}
+
+struct LongRow {
+  const uint64_t* off;
+  __host__ __device__ uint32_t operator()(uint32_t v) const {
+    return off[v + 1] - off[v] > kLongRow ? 1u : 0u;
+  }
+};
+
 template <typename T>
 __global__ void k_gather(const T* __restrict__ src, const uint32_t* __restrict__ idx, uint32_t n,
                          T* __restrict__ dst) {
@@ -120,9 +168,12 @@ unsigned blocks_for(uint64_t work) {
 }
 
 // Build dst_off (exclusive scan of the permuted row degrees) and the rows.
+// `long_prefix` = number of leading destination rows longer than kLongRow (the
+// bucketed layout puts them first; 0 when unknown).
 void permute_csr(const uint64_t* src_off, const uint32_t* src_tgt, const float* src_w,
                  const uint32_t* src_row, const uint32_t* map, uint32_t n, uint64_t m2,
-                 uint64_t* dst_off, uint32_t* dst_tgt, float* dst_w, cudaStream_t s) {
+                 uint64_t* dst_off, uint32_t* dst_tgt, float* dst_w, cudaStream_t s,
+                 uint32_t long_prefix = 0) {
   NULPA_CUDA(cudaMemsetAsync(dst_off, 0, sizeof(uint64_t), s));
   if (n > 0) {
     auto degs = cub::TransformInputIterator<uint64_t, RowDegree, cub::CountingInputIterator<uint32_t>>(
@@ -131,9 +182,12 @@ void permute_csr(const uint64_t* src_off, const uint32_t* src_tgt, const float* 
     cub::DeviceScan::InclusiveSum(nullptr, tb, degs, dst_off + 1, n, s);
     void* tmp = dmalloc(tb);
     cub::DeviceScan::InclusiveSum(tmp, tb, degs, dst_off + 1, n, s);
-    if (m2)
-      k_permute_rows<<<blocks_for(uint64_t(n) / 8 + 1), 256, 0, s>>>(
-          src_off, src_tgt, src_w, src_row, map, dst_off, dst_tgt, dst_w, n);
+    if (m2 && long_prefix)
+      k_permute_long_rows<<<148 * 8, 256, 0, s>>>(src_off, src_tgt, src_w, src_row, map,
+                                                  dst_off, dst_tgt, dst_w, long_prefix);
+    if (m2 && long_prefix < n)
+      k_permute_rows<<<blocks_for(uint64_t(n - long_prefix) / 8 + 1), 256, 0, s>>>(
+          src_off, src_tgt, src_w, src_row, map, dst_off, dst_tgt, dst_w, long_prefix, n);
     NULPA_CUDA(cudaGetLastError());
     NULPA_CUDA(cudaStreamSynchronize(s));
     dfree(tmp);
@@ -173,10 +227,26 @@ void relayout_graph(nulpa_graph* g, cudaStream_t s) {
   uint32_t* inv = dalloc<uint32_t>(n);
   k_invert<<<blocks_for(n), 256, 0, s>>>(perm, n, inv);
   NULPA_CUDA(cudaGetLastError());
+  // Rows longer than kLongRow form a prefix of the position order (their
+  // buckets come first): copy them edge-balanced.
+  uint32_t long_rows = 0;
+  {
+    auto is_long = cub::TransformInputIterator<uint32_t, LongRow, cub::CountingInputIterator<uint32_t>>(
+        cub::CountingInputIterator<uint32_t>(0), LongRow{g->offsets});
+    uint32_t* d_cnt = dalloc<uint32_t>(1);
+    size_t tb = 0;
+    cub::DeviceReduce::Sum(nullptr, tb, is_long, d_cnt, n, s);
+    void* tmp = dmalloc(tb);
+    cub::DeviceReduce::Sum(tmp, tb, is_long, d_cnt, n, s);
+    NULPA_CUDA(cudaMemcpyAsync(&long_rows, d_cnt, 4, cudaMemcpyDeviceToHost, s));
+    NULPA_CUDA(cudaStreamSynchronize(s));
+    dfree(tmp);
+    dfree(d_cnt);
+  }
   uint64_t* off = dalloc<uint64_t>(uint64_t(n) + 1);
   uint32_t* tgt = dalloc<uint32_t>(m2);
   float* w = g->weights ? dalloc<float>(m2) : nullptr;
-  permute_csr(g->offsets, g->targets, g->weights, perm, inv, n, m2, off, tgt, w, s);
+  permute_csr(g->offsets, g->targets, g->weights, perm, inv, n, m2, off, tgt, w, s, long_rows);
   if (g->owns) {
     dfree(g->offsets);
     dfree(g->targets);
