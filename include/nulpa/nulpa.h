@@ -93,9 +93,6 @@ typedef struct nulpa_tuning {
                                  asynchronous schedule; Synchronous/Sequential results do
                                  not depend on it. */
   uint32_t no_identity_first; /* 1: disable the table-free first pass from identity labels */
-  uint32_t stage_rows;        /* 1: team tiers gather their rows' labels ahead into an
-                                 edge-aligned buffer (k_stage_rows), then aggregate from it */
-  uint32_t reserved;
 } nulpa_tuning;
 
 #define NULPA_TIERS 10 /* 0 thread, 1 half-warp, 2 warp, 3/4/5 32/128/256-thread teams with

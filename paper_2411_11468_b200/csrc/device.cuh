@@ -95,13 +95,8 @@ struct PassCtx {
   int strategy;
   int wake;                       // store neighbour wake-ups (0 when provably dead, see engine.cu)
   unsigned int* work;             // dynamic work counter (cluster tier)
-  const uint32_t* vid = nullptr;  // position -> vertex id (layout.cu); nullptr = identity
-  const uint32_t* pos = nullptr;  // vertex id -> position; nullptr = identity
-  // Staged team tiers (k_stage_rows): the neighbour labels of every claimed row,
-  // gathered ahead into an edge-aligned buffer (kEmpty for self-loops), and the
-  // claim result per list entry. nullptr = gather inline.
-  uint32_t* lab_e = nullptr;
-  uint8_t* act = nullptr;
+  const uint32_t* vid;            // position -> vertex id (layout.cu); nullptr = identity
+  const uint32_t* pos;            // vertex id -> position; nullptr = identity
 };
 
 // Vertex id stored at position p (label values are vertex ids).

@@ -72,30 +72,16 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   constexpr size_t big_smem = team_bytes<Tab, kBigCap, kBigMax>();
   constexpr size_t cluster_smem = cluster_bytes<Tab>();
   constexpr size_t hub_smem = kHubCap * Tab::kSlotBytes;
-  const bool staged = p.stage_rows;
-  auto k_wt = staged ? k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, true>
-                     : k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax>;
-  auto k_b1 = staged ? k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax, true>
-                     : k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax>;
-  auto k_b2 = staged ? k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max, true>
-                     : k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max>;
-  auto k_bg = staged ? k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax, true>
-                     : k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax>;
-  if (staged) {
-    c.lab_e = p.lab_e;
-    c.act = p.act;
-  }
+  auto k_wt = k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax>;
+  auto k_b1 = k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax>;
+  auto k_b2 = k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max>;
+  auto k_bg = k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax>;
   static bool init = false;
   if (!init) {
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, true>, wtab_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax, true>, block_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max, true>, block2_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax, true>,
-               big_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax>, wtab_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax>, block_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max>, block2_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax>, big_smem);
+    allow_smem(k_wt, wtab_smem);
+    allow_smem(k_b1, block_smem);
+    allow_smem(k_b2, block2_smem);
+    allow_smem(k_bg, big_smem);
     allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
     allow_smem(k_hub_accum<MODE, W, WEIGHTED>, hub_smem);
     init = true;
@@ -104,11 +90,6 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   auto tier = [&](int t) {
     c.ctr = ctr + t * C_COUNT;
     prof.begin(t, s);
-    if (staged && t >= T_WTAB && t <= T_BIG) {
-      k_stage_rows<MODE><<<grid_for(p.count[t], 8, sms * 16), 256, 0, s>>>(c, p.list[t],
-                                                                          p.count[t]);
-      ++launches;
-    }
   };
   if (p.count[T_THREAD]) {
     tier(T_THREAD);

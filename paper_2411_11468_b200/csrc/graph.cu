@@ -301,8 +301,6 @@ Plan::~Plan() {
   dfree(changed);
   dfree(item_hub);
   dfree(item_start);
-  dfree(lab_e);
-  dfree(act);
 }
 
 TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* t) {
@@ -318,14 +316,13 @@ TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* t) {
   uint32_t bmax = (t && t->block_max_degree) ? t->block_max_degree : uint32_t(dev::kBlockMax);
   bmax = std::max<uint32_t>(std::min<uint32_t>(bmax, dev::kBlockMax), wmax);
   const uint32_t sched = (t && t->schedule) ? t->schedule : 2u;  // default: scrambled
-  return {tmax, wmax, bmax, sched, t && t->stage_rows};
+  return {tmax, wmax, bmax, sched};
 }
 
 Plan* get_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStream_t s) {
   if (g->plan && g->plan->thread_max == tb.thread_max && g->plan->warp_max == tb.warp_max &&
       g->plan->block_max == tb.block_max && g->plan->schedule == tb.schedule &&
-      g->plan->value_bytes == value_bytes && g->plan->v_lo == 0 && g->plan->v_hi == g->n &&
-      g->plan->stage_rows == tb.stage_rows)
+      g->plan->value_bytes == value_bytes && g->plan->v_lo == 0 && g->plan->v_hi == g->n)
     return g->plan;
   delete g->plan;
   g->plan = nullptr;
@@ -390,13 +387,6 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
       for (int t = dev::T_HALF; t < dev::T_HUB; ++t) scramble_list(p->list[t], p->count[t], s);
     }
 
-    if (tb.stage_rows) {
-      p->stage_rows = true;
-      uint32_t most = 1;
-      for (int t = dev::T_WTAB; t <= dev::T_BIG; ++t) most = std::max(most, p->count[t]);
-      p->lab_e = dalloc<uint32_t>(g->m2 + 1);
-      p->act = dalloc<uint8_t>(most);
-    }
     // Hub tier: per-hub global tables and (hub, chunk) work items. Hub counts
     // are small (vertices of degree > block_max), so the layout is built on
     // the host.

@@ -256,65 +256,6 @@ __device__ __forceinline__ void team_gather(const PassCtx& c, uint32_t i, uint64
   }
 }
 
-// Gather edges [e0, e1) of vertex i from the staged label buffer (k_stage_rows).
-template <typename W, bool WEIGHTED, typename Tab, int U = 4>
-__device__ __forceinline__ void team_gather_staged(const PassCtx& c, uint64_t lo, uint32_t e0,
-                                                   uint32_t e1, Tab& tab, uint32_t cap,
-                                                   uint32_t tid, uint32_t T, uint64_t pol,
-                                                   uint16_t* occ, unsigned* occ_n,
-                                                   unsigned long long& fails) {
-  for (uint32_t base = e0; base < e1; base += T * U) {
-    uint32_t lab[U];
-    W w[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t e = base + u * T + tid;
-      lab[u] = e < e1 ? ld_stream(c.lab_e + lo + e, pol) : kEmpty;
-      w[u] = lab[u] != kEmpty ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      gather_insert<W, WEIGHTED>(c, lab[u], w[u], tab, cap, occ, occ_n, fails);
-  }
-}
-
-// Claim every vertex of a tier list and gather its neighbour labels into
-// c.lab_e (one warp per vertex, 4 loads in flight per lane). Any order of the
-// reads is a legal asynchronous schedule; Synchronous mode reads the snapshot.
-template <int MODE>
-__global__ void __launch_bounds__(256) k_stage_rows(PassCtx c, const uint32_t* __restrict__ list,
-                                                    uint32_t count) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  const uint64_t pol = policy_evict_first();
-  for (uint32_t t = gw; t < count; t += nw) {
-    const uint32_t i = __ldg(list + t);
-    int skip = 0;
-    if (lane == 0) {
-      skip = claim_vertex(c, i) ? 1 : 0;
-      c.act[t] = skip ? 0 : 1;
-    }
-    if (__shfl_sync(kFull, skip, 0)) continue;
-    const uint64_t lo = __ldg(c.g.off + i);
-    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
-    constexpr int U = 4;
-    for (uint32_t base = 0; base < d; base += 32 * U) {
-      uint32_t j[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t e = base + u * 32 + lane;
-        j[u] = e < d ? ld_stream(c.g.tgt + lo + e, pol) : i;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t e = base + u * 32 + lane;
-        if (e < d) c.lab_e[lo + e] = j[u] != i ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
-      }
-    }
-  }
-}
-
 // Argmax over the occupied slots [tid, n_occ) step T; resets them as it goes.
 template <typename W, typename Tab>
 __device__ __forceinline__ Best<VBits<W>> occ_argmax_reset(Tab& tab, const uint16_t* occ,
@@ -513,8 +454,7 @@ constexpr size_t team_bytes() {
   return size_t(CAP) * Tab::kSlotBytes + size_t(MAXD) * sizeof(uint16_t);
 }
 
-template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CAP, int MAXD,
-          bool STAGED = false>
+template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CAP, int MAXD>
 __global__ void __launch_bounds__(CTA_THREADS) k_team(PassCtx c, const uint32_t* __restrict__ list,
                                                       uint32_t count) {
   static_assert(CTA_THREADS % TEAM == 0 && TEAM % 32 == 0, "team shape");
@@ -543,10 +483,7 @@ __global__ void __launch_bounds__(CTA_THREADS) k_team(PassCtx c, const uint32_t*
   for (uint32_t t = blockIdx.x * kTeams + team; t < count; t += stride) {
     const uint32_t i = __ldg(list + t);
     if (ttid == 0) {
-      if constexpr (STAGED)
-        s_flag[team] = c.act[t] ? 0 : 1;  // claimed by k_stage_rows
-      else
-        s_flag[team] = claim_vertex(c, i) ? 1 : 0;
+      s_flag[team] = claim_vertex(c, i) ? 1 : 0;
       s_occ_n[team] = 0;
     }
     const uint64_t lo = __ldg(c.g.off + i);
@@ -557,12 +494,8 @@ __global__ void __launch_bounds__(CTA_THREADS) k_team(PassCtx c, const uint32_t*
       sync();  // s_flag is rewritten by the next iteration
       continue;
     }
-    if constexpr (STAGED)
-      team_gather_staged<W, WEIGHTED>(c, lo, 0, d, tab, cap, ttid, TEAM, pol, occ,
-                                      &s_occ_n[team], fails);
-    else
-      team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, ttid, TEAM, pol, occ,
-                                     &s_occ_n[team], fails);
+    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, ttid, TEAM, pol, occ,
+                                   &s_occ_n[team], fails);
     sync();
     Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n[team], ttid, TEAM);
     b = team_best<TEAM>(b, s_red[team], ttid, bar);

@@ -10,9 +10,6 @@ namespace nulpa {
 
 struct Plan {
   uint32_t thread_max = 0, warp_max = 0, block_max = 0, schedule = 1;
-  bool stage_rows = false;  // team tiers staged through lab_e / act
-  uint32_t* lab_e = nullptr;  // [m2] staged neighbour labels (stage_rows)
-  uint8_t* act = nullptr;     // [max team-tier count] claim results (stage_rows)
   uint32_t v_lo = 0, v_hi = 0;  // vertex range the tiers cover
   int value_bytes = 4;  // hashtable value width the hub tables were sized for
   // Tier vertex lists (ascending id unless scrambled), indexed by dev::Tier;
@@ -65,7 +62,6 @@ struct Plan {
 struct TierBounds {
   uint32_t thread_max, warp_max, block_max;
   uint32_t schedule;  // 1 ascending id, 2 scrambled
-  bool stage_rows;
 };
 
 // Resolve the tier bounds from LpaConfig.switch_degree and the tuning struct.

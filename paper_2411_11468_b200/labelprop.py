@@ -103,7 +103,6 @@ class Tuning:
     schedule: int = 0  # 0 default, 1 ascending id, 2 scrambled
     profile: bool = False
     identity_first: bool = True  # table-free first pass from identity labels
-    stage_rows: bool = False  # team tiers: gather labels ahead (k_stage_rows)
 
     def to_c(self) -> _capi.nulpa_tuning:
         t = _capi.nulpa_tuning()
@@ -113,7 +112,6 @@ class Tuning:
         t.schedule = self.schedule
         t.profile = 1 if self.profile else 0
         t.no_identity_first = 0 if self.identity_first else 1
-        t.stage_rows = 1 if self.stage_rows else 0
         return t
 
 

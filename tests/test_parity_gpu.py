@@ -149,20 +149,6 @@ def test_sync_trajectory_vs_port(kind, size):
         assert r.stats.cc_reverts == ws["cc_reverts"]
 
 
-@pytest.mark.parametrize("kind,size", [("rmat", 14), ("web", 20000)])
-def test_staged_rows_bit_exact(kind, size):
-    """Team tiers with the labels gathered ahead (tuning.stage_rows): same sync step and
-    Synchronous trajectory as the reference."""
-    dg, g = _device_graph(kind, size)
-    pg = O.PortGraph(g.offsets, g.targets, None)
-    tn = lp.Tuning(stage_rows=True)
-    want, ws = O.port_lpa(pg, exec_mode=2, pl_period=4)
-    r = dg.lpa(lp.LpaConfig(exec=lp.ExecMode.Synchronous, pl_period=4), tn)
-    assert np.array_equal(r.labels, want) and r.stats.delta_n_per_iter == ws["delta_n"]
-    a = dg.lpa(lp.LpaConfig(), tn)
-    assert 1 <= a.stats.iterations <= 20 and a.labels.max() < g.order()
-
-
 def test_sequential_vs_port_small_rmat():
     dg, g = _device_graph("rmat", 10)
     pg = O.PortGraph(g.offsets, g.targets, None)

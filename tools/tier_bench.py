@@ -6,12 +6,11 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2411_11468_b200 import labelprop as lp, _capi
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 27
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-stage = len(sys.argv) > 3 and sys.argv[3] == "stage"
 t0 = time.time()
 dg = lp.DeviceGraph.rmat(scale, 16, 1)
 print(f"scale {scale}: n={dg.n} m2={dg.m2} build {time.time()-t0:.2f}s", flush=True)
 cfg = lp.LpaConfig()
-t = lp.Tuning(profile=True, stage_rows=stage)
+t = lp.Tuning(profile=True)
 for _ in range(2):
     dg.lpa(cfg, t, want_host=False)
 import ctypes as C, numpy as np
@@ -23,6 +22,6 @@ for _ in range(reps):
     tc = t.to_c()
     _capi.check(_capi.lib().nulpa_run_graph(dg._h, C.byref(o), C.byref(tc), None, None, C.byref(st)))
     tot += np.array([st.tier_ms[i] for i in range(_capi.NULPA_TIERS)]); loop += st.elapsed_seconds
-print(f"{'staged ' if stage else ''}loop {loop/reps*1e3:.1f} ms  iters {st.iterations} dn {dn[:st.iterations].tolist()} "
+print(f"loop {loop/reps*1e3:.1f} ms  iters {st.iterations} dn {dn[:st.iterations].tolist()} "
       f"-> {dg.m2/(loop/reps)/1e9:.2f} G edges/s")
 print("tiers ms:", {n: round(x / reps, 2) for n, x in zip(_capi.TIER_NAMES, tot) if x})
