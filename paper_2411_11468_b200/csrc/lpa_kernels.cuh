@@ -250,9 +250,12 @@ __device__ __forceinline__ void team_gather(const PassCtx& c, uint32_t i, uint64
       lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
       w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
     }
+    // Skip warp-rounds with no edge at all (warp-uniform test): short rows do not
+    // pay for the unrolled tail.
+    const uint32_t wbase = base + (tid & ~31u);
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      gather_insert<W, WEIGHTED>(c, lab[u], w[u], tab, cap, occ, occ_n, fails);
+      if (wbase + u * T < e1) gather_insert<W, WEIGHTED>(c, lab[u], w[u], tab, cap, occ, occ_n, fails);
   }
 }
 
@@ -594,8 +597,10 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
         lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
         w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
       }
+      const uint32_t wbase = base + (threadIdx.x & ~31u);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
+        if (wbase + u * blockDim.x >= e1) break;  // warp-uniform: no edge left for this warp
         const unsigned peers = __match_any_sync(kFull, lab[u]);
         W s;
         if constexpr (WEIGHTED)
