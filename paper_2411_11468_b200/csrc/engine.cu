@@ -45,6 +45,22 @@ void allow_smem(K kernel, size_t bytes) {
                                   static_cast<int>(bytes)));
 }
 
+// Grid for a grid-stride kernel: enough CTAs for `work` items at `per_block`
+// items per CTA, but never more than fit on the device at once (one wave), so no
+// second partial wave leaves most SMs idle at the end of the tier.
+template <typename K>
+unsigned resident_grid(K kernel, int threads, size_t smem, uint64_t work, unsigned per_block,
+                       int sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) !=
+          cudaSuccess ||
+      per_sm < 1) {
+    (void)cudaGetLastError();
+    per_sm = 1;
+  }
+  return grid_for(work, per_block, static_cast<unsigned>(per_sm) * sms);
+}
+
 // Optional per-tier CUDA-event timing (tuning.profile).
 struct Prof {
   bool on = false;
@@ -93,53 +109,58 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   };
   if (p.count[T_THREAD]) {
     tier(T_THREAD);
-    const unsigned gb = grid_for(p.count[T_THREAD], 256, sms * 8);
     if (p.thread_max <= 8)
-      k_thread<MODE, W, WEIGHTED, 8><<<gb, 256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+      k_thread<MODE, W, WEIGHTED, 8>
+          <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8>, 256, 0, p.count[T_THREAD], 256, sms),
+             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
     else
-      k_thread<MODE, W, WEIGHTED, 16><<<gb, 256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+      k_thread<MODE, W, WEIGHTED, 16>
+          <<<resident_grid(k_thread<MODE, W, WEIGHTED, 16>, 256, 0, p.count[T_THREAD], 256, sms),
+             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
     prof.end(T_THREAD, s);
     ++launches;
   }
   if (p.count[T_HALF]) {
     tier(T_HALF);
-    k_group<MODE, W, WEIGHTED, 16><<<grid_for(p.count[T_HALF], 16, sms * 8), 256, 0, s>>>(
-        c, p.list[T_HALF], p.count[T_HALF]);
+    k_group<MODE, W, WEIGHTED, 16>
+        <<<resident_grid(k_group<MODE, W, WEIGHTED, 16>, 256, 0, p.count[T_HALF], 16, sms), 256,
+           0, s>>>(c, p.list[T_HALF], p.count[T_HALF]);
     prof.end(T_HALF, s);
     ++launches;
   }
   if (p.count[T_WARP]) {
     tier(T_WARP);
-    k_group<MODE, W, WEIGHTED, 32><<<grid_for(p.count[T_WARP], 8, sms * 8), 256, 0, s>>>(
-        c, p.list[T_WARP], p.count[T_WARP]);
+    k_group<MODE, W, WEIGHTED, 32>
+        <<<resident_grid(k_group<MODE, W, WEIGHTED, 32>, 256, 0, p.count[T_WARP], 8, sms), 256,
+           0, s>>>(c, p.list[T_WARP], p.count[T_WARP]);
     prof.end(T_WARP, s);
     ++launches;
   }
   if (p.count[T_WTAB]) {
     tier(T_WTAB);
-    k_wt<<<grid_for(p.count[T_WTAB], 8, sms * 6), 256, wtab_smem, s>>>(c, p.list[T_WTAB],
-                                                                      p.count[T_WTAB]);
+    k_wt<<<resident_grid(k_wt, 256, wtab_smem, p.count[T_WTAB], 8, sms), 256, wtab_smem, s>>>(
+        c, p.list[T_WTAB], p.count[T_WTAB]);
     prof.end(T_WTAB, s);
     ++launches;
   }
   if (p.count[T_BLOCK]) {
     tier(T_BLOCK);
-    k_b1<<<grid_for(p.count[T_BLOCK], 2, sms * 6), 256, block_smem, s>>>(c, p.list[T_BLOCK],
-                                                                        p.count[T_BLOCK]);
+    k_b1<<<resident_grid(k_b1, 256, block_smem, p.count[T_BLOCK], 2, sms), 256, block_smem, s>>>(
+        c, p.list[T_BLOCK], p.count[T_BLOCK]);
     prof.end(T_BLOCK, s);
     ++launches;
   }
   if (p.count[T_BLOCK2]) {
     tier(T_BLOCK2);
-    k_b2<<<grid_for(p.count[T_BLOCK2], 1, sms * 3), 256, block2_smem, s>>>(c, p.list[T_BLOCK2],
-                                                                          p.count[T_BLOCK2]);
+    k_b2<<<resident_grid(k_b2, 256, block2_smem, p.count[T_BLOCK2], 1, sms), 256, block2_smem,
+           s>>>(c, p.list[T_BLOCK2], p.count[T_BLOCK2]);
     prof.end(T_BLOCK2, s);
     ++launches;
   }
   if (p.count[T_BIG]) {
     tier(T_BIG);
-    k_bg<<<grid_for(p.count[T_BIG], 1, sms), kBigThreads, big_smem, s>>>(c, p.list[T_BIG],
-                                                                        p.count[T_BIG]);
+    k_bg<<<resident_grid(k_bg, kBigThreads, big_smem, p.count[T_BIG], 1, sms), kBigThreads,
+           big_smem, s>>>(c, p.list[T_BIG], p.count[T_BIG]);
     prof.end(T_BIG, s);
     ++launches;
   }
@@ -156,7 +177,8 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   if (p.n_hubs) {
     tier(T_HUB);
     const HubCtx h = p.hub_ctx();
-    const unsigned gi = grid_for(p.n_items, 1, sms * 6);
+    const unsigned gi =
+        resident_grid(k_hub_accum<MODE, W, WEIGHTED>, kBlockThreads, hub_smem, p.n_items, 1, sms);
     const unsigned gh = grid_for(p.n_hubs, 256, 1024);
     k_hub_select<MODE><<<gh, 256, 0, s>>>(c, h);
     k_hub_accum<MODE, W, WEIGHTED><<<gi, kBlockThreads, hub_smem, s>>>(c, h);
