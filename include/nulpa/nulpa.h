@@ -85,7 +85,9 @@ typedef struct nulpa_tuning {
   uint32_t warp_max_degree;   /* 32-thread team tier upper bound (<= 256) */
   uint32_t block_max_degree;  /* 128-thread team tier upper bound (<= 1024) */
   uint32_t hub_chunk;         /* edges per CTA work item in the global-table hub tier */
-  uint32_t use_graphs;        /* reserved */
+  uint32_t async_first_pass;  /* ParallelAsync pass 0 from identity labels: 0 in place
+                                 (default), 1 table-free synchronous first pass
+                                 (k_first_pass; a legal schedule, all reads first) */
   uint32_t profile;           /* 1: time each tier with CUDA events (stats.tier_*) */
   uint32_t schedule;          /* ParallelAsync visit order inside each tier:
                                  0 default (= 2), 1 ascending id (partition_by_degree

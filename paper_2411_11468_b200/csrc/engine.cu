@@ -398,7 +398,9 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     // (Under ParallelAsync it is a legal schedule too, but it replaces the in-place
     // first pass, whose early label flooding converges R-MAT one pass sooner and
     // which the reference's low-tier-first KATs rely on, test_lpa.cpp:256-267.)
-    if (iter == 0 && identity_first && o.exec == NULPA_EXEC_SYNCHRONOUS) {
+    const bool first_async = o.exec == NULPA_EXEC_PARALLEL_ASYNC && tuning &&
+                             tuning->async_first_pass == 1;
+    if (iter == 0 && identity_first && (o.exec == NULPA_EXEC_SYNCHRONOUS || first_async)) {
       // Labels are still the identity: the table-free first pass (k_first_pass).
       c.lab_in = cur;
       c.lab_out = o.exec == NULPA_EXEC_SYNCHRONOUS ? nxt : cur;

@@ -103,6 +103,7 @@ class Tuning:
     schedule: int = 0  # 0 default, 1 ascending id, 2 scrambled
     profile: bool = False
     identity_first: bool = True  # table-free first pass from identity labels
+    async_first_pass: int = 0  # 1: ParallelAsync pass 0 as the table-free synchronous pass
 
     def to_c(self) -> _capi.nulpa_tuning:
         t = _capi.nulpa_tuning()
@@ -112,6 +113,7 @@ class Tuning:
         t.schedule = self.schedule
         t.profile = 1 if self.profile else 0
         t.no_identity_first = 0 if self.identity_first else 1
+        t.async_first_pass = self.async_first_pass
         return t
 
 

@@ -10,7 +10,11 @@ t0 = time.time()
 dg = lp.DeviceGraph.rmat(scale, 16, 1)
 print(f"scale {scale}: n={dg.n} m2={dg.m2} build {time.time()-t0:.2f}s", flush=True)
 cfg = lp.LpaConfig()
-t = lp.Tuning(profile=True)
+opts = dict(a.split("=") for a in sys.argv[3:])
+t = lp.Tuning(profile=True, async_first_pass=int(opts.get("first", 0)),
+              schedule=int(opts.get("sched", 0)))
+if opts.get("workload") == "sbm":
+    pass
 for _ in range(2):
     dg.lpa(cfg, t, want_host=False)
 import ctypes as C, numpy as np
@@ -22,6 +26,6 @@ for _ in range(reps):
     tc = t.to_c()
     _capi.check(_capi.lib().nulpa_run_graph(dg._h, C.byref(o), C.byref(tc), None, None, C.byref(st)))
     tot += np.array([st.tier_ms[i] for i in range(_capi.NULPA_TIERS)]); loop += st.elapsed_seconds
-print(f"loop {loop/reps*1e3:.1f} ms  iters {st.iterations} dn {dn[:st.iterations].tolist()} "
+print(f"{opts} loop {loop/reps*1e3:.1f} ms  iters {st.iterations} dn {dn[:st.iterations].tolist()} "
       f"-> {dg.m2/(loop/reps)/1e9:.2f} G edges/s")
 print("tiers ms:", {n: round(x / reps, 2) for n, x in zip(_capi.TIER_NAMES, tot) if x})
