@@ -123,7 +123,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   if (p.count[T_HALF]) {
     tier(T_HALF);
     k_group<MODE, W, WEIGHTED, 16>
-        <<<resident_grid(k_group<MODE, W, WEIGHTED, 16>, 256, 0, p.count[T_HALF], 16, sms), 256,
+        <<<resident_grid(k_group<MODE, W, WEIGHTED, 16>, 256, 0, p.count[T_HALF], 256, sms), 256,
            0, s>>>(c, p.list[T_HALF], p.count[T_HALF]);
     prof.end(T_HALF, s);
     ++launches;
@@ -131,35 +131,35 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   if (p.count[T_WARP]) {
     tier(T_WARP);
     k_group<MODE, W, WEIGHTED, 32>
-        <<<resident_grid(k_group<MODE, W, WEIGHTED, 32>, 256, 0, p.count[T_WARP], 8, sms), 256,
+        <<<resident_grid(k_group<MODE, W, WEIGHTED, 32>, 256, 0, p.count[T_WARP], 256, sms), 256,
            0, s>>>(c, p.list[T_WARP], p.count[T_WARP]);
     prof.end(T_WARP, s);
     ++launches;
   }
   if (p.count[T_WTAB]) {
     tier(T_WTAB);
-    k_wt<<<resident_grid(k_wt, 256, wtab_smem, p.count[T_WTAB], 8, sms), 256, wtab_smem, s>>>(
+    k_wt<<<resident_grid(k_wt, 256, wtab_smem, p.count[T_WTAB], 256, sms), 256, wtab_smem, s>>>(
         c, p.list[T_WTAB], p.count[T_WTAB]);
     prof.end(T_WTAB, s);
     ++launches;
   }
   if (p.count[T_BLOCK]) {
     tier(T_BLOCK);
-    k_b1<<<resident_grid(k_b1, 256, block_smem, p.count[T_BLOCK], 2, sms), 256, block_smem, s>>>(
+    k_b1<<<resident_grid(k_b1, 256, block_smem, p.count[T_BLOCK], 2 * kTeamBatch<128>, sms), 256, block_smem, s>>>(
         c, p.list[T_BLOCK], p.count[T_BLOCK]);
     prof.end(T_BLOCK, s);
     ++launches;
   }
   if (p.count[T_BLOCK2]) {
     tier(T_BLOCK2);
-    k_b2<<<resident_grid(k_b2, 256, block2_smem, p.count[T_BLOCK2], 1, sms), 256, block2_smem,
+    k_b2<<<resident_grid(k_b2, 256, block2_smem, p.count[T_BLOCK2], kTeamBatch<256>, sms), 256, block2_smem,
            s>>>(c, p.list[T_BLOCK2], p.count[T_BLOCK2]);
     prof.end(T_BLOCK2, s);
     ++launches;
   }
   if (p.count[T_BIG]) {
     tier(T_BIG);
-    k_bg<<<resident_grid(k_bg, kBigThreads, big_smem, p.count[T_BIG], 1, sms), kBigThreads,
+    k_bg<<<resident_grid(k_bg, kBigThreads, big_smem, p.count[T_BIG], kTeamBatch<kBigThreads>, sms), kBigThreads,
            big_smem, s>>>(c, p.list[T_BIG], p.count[T_BIG]);
     prof.end(T_BIG, s);
     ++launches;

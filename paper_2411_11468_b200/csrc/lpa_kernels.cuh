@@ -61,6 +61,59 @@ __device__ __forceinline__ bool claim_vertex(const PassCtx& c, uint32_t i) {
   return false;
 }
 
+// Apply the move rule given the vertex's current label `cur` (read when the
+// vertex was claimed: only this vertex's own thread ever writes it).
+template <int MODE>
+__device__ __forceinline__ bool apply_move_cur(const PassCtx& c, uint32_t i, uint32_t cand,
+                                               uint32_t cur) {
+  if (cand == kEmpty) return false;
+  const bool allowed = c.pick_less ? (cand < cur) : (cand != cur);
+  if (!allowed) return false;
+  if constexpr (MODE == kAsync) {
+    __stcg(c.lab_out + i, cand);
+  } else {
+    c.lab_out[i] = cand;
+    if (c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
+  }
+  return true;
+}
+
+// Per-vertex prologue for a batch of up to 32 list entries, one per lane: the
+// list entry, the claim (lpa.cpp:143-144), the row bounds and the current
+// label are fetched for 32 vertices at once, so their load latencies overlap
+// instead of being paid one vertex after another.
+struct Meta {
+  uint32_t i, d, cur;
+  uint64_t lo;
+  bool act;
+};
+
+template <int MODE>
+__device__ __forceinline__ Meta fetch_meta(const PassCtx& c, const uint32_t* __restrict__ list,
+                                           uint32_t t, uint32_t count) {
+  Meta m{0u, 0u, 0u, 0ull, false};
+  if (t < count) {
+    m.i = __ldg(list + t);
+    m.act = !claim_vertex(c, m.i);
+    if (m.act) {
+      m.lo = __ldg(c.g.off + m.i);
+      m.d = static_cast<uint32_t>(__ldg(c.g.off + m.i + 1) - m.lo);
+      m.cur = (MODE == kAsync) ? __ldcg(c.lab_out + m.i) : __ldg(c.lab_in + m.i);
+    }
+  }
+  return m;
+}
+
+__device__ __forceinline__ Meta shfl_meta(const Meta& m, int src) {
+  Meta r;
+  r.i = __shfl_sync(kFull, m.i, src);
+  r.d = __shfl_sync(kFull, m.d, src);
+  r.cur = __shfl_sync(kFull, m.cur, src);
+  r.lo = __shfl_sync(kFull, m.lo, src);
+  r.act = __shfl_sync(kFull, m.act ? 1 : 0, src) != 0;
+  return r;
+}
+
 template <bool WEIGHTED>
 constexpr bool kPacked = !WEIGHTED;  // unit weights -> packed 64-bit slots
 
@@ -135,50 +188,53 @@ __device__ __forceinline__ Best<V> group_best(Best<V> b, unsigned gmask) {
 template <int MODE, typename W, bool WEIGHTED, int G>
 __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __restrict__ list,
                                                uint32_t count) {
-  constexpr int kPer = 32 / G;  // vertices per warp
+  constexpr int kPer = 32 / G;  // vertices per warp step
   const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
   const unsigned gmask = (G == 32) ? kFull : (((1u << G) - 1u) << (sub * G));
   const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t base = gw * kPer; base < count; base += nw * kPer) {
-    const uint32_t t = base + sub;
-    bool active = t < count;
-    const uint32_t i = active ? __ldg(list + t) : 0u;
-    int skip = 0;
-    if (active && gl == 0) skip = claim_vertex(c, i) ? 1 : 0;
-    skip = __shfl_sync(kFull, skip, sub * G);
-    active = active && !skip;
-    uint64_t lo = 0;
-    uint32_t d = 0;
-    if (active) {
-      lo = __ldg(c.g.off + i);
-      d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+  // Each warp takes 32 list entries at a time: one batched prologue (fetch_meta),
+  // then kPer vertices per step with the next step's targets loaded ahead.
+  for (uint32_t base = gw * 32; base < count; base += nw * 32) {
+    const Meta mine = fetch_meta<MODE>(c, list, base + lane, count);
+    Meta m = shfl_meta(mine, sub);
+    uint32_t j = (m.act && gl < m.d) ? ld_stream(c.g.tgt + m.lo + gl, pol) : m.i;
+#pragma unroll 1
+    for (int step = 0; step < 32 / kPer; ++step) {
+      // prefetch the next step's targets (immutable) before this step's label reads
+      Meta mn{};
+      uint32_t jn = 0;
+      if (step + 1 < 32 / kPer) {
+        mn = shfl_meta(mine, (step + 1) * kPer + sub);
+        jn = (mn.act && gl < mn.d) ? ld_stream(c.g.tgt + mn.lo + gl, pol) : mn.i;
+      }
+      const bool valid = m.act && gl < m.d && j != m.i;
+      const uint32_t lab = valid ? load_label<MODE>(c.lab_in + j) : kEmpty;
+      const W w = valid ? edge_weight<W, WEIGHTED>(c.g, m.lo + gl) : W(0);
+      const unsigned peers = __match_any_sync(kFull, lab) & gmask;
+      W sm;
+      if constexpr (WEIGHTED)
+        sm = peer_sum(w, peers);
+      else
+        sm = static_cast<W>(__popc(peers));
+      Best<VBits<W>> b{VBits<W>(0), kEmpty};
+      if (lab != kEmpty && (__ffs(peers) - 1) == lane) b = Best<VBits<W>>{to_vbits<W>(sm), lab};
+      b = group_best<VBits<W>, G>(b, gmask);
+      int ch = 0;
+      if (m.act && gl == 0) {
+        ch = apply_move_cur<MODE>(c, m.i, b.k, m.cur) ? 1 : 0;
+        ++n_v;
+        n_e += m.d;
+        n_dn += ch;
+        if (MODE == kAsync && ch && c.wake) n_w += m.d;
+      }
+      ch = __shfl_sync(kFull, ch, sub * G);
+      if (MODE == kAsync && ch && c.wake && m.act && gl < m.d) c.flags[j] = 0;
+      m = mn;
+      j = jn;
     }
-    const uint32_t j = (gl < d) ? ld_stream(c.g.tgt + lo + gl, pol) : i;
-    const bool valid = gl < d && j != i;
-    const uint32_t lab = valid ? load_label<MODE>(c.lab_in + j) : kEmpty;
-    const W w = valid ? edge_weight<W, WEIGHTED>(c.g, lo + gl) : W(0);
-    const unsigned peers = __match_any_sync(kFull, lab) & gmask;
-    W s;
-    if constexpr (WEIGHTED)
-      s = peer_sum(w, peers);
-    else
-      s = static_cast<W>(__popc(peers));
-    Best<VBits<W>> b{VBits<W>(0), kEmpty};
-    if (lab != kEmpty && (__ffs(peers) - 1) == lane) b = Best<VBits<W>>{to_vbits<W>(s), lab};
-    b = group_best<VBits<W>, G>(b, gmask);
-    int ch = 0;
-    if (active && gl == 0) {
-      ch = apply_move<MODE>(c, i, b.k) ? 1 : 0;
-      ++n_v;
-      n_e += d;
-      n_dn += ch;
-      if (MODE == kAsync && ch && c.wake) n_w += d;
-    }
-    ch = __shfl_sync(kFull, ch, sub * G);
-    if (MODE == kAsync && ch && c.wake && gl < d) c.flags[j] = 0;
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
   warp_add_counter(c.ctr, C_PROC_E, n_e);
@@ -452,6 +508,9 @@ __device__ __forceinline__ Best<V> team_best(Best<V> b, Best<V>* red, int team_t
   }
 }
 
+template <int TEAM>
+constexpr uint32_t kTeamBatch = TEAM <= 32 ? 32u : (TEAM <= 128 ? 16u : 4u);
+
 template <typename Tab, int CAP, int MAXD>
 constexpr size_t team_bytes() {
   return size_t(CAP) * Tab::kSlotBytes + size_t(MAXD) * sizeof(uint16_t);
@@ -483,40 +542,53 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? (TEAM == 32 
   for (uint32_t s = ttid; s < CAP; s += TEAM) tab.clear_slot(s);  // once per lifetime
   const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
-  const uint32_t stride = gridDim.x * kTeams;
-  for (uint32_t t = blockIdx.x * kTeams + team; t < count; t += stride) {
-    const uint32_t i = __ldg(list + t);
-    if (ttid == 0) {
-      s_flag[team] = claim_vertex(c, i) ? 1 : 0;
-      s_occ_n[team] = 0;
+  // Teams take kBatch list entries at a time: the team's first warp fetches the
+  // batch prologue (claims, row bounds, current labels) for all of them at once.
+  // Larger teams own fewer, longer rows per batch (load balance at the tail).
+  constexpr uint32_t kBatch = kTeamBatch<TEAM>;
+  __shared__ Meta s_meta[TEAM > 32 ? kTeams : 1][kBatch];
+  const uint32_t nteams = gridDim.x * kTeams;
+  for (uint32_t base = (blockIdx.x * kTeams + team) * kBatch; base < count;
+       base += nteams * kBatch) {
+    Meta mine{};
+    if (ttid < kBatch) mine = fetch_meta<MODE>(c, list, base + ttid, count);
+    if constexpr (TEAM > 32) {
+      if (ttid < kBatch) s_meta[team][ttid] = mine;
+      sync();
     }
-    const uint64_t lo = __ldg(c.g.off + i);
-    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
-    const uint32_t cap = table_cap<CAP>(d);
-    sync();
-    if (s_flag[team]) {
-      sync();  // s_flag is rewritten by the next iteration
-      continue;
+    const uint32_t nb = min(kBatch, count - base);
+    for (uint32_t v = 0; v < nb; ++v) {
+      Meta m;
+      if constexpr (TEAM == 32)
+        m = shfl_meta(mine, v);
+      else
+        m = s_meta[team][v];
+      if (!m.act) continue;  // uniform over the team
+      if (ttid == 0) s_occ_n[team] = 0;
+      const uint32_t cap = table_cap<CAP>(m.d);
+      sync();
+      team_gather<MODE, W, WEIGHTED>(c, m.i, m.lo, 0, m.d, tab, cap, ttid, TEAM, pol, occ,
+                                     &s_occ_n[team], fails);
+      sync();
+      Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n[team], ttid, TEAM);
+      b = team_best<TEAM>(b, s_red[team], ttid, bar);
+      int changed = 0;
+      if (ttid == 0) {
+        changed = apply_move_cur<MODE>(c, m.i, b.k, m.cur) ? 1 : 0;
+        s_flag[team] = changed;
+        ++n_v;
+        n_e += m.d;
+        n_dn += changed;
+        if (MODE == kAsync && changed && c.wake) n_w += m.d;
+      }
+      sync();
+      changed = s_flag[team];
+      if (MODE == kAsync && changed && c.wake)
+        for (uint32_t e = ttid; e < m.d; e += TEAM)
+          c.flags[ld_stream(c.g.tgt + m.lo + e, pol)] = 0;
+      sync();
     }
-    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, ttid, TEAM, pol, occ,
-                                   &s_occ_n[team], fails);
-    sync();
-    Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n[team], ttid, TEAM);
-    b = team_best<TEAM>(b, s_red[team], ttid, bar);
-    int changed = 0;
-    if (ttid == 0) {
-      changed = apply_move<MODE>(c, i, b.k) ? 1 : 0;
-      s_flag[team] = changed;
-      ++n_v;
-      n_e += d;
-      n_dn += changed;
-      if (MODE == kAsync && changed && c.wake) n_w += d;
-    }
-    sync();
-    changed = s_flag[team];
-    if (MODE == kAsync && changed && c.wake)
-      for (uint32_t e = ttid; e < d; e += TEAM) c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
-    sync();
+    if constexpr (TEAM > 32) sync();  // s_meta is rewritten by the next batch
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
   warp_add_counter(c.ctr, C_PROC_E, n_e);
