@@ -368,6 +368,104 @@ struct Table<false, W> {
   __device__ __forceinline__ W value(uint32_t s) const { return v[s]; }
 };
 
+// Unit-weight table in the CTA's OWN shared memory (team and hub-chunk
+// tables): same slot format and probe sequence as Table<true, W>, but with
+// 32-bit shared-window addresses (no generic-pointer conversion in the loop),
+// the first probe inlined and the collision walk kept out of the common path.
+template <typename W>
+struct SmemTable {
+  uint32_t base;  // shared-window address of slot 0
+  static constexpr size_t kSlotBytes = 8;
+  __device__ __forceinline__ void bind(void* p, uint32_t) {
+    base = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  }
+  __device__ __forceinline__ uint32_t ld_key(uint32_t s) const {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + s * 8u + 4u) : "memory");
+    return v;
+  }
+  __device__ __forceinline__ uint32_t cas_key(uint32_t s, uint32_t key) const {
+    uint32_t old;
+    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;"
+                 : "=r"(old)
+                 : "r"(base + s * 8u + 4u), "r"(kEmpty), "r"(key)
+                 : "memory");
+    return old;
+  }
+  __device__ __forceinline__ void add_count(uint32_t s, uint32_t cnt) const {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base + s * 8u), "r"(cnt) : "memory");
+  }
+  __device__ __forceinline__ void clear_slot(uint32_t s) {
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(base + s * 8u), "l"(kEmptyWord) : "memory");
+  }
+  __device__ __forceinline__ void read(uint32_t s, uint32_t& key, VBits<W>& v) const {
+    unsigned long long x;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(x) : "r"(base + s * 8u) : "memory");
+    key = static_cast<uint32_t>(x >> 32);
+    if constexpr (sizeof(W) == 8)
+      v = static_cast<double>(static_cast<uint32_t>(x));
+    else
+      v = static_cast<uint32_t>(x);
+  }
+  __device__ __forceinline__ W value(uint32_t s) const {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + s * 8u) : "memory");
+    return static_cast<W>(v);
+  }
+  // Claim-or-find `key` and add `val`: 2 = claimed a new slot, 1 = existing key,
+  // 0 = table full.
+  __device__ __forceinline__ int add(uint32_t cap, int strategy, uint32_t key, W val,
+                                     uint32_t* slot) {
+    const uint32_t cnt = static_cast<uint32_t>(val);
+    const uint32_t mask = cap - 1;
+    uint32_t idx = hash_start(key, cap);
+    uint32_t s = idx & mask;
+    uint32_t cur = ld_key(s);
+    int r = 1;
+    if (cur == kEmpty) {
+      cur = cas_key(s, key);
+      if (cur == kEmpty) {
+        cur = key;
+        r = 2;
+      }
+    }
+    if (cur == key) {
+      add_count(s, cnt);
+      *slot = s;
+      return r;
+    }
+    return add_collided(cap, strategy, key, cnt, idx, slot);
+  }
+  __device__ __noinline__ int add_collided(uint32_t cap, int strategy, uint32_t key,
+                                           uint32_t cnt, uint32_t idx, uint32_t* slot) {
+    const uint32_t mask = cap - 1, h2 = hash_step(key);
+    uint32_t step = 1;
+    probe_advance(strategy, idx, step, h2);
+    for (uint32_t t = 1; t < 2 * cap; ++t) {
+      const uint32_t s = idx & mask;
+      uint32_t cur = ld_key(s);
+      int r = 1;
+      if (cur == kEmpty) {
+        cur = cas_key(s, key);
+        if (cur == kEmpty) {
+          cur = key;
+          r = 2;
+        }
+      }
+      if (cur == key) {
+        add_count(s, cnt);
+        *slot = s;
+        return r;
+      }
+      if (t + 1 >= cap)
+        idx += 1;  // completeness sweep
+      else
+        probe_advance(strategy, idx, step, h2);
+    }
+    return 0;
+  }
+};
+
 // Smallest power of two >= x (x >= 1).
 __host__ __device__ __forceinline__ uint32_t pow2_ceil(uint32_t x) {
 #ifdef __CUDA_ARCH__

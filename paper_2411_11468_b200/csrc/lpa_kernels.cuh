@@ -332,68 +332,6 @@ __device__ __forceinline__ Best<VBits<W>> occ_argmax_reset(Tab& tab, const uint1
   return b;
 }
 
-// ---- tier: warp per vertex, per-warp shared-memory table -----------------------------
-
-template <typename Tab>
-constexpr size_t wtab_bytes() {
-  return size_t(kWarpTabCap) * Tab::kSlotBytes + size_t(kWarpTabMax) * sizeof(uint16_t);
-}
-
-template <int MODE, typename W, bool WEIGHTED>
-__global__ void __launch_bounds__(kBlockThreads) k_wtab(PassCtx c,
-                                                        const uint32_t* __restrict__ list,
-                                                        uint32_t count) {
-  using Tab = Table<kPacked<WEIGHTED>, W>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ unsigned s_occ_n[kBlockThreads / 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kWarps = kBlockThreads / 32;
-  unsigned char* base = smem_raw + size_t(warp) * wtab_bytes<Tab>();
-  Tab tab;
-  tab.bind(base, kWarpTabCap);
-  uint16_t* occ = reinterpret_cast<uint16_t*>(base + size_t(kWarpTabCap) * Tab::kSlotBytes);
-  unsigned* occ_n = s_occ_n + warp;
-  for (uint32_t s = lane; s < kWarpTabCap; s += 32) tab.clear_slot(s);  // once per lifetime
-  __syncwarp();
-  const uint64_t pol = policy_evict_first();
-  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
-  const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
-  for (uint32_t t = gw; t < count; t += nw) {
-    const uint32_t i = __ldg(list + t);
-    int skip = 0;
-    if (lane == 0) {
-      skip = claim_vertex(c, i) ? 1 : 0;
-      *occ_n = 0;
-    }
-    if (__shfl_sync(kFull, skip, 0)) continue;
-    const uint64_t lo = __ldg(c.g.off + i);
-    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
-    const uint32_t cap = pow2_ceil(2 * d);
-    __syncwarp();
-    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, lane, 32, pol, occ, occ_n, fails);
-    __syncwarp();
-    Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, *occ_n, lane, 32);
-    b = warp_best(b);
-    __syncwarp();
-    int changed = 0;
-    if (lane == 0) {
-      changed = apply_move<MODE>(c, i, b.k) ? 1 : 0;
-      ++n_v;
-      n_e += d;
-      n_dn += changed;
-      if (MODE == kAsync && changed && c.wake) n_w += d;
-    }
-    changed = __shfl_sync(kFull, changed, 0);
-    if (MODE == kAsync && changed && c.wake)
-      for (uint32_t e = lane; e < d; e += 32) c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
-  }
-  warp_add_counter(c.ctr, C_PROC_V, n_v);
-  warp_add_counter(c.ctr, C_PROC_E, n_e);
-  warp_add_counter(c.ctr, C_DN, n_dn);
-  warp_add_counter(c.ctr, C_WAKE_E, n_w);
-  warp_add_counter(c.ctr, C_FAIL, fails);
-}
-
 // ---- block-wide helpers ------------------------------------------------------------
 
 template <typename V>
@@ -411,8 +349,6 @@ __device__ __forceinline__ Best<V> block_best(Best<V> b, Best<V>* red) {
   return red[0];
 }
 
-// ---- tier: CTA per vertex, shared-memory table --------------------------------------
-
 // Table capacity for a row of degree d: load <= 1/2 for the 256-thread tier,
 // <= 3/4 for the 128 KB tiers (always a power of two).
 template <int CAP>
@@ -423,60 +359,6 @@ __device__ __forceinline__ uint32_t table_cap(uint32_t d) {
 template <typename Tab, int CAP, int MAXD>
 constexpr size_t block_bytes() {
   return size_t(CAP) * Tab::kSlotBytes + size_t(MAXD) * sizeof(uint16_t);
-}
-
-template <int MODE, typename W, bool WEIGHTED, int THREADS, int CAP, int MAXD>
-__global__ void __launch_bounds__(THREADS) k_block(PassCtx c, const uint32_t* __restrict__ list,
-                                                   uint32_t count) {
-  using Tab = Table<kPacked<WEIGHTED>, W>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Tab tab;
-  tab.bind(smem_raw, CAP);
-  uint16_t* occ = reinterpret_cast<uint16_t*>(smem_raw + size_t(CAP) * Tab::kSlotBytes);
-  __shared__ Best<VBits<W>> red[32];
-  __shared__ int s_flag;
-  __shared__ unsigned s_occ_n;
-  for (uint32_t s = threadIdx.x; s < CAP; s += THREADS) tab.clear_slot(s);  // once
-  const uint64_t pol = policy_evict_first();
-  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
-  for (uint32_t t = blockIdx.x; t < count; t += gridDim.x) {
-    const uint32_t i = __ldg(list + t);
-    if (threadIdx.x == 0) {
-      s_flag = claim_vertex(c, i) ? 1 : 0;
-      s_occ_n = 0;
-    }
-    const uint64_t lo = __ldg(c.g.off + i);
-    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
-    const uint32_t cap = table_cap<CAP>(d);
-    __syncthreads();
-    if (s_flag) {
-      __syncthreads();  // s_flag is rewritten by the next iteration
-      continue;
-    }
-    team_gather<MODE, W, WEIGHTED>(c, i, lo, 0, d, tab, cap, threadIdx.x, THREADS, pol, occ,
-                                   &s_occ_n, fails);
-    __syncthreads();
-    Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n, threadIdx.x, THREADS);
-    b = block_best(b, red);
-    if (threadIdx.x == 0) {
-      s_flag = apply_move<MODE>(c, i, b.k) ? 1 : 0;
-      ++n_v;
-      n_e += d;
-      n_dn += s_flag;
-      if (MODE == kAsync && s_flag && c.wake) n_w += d;
-    }
-    __syncthreads();
-    const int changed = s_flag;
-    if (MODE == kAsync && changed && c.wake)
-      for (uint32_t e = threadIdx.x; e < d; e += THREADS)
-        c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
-    __syncthreads();
-  }
-  warp_add_counter(c.ctr, C_PROC_V, n_v);
-  warp_add_counter(c.ctr, C_PROC_E, n_e);
-  warp_add_counter(c.ctr, C_DN, n_dn);
-  warp_add_counter(c.ctr, C_WAKE_E, n_w);
-  warp_add_counter(c.ctr, C_FAIL, fails);
 }
 
 // ---- tier: TEAM threads per vertex, several teams per CTA ---------------------------
@@ -522,7 +404,7 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? (TEAM == 32 
                                                       uint32_t count) {
   static_assert(CTA_THREADS % TEAM == 0 && TEAM % 32 == 0, "team shape");
   constexpr int kTeams = CTA_THREADS / TEAM;
-  using Tab = Table<kPacked<WEIGHTED>, W>;
+  using Tab = std::conditional_t<kPacked<WEIGHTED>, SmemTable<W>, Table<false, W>>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Best<VBits<W>> s_red[kTeams][TEAM / 32 > 0 ? TEAM / 32 : 1];
   __shared__ int s_flag[kTeams];
@@ -801,7 +683,7 @@ __device__ __forceinline__ void bind_hub_table(Tab& g, const HubCtx& h, uint32_t
 // warp).
 template <int MODE, typename W, bool WEIGHTED>
 __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h) {
-  using Tab = Table<kPacked<WEIGHTED>, W>;
+  using Tab = std::conditional_t<kPacked<WEIGHTED>, SmemTable<W>, Table<false, W>>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tab tab;
   tab.bind(smem_raw, kHubCap);
@@ -822,8 +704,8 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h
     team_gather<MODE, W, WEIGHTED>(c, i, lo, e0, e1, tab, cap, threadIdx.x, blockDim.x, pol,
                                    nullptr, nullptr, fails);
     __syncthreads();
-    Tab g;
-    bind_hub_table<Tab, W, kPacked<WEIGHTED>>(g, h, x);
+    Table<kPacked<WEIGHTED>, W> g;  // the hub's global table
+    bind_hub_table<Table<kPacked<WEIGHTED>, W>, W, kPacked<WEIGHTED>>(g, h, x);
     uint32_t* occ = h.occ + h.occ_off[x];
     const uint32_t gcap = h.tab_cap[x];
     for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {  // uniform trip count

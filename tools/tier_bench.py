@@ -11,6 +11,8 @@ dg = lp.DeviceGraph.rmat(scale, 16, 1)
 print(f"scale {scale}: n={dg.n} m2={dg.m2} build {time.time()-t0:.2f}s", flush=True)
 cfg = lp.LpaConfig()
 opts = dict(a.split("=") for a in sys.argv[3:])
+if "iters" in opts:
+    cfg = lp.LpaConfig(max_iterations=int(opts["iters"]))
 t = lp.Tuning(profile=True, async_first_pass=int(opts.get("first", 0)),
               schedule=int(opts.get("sched", 0)))
 if opts.get("workload") == "sbm":
@@ -26,6 +28,8 @@ for _ in range(reps):
     tc = t.to_c()
     _capi.check(_capi.lib().nulpa_run_graph(dg._h, C.byref(o), C.byref(tc), None, None, C.byref(st)))
     tot += np.array([st.tier_ms[i] for i in range(_capi.NULPA_TIERS)]); loop += st.elapsed_seconds
+    edges = [st.tier_edges[i] for i in range(_capi.NULPA_TIERS)]
 print(f"{opts} loop {loop/reps*1e3:.1f} ms  iters {st.iterations} dn {dn[:st.iterations].tolist()} "
       f"-> {dg.m2/(loop/reps)/1e9:.2f} G edges/s")
 print("tiers ms:", {n: round(x / reps, 2) for n, x in zip(_capi.TIER_NAMES, tot) if x})
+print("tier edges (last run):", {n: x for n, x in zip(_capi.TIER_NAMES, edges) if x})
