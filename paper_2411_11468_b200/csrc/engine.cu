@@ -99,6 +99,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     allow_smem(k_b2, block2_smem);
     allow_smem(k_bg, big_smem);
     allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
+    if constexpr (!WEIGHTED) allow_smem(k_cluster_x<MODE, W>, cluster_x_bytes());
     allow_smem(k_hub_accum<MODE, W, WEIGHTED>, hub_smem);
     init = true;
   }
@@ -169,8 +170,12 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
     // persistent clusters pull vertices from c.work; grid a multiple of the cluster size
     const unsigned gc = std::max<unsigned>(kClusterSize, (sms / kClusterSize) * kClusterSize);
-    k_cluster<MODE, W, WEIGHTED><<<gc, kBigThreads, cluster_smem, s>>>(c, p.list[T_CLUSTER],
-                                                                      p.count[T_CLUSTER]);
+    if constexpr (WEIGHTED)
+      k_cluster<MODE, W, WEIGHTED><<<gc, kBigThreads, cluster_smem, s>>>(c, p.list[T_CLUSTER],
+                                                                        p.count[T_CLUSTER]);
+    else
+      k_cluster_x<MODE, W><<<gc, kBigThreads, cluster_x_bytes(), s>>>(c, p.list[T_CLUSTER],
+                                                                     p.count[T_CLUSTER]);
     prof.end(T_CLUSTER, s);
     ++launches;
   }
