@@ -95,8 +95,9 @@ struct PassCtx {
   int strategy;
   int wake;                       // store neighbour wake-ups (0 when provably dead, see engine.cu)
   unsigned int* work;             // dynamic work counter (cluster tier)
-  const uint32_t* vid;            // position -> vertex id (layout.cu); nullptr = identity
-  const uint32_t* pos;            // vertex id -> position; nullptr = identity
+  const uint32_t* vid = nullptr;  // position -> vertex id (layout.cu); nullptr = identity
+  const uint32_t* pos = nullptr;  // vertex id -> position; nullptr = identity
+  int fresh = 0;                  // labels are still the identity (first pass of a run)
 };
 
 // Vertex id stored at position p (label values are vertex ids).

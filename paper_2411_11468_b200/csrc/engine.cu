@@ -99,7 +99,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     allow_smem(k_b2, block2_smem);
     allow_smem(k_bg, big_smem);
     allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
-    if constexpr (!WEIGHTED) allow_smem(k_cluster_x<MODE, W>, cluster_x_bytes());
+    if constexpr (!WEIGHTED) allow_smem(k_wide<MODE, W>, wide_bytes());
     allow_smem(k_hub_accum<MODE, W, WEIGHTED>, hub_smem);
     init = true;
   }
@@ -174,8 +174,10 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
       k_cluster<MODE, W, WEIGHTED><<<gc, kBigThreads, cluster_smem, s>>>(c, p.list[T_CLUSTER],
                                                                         p.count[T_CLUSTER]);
     else
-      k_cluster_x<MODE, W><<<gc, kBigThreads, cluster_x_bytes(), s>>>(c, p.list[T_CLUSTER],
-                                                                     p.count[T_CLUSTER]);
+      k_wide<MODE, W><<<resident_grid(k_wide<MODE, W>, kBigThreads, wide_bytes(),
+                                      p.count[T_CLUSTER], 1, sms),
+                        kBigThreads, wide_bytes(), s>>>(c, p.list[T_CLUSTER], p.count[T_CLUSTER],
+                                                        c.fresh);
     prof.end(T_CLUSTER, s);
     ++launches;
   }
@@ -399,6 +401,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     c.work = work.p;
     c.vid = g->perm;
     c.pos = g->inv;
+    c.fresh = iter == 0 ? 1 : 0;
     // Synchronous only: there the identity first pass is exactly the reference's.
     // (Under ParallelAsync it is a legal schedule too, but it replaces the in-place
     // first pass, whose early label flooding converges R-MAT one pass sooner and
@@ -716,6 +719,7 @@ void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* i
   c.work = ss->work.p;
   c.vid = g->perm;
   c.pos = g->inv;
+  c.fresh = ss->fresh ? 1 : 0;
   Prof prof;
   cudaEvent_t e0, e1;
   NULPA_CUDA(cudaEventCreate(&e0));

@@ -606,162 +606,120 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
   warp_add_counter(c.ctr, C_FAIL, fails);
 }
 
-// ---- tier: 8-CTA cluster per vertex, DSMEM bucket exchange (unit weights) ------------
-// The same label partition as k_cluster (owner = owner_of(label)), but labels
-// travel to their owner in bulk instead of one remote atomic at a time:
-//   1. each rank streams 1/8 of the row, gathers the labels and counts them per
-//      owner (one shared atomic per (warp, owner) group), then scatters them into
-//      an owner-sorted outbox in its OWN shared memory;
-//   2. after a cluster barrier each rank pulls its segment from the eight
-//      outboxes with coalesced DSMEM loads and aggregates it in its LOCAL table
-//      (warp dedup + native shared atomics, like the team tiers);
-//   3. each rank sweeps its occupied slots; rank 0 merges the eight partial
-//      argmaxes and decides.
-// Remote traffic is one 4-byte load per edge, issued in bulk; all atomics stay
-// in the rank's own shared memory.
-constexpr int kClusterSlice = kClusterMax / kClusterSize;                   // 12288 edges
-constexpr int kClusterPer = (kClusterSlice + kBigThreads - 1) / kBigThreads;  // 12 per thread
+// ---- tier: wide rows, one 1024-thread CTA per vertex, label-partitioned phases --------
+// Rows of kBigMax < d <= kClusterMax (unit weights). The CTA's 16K-slot shared
+// table holds at most kWideLimit distinct labels, so a row with more distinct
+// labels is aggregated in P phases: phase p streams the whole row but inserts
+// only the labels with phase_of(label, P) == p, sweeps the table into a running
+// (max count, min label) and clears it. The argmax over all phases is exact (each
+// label lives in exactly one phase). The first pass from identity labels
+// (every label distinct) starts at P = ceil(d / kWideLimit); other passes start
+// at P = 1 and double P when the table overflows. Re-streaming the row costs HBM
+// bandwidth for the targets only (labels hit L2); no cluster barriers, no remote
+// atomics, and every SM owns its own vertex.
+constexpr uint32_t kWideLimit = 10240;  // distinct labels per phase (table load <= 5/8 + slack)
 
-constexpr size_t cluster_x_bytes() {
-  return size_t(kClusterCap) * 8 + size_t(kClusterCap) * sizeof(uint16_t) +
-         size_t(kClusterSlice) * sizeof(uint32_t);
+__device__ __forceinline__ uint32_t phase_of(uint32_t key, uint32_t P) {
+  const uint32_t h = (key ^ (key >> 16)) * 0x7FEB352Du;
+  return static_cast<uint32_t>((static_cast<uint64_t>(h) * P) >> 32);
+}
+
+constexpr size_t wide_bytes() {
+  return size_t(kClusterCap) * 8 + size_t(kClusterCap) * sizeof(uint16_t);
 }
 
 template <int MODE, typename W>
-__global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThreads, 1)
-    k_cluster_x(PassCtx c, const uint32_t* __restrict__ list, uint32_t count) {
-  namespace cg = cooperative_groups;
-  static_assert(kClusterSize == 8, "owner_of assumes 8 ranks");
-  cg::cluster_group cl = cg::this_cluster();
-  const unsigned rank = cl.block_rank();
+__global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32_t* __restrict__ list,
+                                                         uint32_t count, int fresh) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemTable<W> tab;
   tab.bind(smem_raw, kClusterCap);
   uint16_t* occ = reinterpret_cast<uint16_t*>(smem_raw + size_t(kClusterCap) * 8);
-  uint32_t* outbox = reinterpret_cast<uint32_t*>(smem_raw + size_t(kClusterCap) * 8 +
-                                                 size_t(kClusterCap) * sizeof(uint16_t));
   __shared__ uint32_t s_item;
-  __shared__ int s_flag, s_changed;
+  __shared__ int s_flag, s_over;
   __shared__ unsigned s_occ_n;
-  __shared__ unsigned s_hist[kClusterSize];
-  __shared__ unsigned s_start[kClusterSize + 1];
-  __shared__ unsigned s_in_off[kClusterSize + 1];  // prefix of incoming segment lengths
-  __shared__ unsigned s_in_src[kClusterSize];      // start of my segment in outbox q
   __shared__ Best<VBits<W>> red[32];
-  __shared__ Best<VBits<W>> part[kClusterSize];
   for (uint32_t x = threadIdx.x; x < kClusterCap; x += blockDim.x) tab.clear_slot(x);  // once
   const uint64_t pol = policy_evict_first();
-  const int lane = threadIdx.x & 31;
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
+  constexpr int U = 4;
   for (;;) {
-    if (threadIdx.x == 0) {
-      s_occ_n = 0;
-      if (rank == 0) s_item = atomicAdd(c.work, 1u);
-    }
-    if (threadIdx.x < kClusterSize) s_hist[threadIdx.x] = 0;
-    cl.sync();                                                   // (A) item published
-    const uint32_t t = *cl.map_shared_rank(&s_item, 0);
-    if (t >= count) break;  // uniform over the cluster
+    if (threadIdx.x == 0) s_item = atomicAdd(c.work, 1u);
+    __syncthreads();
+    const uint32_t t = s_item;
+    if (t >= count) break;
     const uint32_t i = __ldg(list + t);
-    if (rank == 0 && threadIdx.x == 0) s_flag = claim_vertex(c, i) ? 1 : 0;
+    if (threadIdx.x == 0) s_flag = claim_vertex(c, i) ? 1 : 0;
     const uint64_t lo = __ldg(c.g.off + i);
     const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
-    const uint32_t e0 = static_cast<uint32_t>((uint64_t(d) * rank) / kClusterSize);
-    const uint32_t e1 = static_cast<uint32_t>((uint64_t(d) * (rank + 1)) / kClusterSize);
-    // Gather this rank's slice (all loads in flight before the first use).
-    uint32_t lab[kClusterPer];
-#pragma unroll
-    for (int k = 0; k < kClusterPer; ++k) {
-      const uint32_t e = e0 + k * kBigThreads + threadIdx.x;
-      lab[k] = e < e1 ? ld_stream(c.g.tgt + lo + e, pol) : i;
-    }
-    cl.sync();                                                   // (B) flag visible
-    if (*cl.map_shared_rank(&s_flag, 0)) continue;
-#pragma unroll
-    for (int k = 0; k < kClusterPer; ++k)
-      lab[k] = lab[k] != i ? load_label<MODE>(c.lab_in + lab[k]) : kEmpty;  // self-loops skipped
-    // Count per owner; a lane's position inside its owner's bucket comes back
-    // from the (warp, owner) group's single atomicAdd.
-    uint32_t pos[kClusterPer];
-    const uint32_t wbase = e0 + (threadIdx.x & ~31u);
-#pragma unroll
-    for (int k = 0; k < kClusterPer; ++k) {
-      pos[k] = 0;
-      if (wbase + k * kBigThreads >= e1) continue;  // warp-uniform
-      const bool valid = lab[k] != kEmpty;
-      const uint32_t o = valid ? owner_of(lab[k]) : kClusterSize;
-      const unsigned peers = __match_any_sync(kFull, o);
-      const int leader = __ffs(peers) - 1;
-      unsigned b = 0;
-      if (valid && lane == leader) b = atomicAdd(&s_hist[o], static_cast<unsigned>(__popc(peers)));
-      b = __shfl_sync(kFull, b, leader);
-      pos[k] = b + __popc(peers & ((1u << lane) - 1u));
-    }
     __syncthreads();
+    if (s_flag) continue;  // (s_item / s_flag are rewritten only after the next barrier)
+    uint32_t P = fresh ? (d + kWideLimit - 1) / kWideLimit : 1u;
+    Best<VBits<W>> best{VBits<W>(0), kEmpty};  // running result (thread 0)
+    for (uint32_t ph = 0; ph < P; ++ph) {
+      if (threadIdx.x == 0) {
+        s_occ_n = 0;
+        s_over = 0;
+      }
+      __syncthreads();
+      const uint32_t cap = P == 1 ? min(static_cast<uint32_t>(kClusterCap), pow2_ceil(2 * d))
+                                  : static_cast<uint32_t>(kClusterCap);
+      for (uint32_t base = 0; base < d; base += kBigThreads * U) {
+        uint32_t j[U], lab[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t e = base + u * kBigThreads + threadIdx.x;
+          j[u] = e < d ? ld_stream(c.g.tgt + lo + e, pol) : i;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          lab[u] = j[u] != i ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+          if (P > 1 && lab[u] != kEmpty && phase_of(lab[u], P) != ph) lab[u] = kEmpty;
+        }
+        const uint32_t wbase = base + (threadIdx.x & ~31u);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (wbase + u * kBigThreads >= d) break;  // warp-uniform
+          unsigned long long f = 0;
+          gather_insert<W, false>(c, lab[u], W(1), tab, cap, occ, &s_occ_n, f);
+          if (f) s_over = 1;  // table full: treat as overflow
+        }
+        // Stop early once the phase holds too many distinct labels (block-uniform:
+        // every thread reads the counters between the same two barriers).
+        __syncthreads();
+        const bool stop = s_over || s_occ_n > kWideLimit;
+        __syncthreads();
+        if (stop) {
+          if (threadIdx.x == 0) s_over = 1;
+          break;
+        }
+      }
+      __syncthreads();
+      const bool over = s_over != 0;
+      Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n, threadIdx.x, blockDim.x);
+      b = block_best(b, red);  // (ends with a barrier: the table is clear again)
+      if (over) {
+        // restart with twice as many phases (at least enough for all-distinct rows)
+        P = max(2 * P, (d + kWideLimit - 1) / kWideLimit);
+        ph = static_cast<uint32_t>(-1);
+        best = Best<VBits<W>>{VBits<W>(0), kEmpty};
+        continue;
+      }
+      if (threadIdx.x == 0) best_merge(best, b.v, b.k);
+    }
     if (threadIdx.x == 0) {
-      unsigned acc = 0;
-      for (int q = 0; q < kClusterSize; ++q) {
-        s_start[q] = acc;
-        acc += s_hist[q];
-      }
-      s_start[kClusterSize] = acc;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kClusterPer; ++k)
-      if (lab[k] != kEmpty) outbox[s_start[owner_of(lab[k])] + pos[k]] = lab[k];
-    cl.sync();                                                   // (C) outboxes complete
-    // Locate my segment in every outbox.
-    if (threadIdx.x < kClusterSize) {
-      const unsigned* qs = cl.map_shared_rank(s_start, threadIdx.x);
-      s_in_src[threadIdx.x] = qs[rank];
-      s_hist[threadIdx.x] = qs[rank + 1] - qs[rank];  // (reused: incoming length from q)
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned acc = 0;
-      for (int q = 0; q < kClusterSize; ++q) {
-        s_in_off[q] = acc;
-        acc += s_hist[q];
-      }
-      s_in_off[kClusterSize] = acc;
-    }
-    __syncthreads();
-    const uint32_t n_in = s_in_off[kClusterSize];
-    const uint32_t cap = min(static_cast<uint32_t>(kClusterCap), pow2_ceil(n_in + n_in / 3 + 1));
-    for (uint32_t base = 0; base < n_in; base += kBigThreads) {
-      const uint32_t v = base + threadIdx.x;
-      uint32_t l = kEmpty;
-      if (v < n_in) {
-        int q = 0;
-#pragma unroll
-        for (int x = 1; x < kClusterSize; ++x) q += v >= s_in_off[x] ? 1 : 0;
-        const uint32_t* qbox = cl.map_shared_rank(outbox, q);
-        l = qbox[s_in_src[q] + (v - s_in_off[q])];
-      }
-      gather_insert<W, false>(c, l, W(1), tab, cap, occ, &s_occ_n, fails);
-    }
-    __syncthreads();
-    Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n, threadIdx.x, blockDim.x);
-    b = block_best(b, red);
-    if (threadIdx.x == 0) *cl.map_shared_rank(&part[rank], 0) = b;
-    cl.sync();                                                   // (D) partials at rank 0;
-                                                                 //     outboxes free again
-    if (rank == 0 && threadIdx.x == 0) {
-      Best<VBits<W>> f{VBits<W>(0), kEmpty};
-      for (int r = 0; r < kClusterSize; ++r) best_merge(f, part[r].v, part[r].k);
-      s_changed = apply_move<MODE>(c, i, f.k) ? 1 : 0;
+      s_flag = apply_move<MODE>(c, i, best.k) ? 1 : 0;
       ++n_v;
       n_e += d;
-      n_dn += s_changed;
-      if (MODE == kAsync && s_changed && c.wake) n_w += d;
+      n_dn += s_flag;
+      if (MODE == kAsync && s_flag && c.wake) n_w += d;
     }
-    cl.sync();                                                   // (E) decision visible
-    if (MODE == kAsync && c.wake && *cl.map_shared_rank(&s_changed, 0))
-      for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+    __syncthreads();
+    if (MODE == kAsync && c.wake && s_flag)
+      for (uint32_t e = threadIdx.x; e < d; e += blockDim.x)
         c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
+    __syncthreads();
   }
-  cl.sync();
   warp_add_counter(c.ctr, C_PROC_V, n_v);
   warp_add_counter(c.ctr, C_PROC_E, n_e);
   warp_add_counter(c.ctr, C_DN, n_dn);
