@@ -177,7 +177,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
       k_wide<MODE, W><<<resident_grid(k_wide<MODE, W>, kBigThreads, wide_bytes(),
                                       p.count[T_CLUSTER], 1, sms),
                         kBigThreads, wide_bytes(), s>>>(c, p.list[T_CLUSTER], p.count[T_CLUSTER],
-                                                        c.fresh);
+                                                        c.fresh, p.wide_scratch);
     prof.end(T_CLUSTER, s);
     ++launches;
   }

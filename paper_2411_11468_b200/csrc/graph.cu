@@ -301,6 +301,7 @@ Plan::~Plan() {
   dfree(changed);
   dfree(item_hub);
   dfree(item_start);
+  dfree(wide_scratch);
 }
 
 TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* t) {
@@ -387,6 +388,9 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
       for (int t = dev::T_HALF; t < dev::T_HUB; ++t) scramble_list(p->list[t], p->count[t], s);
     }
 
+    // Wide tier (k_wide): one L2-resident row snapshot per resident CTA.
+    if (p->count[dev::T_CLUSTER] && !p->weighted)
+      p->wide_scratch = dalloc<uint32_t>(uint64_t(sm_count()) * dev::kClusterMax);
     // Hub tier: per-hub global tables and (hub, chunk) work items. Hub counts
     // are small (vertices of degree > block_max), so the layout is built on
     // the host.

@@ -630,7 +630,11 @@ constexpr size_t wide_bytes() {
 
 template <int MODE, typename W>
 __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32_t* __restrict__ list,
-                                                         uint32_t count, int fresh) {
+                                                         uint32_t count, int fresh,
+                                                         uint32_t* __restrict__ scratch) {
+  // This CTA's row snapshot: phase 0 of a multi-phase vertex gathers the labels
+  // once and writes them here (L2-resident); later phases stream them back.
+  uint32_t* snap = scratch + size_t(blockIdx.x) * kClusterMax;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemTable<W> tab;
   tab.bind(smem_raw, kClusterCap);
@@ -665,17 +669,30 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
       const uint32_t cap = P == 1 ? min(static_cast<uint32_t>(kClusterCap), pow2_ceil(2 * d))
                                   : static_cast<uint32_t>(kClusterCap);
       for (uint32_t base = 0; base < d; base += kBigThreads * U) {
-        uint32_t j[U], lab[U];
+        uint32_t lab[U];
+        if (ph == 0) {
+          uint32_t j[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t e = base + u * kBigThreads + threadIdx.x;
-          j[u] = e < d ? ld_stream(c.g.tgt + lo + e, pol) : i;
+          for (int u = 0; u < U; ++u) {
+            const uint32_t e = base + u * kBigThreads + threadIdx.x;
+            j[u] = e < d ? ld_stream(c.g.tgt + lo + e, pol) : i;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t e = base + u * kBigThreads + threadIdx.x;
+            lab[u] = j[u] != i ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+            if (P > 1 && e < d) snap[e] = lab[u];
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t e = base + u * kBigThreads + threadIdx.x;
+            lab[u] = e < d ? __ldcg(snap + e) : kEmpty;
+          }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          lab[u] = j[u] != i ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+        for (int u = 0; u < U; ++u)
           if (P > 1 && lab[u] != kEmpty && phase_of(lab[u], P) != ph) lab[u] = kEmpty;
-        }
         const uint32_t wbase = base + (threadIdx.x & ~31u);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
