@@ -430,15 +430,20 @@ struct SmemTable {
         r = 2;
       }
     }
-    if (cur == key) {
+    if (__builtin_expect(cur == key, 1)) {
       add_count(s, cnt);
       *slot = s;
       return r;
     }
-    return add_collided(cap, strategy, key, cnt, idx, slot);
+    return strategy == 3 ? add_collided<3>(cap, key, cnt, idx, slot)
+                         : add_collided<-1>(cap, key, cnt, idx, slot, strategy);
   }
-  __device__ __noinline__ int add_collided(uint32_t cap, int strategy, uint32_t key,
-                                           uint32_t cnt, uint32_t idx, uint32_t* slot) {
+  // Probe walk after a first-probe collision; STRAT = 3 (QuadraticDouble, the
+  // default) is specialised, -1 dispatches on `strategy` at run time.
+  template <int STRAT>
+  __device__ __forceinline__ int add_collided(uint32_t cap, uint32_t key, uint32_t cnt,
+                                              uint32_t idx, uint32_t* slot, int strategy = 3) {
+    if constexpr (STRAT >= 0) strategy = STRAT;
     const uint32_t mask = cap - 1, h2 = hash_step(key);
     uint32_t step = 1;
     probe_advance(strategy, idx, step, h2);

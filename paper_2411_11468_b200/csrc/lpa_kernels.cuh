@@ -349,11 +349,16 @@ __device__ __forceinline__ Best<V> block_best(Best<V> b, Best<V>* red) {
   return red[0];
 }
 
-// Table capacity for a row of degree d: load <= 1/2 for the 256-thread tier,
-// <= 3/4 for the 128 KB tiers (always a power of two).
+// Table capacity for a row of degree d: load <= 1/4 where the team's fixed
+// table allows it (fewer first-probe collisions), never above 1/2 for the
+// <= 256-thread teams or 3/4 for the 128 KB tables (always a power of two).
 template <int CAP>
 __device__ __forceinline__ uint32_t table_cap(uint32_t d) {
-  return CAP <= kBlock2Cap ? pow2_ceil(2 * d) : pow2_ceil(d + d / 3 + 1);
+  const uint32_t want = pow2_ceil(4 * d);
+  if constexpr (CAP <= kBlock2Cap)
+    return min(want, static_cast<uint32_t>(CAP));  // CAP >= 2 * MAXD
+  else
+    return max(min(want, static_cast<uint32_t>(CAP)), pow2_ceil(d + d / 3 + 1));
 }
 
 template <typename Tab, int CAP, int MAXD>
