@@ -420,41 +420,20 @@ struct SmemTable {
     const uint32_t cnt = static_cast<uint32_t>(val);
     const uint32_t mask = cap - 1;
     uint32_t idx = hash_start(key, cap);
-    const uint32_t s = idx & mask;
-    // First probe: the aligned slot pair {s, s^1} with one 16-byte load. Every
-    // inserter of a key tries s, then s^1, then the walk, and slots are never
-    // freed during a vertex, so this order finds a key wherever it was put.
-    uint32_t k2[2];
-    {
-      unsigned long long x0, x1;
-      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];"
-                   : "=l"(x0), "=l"(x1)
-                   : "r"(base + (s & ~1u) * 8u)
-                   : "memory");
-      const uint32_t lo_key = static_cast<uint32_t>(x0 >> 32), hi_key = static_cast<uint32_t>(x1 >> 32);
-      k2[0] = (s & 1u) ? hi_key : lo_key;  // key in slot s
-      k2[1] = (s & 1u) ? lo_key : hi_key;  // key in slot s ^ 1
+    uint32_t s = idx & mask;
+    uint32_t cur = ld_key(s);
+    int r = 1;
+    if (cur == kEmpty) {
+      cur = cas_key(s, key);
+      if (cur == kEmpty) {
+        cur = key;
+        r = 2;
+      }
     }
-    if (__builtin_expect(k2[0] == key, 1)) {
+    if (__builtin_expect(cur == key, 1)) {
       add_count(s, cnt);
       *slot = s;
-      return 1;
-    }
-    if (k2[1] == key) {
-      add_count(s ^ 1u, cnt);
-      *slot = s ^ 1u;
-      return 1;
-    }
-#pragma unroll
-    for (uint32_t q = 0; q < 2; ++q) {
-      if (k2[q] != kEmpty) continue;  // occupied by another key (keys never change)
-      const uint32_t sq = s ^ q;
-      const uint32_t old = cas_key(sq, key);
-      if (old == kEmpty || old == key) {
-        add_count(sq, cnt);
-        *slot = sq;
-        return old == kEmpty ? 2 : 1;
-      }
+      return r;
     }
     return strategy == 3 ? add_collided<3>(cap, key, cnt, idx, slot)
                          : add_collided<-1>(cap, key, cnt, idx, slot, strategy);
