@@ -153,6 +153,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   }
   if (p.count[T_BLOCK2]) {
     tier(T_BLOCK2);
+    NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
     k_b2<<<resident_grid(k_b2, 256, block2_smem, p.count[T_BLOCK2], kTeamBatch<256>, sms), 256, block2_smem,
            s>>>(c, p.list[T_BLOCK2], p.count[T_BLOCK2]);
     prof.end(T_BLOCK2, s);
@@ -160,6 +161,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   }
   if (p.count[T_BIG]) {
     tier(T_BIG);
+    NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
     k_bg<<<resident_grid(k_bg, kBigThreads, big_smem, p.count[T_BIG], kTeamBatch<kBigThreads>, sms), kBigThreads,
            big_smem, s>>>(c, p.list[T_BIG], p.count[T_BIG]);
     prof.end(T_BIG, s);

@@ -316,7 +316,7 @@ TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* t) {
   wmax = std::max<uint32_t>(std::min<uint32_t>(wmax, dev::kWarpTabMax), 32u);
   uint32_t bmax = (t && t->block_max_degree) ? t->block_max_degree : uint32_t(dev::kBlockMax);
   bmax = std::max<uint32_t>(std::min<uint32_t>(bmax, dev::kBlockMax), wmax);
-  const uint32_t sched = (t && t->schedule) ? t->schedule : 2u;  // default: scrambled
+  const uint32_t sched = (t && t->schedule) ? t->schedule : 1u;  // default: position order
   return {tmax, wmax, bmax, sched};
 }
 
@@ -380,12 +380,13 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
     dfree(scratch);
     // Scrambled visit order (ParallelAsync only: any interleaving is a valid
     // asynchronous schedule; Synchronous/Sequential results do not depend on it).
-    // The thread tier is scrambled in 32-id blocks (its tiny rows still stream
-    // coalesced within a warp); the hub tier keeps ascending order (its decisions
-    // land after the tier anyway).
+    // Tiers up to degree block_max are scrambled in 32-position blocks.
     if (tb.schedule == 2) {
-      scramble_list(p->list[dev::T_THREAD], p->count[dev::T_THREAD], s, 5);
-      for (int t = dev::T_HALF; t < dev::T_HUB; ++t) scramble_list(p->list[t], p->count[t], s);
+      // 32-position blocks: a warp's batch of 32 list entries stays contiguous
+      // (coalesced prologue loads), the block order is pseudo-random. The
+      // long-row tiers (>= 1025) keep position order: their vertices then run
+      // largest degree bucket first, which balances the tier's tail.
+      for (int t = dev::T_THREAD; t <= dev::T_BLOCK; ++t) scramble_list(p->list[t], p->count[t], s, 5);
     }
 
     // Wide tier (k_wide): one L2-resident row snapshot per resident CTA.

@@ -435,8 +435,25 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? (TEAM == 32 
   constexpr uint32_t kBatch = kTeamBatch<TEAM>;
   __shared__ Meta s_meta[TEAM > 32 ? kTeams : 1][kBatch];
   const uint32_t nteams = gridDim.x * kTeams;
-  for (uint32_t base = (blockIdx.x * kTeams + team) * kBatch; base < count;
-       base += nteams * kBatch) {
+  // Teams of >= 256 threads own long rows: they pull batches from a work
+  // counter (c.work, zeroed before the launch) so the tier's tail stays balanced;
+  // smaller teams take batches grid-stride.
+  constexpr bool kDynamic = TEAM >= 256;
+  __shared__ uint32_t s_base[kTeams];
+  auto next_base = [&](uint32_t cur) -> uint32_t {
+    if constexpr (kDynamic) {
+      if (ttid == 0) s_base[team] = atomicAdd(c.work, kBatch);
+      sync();
+      const uint32_t b = s_base[team];
+      sync();
+      return b;
+    } else {
+      return cur + nteams * kBatch;
+    }
+  };
+  uint32_t first = (blockIdx.x * kTeams + team) * kBatch;
+  if constexpr (kDynamic) first = next_base(0);
+  for (uint32_t base = first; base < count; base = next_base(base)) {
     Meta mine{};
     if (ttid < kBatch) mine = fetch_meta<MODE>(c, list, base + ttid, count);
     if constexpr (TEAM > 32) {

@@ -14,7 +14,8 @@ opts = dict(a.split("=") for a in sys.argv[3:])
 if "iters" in opts:
     cfg = lp.LpaConfig(max_iterations=int(opts["iters"]))
 t = lp.Tuning(profile=True, async_first_pass=int(opts.get("first", 0)),
-              schedule=int(opts.get("sched", 0)))
+              schedule=int(opts.get("sched", 0)), thread_max_degree=int(opts.get("tmax", 0)),
+              warp_max_degree=int(opts.get("wmax", 0)), block_max_degree=int(opts.get("bmax", 0)))
 if opts.get("workload") == "sbm":
     pass
 for _ in range(2):
