@@ -316,7 +316,7 @@ TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* t) {
   wmax = std::max<uint32_t>(std::min<uint32_t>(wmax, dev::kWarpTabMax), 32u);
   uint32_t bmax = (t && t->block_max_degree) ? t->block_max_degree : uint32_t(dev::kBlockMax);
   bmax = std::max<uint32_t>(std::min<uint32_t>(bmax, dev::kBlockMax), wmax);
-  const uint32_t sched = (t && t->schedule) ? t->schedule : 1u;  // default: position order
+  const uint32_t sched = (t && t->schedule) ? t->schedule : 3u;  // default: see nulpa.h
   return {tmax, wmax, bmax, sched};
 }
 
@@ -381,6 +381,9 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
     // Scrambled visit order (ParallelAsync only: any interleaving is a valid
     // asynchronous schedule; Synchronous/Sequential results do not depend on it).
     // Tiers up to degree block_max are scrambled in 32-position blocks.
+    if (tb.schedule == 3) {  // the register tiers (<= 32) scrambled, position order above
+      for (int t = dev::T_THREAD; t <= dev::T_WARP; ++t) scramble_list(p->list[t], p->count[t], s, 5);
+    }
     if (tb.schedule == 2) {
       // 32-position blocks: a warp's batch of 32 list entries stays contiguous
       // (coalesced prologue loads), the block order is pseudo-random. The
