@@ -116,10 +116,17 @@ def dist_env():
     return rank, world, local
 
 
-def ref_switch_degree(workload: str) -> int:
-    # the team path costs ~210 us per vertex of degree >= 32 per pass, so on
-    # the power-law inputs the reference runs all-scalar (switch_degree = UINT32_MAX, F5).
-    return 0xFFFFFFFF if workload in ("rmat", "web") else 32
+def ref_switch_degree(workload: str, g=None) -> int:
+    # the reference team path costs ~210 us per vertex of degree >= 32 per pass
+    # (six condvar barriers per vertex), so the reference runs all-scalar (switch_degree =
+    # UINT32_MAX) on the power-law inputs, and on any sample that has a vertex of degree
+    # >= 32 (the planted SBM can); switch_degree = 32 is kept where no vertex reaches it,
+    # which is the same computation.
+    if workload in ("rmat", "web"):
+        return 0xFFFFFFFF
+    if g is not None and int(np.diff(g.offsets.astype(np.int64)).max(initial=0)) >= 32:
+        return 0xFFFFFFFF
+    return 32
 
 
 def run_reference_cpu(g, reps: int, workload: str = "rmat"):
@@ -130,7 +137,7 @@ def run_reference_cpu(g, reps: int, workload: str = "rmat"):
     out = []
     for _ in range(reps):
         labels, st = O.ref_lpa(rg, exec_mode=0, workers=workers,
-                               switch_degree=ref_switch_degree(workload))
+                               switch_degree=ref_switch_degree(workload, g))
         out.append((labels, st))
     return rg, out, workers
 
@@ -153,7 +160,7 @@ def bench_reference(args):
     value = m2 * len(timed) / secs
     q = O.ref_modularity(rg, timed[-1][0])
     sample = (f"{desc} (n={g.order()}, m2={m2}), reference ParallelAsync, switch_degree="
-              f"{ref_switch_degree(args.workload)}, workers={workers}")
+              f"{ref_switch_degree(args.workload, g)}, workers={workers}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / len(timed), "higher_is_better": True,
@@ -290,7 +297,7 @@ def bench_nulpa(args):
                        "cores": workers, "kind": "reference",
                        "sample": f"{desc} (m2={g.directed_size()}), reference lpa() "
                                  f"ParallelAsync, switch_degree="
-                                 f"{ref_switch_degree(args.workload)}, "
+                                 f"{ref_switch_degree(args.workload, g)}, "
                                  f"{stc['iterations']} iterations, "
                                  f"{stc['elapsed_seconds']:.2f} s"}
             else:

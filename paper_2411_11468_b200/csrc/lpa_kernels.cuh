@@ -53,6 +53,13 @@ __device__ __forceinline__ bool apply_move(const PassCtx& c, uint32_t i, uint32_
   return true;
 }
 
+// Wake neighbour j (flags[j] = 0, lpa.cpp:163). The store is skipped when the
+// flag already reads 0: hubs are woken by millions of neighbours per pass, and a
+// load of a hot byte is far cheaper than a partial-sector store to it.
+__device__ __forceinline__ void wake_vertex(uint8_t* flags, uint32_t j) {
+  if (load_flag(flags + j)) flags[j] = 0;
+}
+
 // Check-and-set the processed flag (lpa.cpp:143-144). Returns true to skip.
 __device__ __forceinline__ bool claim_vertex(const PassCtx& c, uint32_t i) {
   if (!c.flags) return false;
@@ -158,7 +165,7 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
     if (MODE == kAsync && c.wake) {
 #pragma unroll
       for (int k = 0; k < DMAX; ++k)
-        if (k < d) c.flags[nb[k]] = 0;
+        if (k < d) wake_vertex(c.flags, nb[k]);
       n_w += d;
     }
   }
@@ -231,7 +238,7 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
         if (MODE == kAsync && ch && c.wake) n_w += m.d;
       }
       ch = __shfl_sync(kFull, ch, sub * G);
-      if (MODE == kAsync && ch && c.wake && m.act && gl < m.d) c.flags[j] = 0;
+      if (MODE == kAsync && ch && c.wake && m.act && gl < m.d) wake_vertex(c.flags, j);
       m = mn;
       j = jn;
     }
@@ -489,7 +496,7 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? (TEAM == 32 
       changed = s_flag[team];
       if (MODE == kAsync && changed && c.wake)
         for (uint32_t e = ttid; e < m.d; e += TEAM)
-          c.flags[ld_stream(c.g.tgt + m.lo + e, pol)] = 0;
+          wake_vertex(c.flags, ld_stream(c.g.tgt + m.lo + e, pol));
       sync();
     }
     if constexpr (TEAM > 32) sync();  // s_meta is rewritten by the next batch
@@ -618,7 +625,7 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
     cl.sync();                                                   // (E) decision visible
     if (MODE == kAsync && c.wake && *cl.map_shared_rank(&s_changed, 0))
       for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
-        c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
+        wake_vertex(c.flags, ld_stream(c.g.tgt + lo + e, pol));
   }
   cl.sync();
   warp_add_counter(c.ctr, C_PROC_V, n_v);
@@ -756,7 +763,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
     __syncthreads();
     if (MODE == kAsync && c.wake && s_flag)
       for (uint32_t e = threadIdx.x; e < d; e += blockDim.x)
-        c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
+        wake_vertex(c.flags, ld_stream(c.g.tgt + lo + e, pol));
     __syncthreads();
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
@@ -797,7 +804,7 @@ __global__ void __launch_bounds__(256) k_first_pass(PassCtx c, uint32_t v_lo, ui
     ++n_dn;
     if (MODE == kSync && c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
     if (MODE == kAsync && c.wake) {
-      for (uint32_t e = 0; e < d; ++e) c.flags[__ldg(c.g.tgt + lo + e)] = 0;
+      for (uint32_t e = 0; e < d; ++e) wake_vertex(c.flags, __ldg(c.g.tgt + lo + e));
       n_w += d;
     }
   }
@@ -994,7 +1001,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_wake(PassCtx c, HubCtx h)
     const uint32_t e0 = h.item_start[it];
     const uint32_t e1 = min(d, e0 + kHubChunk);
     for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
-      c.flags[ld_stream(c.g.tgt + lo + e, pol)] = 0;
+      wake_vertex(c.flags, ld_stream(c.g.tgt + lo + e, pol));
     if (threadIdx.x == 0) n_w += e1 - e0;
   }
   warp_add_counter(c.ctr, C_WAKE_E, n_w);
@@ -1013,7 +1020,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_wake_list(Graph g, uint8_t* f
   for (uint32_t t = gw; t < count; t += nw) {
     const uint32_t i = list[t];
     const uint64_t lo = g.off[i], hi = g.off[i + 1];
-    for (uint64_t e = lo + lane; e < hi; e += 32) flags[__ldg(g.tgt + e)] = 0;
+    for (uint64_t e = lo + lane; e < hi; e += 32) wake_vertex(flags, __ldg(g.tgt + e));
     if (lane == 0) n_w += hi - lo;
   }
   warp_add_counter(ctr, C_WAKE_E, n_w);
@@ -1146,7 +1153,7 @@ __global__ void k_cc_apply(Graph g, uint32_t* lab, const uint32_t* prev, const u
       m &= m - 1;
       const uint32_t v = base + b;
       const uint64_t lo = g.off[v], hi = g.off[v + 1];
-      for (uint64_t e = lo + lane; e < hi; e += 32) flags[g.tgt[e]] = 0;
+      for (uint64_t e = lo + lane; e < hi; e += 32) wake_vertex(flags, g.tgt[e]);
     }
   }
   warp_add_counter(reverted, 0, nrev);
