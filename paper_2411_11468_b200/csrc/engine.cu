@@ -79,7 +79,7 @@ struct Prof {
 // C_COUNT block per tier. Returns the number of kernels launched.
 template <int MODE, typename W, bool WEIGHTED>
 int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t s, int sms,
-                Prof& prof) {
+                Prof& prof, unsigned tiers = ~0u) {
   using Tab = Table<kPacked<WEIGHTED>, W>;
   // Team kernels: <CTA threads, team threads, table slots, max degree> per tier.
   constexpr size_t wtab_smem = 8 * team_bytes<Tab, kWarpTabCap, kWarpTabMax>();
@@ -108,7 +108,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     c.ctr = ctr + t * C_COUNT;
     prof.begin(t, s);
   };
-  if (p.count[T_THREAD]) {
+  if (p.count[T_THREAD] && (tiers >> T_THREAD & 1u)) {
     tier(T_THREAD);
     if (p.thread_max <= 8)
       k_thread<MODE, W, WEIGHTED, 8>
@@ -121,7 +121,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     prof.end(T_THREAD, s);
     ++launches;
   }
-  if (p.count[T_HALF]) {
+  if (p.count[T_HALF] && (tiers >> T_HALF & 1u)) {
     tier(T_HALF);
     k_group<MODE, W, WEIGHTED, 16>
         <<<resident_grid(k_group<MODE, W, WEIGHTED, 16>, 256, 0, p.count[T_HALF], 256, sms), 256,
@@ -129,7 +129,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     prof.end(T_HALF, s);
     ++launches;
   }
-  if (p.count[T_WARP]) {
+  if (p.count[T_WARP] && (tiers >> T_WARP & 1u)) {
     tier(T_WARP);
     k_group<MODE, W, WEIGHTED, 32>
         <<<resident_grid(k_group<MODE, W, WEIGHTED, 32>, 256, 0, p.count[T_WARP], 256, sms), 256,
@@ -137,21 +137,21 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     prof.end(T_WARP, s);
     ++launches;
   }
-  if (p.count[T_WTAB]) {
+  if (p.count[T_WTAB] && (tiers >> T_WTAB & 1u)) {
     tier(T_WTAB);
     k_wt<<<resident_grid(k_wt, 256, wtab_smem, p.count[T_WTAB], 256, sms), 256, wtab_smem, s>>>(
         c, p.list[T_WTAB], p.count[T_WTAB]);
     prof.end(T_WTAB, s);
     ++launches;
   }
-  if (p.count[T_BLOCK]) {
+  if (p.count[T_BLOCK] && (tiers >> T_BLOCK & 1u)) {
     tier(T_BLOCK);
     k_b1<<<resident_grid(k_b1, 256, block_smem, p.count[T_BLOCK], 2 * kTeamBatch<128>, sms), 256, block_smem, s>>>(
         c, p.list[T_BLOCK], p.count[T_BLOCK]);
     prof.end(T_BLOCK, s);
     ++launches;
   }
-  if (p.count[T_BLOCK2]) {
+  if (p.count[T_BLOCK2] && (tiers >> T_BLOCK2 & 1u)) {
     tier(T_BLOCK2);
     NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
     k_b2<<<resident_grid(k_b2, 256, block2_smem, p.count[T_BLOCK2], kTeamBatch<256>, sms), 256, block2_smem,
@@ -159,7 +159,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     prof.end(T_BLOCK2, s);
     ++launches;
   }
-  if (p.count[T_BIG]) {
+  if (p.count[T_BIG] && (tiers >> T_BIG & 1u)) {
     tier(T_BIG);
     NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
     k_bg<<<resident_grid(k_bg, kBigThreads, big_smem, p.count[T_BIG], kTeamBatch<kBigThreads>, sms), kBigThreads,
@@ -167,7 +167,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     prof.end(T_BIG, s);
     ++launches;
   }
-  if (p.count[T_CLUSTER]) {
+  if (p.count[T_CLUSTER] && (tiers >> T_CLUSTER & 1u)) {
     tier(T_CLUSTER);
     NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
     // persistent clusters pull vertices from c.work; grid a multiple of the cluster size
@@ -183,7 +183,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     prof.end(T_CLUSTER, s);
     ++launches;
   }
-  if (p.n_hubs) {
+  if (p.n_hubs && (tiers >> T_HUB & 1u)) {
     tier(T_HUB);
     const HubCtx h = p.hub_ctx();
     const unsigned gi =
@@ -211,13 +211,33 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
 
 template <int MODE>
 int dispatch_pass(const Plan& p, const PassCtx& c, unsigned long long* ctr, int value_bytes,
-                  cudaStream_t s, int sms, Prof& prof) {
+                  cudaStream_t s, int sms, Prof& prof, unsigned tiers = ~0u) {
   const bool weighted = c.g.w != nullptr;
   if (value_bytes == 8)
-    return weighted ? launch_pass<MODE, double, true>(p, c, ctr, s, sms, prof)
-                    : launch_pass<MODE, double, false>(p, c, ctr, s, sms, prof);
-  return weighted ? launch_pass<MODE, float, true>(p, c, ctr, s, sms, prof)
-                  : launch_pass<MODE, float, false>(p, c, ctr, s, sms, prof);
+    return weighted ? launch_pass<MODE, double, true>(p, c, ctr, s, sms, prof, tiers)
+                    : launch_pass<MODE, double, false>(p, c, ctr, s, sms, prof, tiers);
+  return weighted ? launch_pass<MODE, float, true>(p, c, ctr, s, sms, prof, tiers)
+                  : launch_pass<MODE, float, false>(p, c, ctr, s, sms, prof, tiers);
+}
+
+// ParallelAsync first pass, long rows first: every tier of degree > block_max runs
+// the table-free identity rule (k_first_pass_list; all of them read identity
+// labels), then the lower tiers run in place and see those moves.
+int long_rows_first_pass(const Plan& p, PassCtx c, unsigned long long* ctr, int value_bytes,
+                         cudaStream_t s, int sms, Prof& prof) {
+  int launches = 0;
+  for (int t = T_HUB; t >= T_BLOCK2; --t) {
+    if (!p.count[t]) continue;
+    c.ctr = ctr + t * C_COUNT;
+    prof.begin(t, s);
+    k_first_pass_list<kAsync><<<grid_for(p.count[t], 256, sms * 8), 256, 0, s>>>(c, p.list[t],
+                                                                                p.count[t]);
+    prof.end(t, s);
+    ++launches;
+  }
+  NULPA_CUDA(cudaGetLastError());
+  const unsigned low = (1u << T_BLOCK2) - 1u;  // T_THREAD .. T_BLOCK
+  return launches + dispatch_pass<kAsync>(p, c, ctr, value_bytes, s, sms, prof, low);
 }
 
 template <typename W, bool WEIGHTED>
@@ -434,6 +454,11 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
         }
         std::swap(cur, nxt);
       }
+    } else if (o.exec == NULPA_EXEC_PARALLEL_ASYNC && iter == 0 && identity_first && tuning &&
+               tuning->async_first_pass == 2) {
+      c.lab_in = cur;
+      c.lab_out = cur;
+      launches += long_rows_first_pass(*p, c, ctr.p, vbytes, s, sms, prof);
     } else if (o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
       c.lab_in = cur;
       c.lab_out = cur;

@@ -814,6 +814,37 @@ __global__ void __launch_bounds__(256) k_first_pass(PassCtx c, uint32_t v_lo, ui
   warp_add_counter(c.ctr, C_WAKE_E, n_w);
 }
 
+// The same table-free rule over a tier list (used for the long-row tiers at the
+// start of a ParallelAsync run: they are processed first, all of them reading
+// identity labels, before the lower tiers run in place).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_first_pass_list(PassCtx c, const uint32_t* __restrict__ list,
+                                                         uint32_t count) {
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0;
+  const uint32_t bound = (count + 31u) & ~31u;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < bound; t += gridDim.x * blockDim.x) {
+    if (t >= count) continue;
+    const uint32_t i = __ldg(list + t);
+    if (claim_vertex(c, i)) continue;
+    const uint64_t lo = __ldg(c.g.off + i);
+    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+    if (d == 0) continue;
+    uint32_t cand = __ldg(c.g.tgt + lo);
+    if (cand == i) cand = d > 1 ? __ldg(c.g.tgt + lo + 1) : kEmpty;  // self-loop skipped
+    if (cand != kEmpty) cand = vertex_id(c.vid, cand);
+    const uint32_t own = vertex_id(c.vid, i);
+    ++n_v;
+    n_e += d > 1 ? 2 : 1;
+    const bool allowed = cand != kEmpty && (c.pick_less ? cand < own : cand != own);
+    if (!allowed) continue;
+    c.lab_out[i] = cand;
+    ++n_dn;
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+}
+
 // ---- tier: hubs, global tables -------------------------------------------------------
 
 template <int MODE>
