@@ -444,37 +444,6 @@ struct SmemTable {
     return strategy == 3 ? add_collided<3>(cap, key, cnt, idx, slot)
                          : add_collided<-1>(cap, key, cnt, idx, slot, strategy);
   }
-  // Find `key` (no insert) and add `cnt` to it: false when the key is absent. Walks
-  // the insertion sequence of add(); valid once every insert of the vertex is done
-  // (an EMPTY slot on the way means the key was never inserted).
-  __device__ __forceinline__ bool find_add(uint32_t cap, int strategy, uint32_t key,
-                                           uint32_t cnt) {
-    const uint32_t mask = cap - 1;
-    uint32_t idx = hash_start(key, cap);
-    uint32_t cur = ld_key(idx & mask);
-    if (cur == key) {
-      add_count(idx & mask, cnt);
-      return true;
-    }
-    if (cur == kEmpty) return false;
-    const uint32_t h2 = hash_step(key);
-    uint32_t step = 1;
-    probe_advance(strategy, idx, step, h2);
-    for (uint32_t t = 1; t < 2 * cap; ++t) {
-      const uint32_t s = idx & mask;
-      cur = ld_key(s);
-      if (cur == key) {
-        add_count(s, cnt);
-        return true;
-      }
-      if (cur == kEmpty) return false;
-      if (t + 1 >= cap)
-        idx += 1;
-      else
-        probe_advance(strategy, idx, step, h2);
-    }
-    return false;
-  }
   // Probe walk after a first-probe collision; STRAT = 3 (QuadraticDouble, the
   // default) is specialised, -1 dispatches on `strategy` at run time.
   template <int STRAT>

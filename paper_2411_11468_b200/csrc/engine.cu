@@ -97,31 +97,16 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   constexpr size_t big_smem = team_bytes<Tab, kBigCap, kBigMax>();
   constexpr size_t cluster_smem = cluster_bytes<Tab>();
   constexpr size_t hub_smem = kHubCap * Tab::kSlotBytes;
-  // First ParallelAsync pass with self-label bits: the FRESH team kernels (count-only
-  // lookups for self-labelled neighbours, team_scan_fresh).
-  constexpr bool kFreshOk = MODE == kAsync && !WEIGHTED;
-  const bool fresh = kFreshOk && c.lmask != 0xFFFFFFFFu;
-  auto k_wt = fresh ? k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, kFreshOk>
-                    : k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax>;
-  auto k_b1 = fresh ? k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax, kFreshOk>
-                    : k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax>;
-  auto k_b2 = fresh ? k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max, kFreshOk>
-                    : k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max>;
-  auto k_bg = fresh
-                  ? k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax, kFreshOk>
-                  : k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax>;
+  auto k_wt = k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax>;
+  auto k_b1 = k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax>;
+  auto k_b2 = k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max>;
+  auto k_bg = k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax>;
   static bool init = false;
   if (!init) {
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax>, wtab_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax>, block_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max>, block2_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax>, big_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, kFreshOk>, wtab_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax, kFreshOk>, block_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max, kFreshOk>,
-               block2_smem);
-    allow_smem(k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax, kFreshOk>,
-               big_smem);
+    allow_smem(k_wt, wtab_smem);
+    allow_smem(k_b1, block_smem);
+    allow_smem(k_b2, block2_smem);
+    allow_smem(k_bg, big_smem);
     allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
     if constexpr (!WEIGHTED) allow_smem(k_wide<MODE, W>, wide_bytes());
     allow_smem(k_hub_accum<MODE, W, WEIGHTED>, hub_smem);

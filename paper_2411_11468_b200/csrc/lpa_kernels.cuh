@@ -402,11 +402,6 @@ __device__ __forceinline__ Best<V> team_best(Best<V> b, Best<V>* red, int team_t
   }
 }
 
-// CTAs per SM the team kernels are compiled for (register budget): team32 5
-// (48 registers), team128 6, team256 3 (its 72 KB table caps it at 3 anyway).
-template <int CTA_THREADS, int TEAM>
-constexpr int kTeamMinBlocks = CTA_THREADS > 256 ? 1 : (TEAM == 32 ? 5 : (TEAM == 128 ? 6 : 3));
-
 template <int TEAM>
 constexpr uint32_t kTeamBatch = TEAM <= 32 ? 32u : (TEAM <= 128 ? 16u : 4u);
 
@@ -415,64 +410,8 @@ constexpr size_t team_bytes() {
   return size_t(CAP) * Tab::kSlotBytes + size_t(MAXD) * sizeof(uint16_t);
 }
 
-// First ParallelAsync pass (labels may carry kSelfBit), unit weights: the count of
-// label L is cA(L) + [L is the untouched identity label of a neighbour], and a
-// self label occurs at most once per (simple) row. So only the labels WITHOUT the
-// bit go into the table; each self label is then looked up: found -> +1 to its
-// count, absent -> a count-1 candidate (the smallest such one is kept). The table
-// holds the few distinct labels the already-processed neighbours adopted instead
-// of one slot per neighbour. The whole row is gathered into registers first
-// (R labels per thread) so both rounds see the same label values.
-template <int TEAM, int MAXD, typename W, typename Tab>
-__device__ __forceinline__ Best<VBits<W>> team_scan_fresh(const PassCtx& c, const Meta& m,
-                                                          Tab& tab, uint32_t cap, uint32_t ttid,
-                                                          uint64_t pol, uint16_t* occ,
-                                                          unsigned* occ_n,
-                                                          unsigned long long& fails,
-                                                          uint32_t* s_min, int bar) {
-  constexpr int R = (MAXD + TEAM - 1) / TEAM;
-  uint32_t raw[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t e = r * TEAM + ttid;
-    raw[r] = e < m.d ? ld_stream(c.g.tgt + m.lo + e, pol) : m.i;
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-    raw[r] = raw[r] != m.i ? load_label<kAsync>(c.lab_in + raw[r]) : kEmpty;  // self-loops skipped
-  const uint32_t wbase = ttid & ~31u;
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (wbase + r * TEAM < m.d) {
-      const uint32_t a = (raw[r] & kSelfBit) ? kEmpty : raw[r];  // (kEmpty has the bit set)
-      gather_insert<W, false>(c, a, W(1), tab, cap, occ, occ_n, fails);
-    }
-  if constexpr (TEAM == 32)
-    __syncwarp();
-  else
-    team_sync(bar, TEAM);
-  uint32_t bmin = kEmpty;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    if (raw[r] == kEmpty || !(raw[r] & kSelfBit)) continue;
-    const uint32_t l = raw[r] & ~kSelfBit;
-    if (!tab.find_add(cap, c.strategy, l, 1u)) bmin = min(bmin, l);
-  }
-  bmin = __reduce_min_sync(kFull, bmin);
-  if constexpr (TEAM > 32) {
-    if ((ttid & 31) == 0) atomicMin(s_min, bmin);
-  }
-  if constexpr (TEAM == 32)
-    __syncwarp();
-  else
-    team_sync(bar, TEAM);
-  if constexpr (TEAM > 32) bmin = *s_min;
-  return Best<VBits<W>>{VBits<W>(1), bmin};
-}
-
-template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CAP, int MAXD,
-          bool FRESH = false>
-__global__ void __launch_bounds__(CTA_THREADS, kTeamMinBlocks<CTA_THREADS, TEAM>)
+template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CAP, int MAXD>
+__global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? (TEAM == 32 ? 5 : 6) : 1)
     k_team(PassCtx c, const uint32_t* __restrict__ list,
                                                       uint32_t count) {
   static_assert(CTA_THREADS % TEAM == 0 && TEAM % 32 == 0, "team shape");
@@ -482,7 +421,6 @@ __global__ void __launch_bounds__(CTA_THREADS, kTeamMinBlocks<CTA_THREADS, TEAM>
   __shared__ Best<VBits<W>> s_red[kTeams][TEAM / 32 > 0 ? TEAM / 32 : 1];
   __shared__ int s_flag[kTeams];
   __shared__ unsigned s_occ_n[kTeams];
-  __shared__ uint32_t s_bmin[kTeams];
   const int team = threadIdx.x / TEAM, ttid = threadIdx.x % TEAM;
   const int bar = 1 + team;  // named barrier 0 is __syncthreads
   unsigned char* base = smem_raw + size_t(team) * team_bytes<Tab, CAP, MAXD>();
@@ -537,23 +475,14 @@ __global__ void __launch_bounds__(CTA_THREADS, kTeamMinBlocks<CTA_THREADS, TEAM>
       else
         m = s_meta[team][v];
       if (!m.act) continue;  // uniform over the team
-      if (ttid == 0) {
-        s_occ_n[team] = 0;
-        s_bmin[team] = kEmpty;
-      }
+      if (ttid == 0) s_occ_n[team] = 0;
       const uint32_t cap = table_cap<CAP>(m.d);
       sync();
-      Best<VBits<W>> bself{VBits<W>(0), kEmpty};
-      if constexpr (FRESH)
-        bself = team_scan_fresh<TEAM, MAXD, W>(c, m, tab, cap, ttid, pol, occ, &s_occ_n[team],
-                                               fails, &s_bmin[team], bar);
-      else
-        team_gather<MODE, W, WEIGHTED>(c, m.i, m.lo, 0, m.d, tab, cap, ttid, TEAM, pol, occ,
-                                       &s_occ_n[team], fails);
+      team_gather<MODE, W, WEIGHTED>(c, m.i, m.lo, 0, m.d, tab, cap, ttid, TEAM, pol, occ,
+                                     &s_occ_n[team], fails);
       sync();
       Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n[team], ttid, TEAM);
       b = team_best<TEAM>(b, s_red[team], ttid, bar);
-      if constexpr (FRESH) best_merge(b, bself.v, bself.k);
       int changed = 0;
       if (ttid == 0) {
         changed = apply_move_cur<MODE>(c, m.i, b.k, m.cur) ? 1 : 0;
