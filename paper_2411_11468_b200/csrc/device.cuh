@@ -98,13 +98,7 @@ struct PassCtx {
   const uint32_t* vid = nullptr;  // position -> vertex id (layout.cu); nullptr = identity
   const uint32_t* pos = nullptr;  // vertex id -> position; nullptr = identity
   int fresh = 0;                  // labels are still the identity (first pass of a run)
-  // Self-label bit (first ParallelAsync pass only, see engine.cu): a label word with
-  // kSelfBit set is the untouched identity label of its vertex. Every label read is
-  // masked with lmask (0x7FFFFFFF while the bit may be present, else all ones).
-  uint32_t lmask = 0xFFFFFFFFu;
 };
-
-constexpr uint32_t kSelfBit = 0x80000000u;
 
 // Vertex id stored at position p (label values are vertex ids).
 __device__ __forceinline__ uint32_t vertex_id(const uint32_t* vid, uint32_t p) {

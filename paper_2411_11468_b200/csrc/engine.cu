@@ -26,21 +26,12 @@ using namespace dev;
 namespace {
 
 // labels = identity (lpa.cpp:250): position p holds the vertex id stored there.
-// `self_bit` marks every label as its vertex's untouched identity (kSelfBit).
 __global__ void k_init(uint32_t* lab, uint8_t* flags, const uint64_t* off, uint32_t n,
-                       const uint32_t* vid, uint32_t self_bit = 0) {
+                       const uint32_t* vid) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    lab[i] = (vid ? vid[i] : i) | self_bit;
+    lab[i] = vid ? vid[i] : i;
     if (flags) flags[i] = (off[i + 1] == off[i]) ? 1 : 0;  // isolated: never examined
   }
-}
-
-// The self-label bit (kSelfBit) needs ids below 2^31, unit weights (the count-only
-// shortcut for self-labelled neighbours) and simple rows (a self label occurs at most
-// once per row). ParallelAsync only.
-inline bool self_labels_ok(const nulpa_graph* g, const nulpa_opts& o) {
-  return o.exec == NULPA_EXEC_PARALLEL_ASYNC && g->weights == nullptr && g->rows_simple &&
-         g->n < kSelfBit;
 }
 
 inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap) {
@@ -375,11 +366,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       NULPA_CUDA(cudaEventCreate(&e[0]));
       NULPA_CUDA(cudaEventCreate(&e[1]));
     }
-  // The self-label bit is used by the first ParallelAsync pass on unit-weight
-  // graphs whose ids fit in 31 bits (self_labels_ok); it is cleared after that pass.
-  const bool self_bits = self_labels_ok(g, o) && !(tuning && tuning->async_first_pass);
-  k_init<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(lab0.p, flags.p, g->offsets, n, g->perm,
-                                                   self_bits ? kSelfBit : 0u);
+  k_init<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(lab0.p, flags.p, g->offsets, n, g->perm);
   NULPA_CUDA(cudaGetLastError());
   NULPA_CUDA(cudaStreamSynchronize(s));
   const double setup_s =
@@ -437,7 +424,6 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     c.vid = g->perm;
     c.pos = g->inv;
     c.fresh = iter == 0 ? 1 : 0;
-    c.lmask = (iter == 0 && self_bits) ? ~kSelfBit : 0xFFFFFFFFu;
     // Synchronous only: there the identity first pass is exactly the reference's.
     // (Under ParallelAsync it is a legal schedule too, but it replaces the in-place
     // first pass, whose early label flooding converges R-MAT one pass sooner and
@@ -512,14 +498,6 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       }
       prof.end(T_OTHER, s);
       ++launches;
-    }
-    if (iter == 0 && self_bits) {
-      k_clear_self<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(cur, 0, n);
-      ++launches;
-      if (check) {  // the cross-check snapshot was taken with the bit set
-        k_clear_self<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(prev.p, 0, n);
-        ++launches;
-      }
     }
     uint64_t reverted = 0;
     if (check)
@@ -713,7 +691,6 @@ struct nulpa_session {
   nulpa::Stream stream;
   int sms = 148, vbytes = 4;
   bool fresh = false;           // labels are the identity (after nulpa_session_init)
-  bool self_bits = false;       // nulpa_session_init set kSelfBit (cleared after the pass)
   bool identity_first = false;  // graph allows the table-free first pass
   ~nulpa_session() { delete plan; }
 };
@@ -770,7 +747,6 @@ void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* i
   c.vid = g->perm;
   c.pos = g->inv;
   c.fresh = ss->fresh ? 1 : 0;
-  c.lmask = (ss->fresh && ss->self_bits) ? ~kSelfBit : 0xFFFFFFFFu;
   Prof prof;
   cudaEvent_t e0, e1;
   NULPA_CUDA(cudaEventCreate(&e0));
@@ -815,11 +791,6 @@ void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* i
       ++launches;
     }
     NULPA_CUDA(cudaGetLastError());
-  }
-  if (c.lmask != 0xFFFFFFFFu) {  // first pass done: drop the self-label bit from the owned range
-    k_clear_self<<<grid_for(ss->hi - ss->lo, 256, ss->sms * 8), 256, 0, s>>>(ss->labels, ss->lo,
-                                                                          ss->hi);
-    ++launches;
   }
   NULPA_CUDA(cudaEventRecord(e1, s));
   NULPA_CUDA(cudaMemcpyAsync(ss->hc.p, ss->ctr.p, kCtr * sizeof(unsigned long long),
@@ -1035,10 +1006,8 @@ int nulpa_session_init(nulpa_session* ss) {
   return guarded([&] {
     if (!ss) throw Error(NULPA_EINVAL, "null session");
     use_device(ss->g->device);
-    ss->self_bits = self_labels_ok(ss->g, ss->o);
     k_init<<<grid_for(ss->g->n, 256, ss->sms * 8), 256, 0, ss->stream.s>>>(
-        ss->labels, ss->flags, ss->g->offsets, ss->g->n, ss->g->perm,
-        ss->self_bits ? kSelfBit : 0u);
+        ss->labels, ss->flags, ss->g->offsets, ss->g->n, ss->g->perm);
     NULPA_CUDA(cudaGetLastError());
     NULPA_CUDA(cudaStreamSynchronize(ss->stream.s));
     ss->fresh = true;

@@ -41,7 +41,7 @@ namespace dev {
 template <int MODE>
 __device__ __forceinline__ bool apply_move(const PassCtx& c, uint32_t i, uint32_t cand) {
   if (cand == kEmpty) return false;
-  const uint32_t cur = ((MODE == kAsync) ? __ldcg(c.lab_out + i) : __ldg(c.lab_in + i)) & c.lmask;
+  const uint32_t cur = (MODE == kAsync) ? __ldcg(c.lab_out + i) : __ldg(c.lab_in + i);
   const bool allowed = c.pick_less ? (cand < cur) : (cand != cur);
   if (!allowed) return false;
   if constexpr (MODE == kAsync) {
@@ -105,7 +105,7 @@ __device__ __forceinline__ Meta fetch_meta(const PassCtx& c, const uint32_t* __r
     if (m.act) {
       m.lo = __ldg(c.g.off + m.i);
       m.d = static_cast<uint32_t>(__ldg(c.g.off + m.i + 1) - m.lo);
-      m.cur = ((MODE == kAsync) ? __ldcg(c.lab_out + m.i) : __ldg(c.lab_in + m.i)) & c.lmask;
+      m.cur = (MODE == kAsync) ? __ldcg(c.lab_out + m.i) : __ldg(c.lab_in + m.i);
     }
   }
   return m;
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
 #pragma unroll
     for (int k = 0; k < DMAX; ++k) {
       const bool valid = k < d && nb[k] != i;  // self-loops skipped (lpa.hpp:102)
-      lab[k] = valid ? (load_label<MODE>(c.lab_in + nb[k]) & c.lmask) : kEmpty;
+      lab[k] = valid ? load_label<MODE>(c.lab_in + nb[k]) : kEmpty;
       wt[k] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + k) : W(0);
     }
     // Per-label total in neighbour order (bit-identical to the reference's
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
         jn = (mn.act && gl < mn.d) ? ld_stream(c.g.tgt + mn.lo + gl, pol) : mn.i;
       }
       const bool valid = m.act && gl < m.d && j != m.i;
-      const uint32_t lab = valid ? (load_label<MODE>(c.lab_in + j) & c.lmask) : kEmpty;
+      const uint32_t lab = valid ? load_label<MODE>(c.lab_in + j) : kEmpty;
       const W w = valid ? edge_weight<W, WEIGHTED>(c.g, m.lo + gl) : W(0);
       const unsigned peers = __match_any_sync(kFull, lab) & gmask;
       W sm;
@@ -310,7 +310,7 @@ __device__ __forceinline__ void team_gather(const PassCtx& c, uint32_t i, uint64
     for (int u = 0; u < U; ++u) {
       const uint32_t e = base + u * T + tid;
       const bool valid = e < e1 && j[u] != i;
-      lab[u] = valid ? (load_label<MODE>(c.lab_in + j[u]) & c.lmask) : kEmpty;
+      lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
       w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
     }
     // Skip warp-rounds with no edge at all (warp-uniform test): short rows do not
@@ -578,7 +578,7 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
       for (int u = 0; u < U; ++u) {
         const uint32_t e = base + u * blockDim.x + threadIdx.x;
         const bool valid = e < e1 && j[u] != i;
-        lab[u] = valid ? (load_label<MODE>(c.lab_in + j[u]) & c.lmask) : kEmpty;
+        lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
         w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
       }
       const uint32_t wbase = base + (threadIdx.x & ~31u);
@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint32_t e = base + u * kBigThreads + threadIdx.x;
-            lab[u] = j[u] != i ? (load_label<MODE>(c.lab_in + j[u]) & c.lmask) : kEmpty;
+            lab[u] = j[u] != i ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
             if (P > 1 && e < d) snap[e] = lab[u];
           }
         } else {
@@ -843,12 +843,6 @@ __global__ void __launch_bounds__(256) k_first_pass_list(PassCtx c, const uint32
   warp_add_counter(c.ctr, C_PROC_V, n_v);
   warp_add_counter(c.ctr, C_PROC_E, n_e);
   warp_add_counter(c.ctr, C_DN, n_dn);
-}
-
-// End of the first ParallelAsync pass: drop the self-label bit from [lo, hi).
-__global__ void k_clear_self(uint32_t* lab, uint32_t lo, uint32_t hi) {
-  for (uint32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x)
-    lab[i] &= ~kSelfBit;
 }
 
 // ---- tier: hubs, global tables -------------------------------------------------------
