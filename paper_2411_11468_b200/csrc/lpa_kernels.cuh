@@ -290,6 +290,81 @@ __device__ __forceinline__ void gather_insert(const PassCtx& c, uint32_t lab, W 
   if (occ) occ_append(r == 2, slot, occ, occ_n);
 }
 
+// U rounds of a team gather at once, unit weights, the CTA's own shared table:
+// the same result as U calls of gather_insert, but every step is issued for all
+// U rounds before the next step (U match_any, then U first probes, U claims, U
+// count adds, one occupancy append), so the rounds' latency chains overlap
+// instead of running back to back. `live` has bit u set when round u holds at
+// least one of the warp's edges (warp-uniform). All 32 lanes call it.
+template <int U, typename W>
+__device__ __forceinline__ void gather_insert_multi(const PassCtx& c, const uint32_t (&lab)[U],
+                                                    unsigned live, SmemTable<W>& tab,
+                                                    uint32_t cap, uint16_t* occ, unsigned* occ_n,
+                                                    unsigned long long& fails) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint32_t mask = cap - 1;
+  unsigned peers[U];
+  uint32_t idx[U], cur[U];
+  bool lead[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) peers[u] = (live >> u & 1u) ? __match_any_sync(kFull, lab[u]) : 0u;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    lead[u] = lab[u] != kEmpty && (peers[u] & lt) == 0u && peers[u] != 0u;
+    idx[u] = hash_start(lab[u], cap);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) cur[u] = lead[u] ? tab.ld_key(idx[u] & mask) : 0u;
+  int r[U];
+  uint32_t slot[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    slot[u] = idx[u] & mask;
+    r[u] = -1;
+    if (lead[u]) {
+      r[u] = 1;
+      if (cur[u] == kEmpty) {
+        cur[u] = tab.cas_key(slot[u], lab[u]);
+        if (cur[u] == kEmpty) {
+          cur[u] = lab[u];
+          r[u] = 2;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!lead[u]) continue;
+    if (cur[u] == lab[u]) {
+      tab.add_count(slot[u], __popc(peers[u]));
+    } else {  // first-probe collision: the probe walk (rare)
+      r[u] = c.strategy == 3
+                 ? tab.template add_collided<3>(cap, lab[u], __popc(peers[u]), idx[u], &slot[u])
+                 : tab.template add_collided<-1>(cap, lab[u], __popc(peers[u]), idx[u], &slot[u],
+                                                 c.strategy);
+      if (r[u] == 0) ++fails;
+    }
+  }
+  // One occupancy append for every slot claimed in the U rounds.
+  if (occ == nullptr) return;  // (hub chunk tables are swept whole)
+  unsigned m[U], tot = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    m[u] = __ballot_sync(kFull, r[u] == 2);
+    tot += __popc(m[u]);
+  }
+  if (tot == 0) return;
+  unsigned b = 0;
+  if (lane == 0) b = atomicAdd(occ_n, tot);
+  b = __shfl_sync(kFull, b, 0);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (r[u] == 2) occ[b + __popc(m[u] & lt)] = static_cast<uint16_t>(slot[u]);
+    b += __popc(m[u]);
+  }
+}
+
 // Gather edges [e0, e1) of vertex i (U edges per thread in flight) into `tab`.
 // `T` threads cooperate; all of them call it with the same bounds.
 template <int MODE, typename W, bool WEIGHTED, typename Tab, int U = 4>
@@ -316,9 +391,17 @@ __device__ __forceinline__ void team_gather(const PassCtx& c, uint32_t i, uint64
     // Skip warp-rounds with no edge at all (warp-uniform test): short rows do not
     // pay for the unrolled tail.
     const uint32_t wbase = base + (tid & ~31u);
+    if constexpr (std::is_same_v<Tab, SmemTable<W>>) {
+      unsigned live = 0;
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (wbase + u * T < e1) gather_insert<W, WEIGHTED>(c, lab[u], w[u], tab, cap, occ, occ_n, fails);
+      for (int u = 0; u < U; ++u) live |= (wbase + u * T < e1 ? 1u : 0u) << u;
+      gather_insert_multi<U, W>(c, lab, live, tab, cap, occ, occ_n, fails);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (wbase + u * T < e1)
+          gather_insert<W, WEIGHTED>(c, lab[u], w[u], tab, cap, occ, occ_n, fails);
+    }
   }
 }
 
