@@ -494,7 +494,7 @@ constexpr size_t team_bytes() {
 }
 
 template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CAP, int MAXD>
-__global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? (TEAM == 32 ? 5 : 6) : 1)
+__global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : 1)
     k_team(PassCtx c, const uint32_t* __restrict__ list,
                                                       uint32_t count) {
   static_assert(CTA_THREADS % TEAM == 0 && TEAM % 32 == 0, "team shape");
