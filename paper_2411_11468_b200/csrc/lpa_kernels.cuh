@@ -485,6 +485,11 @@ __device__ __forceinline__ Best<V> team_best(Best<V> b, Best<V>* red, int team_t
   }
 }
 
+#ifndef NULPA_TEAM_U
+#define NULPA_TEAM_U 4
+#endif
+constexpr int kTeamU = NULPA_TEAM_U;  // gather rounds in flight per team thread
+
 template <int TEAM>
 constexpr uint32_t kTeamBatch = TEAM <= 32 ? 32u : (TEAM <= 128 ? 16u : 4u);
 
@@ -561,7 +566,7 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : 1)
       if (ttid == 0) s_occ_n[team] = 0;
       const uint32_t cap = table_cap<CAP>(m.d);
       sync();
-      team_gather<MODE, W, WEIGHTED>(c, m.i, m.lo, 0, m.d, tab, cap, ttid, TEAM, pol, occ,
+      team_gather<MODE, W, WEIGHTED, Tab, kTeamU>(c, m.i, m.lo, 0, m.d, tab, cap, ttid, TEAM, pol, occ,
                                      &s_occ_n[team], fails);
       sync();
       Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n[team], ttid, TEAM);
