@@ -734,7 +734,10 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
 // at P = 1 and double P when the table overflows. Re-streaming the row costs HBM
 // bandwidth for the targets only (labels hit L2); no cluster barriers, no remote
 // atomics, and every SM owns its own vertex.
-constexpr uint32_t kWideLimit = 10240;  // distinct labels per phase (table load <= 5/8 + slack)
+#ifndef NULPA_WIDE_LIMIT
+#define NULPA_WIDE_LIMIT 12288
+#endif
+constexpr uint32_t kWideLimit = NULPA_WIDE_LIMIT;  // distinct labels per phase (load <= 3/4)
 
 __device__ __forceinline__ uint32_t phase_of(uint32_t key, uint32_t P) {
   const uint32_t h = (key ^ (key >> 16)) * 0x7FEB352Du;
