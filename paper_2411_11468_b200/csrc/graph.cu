@@ -510,6 +510,11 @@ int nulpa_graph_upload(const nulpa_csr* csr, int device, nulpa_graph** out) {
       g->n = csr->n;
       g->m2 = csr->m2;
       g->owns = true;
+      if (can_upload_pipelined(csr)) {
+        upload_pipelined(csr, g);
+        *out = g;
+        return;
+      }
       g->offsets = dalloc<uint64_t>(uint64_t(csr->n) + 1);
       g->targets = dalloc<uint32_t>(csr->m2);
       NULPA_CUDA(cudaMemcpy(g->offsets, csr->offsets, (uint64_t(csr->n) + 1) * 8,

@@ -22,7 +22,9 @@
 // summation order and the identity first pass depend on it).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "internal.hpp"
 #include "layout.hpp"
@@ -194,20 +196,383 @@ void permute_csr(const uint64_t* src_off, const uint32_t* src_tgt, const float* 
   }
 }
 
+// ---- pipelined upload: the host CSR streamed in row chunks, each chunk scattered
+// straight into position order while the next one is in flight ----------------------
+
+// Short rows (degree <= kLongRow) of the input rows [v_a, v_b), whose targets sit in
+// `stage` (stage[0] is entry off[v_a]). Validates every target (< n) and counts
+// in-row descents (rows_simple) on the way.
+__global__ void __launch_bounds__(256) k_scatter_short(
+    const uint64_t* __restrict__ off, const uint32_t* __restrict__ stage, uint32_t v_a,
+    uint32_t v_b, const uint32_t* __restrict__ inv, const uint64_t* __restrict__ dst_off,
+    uint32_t* __restrict__ dst_tgt, uint32_t n, unsigned* bad, unsigned long long* desc,
+    const float* __restrict__ wstage, float* __restrict__ dst_w, unsigned long long* nonunit) {
+  constexpr uint32_t kShort = 8;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t e_base = off[v_a];
+  unsigned long long nd = 0, nnu = 0;
+  unsigned nbad = 0;
+  for (uint32_t base = v_a + gw * 32; base < v_b; base += nw * 32) {
+    const uint32_t v = base + lane;
+    uint64_t slo = 0, dlo = 0;
+    uint32_t d = 0;
+    if (v < v_b) {
+      slo = off[v] - e_base;
+      d = static_cast<uint32_t>(off[v + 1] - off[v]);
+      if (d > kLongRow) d = 0;  // k_scatter_long
+      if (d) dlo = dst_off[inv[v]];
+    }
+    if (d <= kShort) {
+      uint32_t prev = 0;
+      for (uint32_t e = 0; e < d; ++e) {
+        const uint32_t t = stage[slo + e];
+        nbad |= t >= n;
+        nd += e > 0 && prev >= t;
+        prev = t;
+        dst_tgt[dlo + e] = t < n ? inv[t] : 0u;
+        if (wstage) {
+          const float w = wstage[slo + e];
+          nnu += w != 1.0f;
+          dst_w[dlo + e] = w;
+        }
+      }
+    }
+    unsigned long_rows = __ballot_sync(0xFFFFFFFFu, d > kShort);
+    while (long_rows) {
+      const int b = __ffs(long_rows) - 1;
+      long_rows &= long_rows - 1;
+      const uint64_t bs = __shfl_sync(0xFFFFFFFFu, slo, b);
+      const uint64_t bd = __shfl_sync(0xFFFFFFFFu, dlo, b);
+      const uint32_t bdeg = __shfl_sync(0xFFFFFFFFu, d, b);
+      for (uint32_t e = lane; e < bdeg; e += 32) {
+        const uint32_t t = stage[bs + e];
+        nbad |= t >= n;
+        nd += e > 0 && stage[bs + e - 1] >= t;
+        dst_tgt[bd + e] = t < n ? inv[t] : 0u;
+        if (wstage) {
+          const float w = wstage[bs + e];
+          nnu += w != 1.0f;
+          dst_w[bd + e] = w;
+        }
+      }
+    }
+  }
+  if (nbad) atomicOr(bad, 4u);
+  if (nd) atomicAdd(desc, nd);
+  if (nnu) atomicAdd(nonunit, nnu);
+}
+
+// [la, lb): the entries of the long-row list L (ascending input ids) inside [v_a, v_b).
+__global__ void k_long_range(const uint32_t* L, uint32_t nL, uint32_t v_a, uint32_t v_b,
+                             uint32_t* out) {
+  uint32_t lo = 0, hi = nL;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) / 2;
+    if (L[mid] < v_a) lo = mid + 1; else hi = mid;
+  }
+  out[0] = lo;
+  hi = nL;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) / 2;
+    if (L[mid] < v_b) lo = mid + 1; else hi = mid;
+  }
+  out[1] = lo;
+}
+
+// Long rows of the chunk, edge-balanced: warps own kSpan entries of the stream of
+// the chunk's long-row entries (LP = exclusive prefix of the long rows' degrees).
+__global__ void __launch_bounds__(256) k_scatter_long(
+    const uint64_t* __restrict__ off, const uint32_t* __restrict__ stage, uint32_t v_a,
+    const uint32_t* __restrict__ L, const uint64_t* __restrict__ LP, const uint32_t* range,
+    const uint32_t* __restrict__ inv, const uint64_t* __restrict__ dst_off,
+    uint32_t* __restrict__ dst_tgt, uint32_t n, unsigned* bad, unsigned long long* desc,
+    const float* __restrict__ wstage, float* __restrict__ dst_w, unsigned long long* nonunit) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t la = range[0], lb = range[1];
+  if (la >= lb) return;
+  const uint64_t E0 = LP[la], E1 = LP[lb];
+  const uint64_t e_base = off[v_a];
+  const uint64_t gw = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (gridDim.x * uint64_t(blockDim.x)) >> 5;
+  unsigned long long nd = 0, nnu = 0;
+  unsigned nbad = 0;
+  for (uint64_t s0 = E0 + gw * kSpan; s0 < E1; s0 += nw * kSpan) {
+    const uint64_t s1 = min(E1, s0 + kSpan);
+    uint32_t lo = la, hi = lb;  // LP[lo] <= s0 < LP[hi]
+    while (hi - lo > 1) {
+      const uint32_t mid = lo + (hi - lo) / 2;
+      if (LP[mid] <= s0) lo = mid; else hi = mid;
+    }
+    for (uint32_t k = lo; s0 < s1; ++k) {
+      const uint32_t v = L[k];
+      const uint64_t row_end = min(LP[k + 1], s1);
+      const uint64_t r0 = s0 - LP[k];  // offset inside the row
+      const uint64_t src = off[v] - e_base + r0;
+      const uint64_t dst = dst_off[inv[v]] + r0;
+      const uint32_t len = static_cast<uint32_t>(row_end - s0);
+      for (uint32_t x = lane; x < len; x += 32) {
+        const uint32_t t = stage[src + x];
+        nbad |= t >= n;
+        nd += (r0 + x) > 0 && stage[src + x - 1] >= t;
+        dst_tgt[dst + x] = t < n ? inv[t] : 0u;
+        if (wstage) {
+          const float w = wstage[src + x];
+          nnu += w != 1.0f;
+          dst_w[dst + x] = w;
+        }
+      }
+      s0 = row_end;
+    }
+  }
+  if (nbad) atomicOr(bad, 4u);
+  nd = __reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned>(nd));
+  if (lane == 0 && nd) atomicAdd(desc, nd);
+  if (nnu) atomicAdd(nonunit, nnu);
+}
+
+struct LongDeg {
+  const uint64_t* off;
+  const uint32_t* L;
+  __host__ __device__ uint64_t operator()(uint32_t k) const { return off[L[k] + 1] - off[L[k]]; }
+};
+
+struct DegreeOfRow {
+  const uint64_t* off;
+  __host__ __device__ uint32_t operator()(uint32_t v) const {
+    return static_cast<uint32_t>(off[v + 1] - off[v]);
+  }
+};
+
+__global__ void k_offsets_ok(const uint64_t* off, uint32_t n, uint64_t m2, unsigned* bad) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (off[i + 1] < off[i]) atomicOr(bad, 1u);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (off[0] != 0 || off[n] != m2)) atomicOr(bad, 2u);
+}
+
 }  // namespace
 
 int default_layout() { return g_default_layout.load(); }
 
-void relayout_graph(nulpa_graph* g, cudaStream_t s) {
-  g->layout = NULPA_LAYOUT_IDENTITY;
-  if (default_layout() != NULPA_LAYOUT_DEGREE_BUCKETS || g->n < 2) return;
-  const uint32_t n = g->n;
-  const uint64_t m2 = g->m2;
+void build_perm(const uint64_t* off, uint32_t n, uint32_t** perm_out, uint32_t** inv_out,
+                cudaStream_t s);
+
+bool can_upload_pipelined(const nulpa_csr* csr) {
+  return default_layout() == NULPA_LAYOUT_DEGREE_BUCKETS && csr->n >= 2 && csr->m2 > 0;
+}
+
+namespace {
+struct ToDoubleW {
+  __host__ __device__ double operator()(float w) const { return static_cast<double>(w); }
+};
+}  // namespace
+
+// Host CSR (unit weights) -> resident position-order graph. The offsets go first
+// (the permutation needs only degrees); the targets then stream in row chunks of
+// ~256 MB on one stream while the previous chunk is validated and scattered into
+// position order on another, so the relayout and the structural checks hide behind
+// the PCIe transfer.
+void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g) {
+  // Entries per staging buffer (NULPA_UPLOAD_CHUNK overrides it: the tests force
+  // many small chunks and rows longer than a chunk).
+  uint64_t kChunk = 64ull << 20;
+  if (const char* e = std::getenv("NULPA_UPLOAD_CHUNK")) kChunk = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+  const uint32_t n = csr->n;
+  const uint64_t m2 = csr->m2;
+  cudaStream_t sa = nullptr, sb = nullptr;
+  cudaEvent_t ready[2] = {}, freed[2] = {};
+  uint64_t* src_off = nullptr;
+  uint32_t* stage[2] = {nullptr, nullptr};
+  float* wstage[2] = {nullptr, nullptr};
+  uint64_t stage_cap[2] = {0, 0};
+  const bool weighted = csr->weights != nullptr;
+  unsigned long long* d_nonunit = nullptr;
+  uint32_t *L = nullptr, *range = nullptr;
+  uint64_t* LP = nullptr;
+  unsigned* d_bad = nullptr;
+  unsigned long long* d_desc = nullptr;
+  uint32_t* d_max = nullptr;
+  void* tmp = nullptr;
+  auto cleanup = [&]() {
+    if (sa) cudaStreamSynchronize(sa);
+    if (sb) cudaStreamSynchronize(sb);
+    dfree(src_off);
+    dfree(stage[0]);
+    dfree(stage[1]);
+    dfree(wstage[0]);
+    dfree(wstage[1]);
+    dfree(d_nonunit);
+    dfree(L);
+    dfree(LP);
+    dfree(range);
+    dfree(d_bad);
+    dfree(d_desc);
+    dfree(d_max);
+    dfree(tmp);
+    for (int k = 0; k < 2; ++k) {
+      if (ready[k]) cudaEventDestroy(ready[k]);
+      if (freed[k]) cudaEventDestroy(freed[k]);
+    }
+    if (sa) cudaStreamDestroy(sa);
+    if (sb) cudaStreamDestroy(sb);
+  };
+  try {
+    NULPA_CUDA(cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking));
+    NULPA_CUDA(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      NULPA_CUDA(cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming));
+      NULPA_CUDA(cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming));
+    }
+    src_off = dalloc<uint64_t>(uint64_t(n) + 1);
+    d_bad = dalloc<unsigned>(1);
+    d_desc = dalloc<unsigned long long>(1);
+    d_max = dalloc<uint32_t>(1);
+    d_nonunit = dalloc<unsigned long long>(1);
+    NULPA_CUDA(cudaMemsetAsync(d_nonunit, 0, 8, sb));
+    range = dalloc<uint32_t>(2);
+    NULPA_CUDA(cudaMemsetAsync(d_bad, 0, 4, sb));
+    NULPA_CUDA(cudaMemsetAsync(d_desc, 0, 8, sb));
+    NULPA_CUDA(cudaMemcpyAsync(src_off, csr->offsets, (uint64_t(n) + 1) * 8,
+                               cudaMemcpyHostToDevice, sb));
+    k_offsets_ok<<<blocks_for(n), 256, 0, sb>>>(src_off, n, m2, d_bad);
+    NULPA_CUDA(cudaGetLastError());
+    unsigned bad = 0;
+    NULPA_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, sb));
+    NULPA_CUDA(cudaStreamSynchronize(sb));
+    if (bad) throw Error(NULPA_EINVAL, "inconsistent CSR arrays");
+    // Permutation, position-order offsets, the long-row list of the input order.
+    build_perm(src_off, n, &g->perm, &g->inv, sb);
+    g->offsets = dalloc<uint64_t>(uint64_t(n) + 1);
+    g->targets = dalloc<uint32_t>(m2);
+    if (weighted) g->weights = dalloc<float>(m2);
+    NULPA_CUDA(cudaMemsetAsync(g->offsets, 0, 8, sb));
+    {
+      auto degs = cub::TransformInputIterator<uint64_t, RowDegree, cub::CountingInputIterator<uint32_t>>(
+          cub::CountingInputIterator<uint32_t>(0), RowDegree{src_off, g->perm});
+      size_t tb = 0;
+      cub::DeviceScan::InclusiveSum(nullptr, tb, degs, g->offsets + 1, n, sb);
+      auto is_long = cub::TransformInputIterator<uint32_t, LongRow, cub::CountingInputIterator<uint32_t>>(
+          cub::CountingInputIterator<uint32_t>(0), LongRow{src_off});
+      size_t tb2 = 0;
+      L = dalloc<uint32_t>(uint64_t(n) + 1);
+      cub::DeviceSelect::Flagged(nullptr, tb2, cub::CountingInputIterator<uint32_t>(0), is_long, L,
+                                 range, n, sb);
+      auto dg = cub::TransformInputIterator<uint32_t, DegreeOfRow, cub::CountingInputIterator<uint32_t>>(
+          cub::CountingInputIterator<uint32_t>(0), DegreeOfRow{src_off});
+      size_t tb3 = 0;
+      cub::DeviceReduce::Max(nullptr, tb3, dg, d_max, n, sb);
+      tmp = dmalloc(std::max(tb, std::max(tb2, tb3)));
+      cub::DeviceScan::InclusiveSum(tmp, tb, degs, g->offsets + 1, n, sb);
+      cub::DeviceSelect::Flagged(tmp, tb2, cub::CountingInputIterator<uint32_t>(0), is_long, L,
+                                 range, n, sb);
+      cub::DeviceReduce::Max(tmp, tb3, dg, d_max, n, sb);
+      uint32_t nL = 0;
+      NULPA_CUDA(cudaMemcpyAsync(&nL, range, 4, cudaMemcpyDeviceToHost, sb));
+      NULPA_CUDA(cudaMemcpyAsync(&g->max_degree, d_max, 4, cudaMemcpyDeviceToHost, sb));
+      NULPA_CUDA(cudaStreamSynchronize(sb));
+      LP = dalloc<uint64_t>(uint64_t(nL) + 1);
+      NULPA_CUDA(cudaMemsetAsync(LP, 0, 8, sb));
+      if (nL) {
+        auto ld = cub::TransformInputIterator<uint64_t, LongDeg, cub::CountingInputIterator<uint32_t>>(
+            cub::CountingInputIterator<uint32_t>(0), LongDeg{src_off, L});
+        size_t tb4 = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tb4, ld, LP + 1, nL, sb);
+        void* tmp4 = dmalloc(tb4);
+        cub::DeviceScan::InclusiveSum(tmp4, tb4, ld, LP + 1, nL, sb);
+        NULPA_CUDA(cudaStreamSynchronize(sb));
+        dfree(tmp4);
+      }
+      // Chunk loop: H2D of chunk k on sa overlaps the scatter of chunk k-1 on sb.
+      const uint64_t* ho = csr->offsets;
+      uint32_t v_a = 0;
+      for (int k = 0; v_a < n; ++k) {
+        const int b = k & 1;
+        // largest v_b with ho[v_b] - ho[v_a] <= kChunk (at least one row)
+        uint32_t lo = v_a + 1, hi = n;
+        while (lo < hi) {
+          const uint32_t mid = lo + (hi - lo + 1) / 2;
+          if (ho[mid] - ho[v_a] <= kChunk) lo = mid; else hi = mid - 1;
+        }
+        const uint32_t v_b = lo;
+        const uint64_t cnt = ho[v_b] - ho[v_a];
+        if (cnt > stage_cap[b]) {  // (only a row longer than kChunk grows a buffer)
+          NULPA_CUDA(cudaStreamSynchronize(sb));
+          dfree(stage[b]);
+          dfree(wstage[b]);
+          stage[b] = nullptr;
+          wstage[b] = nullptr;
+          stage_cap[b] = std::max(cnt, kChunk);
+          stage[b] = dalloc<uint32_t>(stage_cap[b]);
+          if (weighted) wstage[b] = dalloc<float>(stage_cap[b]);
+        }
+        if (k >= 2) NULPA_CUDA(cudaStreamWaitEvent(sa, freed[b], 0));
+        if (cnt) {
+          NULPA_CUDA(cudaMemcpyAsync(stage[b], csr->targets + ho[v_a], cnt * 4,
+                                     cudaMemcpyHostToDevice, sa));
+          if (weighted)
+            NULPA_CUDA(cudaMemcpyAsync(wstage[b], csr->weights + ho[v_a], cnt * 4,
+                                       cudaMemcpyHostToDevice, sa));
+        }
+        NULPA_CUDA(cudaEventRecord(ready[b], sa));
+        NULPA_CUDA(cudaStreamWaitEvent(sb, ready[b], 0));
+        k_long_range<<<1, 1, 0, sb>>>(L, nL, v_a, v_b, range);
+        k_scatter_short<<<blocks_for((uint64_t(v_b - v_a) + 7) / 8), 256, 0, sb>>>(
+            src_off, stage[b], v_a, v_b, g->inv, g->offsets, g->targets, n, d_bad, d_desc,
+            wstage[b], g->weights, d_nonunit);
+        if (nL)
+          k_scatter_long<<<148 * 4, 256, 0, sb>>>(src_off, stage[b], v_a, L, LP, range, g->inv,
+                                                  g->offsets, g->targets, n, d_bad, d_desc,
+                                                  wstage[b], g->weights, d_nonunit);
+        NULPA_CUDA(cudaGetLastError());
+        NULPA_CUDA(cudaEventRecord(freed[b], sb));
+        v_a = v_b;
+      }
+    }
+    unsigned long long desc = 0;
+    NULPA_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, sb));
+    NULPA_CUDA(cudaMemcpyAsync(&desc, d_desc, 8, cudaMemcpyDeviceToHost, sb));
+    NULPA_CUDA(cudaStreamSynchronize(sb));
+    if (bad) throw Error(NULPA_EINVAL, bad & 4u ? "CSR target id out of range" : "inconsistent CSR arrays");
+    g->total_2m = static_cast<double>(m2);
+    if (weighted) {
+      unsigned long long nonunit = 0;
+      NULPA_CUDA(cudaMemcpy(&nonunit, d_nonunit, 8, cudaMemcpyDeviceToHost));
+      if (nonunit == 0) {
+        // every weight is 1.0f: drop the array (results identical, 4 B/edge saved)
+        dfree(g->weights);
+        g->weights = nullptr;
+      } else {
+        double* d_sum = dalloc<double>(1);
+        auto wd = cub::TransformInputIterator<double, ToDoubleW, const float*>(g->weights, ToDoubleW{});
+        size_t tb = 0;
+        cub::DeviceReduce::Sum(nullptr, tb, wd, d_sum, m2, sb);
+        void* t2 = dmalloc(tb);
+        cub::DeviceReduce::Sum(t2, tb, wd, d_sum, m2, sb);
+        NULPA_CUDA(cudaMemcpyAsync(&g->total_2m, d_sum, 8, cudaMemcpyDeviceToHost, sb));
+        NULPA_CUDA(cudaStreamSynchronize(sb));
+        dfree(t2);
+        dfree(d_sum);
+      }
+    }
+    g->rows_simple = desc == 0;
+    g->layout = NULPA_LAYOUT_DEGREE_BUCKETS;
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
+// perm (position -> vertex) and inv (vertex -> position) of the bucketed order,
+// from the input's offsets.
+void build_perm(const uint64_t* off, uint32_t n, uint32_t** perm_out, uint32_t** inv_out,
+                cudaStream_t s) {
   uint8_t* k0 = dalloc<uint8_t>(n);
   uint8_t* k1 = dalloc<uint8_t>(n);
   uint32_t* ids = dalloc<uint32_t>(n);
   uint32_t* perm = dalloc<uint32_t>(n);
-  k_layout_keys<<<blocks_for(n), 256, 0, s>>>(g->offsets, n, k0, ids);
+  k_layout_keys<<<blocks_for(n), 256, 0, s>>>(off, n, k0, ids);
   NULPA_CUDA(cudaGetLastError());
   {
     // Stable LSD radix sort on the 6-bit bucket key: ascending id inside a bucket.
@@ -227,6 +592,17 @@ void relayout_graph(nulpa_graph* g, cudaStream_t s) {
   uint32_t* inv = dalloc<uint32_t>(n);
   k_invert<<<blocks_for(n), 256, 0, s>>>(perm, n, inv);
   NULPA_CUDA(cudaGetLastError());
+  *perm_out = perm;
+  *inv_out = inv;
+}
+
+void relayout_graph(nulpa_graph* g, cudaStream_t s) {
+  g->layout = NULPA_LAYOUT_IDENTITY;
+  if (default_layout() != NULPA_LAYOUT_DEGREE_BUCKETS || g->n < 2) return;
+  const uint32_t n = g->n;
+  const uint64_t m2 = g->m2;
+  uint32_t *perm = nullptr, *inv = nullptr;
+  build_perm(g->offsets, n, &perm, &inv, s);
   // Rows longer than kLongRow form a prefix of the position order (their
   // buckets come first): copy them edge-balanced.
   uint32_t long_rows = 0;

@@ -18,6 +18,10 @@ void to_positions_u32(const nulpa_graph* g, const uint32_t* vtx, uint32_t* pos, 
 void to_vertices_u32(const nulpa_graph* g, const uint32_t* pos, uint32_t* vtx, cudaStream_t s);
 void to_positions_u8(const nulpa_graph* g, const uint8_t* vtx, uint8_t* pos, cudaStream_t s);
 void to_vertices_u8(const nulpa_graph* g, const uint8_t* pos, uint8_t* vtx, cudaStream_t s);
+// Host CSR upload with the relayout overlapped with the transfer (unit weights,
+// bucketed layout); fills offsets/targets/perm/inv/max_degree/total_2m/rows_simple.
+bool can_upload_pipelined(const nulpa_csr* csr);
+void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g);
 // Download the CSR in the input's vertex numbering.
 void download_vertex_order(const nulpa_graph* g, uint64_t* off_h, uint32_t* tgt_h, float* w_h);
 
