@@ -18,6 +18,10 @@
 #include "layout.hpp"
 #include "plan.hpp"
 
+#ifndef NULPA_BLOCK2_SPLIT
+#define NULPA_BLOCK2_SPLIT dev::kBlockMax  // rows above block_max go to the 1024-thread CTA tier
+#endif
+
 namespace nulpa {
 
 namespace {
@@ -352,8 +356,8 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
         {std::max<uint64_t>(tm, 16) + 1, 32},           // T_WARP
         {33, tb.warp_max},                              // T_WTAB
         {uint64_t(tb.warp_max) + 1, tb.block_max},      // T_BLOCK
-        {uint64_t(tb.block_max) + 1, dev::kBlock2Max},   // T_BLOCK2
-        {uint64_t(dev::kBlock2Max) + 1, dev::kBigMax},   // T_BIG
+        {uint64_t(tb.block_max) + 1, NULPA_BLOCK2_SPLIT},   // T_BLOCK2
+        {uint64_t(NULPA_BLOCK2_SPLIT) + 1, dev::kBigMax},   // T_BIG
         {uint64_t(dev::kBigMax) + 1, dev::kClusterMax},  // T_CLUSTER
         {uint64_t(dev::kClusterMax) + 1, ~0ull}};        // T_HUB
     uint64_t* d_num = dalloc<uint64_t>(1);
