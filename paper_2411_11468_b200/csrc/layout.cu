@@ -305,13 +305,13 @@ __global__ void __launch_bounds__(256) k_scatter_long(
       const uint32_t mid = lo + (hi - lo) / 2;
       if (LP[mid] <= s0) lo = mid; else hi = mid;
     }
-    for (uint32_t k = lo; s0 < s1; ++k) {
+    for (uint64_t cur = s0, k = lo; cur < s1; ++k) {
       const uint32_t v = L[k];
       const uint64_t row_end = min(LP[k + 1], s1);
-      const uint64_t r0 = s0 - LP[k];  // offset inside the row
+      const uint64_t r0 = cur - LP[k];  // offset inside the row
       const uint64_t src = off[v] - e_base + r0;
       const uint64_t dst = dst_off[inv[v]] + r0;
-      const uint32_t len = static_cast<uint32_t>(row_end - s0);
+      const uint32_t len = static_cast<uint32_t>(row_end - cur);
       for (uint32_t x = lane; x < len; x += 32) {
         const uint32_t t = stage[src + x];
         nbad |= t >= n;
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(256) k_scatter_long(
           dst_w[dst + x] = w;
         }
       }
-      s0 = row_end;
+      cur = row_end;
     }
   }
   if (nbad) atomicOr(bad, 4u);

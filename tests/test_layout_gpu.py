@@ -152,3 +152,18 @@ def test_pipelined_upload_golden_weighted(name, golden_index, monkeypatch):
         assert r.stats.delta_n_per_iter == run["delta_n"]
     for k, q in enumerate(meta["modularity"]):
         assert abs(lp.modularity(g, d[f"mod{k}_labels"]) - q) < 1e-12
+
+
+def test_pipelined_upload_many_long_row_spans(monkeypatch):
+    """More long-row spans than warps in the scatter grid (each warp walks several
+    4096-entry spans): R-MAT scale 20 in one chunk and in small chunks."""
+    dg = lp.DeviceGraph.rmat(20, 16, 1)
+    g = dg.download()
+    dg.free()
+    for chunk in (None, "300000"):
+        if chunk:
+            monkeypatch.setenv("NULPA_UPLOAD_CHUNK", chunk)
+        up = lp.DeviceGraph.upload(lp.CsrGraph(g.offsets, g.targets, None))
+        h = up.download()
+        assert np.array_equal(h.offsets, g.offsets) and np.array_equal(h.targets, g.targets)
+        up.free()
