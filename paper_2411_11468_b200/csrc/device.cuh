@@ -253,10 +253,10 @@ __device__ __forceinline__ void probe_advance(int strategy, uint32_t& idx, uint3
 template <bool PACKED, typename W>
 struct Table;
 
-// Unit weights: one 64-bit word per slot, (key << 32) | count, so the argmax
-// sweep reads a slot with one load. Updates use native 32-bit shared/global
-// atomics on the two halves (a 64-bit atomicAdd on shared memory is a CAS spin
-// loop in SASS): CAS on the key half to claim, atomicAdd on the count half.
+// Unit weights in GLOBAL memory (hub tables): one 64-bit word per slot,
+// (key << 32) | count. A new key is claimed together with its count by one
+// 64-bit CAS, an existing key is counted by one 64-bit atomicAdd (both native on
+// global memory; the count never carries into the key half).
 template <typename W>
 struct Table<true, W> {
   unsigned long long* w;
@@ -267,33 +267,27 @@ struct Table<true, W> {
   __device__ __forceinline__ void bind_split(void* base, void*) {
     w = static_cast<unsigned long long*>(base);
   }
-  __device__ __forceinline__ uint32_t* key_word(uint32_t s) const {
-    return reinterpret_cast<uint32_t*>(w + s) + 1;  // little-endian: high half
-  }
-  __device__ __forceinline__ uint32_t* count_word(uint32_t s) const {
-    return reinterpret_cast<uint32_t*>(w + s);
-  }
   __device__ __forceinline__ void clear_slot(uint32_t s) { w[s] = kEmptyWord; }
   __device__ __forceinline__ int add(uint32_t cap, int strategy, uint32_t key, W v,
                                      uint32_t* slot) {
     const uint32_t cnt = static_cast<uint32_t>(v);
+    const unsigned long long mine = (static_cast<unsigned long long>(key) << 32) | cnt;
     const uint32_t mask = cap - 1;
     uint32_t idx = hash_start(key, cap), step = 1, h2 = 0;
     for (uint32_t t = 0; t < 2 * cap; ++t) {
       const uint32_t s = idx & mask;
-      uint32_t cur = *((volatile uint32_t*)key_word(s));
-      int r = 1;
-      if (cur == kEmpty) {
-        cur = atomicCAS(key_word(s), kEmpty, key);
-        if (cur == kEmpty) {
-          cur = key;
-          r = 2;
+      unsigned long long cur = *((volatile unsigned long long*)(w + s));
+      if (cur == kEmptyWord) {
+        cur = atomicCAS(w + s, kEmptyWord, mine);
+        if (cur == kEmptyWord) {
+          *slot = s;
+          return 2;
         }
       }
-      if (cur == key) {
-        atomicAdd(count_word(s), cnt);
+      if (static_cast<uint32_t>(cur >> 32) == key) {
+        atomicAdd(w + s, static_cast<unsigned long long>(cnt));
         *slot = s;
-        return r;
+        return 1;
       }
       if (t == 0) h2 = hash_step(key);  // second hash only after a collision
       if (t + 1 >= cap)

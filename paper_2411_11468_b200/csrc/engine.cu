@@ -87,7 +87,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   constexpr size_t block2_smem = 1 * team_bytes<Tab, kBlock2Cap, kBlock2Max>();
   constexpr size_t big_smem = team_bytes<Tab, kBigCap, kBigMax>();
   constexpr size_t cluster_smem = cluster_bytes<Tab>();
-  constexpr size_t hub_smem = kHubCap * Tab::kSlotBytes;
+  constexpr size_t hub_smem = kHubCap * Tab::kSlotBytes + kHubChunk * sizeof(uint16_t);
   auto k_wt = k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax>;
   auto k_b1 = k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax>;
   auto k_b2 = k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max>;

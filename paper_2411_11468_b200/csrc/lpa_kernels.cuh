@@ -974,8 +974,13 @@ template <int MODE, typename W, bool WEIGHTED>
 __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h) {
   using Tab = std::conditional_t<kPacked<WEIGHTED>, SmemTable<W>, Table<false, W>>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ unsigned s_occ_n;
   Tab tab;
   tab.bind(smem_raw, kHubCap);
+  // The chunk table is kept empty between items: its occupied slots are listed
+  // (as in the team tables) and the flush reads and resets only those.
+  uint16_t* socc = reinterpret_cast<uint16_t*>(smem_raw + size_t(kHubCap) * Tab::kSlotBytes);
+  for (uint32_t s = threadIdx.x; s < kHubCap; s += blockDim.x) tab.clear_slot(s);  // once
   const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31;
   unsigned long long fails = 0;
@@ -988,24 +993,28 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h
     const uint32_t e0 = h.item_start[it];
     const uint32_t e1 = min(d, e0 + kHubChunk);
     const uint32_t cap = kHubCap;
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) tab.clear_slot(s);
+    if (threadIdx.x == 0) s_occ_n = 0;
     __syncthreads();
     team_gather<MODE, W, WEIGHTED>(c, i, lo, e0, e1, tab, cap, threadIdx.x, blockDim.x, pol,
-                                   nullptr, nullptr, fails);
+                                   socc, &s_occ_n, fails);
     __syncthreads();
     Table<kPacked<WEIGHTED>, W> g;  // the hub's global table
     bind_hub_table<Table<kPacked<WEIGHTED>, W>, W, kPacked<WEIGHTED>>(g, h, x);
     uint32_t* occ = h.occ + h.occ_off[x];
     const uint32_t gcap = h.tab_cap[x];
-    for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {  // uniform trip count
-      uint32_t k;
-      VBits<W> vb;
-      tab.read(s, k, vb);
+    const uint32_t n_occ = s_occ_n;
+    for (uint32_t base = 0; base < n_occ; base += blockDim.x) {  // uniform trip count
+      const uint32_t p = base + threadIdx.x;
       int r = -1;
       uint32_t gslot = 0;
-      if (k != kEmpty) {
-        r = g.add(gcap, c.strategy, k, tab.value(s), &gslot);
+      if (p < n_occ) {
+        const uint32_t sl = socc[p];
+        uint32_t k;
+        VBits<W> vb;
+        tab.read(sl, k, vb);
+        r = g.add(gcap, c.strategy, k, tab.value(sl), &gslot);
         if (r == 0) ++fails;
+        tab.clear_slot(sl);
       }
       const unsigned claimed = __ballot_sync(kFull, r == 2);
       if (claimed) {
