@@ -75,6 +75,7 @@ constexpr int kClusterSize = 8;     // portable cluster size
 constexpr int kClusterCap = 16384;  // slots per CTA of the cluster
 constexpr int kClusterMax = kClusterSize * kClusterCap * 3 / 4;  // 98304, load <= 3/4
 constexpr int kHubChunk = 2048;     // edges per hub work item (<= kBlockCap / 2)
+constexpr int kHubSweep = 8192;     // table slots per hub sweep item
 
 struct Graph {
   const uint64_t* __restrict__ off;
@@ -113,9 +114,6 @@ struct HubCtx {
   const uint32_t* hub_v;      // [H] vertex ids
   const uint64_t* tab_off;    // [H] slot offset into the global table
   const uint32_t* tab_cap;    // [H] power-of-two capacity
-  const uint64_t* occ_off;    // [H] offset into occ
-  uint32_t* occ_n;            // [H] occupied-slot counts
-  uint32_t* occ;              // occupied-slot lists
   void* tab;                  // packed words (unit weights) or keys (split)
   void* tab_vals;             // split tables: values
   unsigned long long* best;   // [H] packed argmax (value bits << 32 | ~key), or double bits
@@ -124,8 +122,11 @@ struct HubCtx {
   uint8_t* changed;           // [H]
   const uint32_t* item_hub;   // [I] hub index of each work item
   const uint32_t* item_start; // [I] first edge of the item within the hub row
+  const uint32_t* sitem_hub;  // [S] hub index of each table-sweep item
+  const uint32_t* sitem_start;// [S] first slot of the sweep item
   uint32_t n_hubs;
   uint32_t n_items;
+  uint32_t n_sitems;
 };
 
 // ---- memory access helpers -------------------------------------------------

@@ -191,10 +191,11 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     const unsigned gh = grid_for(p.n_hubs, 256, 1024);
     k_hub_select<MODE><<<gh, 256, 0, s>>>(c, h);
     k_hub_accum<MODE, W, WEIGHTED><<<gi, kBlockThreads, hub_smem, s>>>(c, h);
-    k_hub_argmax<W, WEIGHTED><<<gi, kBlockThreads, 0, s>>>(h);
+    const unsigned gs = grid_for(p.n_sitems, 1, sms * 8);
+    k_hub_sweep<W, WEIGHTED><<<gs, kBlockThreads, 0, s>>>(h);
     launches += 3;
     if constexpr (sizeof(VBits<W>) == 8) {
-      k_hub_argmax_key_f64<<<gi, kBlockThreads, 0, s>>>(h);
+      k_hub_sweep_key_f64<<<gs, kBlockThreads, 0, s>>>(h);
       ++launches;
     }
     k_hub_decide<MODE, W, WEIGHTED><<<gh, 256, 0, s>>>(c, h);

@@ -294,9 +294,8 @@ Plan::~Plan() {
   for (auto* p : list) dfree(p);
   dfree(tab_off);
   dfree(tab_cap);
-  dfree(occ_off);
-  dfree(occ_n);
-  dfree(occ);
+  dfree(sitem_hub);
+  dfree(sitem_start);
   dfree(tab);
   dfree(tab_vals);
   dfree(best);
@@ -413,35 +412,34 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
       NULPA_CUDA(cudaStreamSynchronize(s));
       dfree(d_deg);
     }
-    std::vector<uint64_t> toff(H), ooff(H);
-    std::vector<uint32_t> tcap(H), ihub, istart;
-    uint64_t slots = 0, occs = 0;
+    std::vector<uint64_t> toff(H);
+    std::vector<uint32_t> tcap(H), ihub, istart, shub, sstart;
+    uint64_t slots = 0;
     for (uint32_t x = 0; x < H; ++x) {
       const uint32_t d = hdeg[x];
       const uint32_t cap = dev::pow2_ceil(d + d / 2 + 1);  // load factor <= 2/3
       toff[x] = slots;
       tcap[x] = cap;
-      ooff[x] = occs;
       slots += cap;
-      occs += d;
       for (uint32_t e = 0; e < d; e += dev::kHubChunk) {
         ihub.push_back(x);
         istart.push_back(e);
       }
+      for (uint32_t sl = 0; sl < cap; sl += dev::kHubSweep) {
+        shub.push_back(x);
+        sstart.push_back(sl);
+      }
     }
     p->n_items = static_cast<uint32_t>(ihub.size());
+    p->n_sitems = static_cast<uint32_t>(shub.size());
     p->table_slots = slots;
-    p->occ_slots = occs;
     // (+1 entries so every array is non-empty and the memsets below stay in bounds)
     p->tab_off = dalloc<uint64_t>(H + 1);
     p->tab_cap = dalloc<uint32_t>(H + 1);
-    p->occ_off = dalloc<uint64_t>(H + 1);
-    p->occ_n = dalloc<uint32_t>(H + 1);
     p->best = dalloc<unsigned long long>(H + 1);
     p->best_k = dalloc<uint32_t>(H + 1);
     p->active = dalloc<uint8_t>(H + 1);
     p->changed = dalloc<uint8_t>(H + 1);
-    p->occ = dalloc<uint32_t>(occs + 1);
     if (p->weighted) {
       p->tab = dalloc<uint32_t>(slots + 1);
       p->tab_vals = dmalloc(slots * value_bytes + 16);
@@ -450,14 +448,16 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
     }
     p->item_hub = dalloc<uint32_t>(p->n_items + 1);
     p->item_start = dalloc<uint32_t>(p->n_items + 1);
+    p->sitem_hub = dalloc<uint32_t>(p->n_sitems + 1);
+    p->sitem_start = dalloc<uint32_t>(p->n_sitems + 1);
     if (H) {
       NULPA_CUDA(cudaMemcpy(p->tab_off, toff.data(), H * 8, cudaMemcpyHostToDevice));
       NULPA_CUDA(cudaMemcpy(p->tab_cap, tcap.data(), H * 4, cudaMemcpyHostToDevice));
-      NULPA_CUDA(cudaMemcpy(p->occ_off, ooff.data(), H * 8, cudaMemcpyHostToDevice));
+      NULPA_CUDA(cudaMemcpy(p->sitem_hub, shub.data(), shub.size() * 4, cudaMemcpyHostToDevice));
+      NULPA_CUDA(cudaMemcpy(p->sitem_start, sstart.data(), sstart.size() * 4, cudaMemcpyHostToDevice));
       NULPA_CUDA(cudaMemcpy(p->item_hub, ihub.data(), ihub.size() * 4, cudaMemcpyHostToDevice));
       NULPA_CUDA(cudaMemcpy(p->item_start, istart.data(), istart.size() * 4, cudaMemcpyHostToDevice));
     }
-    NULPA_CUDA(cudaMemsetAsync(p->occ_n, 0, H * 4 + 4, s));
     NULPA_CUDA(cudaMemsetAsync(p->best, 0, H * 8 + 8, s));
     NULPA_CUDA(cudaMemsetAsync(p->best_k, 0xFF, H * 4 + 4, s));
     NULPA_CUDA(cudaMemsetAsync(p->changed, 0, H + 1, s));

@@ -998,62 +998,47 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h
     team_gather<MODE, W, WEIGHTED>(c, i, lo, e0, e1, tab, cap, threadIdx.x, blockDim.x, pol,
                                    socc, &s_occ_n, fails);
     __syncthreads();
-    Table<kPacked<WEIGHTED>, W> g;  // the hub's global table
+    Table<kPacked<WEIGHTED>, W> g;  // the hub's global table (swept densely, k_hub_sweep)
     bind_hub_table<Table<kPacked<WEIGHTED>, W>, W, kPacked<WEIGHTED>>(g, h, x);
-    uint32_t* occ = h.occ + h.occ_off[x];
     const uint32_t gcap = h.tab_cap[x];
     const uint32_t n_occ = s_occ_n;
-    for (uint32_t base = 0; base < n_occ; base += blockDim.x) {  // uniform trip count
-      const uint32_t p = base + threadIdx.x;
-      int r = -1;
-      uint32_t gslot = 0;
-      if (p < n_occ) {
-        const uint32_t sl = socc[p];
-        uint32_t k;
-        VBits<W> vb;
-        tab.read(sl, k, vb);
-        r = g.add(gcap, c.strategy, k, tab.value(sl), &gslot);
-        if (r == 0) ++fails;
-        tab.clear_slot(sl);
-      }
-      const unsigned claimed = __ballot_sync(kFull, r == 2);
-      if (claimed) {
-        const int leader = __ffs(claimed) - 1;
-        uint32_t basepos = 0;
-        if (lane == leader) basepos = atomicAdd(h.occ_n + x, static_cast<uint32_t>(__popc(claimed)));
-        basepos = __shfl_sync(kFull, basepos, leader);
-        if (r == 2) occ[basepos + __popc(claimed & ((1u << lane) - 1u))] = gslot;
-      }
+    for (uint32_t p = threadIdx.x; p < n_occ; p += blockDim.x) {
+      const uint32_t sl = socc[p];
+      uint32_t k;
+      VBits<W> vb;
+      tab.read(sl, k, vb);
+      uint32_t gslot;
+      if (g.add(gcap, c.strategy, k, tab.value(sl), &gslot) == 0) ++fails;
+      tab.clear_slot(sl);
     }
     __syncthreads();
   }
   warp_add_counter(c.ctr, C_FAIL, fails);
 }
 
-// Sparse argmax over the occupied slots of each active hub; the slots it reads
-// are reset (u32-bits path) so the tables are idle for the next pass.
+// Dense argmax over each active hub's table, (hub, kHubSweep-slot) items: the
+// slots are read and reset in order (coalesced), so a pass costs two streams over
+// the hub tables instead of one random access per distinct label (the first pass
+// from identity labels fills the tables with ~one label per edge).
 template <typename W, bool WEIGHTED>
-__global__ void __launch_bounds__(kBlockThreads) k_hub_argmax(HubCtx h) {
+__global__ void __launch_bounds__(kBlockThreads) k_hub_sweep(HubCtx h) {
   using Tab = Table<kPacked<WEIGHTED>, W>;
   __shared__ Best<VBits<W>> red[32];
-  for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
-    const uint32_t x = h.item_hub[it];
-    if (!h.active[x]) continue;
-    const uint32_t e0 = h.item_start[it];
-    const uint32_t n_occ = h.occ_n[x];
-    if (e0 >= n_occ) continue;
-    const uint32_t e1 = min(n_occ, e0 + kHubChunk);
+  for (uint32_t it = blockIdx.x; it < h.n_sitems; it += gridDim.x) {
+    const uint32_t x = h.sitem_hub[it];
+    if (!h.active[x]) continue;  // (uniform) untouched tables stay empty
+    const uint32_t s0 = h.sitem_start[it];
+    const uint32_t s1 = min(h.tab_cap[x], s0 + kHubSweep);
     Tab g;
     bind_hub_table<Tab, W, kPacked<WEIGHTED>>(g, h, x);
-    const uint32_t* occ = h.occ + h.occ_off[x];
     Best<VBits<W>> b{VBits<W>(0), kEmpty};
-    for (uint32_t p = e0 + threadIdx.x; p < e1; p += blockDim.x) {
-      const uint32_t s = occ[p];
+    for (uint32_t sl = s0 + threadIdx.x; sl < s1; sl += blockDim.x) {
       uint32_t k;
       VBits<W> v;
-      g.read(s, k, v);
+      g.read(sl, k, v);
+      if (k == kEmpty) continue;
       best_merge(b, v, k);
-      if constexpr (sizeof(VBits<W>) == 4) g.clear_slot(s);
+      if constexpr (sizeof(VBits<W>) == 4) g.clear_slot(sl);
     }
     b = block_best(b, red);
     if (threadIdx.x == 0 && b.k != kEmpty) {
@@ -1070,24 +1055,21 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_argmax(HubCtx h) {
 }
 
 // fp64 weighted path only: the smallest key among slots holding the maximum
-// value; resets the slots.
-__global__ void __launch_bounds__(kBlockThreads) k_hub_argmax_key_f64(HubCtx h) {
+// value (dense, like k_hub_sweep); resets the slots.
+__global__ void __launch_bounds__(kBlockThreads) k_hub_sweep_key_f64(HubCtx h) {
   Table<false, double> g;
-  for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
-    const uint32_t x = h.item_hub[it];
+  for (uint32_t it = blockIdx.x; it < h.n_sitems; it += gridDim.x) {
+    const uint32_t x = h.sitem_hub[it];
     if (!h.active[x]) continue;
-    const uint32_t e0 = h.item_start[it];
-    const uint32_t n_occ = h.occ_n[x];
-    if (e0 >= n_occ) continue;
-    const uint32_t e1 = min(n_occ, e0 + kHubChunk);
+    const uint32_t s0 = h.sitem_start[it];
+    const uint32_t s1 = min(h.tab_cap[x], s0 + kHubSweep);
     g.bind_split(static_cast<uint32_t*>(h.tab) + h.tab_off[x],
                  static_cast<double*>(h.tab_vals) + h.tab_off[x]);
-    const uint32_t* occ = h.occ + h.occ_off[x];
     const double bestv = __longlong_as_double(static_cast<long long>(h.best[x]));
-    for (uint32_t p = e0 + threadIdx.x; p < e1; p += blockDim.x) {
-      const uint32_t s = occ[p];
-      if (g.v[s] == bestv) atomicMin(h.best_k + x, g.k[s]);
-      g.clear_slot(s);
+    for (uint32_t sl = s0 + threadIdx.x; sl < s1; sl += blockDim.x) {
+      if (g.k[sl] == kEmpty) continue;
+      if (g.v[sl] == bestv) atomicMin(h.best_k + x, g.k[sl]);
+      g.clear_slot(sl);
     }
   }
 }
@@ -1101,18 +1083,16 @@ __global__ void k_hub_decide(PassCtx c, HubCtx h) {
     if (x >= h.n_hubs) continue;
     uint8_t ch = 0;
     if (h.active[x]) {
-      uint32_t cand = kEmpty;
-      if (h.occ_n[x] > 0) {
-        if constexpr (sizeof(VBits<W>) == 4)
-          cand = ~static_cast<uint32_t>(h.best[x] & 0xFFFFFFFFull);
-        else
-          cand = h.best_k[x];
+      uint32_t cand = kEmpty;  // stays kEmpty when the row held only self-loops
+      if constexpr (sizeof(VBits<W>) == 4) {
+        if (h.best[x] != 0) cand = ~static_cast<uint32_t>(h.best[x] & 0xFFFFFFFFull);
+      } else {
+        cand = h.best_k[x];
       }
       ch = apply_move<MODE>(c, h.hub_v[x], cand) ? 1 : 0;
       n_dn += ch;
     }
     h.changed[x] = ch;
-    h.occ_n[x] = 0;
     h.best[x] = 0;
     h.best_k[x] = kEmpty;
   }

@@ -21,12 +21,12 @@ struct Plan {
   bool weighted = false;  // hub tables: packed 64-bit words (unit weights) or split
   // Hub tier.
   uint32_t n_hubs = 0, n_items = 0;
-  uint64_t table_slots = 0, occ_slots = 0;
+  uint32_t n_sitems = 0;
+  uint64_t table_slots = 0;
   uint64_t* tab_off = nullptr;
   uint32_t* tab_cap = nullptr;
-  uint64_t* occ_off = nullptr;
-  uint32_t* occ_n = nullptr;
-  uint32_t* occ = nullptr;
+  uint32_t* sitem_hub = nullptr;
+  uint32_t* sitem_start = nullptr;
   void* tab = nullptr;       // packed words, or keys (weighted)
   void* tab_vals = nullptr;  // weighted: values
   unsigned long long* best = nullptr;
@@ -42,9 +42,9 @@ struct Plan {
     h.hub_v = list[dev::T_HUB];
     h.tab_off = tab_off;
     h.tab_cap = tab_cap;
-    h.occ_off = occ_off;
-    h.occ_n = occ_n;
-    h.occ = occ;
+    h.sitem_hub = sitem_hub;
+    h.sitem_start = sitem_start;
+    h.n_sitems = n_sitems;
     h.tab = tab;
     h.tab_vals = tab_vals;
     h.best = best;
