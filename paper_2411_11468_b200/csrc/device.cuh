@@ -68,9 +68,15 @@ constexpr int kBlockCap = 2048;     // per-team slots (load <= 1/2)
 constexpr int kBlock2Max = 4096;    // T_BLOCK2 degree bound
 constexpr int kBlock2Cap = 8192;    // per-team slots (load <= 1/2)
 constexpr int kHubCap = 4096;       // hub pre-aggregation slots per CTA
-constexpr int kBigThreads = 1024;
-constexpr int kBigCap = 16384;      // 128 KB packed
-constexpr int kBigMax = 12288;      // load <= 3/4
+constexpr int kBigThreads = 1024;   // wide-row CTAs (k_wide, k_cluster)
+#ifndef NULPA_MID_THREADS
+#define NULPA_MID_THREADS 1024
+#define NULPA_MID_CAP 16384
+#define NULPA_MID_MAX 12288
+#endif
+constexpr int kMidThreads = NULPA_MID_THREADS;  // T_BIG: one CTA per vertex
+constexpr int kBigCap = NULPA_MID_CAP;          // its table (128 KB packed)
+constexpr int kBigMax = NULPA_MID_MAX;          // load <= 3/4
 constexpr int kClusterSize = 8;     // portable cluster size
 constexpr int kClusterCap = 16384;  // slots per CTA of the cluster
 constexpr int kClusterMax = kClusterSize * kClusterCap * 3 / 4;  // 98304, load <= 3/4

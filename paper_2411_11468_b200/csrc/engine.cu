@@ -91,7 +91,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   auto k_wt = k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax>;
   auto k_b1 = k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax>;
   auto k_b2 = k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max>;
-  auto k_bg = k_team<MODE, W, WEIGHTED, kBigThreads, kBigThreads, kBigCap, kBigMax>;
+  auto k_bg = k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax>;
   static bool init = false;
   if (!init) {
     allow_smem(k_wt, wtab_smem);
@@ -162,7 +162,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   if (p.count[T_BIG] && (tiers >> T_BIG & 1u)) {
     tier(T_BIG);
     NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
-    k_bg<<<resident_grid(k_bg, kBigThreads, big_smem, p.count[T_BIG], kTeamBatch<kBigThreads>, sms), kBigThreads,
+    k_bg<<<resident_grid(k_bg, kMidThreads, big_smem, p.count[T_BIG], kTeamBatch<kMidThreads>, sms), kMidThreads,
            big_smem, s>>>(c, p.list[T_BIG], p.count[T_BIG]);
     prof.end(T_BIG, s);
     ++launches;

@@ -499,7 +499,7 @@ constexpr size_t team_bytes() {
 }
 
 template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CAP, int MAXD>
-__global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : 1)
+__global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : (CTA_THREADS == 512 ? 2 : 1))
     k_team(PassCtx c, const uint32_t* __restrict__ list,
                                                       uint32_t count) {
   static_assert(CTA_THREADS % TEAM == 0 && TEAM % 32 == 0, "team shape");
@@ -814,13 +814,12 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
         for (int u = 0; u < U; ++u)
           if (P > 1 && lab[u] != kEmpty && phase_of(lab[u], P) != ph) lab[u] = kEmpty;
         const uint32_t wbase = base + (threadIdx.x & ~31u);
+        unsigned live = 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (wbase + u * kBigThreads >= d) break;  // warp-uniform
-          unsigned long long f = 0;
-          gather_insert<W, false>(c, lab[u], W(1), tab, cap, occ, &s_occ_n, f);
-          if (f) s_over = 1;  // table full: treat as overflow
-        }
+        for (int u = 0; u < U; ++u) live |= (wbase + u * kBigThreads < d ? 1u : 0u) << u;
+        unsigned long long f = 0;
+        gather_insert_multi<U, W>(c, lab, live, tab, cap, occ, &s_occ_n, f);
+        if (f) s_over = 1;  // table full: treat as overflow
         // Stop early once the phase holds too many distinct labels (block-uniform:
         // every thread reads the counters between the same two barriers).
         __syncthreads();
