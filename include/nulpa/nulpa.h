@@ -101,8 +101,10 @@ typedef struct nulpa_tuning {
 } nulpa_tuning;
 
 #define NULPA_TIERS 10 /* 0 thread, 1 half-warp, 2 warp, 3/4/5 32/128/256-thread teams with
-                          shared tables, 6 1024-thread CTA, 7 8-CTA cluster (DSMEM table),
-                          8 hub (global table), 9 other (deferred wake, cross-check, sequential) */
+                          shared tables, 6 512-thread CTA per vertex (degree <= 6144), 7 wide
+                          rows (one 1024-thread CTA per vertex, label-partitioned phases; an
+                          8-CTA DSMEM cluster for weighted graphs), 8 hub (global table),
+                          9 other (deferred wake, cross-check, sequential) */
 
 /* labelprop::RunStats (lpa.hpp:39-46) plus device counters for roofline
  * accounting. delta_n must point at >= max_iterations u64 (or be NULL). */

@@ -36,8 +36,8 @@ class nulpa_tuning(C.Structure):
                 ("schedule", C.c_uint32), ("no_identity_first", C.c_uint32)]
 
 NULPA_TIERS = 10
-TIER_NAMES = ["thread", "half_warp", "warp", "team32", "team128", "team256", "cta1024",
-              "cluster", "hub", "other"]
+TIER_NAMES = ["thread", "half_warp", "warp", "team32", "team128", "team256", "cta512",
+              "wide", "hub", "other"]
 
 
 class nulpa_stats(C.Structure):

@@ -70,13 +70,16 @@ constexpr int kBlock2Cap = 8192;    // per-team slots (load <= 1/2)
 constexpr int kHubCap = 4096;       // hub pre-aggregation slots per CTA
 constexpr int kBigThreads = 1024;   // wide-row CTAs (k_wide, k_cluster)
 #ifndef NULPA_MID_THREADS
-#define NULPA_MID_THREADS 1024
-#define NULPA_MID_CAP 16384
-#define NULPA_MID_MAX 12288
+#define NULPA_MID_THREADS 512
+#define NULPA_MID_CAP 8192
+#define NULPA_MID_MAX 6144
 #endif
-constexpr int kMidThreads = NULPA_MID_THREADS;  // T_BIG: one CTA per vertex
-constexpr int kBigCap = NULPA_MID_CAP;          // its table (128 KB packed)
-constexpr int kBigMax = NULPA_MID_MAX;          // load <= 3/4
+// T_BIG: one CTA per vertex, two CTAs per SM (measured 37.3 -> 18.7 ms per R27 run
+// for degree 1025-6144 against one 1024-thread CTA per SM; the 6145-12288 rows then
+// run on the wide tier).
+constexpr int kMidThreads = NULPA_MID_THREADS;
+constexpr int kBigCap = NULPA_MID_CAP;  // its table (64 KB packed)
+constexpr int kBigMax = NULPA_MID_MAX;  // load <= 3/4
 constexpr int kClusterSize = 8;     // portable cluster size
 constexpr int kClusterCap = 16384;  // slots per CTA of the cluster
 constexpr int kClusterMax = kClusterSize * kClusterCap * 3 / 4;  // 98304, load <= 3/4

@@ -763,22 +763,29 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
   __shared__ int s_flag, s_over;
   __shared__ unsigned s_occ_n;
   __shared__ Best<VBits<W>> red[32];
+  constexpr uint32_t kWideBatch = 4;  // vertices per work-counter fetch (batched prologue)
+  __shared__ Meta s_meta[kWideBatch];
   for (uint32_t x = threadIdx.x; x < kClusterCap; x += blockDim.x) tab.clear_slot(x);  // once
   const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
   constexpr int U = 4;
   for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(c.work, 1u);
+    if (threadIdx.x == 0) s_item = atomicAdd(c.work, kWideBatch);
     __syncthreads();
-    const uint32_t t = s_item;
-    if (t >= count) break;
-    const uint32_t i = __ldg(list + t);
-    if (threadIdx.x == 0) s_flag = claim_vertex(c, i) ? 1 : 0;
-    const uint64_t lo = __ldg(c.g.off + i);
-    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+    const uint32_t t0 = s_item;
+    if (t0 >= count) break;
+    if (threadIdx.x < kWideBatch) s_meta[threadIdx.x] = fetch_meta<MODE>(c, list, t0 + threadIdx.x, count);
     __syncthreads();
-    if (s_flag) continue;  // (s_item / s_flag are rewritten only after the next barrier)
+    const uint32_t nb = min(kWideBatch, count - t0);
+    for (uint32_t vb = 0; vb < nb; ++vb) {
+    const Meta m = s_meta[vb];
+    if (!m.act) continue;  // (uniform; s_meta is rewritten only after the next fetch barrier)
+    const uint32_t i = m.i;
+    const uint64_t lo = m.lo;
+    const uint32_t d = m.d;
     uint32_t P = fresh ? (d + kWideLimit - 1) / kWideLimit : 1u;
+    // A phase can only overflow when it may hold more than kWideLimit labels.
+    const bool may_overflow = P > 1 || d > kWideLimit;
     Best<VBits<W>> best{VBits<W>(0), kEmpty};  // running result (thread 0)
     for (uint32_t ph = 0; ph < P; ++ph) {
       if (threadIdx.x == 0) {
@@ -822,12 +829,14 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
         if (f) s_over = 1;  // table full: treat as overflow
         // Stop early once the phase holds too many distinct labels (block-uniform:
         // every thread reads the counters between the same two barriers).
-        __syncthreads();
-        const bool stop = s_over || s_occ_n > kWideLimit;
-        __syncthreads();
-        if (stop) {
-          if (threadIdx.x == 0) s_over = 1;
-          break;
+        if (may_overflow) {
+          __syncthreads();
+          const bool stop = s_over || s_occ_n > kWideLimit;
+          __syncthreads();
+          if (stop) {
+            if (threadIdx.x == 0) s_over = 1;
+            break;
+          }
         }
       }
       __syncthreads();
@@ -844,7 +853,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
       if (threadIdx.x == 0) best_merge(best, b.v, b.k);
     }
     if (threadIdx.x == 0) {
-      s_flag = apply_move<MODE>(c, i, best.k) ? 1 : 0;
+      s_flag = apply_move_cur<MODE>(c, i, best.k, m.cur) ? 1 : 0;
       ++n_v;
       n_e += d;
       n_dn += s_flag;
@@ -855,6 +864,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
       for (uint32_t e = threadIdx.x; e < d; e += blockDim.x)
         wake_vertex(c.flags, ld_stream(c.g.tgt + lo + e, pol));
     __syncthreads();
+    }
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
   warp_add_counter(c.ctr, C_PROC_E, n_e);
