@@ -361,14 +361,23 @@ def bench_partitioned(args):
     import torch
     import torch.distributed as dist
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    # NULPA_BENCH_GLOO=1 runs the same driver with gloo and host-staged exchanges, ranks
+    # sharing the visible GPUs: a functional check of the N > 1 path on a one-GPU box
+    # (NCCL refuses two ranks on one device). Never used for a reported number.
+    gloo = os.environ.get("NULPA_BENCH_GLOO") == "1"
+    if gloo:
+        local = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2411_11468_b200 import _capi
     from paper_2411_11468_b200 import labelprop as lp
     from paper_2411_11468_b200.dist import DeviceRangeEngine, Exchange, run_partitioned
 
     def dmax(x: float) -> float:
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if gloo else f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -384,7 +393,7 @@ def bench_partitioned(args):
     tuning = lp.Tuning(thread_max_degree=args.thread_max, warp_max_degree=args.warp_max,
                        block_max_degree=args.block_max)
     eng = DeviceRangeEngine(dg, cfg, bounds[rank], bounds[rank + 1], tuning)
-    ex = Exchange(bounds)
+    ex = Exchange(bounds, staged=gloo)
     for _ in range(args.warmup):
         run_partitioned(eng, cfg, rank, world, ex, n)
     stats = []
