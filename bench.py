@@ -109,6 +109,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+TRAFFIC_JSON = ROOT / "profiles" / "r1s2" / "ncu_traffic_r27.json"
+
+
+def ncu_traffic(tier: str, args):
+    """DRAM bytes (read + write) per launch of `tier`'s kernel, averaged over every launch
+    of one R-MAT scale-27 lpa() run, from the committed ncu --set full capture
+    (tools/ncu_traffic.py); None for other workloads."""
+    if args.workload != "rmat" or args.scale != 27 or not TRAFFIC_JSON.exists():
+        return None, None
+    try:
+        t = json.loads(TRAFFIC_JSON.read_text())[tier]
+        return t["dram_bytes_per_launch"], (f"ncu --set full, {t['launches']} launches of the "
+                                            f"{tier} kernel in one run ({TRAFFIC_JSON.name})")
+    except Exception:
+        return None, None
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -245,6 +262,7 @@ def bench_nulpa(args):
     tier_passes = np.sum([[s.tier_passes[i] for i in range(_capi.NULPA_TIERS)] for s, _ in stats], axis=0)
     top = int(np.argmax(tier_ms))
     achieved = tier_bytes[top] / (tier_ms[top] * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic(_capi.TIER_NAMES[top], args)
     total_alg = sum(s.algorithmic_bytes for s, _ in stats)
     launches = sum(s.kernel_launches for s, _ in stats)
 
@@ -336,7 +354,8 @@ def bench_nulpa(args):
                 "tier_names": _capi.TIER_NAMES,
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "kernel": f"tier:{_capi.TIER_NAMES[top]}",
                          "peak_source": peak_src,
                          "alg_bytes_per_launch": tier_bytes[top] / max(1, tier_passes[top]),

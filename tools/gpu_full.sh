@@ -11,3 +11,6 @@ timeout 900 python bench.py --scale 24 --steps 3 --warmup 3 --e2e-steps 1 --ref-
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/${TAG}_launches_bench.log 2>&1
 timeout 1200 bash tools/profile_kernels.sh 27 ${TAG}_r27_full 0 6 > gpurun_out/${TAG}_ncu_full.log 2>&1
+# every tier kernel of one run (3 passes): DRAM bytes per launch for bench.py's roofline.traffic
+timeout 1500 ncu --set full --clock-control none -k regex:"k_(thread|group|team|wide|cluster|hub_accum)" -c 40 \
+  -o gpurun_out/${TAG}_r27_tiers python tools/profile_run.py 27 0 1 > gpurun_out/${TAG}_ncu_tiers.log 2>&1
