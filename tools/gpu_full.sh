@@ -14,3 +14,6 @@ timeout 1200 bash tools/profile_kernels.sh 27 ${TAG}_r27_full 0 6 > gpurun_out/$
 # every tier kernel of one run (3 passes): DRAM bytes per launch for bench.py's roofline.traffic
 timeout 1500 ncu --set full --clock-control none -k regex:"k_(thread|group|team|wide|cluster|hub_accum)" -c 40 \
   -o gpurun_out/${TAG}_r27_tiers python tools/profile_run.py 27 0 1 > gpurun_out/${TAG}_ncu_tiers.log 2>&1
+python tools/ncu_traffic.py gpurun_out/${TAG}_r27_tiers.ncu-rep > gpurun_out/${TAG}_ncu_traffic_r27.json 2>&1
+python tools/ncu_summary.py gpurun_out/${TAG}_launches.csv gpurun_out/${TAG}_r27_full.ncu-rep gpurun_out/${TAG}_r27_tiers.ncu-rep > gpurun_out/${TAG}_ncu_summary.txt 2>&1
+rm -f gpurun_out/${TAG}_r27_tiers.ncu-rep   # (the result directory comes back only under 64 MiB)
