@@ -225,9 +225,9 @@ int dispatch_pass(const Plan& p, const PassCtx& c, unsigned long long* ctr, int 
 // the table-free identity rule (k_first_pass_list; all of them read identity
 // labels), then the lower tiers run in place and see those moves.
 int long_rows_first_pass(const Plan& p, PassCtx c, unsigned long long* ctr, int value_bytes,
-                         cudaStream_t s, int sms, Prof& prof) {
+                         cudaStream_t s, int sms, Prof& prof, int first_tier = T_BLOCK2) {
   int launches = 0;
-  for (int t = T_HUB; t >= T_BLOCK2; --t) {
+  for (int t = T_HUB; t >= first_tier; --t) {
     if (!p.count[t]) continue;
     c.ctr = ctr + t * C_COUNT;
     prof.begin(t, s);
@@ -237,7 +237,7 @@ int long_rows_first_pass(const Plan& p, PassCtx c, unsigned long long* ctr, int 
     ++launches;
   }
   NULPA_CUDA(cudaGetLastError());
-  const unsigned low = (1u << T_BLOCK2) - 1u;  // T_THREAD .. T_BLOCK
+  const unsigned low = (1u << first_tier) - 1u;  // the tiers below first_tier
   return launches + dispatch_pass<kAsync>(p, c, ctr, value_bytes, s, sms, prof, low);
 }
 
@@ -456,10 +456,13 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
         std::swap(cur, nxt);
       }
     } else if (o.exec == NULPA_EXEC_PARALLEL_ASYNC && iter == 0 && identity_first && tuning &&
-               tuning->async_first_pass == 2) {
+               tuning->async_first_pass >= 2) {
+      // 2: degree > block_max first, 3: the wide and hub tiers first, 4: hubs first
       c.lab_in = cur;
       c.lab_out = cur;
-      launches += long_rows_first_pass(*p, c, ctr.p, vbytes, s, sms, prof);
+      const int ft = tuning->async_first_pass == 2 ? T_BLOCK2
+                     : tuning->async_first_pass == 3 ? T_CLUSTER : T_HUB;
+      launches += long_rows_first_pass(*p, c, ctr.p, vbytes, s, sms, prof, ft);
     } else if (o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
       c.lab_in = cur;
       c.lab_out = cur;
