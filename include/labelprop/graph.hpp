@@ -5,13 +5,16 @@
 // weights f32[m2], total weight 2m as double), so code compiled against either
 // header can hand its graph to nulpa's labelprop::lpa. The constructor and
 // weighted_degree are defined in paper_2411_11468_b200/csrc/dropin.cpp with the
-// reference's validation message (graph.cpp:165-178). File loading and
-// build_csr (graph.cpp:18-161,186-325) are outside the accelerated path.
+// reference's validation message (graph.cpp:165-178). load_graph, build_csr and
+// write_edge_list (graph.cpp:18-161,180-325) are restated in loaders.cpp (host
+// parsing) and build_csr.cu (the CSR built on the device, bit-exact).
 #pragma once
 
 #include <cstdint>
+#include <optional>
 #include <span>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 namespace labelprop {
@@ -28,6 +31,18 @@ struct ValidationError : std::runtime_error {
 };
 struct InternalError : std::runtime_error {
   using std::runtime_error::runtime_error;
+};
+
+// graph.hpp:33-44
+struct WeightedEdge {
+  VertexId u = 0;
+  VertexId v = 0;
+  double w = 1.0;
+};
+
+struct EdgeList {
+  std::vector<WeightedEdge> edges;
+  std::optional<std::uint64_t> n_declared;
 };
 
 class CsrGraph {
@@ -61,5 +76,11 @@ class CsrGraph {
   std::vector<float> weights_;
   double total_weight_2m_ = 0.0;
 };
+
+enum class FileFormat { MatrixMarket, EdgeListText };  // graph.hpp:86
+
+EdgeList load_graph(const std::string& path, FileFormat format);  // graph.hpp:96
+CsrGraph build_csr(const EdgeList& el, bool symmetrize);           // graph.hpp:107
+void write_edge_list(const CsrGraph& g, const std::string& path);   // graph.hpp:112
 
 }  // namespace labelprop

@@ -38,6 +38,11 @@ extern "C" {
 #define NULPA_EINTERNAL 3
 #define NULPA_ECUDA 4
 #define NULPA_EOTHER 5
+#define NULPA_EFORMAT 6 /* malformed input file (FormatError, graph.hpp:17-19) */
+
+/* Input file formats: labelprop::FileFormat (graph.hpp:86), same values. */
+#define NULPA_FORMAT_MATRIX_MARKET 0
+#define NULPA_FORMAT_EDGE_LIST 1
 
 /* Probe strategies: labelprop::ProbeStrategy, hashtable.hpp:25 (same values). */
 #define NULPA_PROBE_LINEAR 0
@@ -222,6 +227,32 @@ int nulpa_gen_web(uint32_t n, uint64_t edges, double gamma, uint32_t hubs,
  * device (duplicate pairs dropped, unit weights) — for SBM-style inputs. */
 int nulpa_graph_from_edges(const uint32_t* u, const uint32_t* v, uint64_t ne, uint32_t n,
                            int device, nulpa_graph** out);
+
+/* ---- graph files and build_csr ----------------------------------- */
+
+/* labelprop::EdgeList (graph.hpp:40-43) as arrays in listing order; n_declared < 0 when
+ * the file declares no vertex count. Arrays are malloc'd by the library. */
+typedef struct nulpa_edge_list {
+  uint64_t ne;
+  int64_t n_declared;
+  uint32_t* u;
+  uint32_t* v;
+  double* w;
+} nulpa_edge_list;
+
+/* labelprop::load_graph (graph.hpp:95-96, graph.cpp:68-161,180-184): same inputs, same
+ * messages; NULPA_EFORMAT for FormatError, NULPA_EINVAL for ValidationError. */
+int nulpa_load_edge_list(const char* path, int format, nulpa_edge_list* out);
+void nulpa_edge_list_free(nulpa_edge_list* el);
+/* labelprop::build_csr (graph.hpp:107, graph.cpp:186-307) on the device, bit-exact:
+ * duplicate merging by weight summation in listing order, first-listed direction kept
+ * (symmetrize), self-loops once, rows sorted by target. w NULL = every weight 1.0;
+ * n_declared < 0 = none. The result is a resident graph (download it for a CsrGraph). */
+int nulpa_graph_from_edge_list(const uint32_t* u, const uint32_t* v, const double* w,
+                               uint64_t ne, int64_t n_declared, int symmetrize, int device,
+                               nulpa_graph** out);
+/* load_graph + build_csr. */
+int nulpa_graph_load(const char* path, int format, int symmetrize, int device, nulpa_graph** out);
 
 /* ---- pass-level sessions: the partitioned multi-GPU path --------
  * A session runs single passes over the POSITION range [v_begin, v_end) of a

@@ -181,6 +181,8 @@ def ref() -> C.CDLL:
         for name, res, args in [
             ("ref_graph_from_csr", vp, [vp, vp, vp, C.c_uint32, C.c_uint64]),
             ("ref_graph_from_edges", vp, [vp, vp, vp, C.c_uint64, C.c_int64, C.c_int]),
+            ("ref_load_graph", C.c_int64, [C.c_char_p, C.c_int, C.c_uint64, vp, vp, vp,
+                                           C.POINTER(C.c_int64)]),
             ("ref_graph_planted", vp, [C.c_uint32, C.c_uint32, C.c_double, C.c_double,
                                        C.c_uint64, vp]),
             ("ref_planted_edges", C.c_int64, [C.c_uint32, C.c_uint32, C.c_double, C.c_double,
@@ -341,6 +343,20 @@ def ref_modularity_oracle(g: RefGraph, labels) -> float:
     q = C.c_double()
     _ref_check(ref().ref_modularity_oracle(g.h, _p(_u32(labels)), C.byref(q)))
     return q.value
+
+
+def ref_load_graph(path, fmt):
+    """labelprop_ref::load_graph -> (u, v, w, n_declared) in listing order, or raises
+    ValueError('F:<message>') / ValueError('V:<message>')."""
+    nd = C.c_int64()
+    ne = ref().ref_load_graph(str(path).encode(), fmt, 0, None, None, None, C.byref(nd))
+    if ne < 0:
+        raise ValueError(ref().ref_last_error().decode())
+    u = np.empty(ne, np.uint32)
+    v = np.empty(ne, np.uint32)
+    w = np.empty(ne, np.float64)
+    ref().ref_load_graph(str(path).encode(), fmt, ne, _p(u), _p(v), _p(w), C.byref(nd))
+    return u, v, w, nd.value
 
 
 def ref_planted_edges(n, communities, p_in, p_out, seed):

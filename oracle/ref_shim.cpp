@@ -123,6 +123,31 @@ REF_API void* ref_graph_from_edges(const uint32_t* u, const uint32_t* v, const d
   }
 }
 
+// load_graph(path, format)  graph.cpp:68-161,180-184. Returns the number of edges (or
+// -1 with the message in ref_last_error, prefixed "F:" for FormatError and "V:" for
+// ValidationError); fills the arrays when cap >= that number.
+REF_API int64_t ref_load_graph(const char* path, int format, uint64_t cap, uint32_t* u,
+                               uint32_t* v, double* w, int64_t* n_declared) {
+  try {
+    EdgeList el = load_graph(path, format == 0 ? FileFormat::MatrixMarket : FileFormat::EdgeListText);
+    if (cap >= el.edges.size())
+      for (size_t k = 0; k < el.edges.size(); ++k) {
+        u[k] = el.edges[k].u;
+        v[k] = el.edges[k].v;
+        w[k] = el.edges[k].w;
+      }
+    *n_declared = el.n_declared ? static_cast<int64_t>(*el.n_declared) : -1;
+    return static_cast<int64_t>(el.edges.size());
+  } catch (const FormatError& e) {
+    g_err = std::string("F:") + e.what();
+  } catch (const ValidationError& e) {
+    g_err = std::string("V:") + e.what();
+  } catch (const std::exception& e) {
+    g_err = std::string("E:") + e.what();
+  }
+  return -1;
+}
+
 // planted_partition(...)  generators.cpp:45-88, then build_csr(symmetrize)
 REF_API void* ref_graph_planted(uint32_t n, uint32_t communities, double p_in, double p_out,
                                 uint64_t seed, uint32_t* ground_truth_out) {

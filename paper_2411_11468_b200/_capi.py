@@ -12,7 +12,8 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libnulpa.so"
 
-NULPA_OK, NULPA_EINVAL, NULPA_ENOMEM, NULPA_EINTERNAL, NULPA_ECUDA, NULPA_EOTHER = range(6)
+NULPA_OK, NULPA_EINVAL, NULPA_ENOMEM, NULPA_EINTERNAL, NULPA_ECUDA, NULPA_EOTHER, NULPA_EFORMAT = range(7)
+NULPA_FORMAT_MATRIX_MARKET, NULPA_FORMAT_EDGE_LIST = 0, 1
 NULPA_LAYOUT_IDENTITY, NULPA_LAYOUT_DEGREE_BUCKETS = 0, 1
 
 
@@ -50,6 +51,11 @@ class nulpa_stats(C.Structure):
                 ("kernel_launches", C.c_uint64), ("tier_ms", C.c_double * 10),
                 ("tier_bytes", C.c_double * 10), ("tier_edges", C.c_uint64 * 10),
                 ("tier_passes", C.c_uint32 * 10), ("reserved2", C.c_uint32)]
+
+
+class nulpa_edge_list(C.Structure):
+    _fields_ = [("ne", C.c_uint64), ("n_declared", C.c_int64), ("u", C.POINTER(C.c_uint32)),
+                ("v", C.POINTER(C.c_uint32)), ("w", C.POINTER(C.c_double))]
 
 
 class nulpa_pass_info(C.Structure):
@@ -108,6 +114,11 @@ _SIGS = {
     "nulpa_graph_from_edges": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_int,
                                          C.POINTER(C.c_void_p)]),
     "nulpa_graph_edge_ranges": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "nulpa_load_edge_list": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(nulpa_edge_list)]),
+    "nulpa_edge_list_free": (None, [C.POINTER(nulpa_edge_list)]),
+    "nulpa_graph_from_edge_list": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                             C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "nulpa_graph_load": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "nulpa_session_create": (C.c_int, [C.c_void_p, C.POINTER(nulpa_opts),
                                        C.POINTER(nulpa_tuning), C.c_uint32, C.c_uint32,
                                        C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
@@ -148,4 +159,6 @@ def check(rc: int) -> None:
             raise MemoryError(msg)
         if rc == NULPA_EINTERNAL:
             raise lp.InternalError(msg)
+        if rc == NULPA_EFORMAT:
+            raise lp.FormatError(msg)
         raise NulpaError(rc, msg)

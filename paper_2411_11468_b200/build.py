@@ -24,8 +24,8 @@ OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libnulpa.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["graph.cu", "layout.cu", "engine.cu", "quality.cu", "gen.cu"]
-CXX_SOURCES = ["dropin.cpp"]
+CU_SOURCES = ["graph.cu", "layout.cu", "engine.cu", "quality.cu", "gen.cu", "build_csr.cu"]
+CXX_SOURCES = ["dropin.cpp", "loaders.cpp"]
 
 
 def _run(cmd: list[str]) -> None:
@@ -62,7 +62,8 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
         o = OBJ / (src + ".o")
         objs.append(o)
         if force or not _newer(o, [s] + headers):
-            jobs.append(["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", *inc, "-c",
+            jobs.append(["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", *inc,
+                         "-I", os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include"), "-c",
                          str(s), "-o", str(o)])
     if jobs:
         with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:

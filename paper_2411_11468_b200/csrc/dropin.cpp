@@ -8,7 +8,9 @@
 //   CsrGraph::CsrGraph / weighted_degree   src/graph.cpp:165-178
 // Error codes from the C ABI map back onto the reference exceptions:
 // 1 → ValidationError, 2 → std::bad_alloc, 3 → InternalError, else runtime_error.
+#include <charconv>
 #include <cstdlib>
+#include <fstream>
 #include <new>
 #include <string>
 
@@ -27,6 +29,7 @@ namespace {
     case NULPA_EINVAL: throw ValidationError(msg);
     case NULPA_ENOMEM: throw std::bad_alloc();
     case NULPA_EINTERNAL: throw InternalError(msg);
+    case NULPA_EFORMAT: throw FormatError(msg);
     default: throw std::runtime_error(msg);
   }
 }
@@ -48,6 +51,67 @@ int device_from_env() {
 }
 
 }  // namespace
+
+// load_graph (graph.cpp:180-184) over nulpa_load_edge_list (loaders.cpp).
+EdgeList load_graph(const std::string& path, FileFormat format) {
+  nulpa_edge_list el{};
+  const int rc = nulpa_load_edge_list(
+      path.c_str(),
+      format == FileFormat::MatrixMarket ? NULPA_FORMAT_MATRIX_MARKET : NULPA_FORMAT_EDGE_LIST, &el);
+  if (rc != NULPA_OK) raise(rc);
+  EdgeList out;
+  out.edges.resize(el.ne);
+  for (std::uint64_t k = 0; k < el.ne; ++k) out.edges[k] = {el.u[k], el.v[k], el.w[k]};
+  if (el.n_declared >= 0) out.n_declared = static_cast<std::uint64_t>(el.n_declared);
+  nulpa_edge_list_free(&el);
+  return out;
+}
+
+// build_csr (graph.cpp:186-307) on the device (build_csr.cu), downloaded.
+CsrGraph build_csr(const EdgeList& el, bool symmetrize) {
+  const std::size_t ne = el.edges.size();
+  std::vector<VertexId> u(ne), v(ne);
+  std::vector<double> w(ne);
+  for (std::size_t k = 0; k < ne; ++k) {
+    u[k] = el.edges[k].u;
+    v[k] = el.edges[k].v;
+    w[k] = el.edges[k].w;
+  }
+  nulpa_graph* g = nullptr;
+  int rc = nulpa_graph_from_edge_list(u.data(), v.data(), w.data(), ne,
+                                      el.n_declared ? static_cast<std::int64_t>(*el.n_declared) : -1,
+                                      symmetrize ? 1 : 0, device_from_env(), &g);
+  if (rc != NULPA_OK) raise(rc);
+  std::uint32_t n = 0;
+  std::uint64_t m2 = 0;
+  nulpa_graph_info(g, &n, &m2, nullptr, nullptr);
+  std::vector<std::uint64_t> off(std::uint64_t(n) + 1);
+  std::vector<VertexId> tgt(m2);
+  std::vector<float> wt(m2);
+  rc = nulpa_graph_download(g, off.data(), tgt.data(), wt.data());
+  nulpa_graph_free(g);
+  if (rc != NULPA_OK) raise(rc);
+  return CsrGraph(std::move(off), std::move(tgt), std::move(wt));
+}
+
+// write_edge_list (graph.cpp:309-325): host output, same text.
+void write_edge_list(const CsrGraph& g, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) throw ValidationError("cannot open output file: " + path);
+  out << "% undirected weighted edge list: u v w (each edge once, u <= v)\n";
+  out << "% vertices " << g.order() << '\n';
+  char buf[64];
+  for (VertexId i = 0; i < g.order(); ++i) {
+    auto nbrs = g.neighbors(i);
+    auto ws = g.edge_weights(i);
+    for (std::size_t p = 0; p < nbrs.size(); ++p) {
+      if (nbrs[p] < i) continue;  // u <= v once; self-loops included
+      auto r = std::to_chars(buf, buf + sizeof buf, ws[p]);
+      out << i << ' ' << nbrs[p] << ' ' << std::string_view(buf, r.ptr - buf) << '\n';
+    }
+  }
+  if (!out) throw ValidationError("failed writing " + path);
+}
 
 CsrGraph::CsrGraph(std::vector<std::uint64_t> offsets, std::vector<VertexId> targets,
                    std::vector<float> weights)

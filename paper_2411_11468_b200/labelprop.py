@@ -25,6 +25,10 @@ import numpy as np
 from . import _capi
 
 
+class FormatError(ValueError):
+    """labelprop::FormatError (graph.hpp:17-19): a malformed input file."""
+
+
 class ValidationError(ValueError):
     """labelprop::ValidationError (graph.hpp:23-25)."""
 
@@ -86,6 +90,22 @@ class RunStats:
 class LpaResult:
     labels: np.ndarray
     stats: RunStats
+
+
+@dataclass
+class FileFormat(IntEnum):
+    """labelprop::FileFormat (graph.hpp:86)."""
+    MatrixMarket = 0
+    EdgeListText = 1
+
+
+@dataclass
+class EdgeList:
+    """labelprop::EdgeList (graph.hpp:40-43) as arrays in listing order."""
+    u: np.ndarray
+    v: np.ndarray
+    w: np.ndarray
+    n_declared: int | None = None
 
 
 @dataclass
@@ -238,6 +258,30 @@ def community_count(g: CsrGraph, labels) -> int:
     return int(cnt.value)
 
 
+def load_graph(path, fmt: FileFormat) -> EdgeList:
+    """labelprop::load_graph (graph.hpp:95-96): FormatError / ValidationError as the reference."""
+    el = _capi.nulpa_edge_list()
+    _capi.check(_capi.lib().nulpa_load_edge_list(str(path).encode(), int(fmt), C.byref(el)))
+    try:
+        ne = int(el.ne)
+        u = np.ctypeslib.as_array(el.u, (ne,)).copy() if ne else np.empty(0, np.uint32)
+        v = np.ctypeslib.as_array(el.v, (ne,)).copy() if ne else np.empty(0, np.uint32)
+        w = np.ctypeslib.as_array(el.w, (ne,)).copy() if ne else np.empty(0, np.float64)
+        nd = int(el.n_declared)
+    finally:
+        _capi.lib().nulpa_edge_list_free(C.byref(el))
+    return EdgeList(u, v, w, None if nd < 0 else nd)
+
+
+def build_csr(el: EdgeList, symmetrize: bool, device: int = 0) -> CsrGraph:
+    """labelprop::build_csr (graph.hpp:107), built on the device (bit-exact)."""
+    dg = DeviceGraph.from_edge_list(el, symmetrize, device)
+    try:
+        return dg.download()
+    finally:
+        dg.free()
+
+
 def partition_by_degree(g: CsrGraph, switch_degree: int) -> DegreePartition:
     """labelprop::partition_by_degree (lpa.hpp:63)."""
     n = g.order()
@@ -312,6 +356,28 @@ class DeviceGraph:
         h = C.c_void_p()
         _capi.check(_capi.lib().nulpa_gen_web(n, edges, gamma, hubs, hub_degree, seed, device,
                                               C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
+    def from_edge_list(cls, el: "EdgeList", symmetrize: bool = True, device: int = 0):
+        """build_csr on the device (nulpa_graph_from_edge_list)."""
+        u = np.ascontiguousarray(el.u, dtype=np.uint32)
+        v = np.ascontiguousarray(el.v, dtype=np.uint32)
+        w = None if el.w is None else np.ascontiguousarray(el.w, dtype=np.float64)
+        nd = -1 if el.n_declared is None else int(el.n_declared)
+        h = C.c_void_p()
+        _capi.check(_capi.lib().nulpa_graph_from_edge_list(
+            _ptr(u) if u.size else None, _ptr(v) if v.size else None,
+            _ptr(w) if w is not None and w.size else None, u.size, nd, int(symmetrize), device,
+            C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
+    def load(cls, path, fmt: "FileFormat", symmetrize: bool = True, device: int = 0):
+        """load_graph + build_csr (nulpa_graph_load)."""
+        h = C.c_void_p()
+        _capi.check(_capi.lib().nulpa_graph_load(str(path).encode(), int(fmt), int(symmetrize),
+                                                 device, C.byref(h)))
         return cls(h.value, device)
 
     @classmethod
