@@ -165,6 +165,13 @@ int nulpa_sync_step(const nulpa_csr* csr, const uint32_t* labels_in, int pick_le
 
 int nulpa_modularity(const nulpa_csr* csr, const uint32_t* labels, double* q);
 int nulpa_community_count(const nulpa_csr* csr, const uint32_t* labels, uint64_t* count);
+/* labelprop::community_stats (quality.hpp:32-38, quality.cpp:56-78): the *count
+ * communities present (ascending label) with their sigma (intra weight) and big_sigma
+ * (total weighted degree), and the size histogram as *hist_len (size, how many) pairs in
+ * ascending size. Host arrays of n entries each (any of the five may be NULL). */
+int nulpa_community_stats(const nulpa_csr* csr, const uint32_t* labels, uint64_t* count,
+                          uint32_t* communities, double* sigma, double* big_sigma,
+                          uint64_t* hist_size, uint64_t* hist_count, uint64_t* hist_len);
 
 /* labelprop::cross_check on host arrays (labels and flags updated in place). */
 int nulpa_cross_check(const nulpa_csr* csr, uint32_t* labels, const uint32_t* prev,
@@ -209,6 +216,10 @@ int nulpa_sync_step_graph(nulpa_graph* g, const uint32_t* labels_in_dev, int pic
 /* Modularity on a resident graph; labels is a DEVICE pointer. */
 int nulpa_modularity_graph(nulpa_graph* g, const uint32_t* labels_dev, double* q);
 int nulpa_community_count_graph(nulpa_graph* g, const uint32_t* labels_dev, uint64_t* count);
+/* community_stats on a resident graph; labels is a DEVICE pointer, outputs are host. */
+int nulpa_community_stats_graph(nulpa_graph* g, const uint32_t* labels_dev, uint64_t* count,
+                                uint32_t* communities, double* sigma, double* big_sigma,
+                                uint64_t* hist_size, uint64_t* hist_count, uint64_t* hist_len);
 
 /* ---- synthetic inputs built on the device (bench / tests) ----------------- */
 

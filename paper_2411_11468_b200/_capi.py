@@ -114,6 +114,12 @@ _SIGS = {
     "nulpa_graph_from_edges": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_int,
                                          C.POINTER(C.c_void_p)]),
     "nulpa_graph_edge_ranges": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "nulpa_community_stats": (C.c_int, [C.POINTER(nulpa_csr), C.c_void_p, C.POINTER(C.c_uint64),
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.POINTER(C.c_uint64)]),
+    "nulpa_community_stats_graph": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
+                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.POINTER(C.c_uint64)]),
     "nulpa_load_edge_list": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(nulpa_edge_list)]),
     "nulpa_edge_list_free": (None, [C.POINTER(nulpa_edge_list)]),
     "nulpa_graph_from_edge_list": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,

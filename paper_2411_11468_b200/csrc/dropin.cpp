@@ -8,6 +8,8 @@
 //   CsrGraph::CsrGraph / weighted_degree   src/graph.cpp:165-178
 // Error codes from the C ABI map back onto the reference exceptions:
 // 1 → ValidationError, 2 → std::bad_alloc, 3 → InternalError, else runtime_error.
+#include <algorithm>
+#include <cctype>
 #include <charconv>
 #include <cstdlib>
 #include <fstream>
@@ -15,6 +17,7 @@
 #include <string>
 
 #include "labelprop/graph.hpp"
+#include "labelprop/io.hpp"
 #include "labelprop/lpa.hpp"
 #include "labelprop/quality.hpp"
 #include "nulpa/nulpa.h"
@@ -194,6 +197,84 @@ double modularity(const CsrGraph& g, std::span<const VertexId> labels) {
   const int rc = nulpa_modularity(&c, labels.data(), &q);
   if (rc != NULPA_OK) raise(rc);
   return q;
+}
+
+// delta_modularity (quality.cpp:51-54): closed form.
+double delta_modularity(double m, double ki, double ki_to_c, double ki_to_d, double sigma_c,
+                        double sigma_d) {
+  return (ki_to_c - ki_to_d) / m - ki * (ki + sigma_c - sigma_d) / (2.0 * m * m);
+}
+
+// community_stats (quality.cpp:56-78) over nulpa_community_stats (device).
+CommunityStats community_stats(const CsrGraph& g, std::span<const VertexId> labels) {
+  if (labels.size() != g.order())
+    throw ValidationError("labeling has " + std::to_string(labels.size()) + " entries for " +
+                          std::to_string(g.order()) + " vertices");
+  const std::size_t n = std::max<std::size_t>(1, g.order());
+  std::vector<std::uint32_t> comm(n);
+  std::vector<double> sg(n), bg(n);
+  std::vector<std::uint64_t> hs(n), hc(n);
+  std::uint64_t count = 0, hl = 0;
+  const nulpa_csr c = view(g);
+  const int rc = nulpa_community_stats(&c, labels.data(), &count, comm.data(), sg.data(),
+                                       bg.data(), hs.data(), hc.data(), &hl);
+  if (rc != NULPA_OK) raise(rc);
+  CommunityStats st;
+  st.count = count;
+  for (std::uint64_t k = 0; k < count; ++k) {
+    st.sigma[comm[k]] = sg[k];
+    st.big_sigma[comm[k]] = bg[k];
+  }
+  for (std::uint64_t k = 0; k < hl; ++k) st.size_histogram[hs[k]] = hc[k];
+  return st;
+}
+
+// write_membership / read_membership (io.cpp:9-56): host I/O, the reference's messages.
+void write_membership(const std::string& path, std::span<const VertexId> labels) {
+  std::ofstream out(path);
+  if (!out) throw ValidationError("cannot open output file: " + path);
+  for (std::size_t i = 0; i < labels.size(); ++i) out << i << '\t' << labels[i] << '\n';
+  if (!out) throw ValidationError("failed writing " + path);
+}
+
+std::vector<VertexId> read_membership(const std::string& path, std::uint32_t n) {
+  std::ifstream in(path);
+  if (!in) throw ValidationError("cannot open membership file: " + path);
+  std::vector<VertexId> labels(n, 0);
+  std::vector<std::uint8_t> seen(n, 0);
+  std::string line;
+  for (std::size_t lineno = 1; std::getline(in, line); ++lineno) {
+    std::size_t a = 0;
+    auto skip_ws = [&] {
+      while (a < line.size() && std::isspace(static_cast<unsigned char>(line[a]))) ++a;
+    };
+    skip_ws();
+    if (a == line.size() || line[a] == '#' || line[a] == '%') continue;
+    const std::string where = path + ":" + std::to_string(lineno) + ": ";
+    std::uint64_t field[2] = {0, 0};
+    for (auto& f : field) {
+      auto [p, ec] = std::from_chars(line.data() + a, line.data() + line.size(), f);
+      if (ec != std::errc() || p == line.data() + a)
+        throw FormatError(where + "expected 'vertex<TAB>label'");
+      a = static_cast<std::size_t>(p - line.data());
+      skip_ws();
+    }
+    if (a != line.size()) throw FormatError(where + "trailing content after label");
+    const std::uint64_t vertex = field[0], label = field[1];
+    if (vertex >= n)
+      throw ValidationError(where + "vertex " + std::to_string(vertex) + " out of range for n=" +
+                            std::to_string(n));
+    if (label >= n)
+      throw ValidationError(where + "label " + std::to_string(label) + " out of range for n=" +
+                            std::to_string(n));
+    if (seen[vertex])
+      throw ValidationError(where + "vertex " + std::to_string(vertex) + " assigned twice");
+    seen[vertex] = 1;
+    labels[vertex] = static_cast<VertexId>(label);
+  }
+  for (std::uint32_t i = 0; i < n; ++i)
+    if (!seen[i]) throw ValidationError(path + ": no label for vertex " + std::to_string(i));
+  return labels;
 }
 
 }  // namespace labelprop

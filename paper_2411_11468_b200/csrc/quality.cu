@@ -9,6 +9,8 @@
 // community_stats(...).count (quality.cpp:56-78) = number of distinct labels.
 #include <cub/cub.cuh>
 
+#include <vector>
+
 #include "internal.hpp"
 #include "layout.hpp"
 #include "plan.hpp"
@@ -158,6 +160,28 @@ void check_labels(nulpa_graph* g, const uint32_t* lab, cudaStream_t s) {
 
 }  // namespace
 
+// sigma[c] (intra-community stored weight) and big[c] (summed weighted degree) for
+// every community c, from position-order labels `lab` (quality.cpp:29-40).
+void accumulate_sigma(nulpa_graph* g, const uint32_t* lab, double* sigma, double* big,
+                      cudaStream_t s) {
+  const uint32_t n = g->n;
+  // Any tiering covers every row once: reuse the cached plan when there is one.
+  Plan* p = g->plan ? g->plan : get_plan(g, resolve_tiers(32, nullptr), 4, s);
+  const Graph dg{g->offsets, g->targets, g->weights, n};
+  const int sms = sm_count();
+  if (p->count[T_THREAD])
+    k_mod_thread<<<std::min<uint32_t>((p->count[T_THREAD] + 255) / 256, sms * 8), 256, 0, s>>>(
+        dg, lab, p->list[T_THREAD], p->count[T_THREAD], sigma, big);
+  for (int t = T_HALF; t <= T_CLUSTER; ++t)
+    if (p->count[t])
+      k_mod_warp<<<std::min<uint32_t>((p->count[t] + 7) / 8, sms * 8), 256, 0, s>>>(
+          dg, lab, p->list[t], p->count[t], sigma, big);
+  if (p->n_items)
+    k_mod_hub<<<std::min<uint32_t>(p->n_items, sms * 4), 256, 0, s>>>(dg, lab, p->hub_ctx(), sigma,
+                                                                      big);
+  NULPA_CUDA(cudaGetLastError());
+}
+
 // `labels` in vertex order (community ids are label values, so only the row
 // order changes under the position layout).
 double modularity_device(nulpa_graph* g, const uint32_t* labels, cudaStream_t s) {
@@ -172,24 +196,12 @@ double modularity_device(nulpa_graph* g, const uint32_t* labels, cudaStream_t s)
     to_positions_u32(g, labels, lab_pos, s);
     lab = lab_pos;
   }
-  // Any tiering covers every row once: reuse the cached plan when there is one.
-  Plan* p = g->plan ? g->plan : get_plan(g, resolve_tiers(32, nullptr), 4, s);
   double* sigma = dalloc<double>(2ull * n + 1);
   double* big = sigma + n;
   double* d_q = sigma + 2ull * n;
   NULPA_CUDA(cudaMemsetAsync(sigma, 0, (2ull * n + 1) * sizeof(double), s));
-  const Graph dg{g->offsets, g->targets, g->weights, n};
+  accumulate_sigma(g, lab, sigma, big, s);
   const int sms = sm_count();
-  if (p->count[T_THREAD])
-    k_mod_thread<<<std::min<uint32_t>((p->count[T_THREAD] + 255) / 256, sms * 8), 256, 0, s>>>(
-        dg, lab, p->list[T_THREAD], p->count[T_THREAD], sigma, big);
-  for (int t = T_HALF; t <= T_CLUSTER; ++t)
-    if (p->count[t])
-      k_mod_warp<<<std::min<uint32_t>((p->count[t] + 7) / 8, sms * 8), 256, 0, s>>>(
-          dg, lab, p->list[t], p->count[t], sigma, big);
-  if (p->n_items)
-    k_mod_hub<<<std::min<uint32_t>(p->n_items, sms * 4), 256, 0, s>>>(dg, lab, p->hub_ctx(), sigma,
-                                                                      big);
   k_mod_fold<<<std::min<uint32_t>((n + 255) / 256, sms * 4), 256, 0, s>>>(sigma, big, n,
                                                                           g->total_2m, d_q);
   NULPA_CUDA(cudaGetLastError());
@@ -199,6 +211,106 @@ double modularity_device(nulpa_graph* g, const uint32_t* labels, cudaStream_t s)
   dfree(sigma);
   dfree(lab_pos);
   return q;
+}
+
+namespace {
+__global__ void k_sizes(const uint32_t* lab, uint32_t n, uint32_t* size) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(size + lab[i], 1u);
+}
+struct Present {
+  const uint32_t* size;
+  __host__ __device__ bool operator()(uint32_t c) const { return size[c] != 0; }
+};
+__global__ void k_gather_stats(const uint32_t* comm, uint64_t k, const uint32_t* size,
+                               const double* sigma, const double* big, uint32_t* sz_out,
+                               double* sg_out, double* bg_out) {
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < k;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t c = comm[t];
+    sz_out[t] = size[c];
+    sg_out[t] = sigma[c];
+    bg_out[t] = big[c];
+  }
+}
+}  // namespace
+
+// community_stats (quality.cpp:56-78): the communities present (ascending label),
+// their sizes, sigma and big_sigma, and the histogram size -> number of communities.
+// Host outputs; arrays hold at most n entries.
+void community_stats_device(nulpa_graph* g, const uint32_t* labels, cudaStream_t s,
+                            uint64_t* count, uint32_t* comm_h, double* sigma_h, double* big_h,
+                            uint64_t* hist_size_h, uint64_t* hist_count_h, uint64_t* hist_len) {
+  check_labels(g, labels, s);
+  const uint32_t n = g->n;
+  uint32_t* lab_pos = nullptr;
+  const uint32_t* lab = labels;
+  if (g->perm) {
+    lab_pos = dalloc<uint32_t>(n);
+    to_positions_u32(g, labels, lab_pos, s);
+    lab = lab_pos;
+  }
+  double* sigma = dalloc<double>(2ull * n + 1);
+  double* big = sigma + n;
+  uint32_t* size = dalloc<uint32_t>(n);
+  uint32_t* comm = dalloc<uint32_t>(n);
+  uint32_t* sz = dalloc<uint32_t>(n);
+  uint32_t* sz_sorted = dalloc<uint32_t>(n);
+  double* sg = dalloc<double>(n);
+  double* bg = dalloc<double>(n);
+  uint64_t* d_num = dalloc<uint64_t>(1);
+  uint32_t* runs = dalloc<uint32_t>(n);
+  uint32_t* run_len = dalloc<uint32_t>(n);
+  void* tmp = nullptr;
+  try {
+    NULPA_CUDA(cudaMemsetAsync(sigma, 0, (2ull * n + 1) * sizeof(double), s));
+    NULPA_CUDA(cudaMemsetAsync(size, 0, n * 4ull, s));
+    accumulate_sigma(g, lab, sigma, big, s);
+    k_sizes<<<std::min<uint32_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(lab, n, size);
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    cub::CountingInputIterator<uint32_t> ids(0);
+    cub::DeviceSelect::If(nullptr, t1, ids, comm, d_num, n, Present{size}, s);
+    cub::DeviceRadixSort::SortKeys(nullptr, t2, sz, sz_sorted, n, 0, 32, s);
+    cub::DeviceRunLengthEncode::Encode(nullptr, t3, sz_sorted, runs, run_len, d_num, n, s);
+    tmp = dmalloc(std::max(t1, std::max(t2, t3)));
+    cub::DeviceSelect::If(tmp, t1, ids, comm, d_num, n, Present{size}, s);
+    uint64_t k = 0;
+    NULPA_CUDA(cudaMemcpyAsync(&k, d_num, 8, cudaMemcpyDeviceToHost, s));
+    NULPA_CUDA(cudaStreamSynchronize(s));
+    if (k) {
+      k_gather_stats<<<std::min<uint64_t>((k + 255) / 256, 148 * 8), 256, 0, s>>>(
+          comm, k, size, sigma, big, sz, sg, bg);
+      cub::DeviceRadixSort::SortKeys(tmp, t2, sz, sz_sorted, k, 0, 32, s);
+      cub::DeviceRunLengthEncode::Encode(tmp, t3, sz_sorted, runs, run_len, d_num, k, s);
+    }
+    uint64_t nh = 0;
+    if (k) NULPA_CUDA(cudaMemcpyAsync(&nh, d_num, 8, cudaMemcpyDeviceToHost, s));
+    NULPA_CUDA(cudaStreamSynchronize(s));
+    *count = k;
+    *hist_len = nh;
+    if (k) {
+      if (comm_h) NULPA_CUDA(cudaMemcpy(comm_h, comm, k * 4, cudaMemcpyDeviceToHost));
+      if (sigma_h) NULPA_CUDA(cudaMemcpy(sigma_h, sg, k * 8, cudaMemcpyDeviceToHost));
+      if (big_h) NULPA_CUDA(cudaMemcpy(big_h, bg, k * 8, cudaMemcpyDeviceToHost));
+      std::vector<uint32_t> hs(nh), hc(nh);
+      NULPA_CUDA(cudaMemcpy(hs.data(), runs, nh * 4, cudaMemcpyDeviceToHost));
+      NULPA_CUDA(cudaMemcpy(hc.data(), run_len, nh * 4, cudaMemcpyDeviceToHost));
+      for (uint64_t x = 0; x < nh; ++x) {
+        if (hist_size_h) hist_size_h[x] = hs[x];
+        if (hist_count_h) hist_count_h[x] = hc[x];
+      }
+    }
+  } catch (...) {
+    for (void* q : {(void*)lab_pos, (void*)sigma, (void*)size, (void*)comm, (void*)sz,
+                    (void*)sz_sorted, (void*)sg, (void*)bg, (void*)d_num, (void*)runs,
+                    (void*)run_len, tmp})
+      dfree(q);
+    throw;
+  }
+  for (void* q : {(void*)lab_pos, (void*)sigma, (void*)size, (void*)comm, (void*)sz,
+                  (void*)sz_sorted, (void*)sg, (void*)bg, (void*)d_num, (void*)runs,
+                  (void*)run_len, tmp})
+    dfree(q);
 }
 
 uint64_t community_count_device(nulpa_graph* g, const uint32_t* lab, cudaStream_t s) {
@@ -234,6 +346,42 @@ int nulpa_modularity_graph(nulpa_graph* g, const uint32_t* labels_dev, double* q
     if (!g) throw Error(NULPA_EINVAL, "null graph");
     use_device(g->device);
     *q = modularity_device(g, labels_dev, 0);
+  });
+}
+
+int nulpa_community_stats_graph(nulpa_graph* g, const uint32_t* labels_dev, uint64_t* count,
+                                uint32_t* communities, double* sigma, double* big_sigma,
+                                uint64_t* hist_size, uint64_t* hist_count, uint64_t* hist_len) {
+  return guarded([&] {
+    if (!g || !count || !hist_len) throw Error(NULPA_EINVAL, "null argument");
+    use_device(g->device);
+    community_stats_device(g, labels_dev, 0, count, communities, sigma, big_sigma, hist_size,
+                           hist_count, hist_len);
+  });
+}
+
+int nulpa_community_stats(const nulpa_csr* csr, const uint32_t* labels, uint64_t* count,
+                          uint32_t* communities, double* sigma, double* big_sigma,
+                          uint64_t* hist_size, uint64_t* hist_count, uint64_t* hist_len) {
+  return guarded([&] {
+    check_host_csr(csr);
+    if (!count || !hist_len) throw Error(NULPA_EINVAL, "null argument");
+    nulpa_graph* g = nullptr;
+    int rc = nulpa_graph_upload(csr, 0, &g);
+    if (rc) throw Error(rc, nulpa_last_error());
+    uint32_t* d = nullptr;
+    try {
+      d = dalloc<uint32_t>(csr->n);
+      NULPA_CUDA(cudaMemcpy(d, labels, csr->n * 4ull, cudaMemcpyHostToDevice));
+      community_stats_device(g, d, 0, count, communities, sigma, big_sigma, hist_size,
+                             hist_count, hist_len);
+    } catch (...) {
+      dfree(d);
+      nulpa_graph_free(g);
+      throw;
+    }
+    dfree(d);
+    nulpa_graph_free(g);
   });
 }
 

@@ -282,6 +282,86 @@ def build_csr(el: EdgeList, symmetrize: bool, device: int = 0) -> CsrGraph:
         dg.free()
 
 
+@dataclass
+class CommunityStats:
+    """labelprop::CommunityStats (quality.hpp:32-38)."""
+    count: int
+    size_histogram: dict
+    sigma: dict
+    big_sigma: dict
+
+
+def community_stats(g: CsrGraph, labels) -> CommunityStats:
+    """labelprop::community_stats (quality.cpp:56-78), on the device."""
+    lab = np.ascontiguousarray(labels, dtype=np.uint32)
+    if lab.size != g.order():
+        raise ValidationError(f"labeling has {lab.size} entries for {g.order()} vertices")
+    n = max(1, g.order())
+    comm = np.empty(n, np.uint32)
+    sg = np.empty(n, np.float64)
+    bg = np.empty(n, np.float64)
+    hs = np.empty(n, np.uint64)
+    hc = np.empty(n, np.uint64)
+    cnt, hl = C.c_uint64(), C.c_uint64()
+    csr = g.csr_view()
+    _capi.check(_capi.lib().nulpa_community_stats(C.byref(csr), _ptr(lab), C.byref(cnt),
+                                                  _ptr(comm), _ptr(sg), _ptr(bg), _ptr(hs),
+                                                  _ptr(hc), C.byref(hl)))
+    k, h = int(cnt.value), int(hl.value)
+    return CommunityStats(k, {int(a): int(b) for a, b in zip(hs[:h], hc[:h])},
+                          {int(c): float(x) for c, x in zip(comm[:k], sg[:k])},
+                          {int(c): float(x) for c, x in zip(comm[:k], bg[:k])})
+
+
+def delta_modularity(m: float, ki: float, ki_to_c: float, ki_to_d: float, sigma_c: float,
+                     sigma_d: float) -> float:
+    """labelprop::delta_modularity (quality.cpp:51-54), closed form."""
+    return (ki_to_c - ki_to_d) / m - ki * (ki + sigma_c - sigma_d) / (2.0 * m * m)
+
+
+def write_membership(path, labels) -> None:
+    """labelprop::write_membership (io.cpp:9-14): `vertex<TAB>label` per line."""
+    lab = np.asarray(labels)
+    try:
+        with open(path, "w") as f:
+            f.writelines(f"{i}\t{int(c)}\n" for i, c in enumerate(lab))
+    except OSError:
+        raise ValidationError(f"cannot open output file: {path}") from None
+
+
+def read_membership(path, n: int) -> np.ndarray:
+    """labelprop::read_membership (io.cpp:16-56): same checks and messages."""
+    try:
+        f = open(path)
+    except OSError:
+        raise ValidationError(f"cannot open membership file: {path}") from None
+    labels = np.zeros(n, np.uint32)
+    seen = np.zeros(n, bool)
+    with f:
+        for lineno, line in enumerate(f, 1):
+            s = line.strip()
+            if not s or s[0] in "#%":
+                continue
+            toks = s.split()
+            if not toks[0].isdigit() or len(toks) < 2 or not toks[1].isdigit():
+                raise FormatError(f"{path}:{lineno}: expected 'vertex<TAB>label'")
+            if len(toks) > 2:
+                raise FormatError(f"{path}:{lineno}: trailing content after label")
+            v, c = int(toks[0]), int(toks[1])
+            if v >= n:
+                raise ValidationError(f"{path}:{lineno}: vertex {v} out of range for n={n}")
+            if c >= n:
+                raise ValidationError(f"{path}:{lineno}: label {c} out of range for n={n}")
+            if seen[v]:
+                raise ValidationError(f"{path}:{lineno}: vertex {v} assigned twice")
+            seen[v] = True
+            labels[v] = c
+    missing = np.flatnonzero(~seen)
+    if missing.size:
+        raise ValidationError(f"{path}: no label for vertex {int(missing[0])}")
+    return labels
+
+
 def partition_by_degree(g: CsrGraph, switch_degree: int) -> DegreePartition:
     """labelprop::partition_by_degree (lpa.hpp:63)."""
     n = g.order()
