@@ -211,20 +211,20 @@ nulpa_graph* build_csr_device(const uint32_t* u_h, const uint32_t* v_h, const do
   if (ne) {
     k_edge_keys<<<blocks(ne), 256, 0, s>>>(u, v, ne, symmetrize, keys, idx);
     size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, skeys, idx, sidx, ne, 0, 64, s);
+    NULPA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, skeys, idx, sidx, ne, 0, 64, s));
     void* tmp = sc.get<unsigned char>(tb);
-    cub::DeviceRadixSort::SortPairs(tmp, tb, keys, skeys, idx, sidx, ne, 0, 64, s);
+    NULPA_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, skeys, idx, sidx, ne, 0, 64, s));
     // group starts: flags -> exclusive positions via select
     uint64_t* flags = keys;  // reuse
     k_group_starts<<<blocks(ne), 256, 0, s>>>(skeys, ne, flags);
     uint64_t* gstart = idx;  // reuse
     uint64_t* d_n = sc.get<uint64_t>(1);
     size_t tb2 = 0;
-    cub::DeviceSelect::Flagged(nullptr, tb2, cub::CountingInputIterator<uint64_t>(0), flags,
-                               gstart, d_n, ne, s);
+    NULPA_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, cub::CountingInputIterator<uint64_t>(0), flags,
+                               gstart, d_n, ne, s));
     void* tmp2 = sc.get<unsigned char>(tb2);
-    cub::DeviceSelect::Flagged(tmp2, tb2, cub::CountingInputIterator<uint64_t>(0), flags, gstart,
-                               d_n, ne, s);
+    NULPA_CUDA(cub::DeviceSelect::Flagged(tmp2, tb2, cub::CountingInputIterator<uint64_t>(0), flags, gstart,
+                               d_n, ne, s));
     NULPA_CUDA(cudaMemcpy(&ngroups, d_n, 8, cudaMemcpyDeviceToHost));
     gkey = sc.get<uint64_t>(ngroups);
     gw = sc.get<double>(ngroups);
@@ -265,9 +265,9 @@ nulpa_graph* build_csr_device(const uint32_t* u_h, const uint32_t* v_h, const do
       uint64_t* ekey2 = sc.get<uint64_t>(m2);
       k_emit<<<blocks(ngroups), 256, 0, s>>>(gkey, gw, ngroups, npairs, symmetrize, ekey, ew);
       size_t tb = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tb, ekey, ekey2, ew, g->weights, m2, 0, 64, s);
+      NULPA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ekey, ekey2, ew, g->weights, m2, 0, 64, s));
       void* tmp = sc.get<unsigned char>(tb);
-      cub::DeviceRadixSort::SortPairs(tmp, tb, ekey, ekey2, ew, g->weights, m2, 0, 64, s);
+      NULPA_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, ekey, ekey2, ew, g->weights, m2, 0, 64, s));
       k_csr_from_keys<<<blocks(n + 1), 256, 0, s>>>(ekey2, m2, static_cast<uint32_t>(n),
                                                      g->offsets, g->targets);
     } else {

@@ -187,17 +187,17 @@ nulpa_graph* keys_to_graph(uint64_t* keys, uint64_t nkeys, uint32_t n, int devic
   try {
     cub::DoubleBuffer<uint64_t> db(keys, alt);
     size_t tb = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tb, db, nkeys, 0, end_bit, s);
+    NULPA_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, nkeys, 0, end_bit, s));
     void* tmp = dmalloc(tb);
-    cub::DeviceRadixSort::SortKeys(tmp, tb, db, nkeys, 0, end_bit, s);
+    NULPA_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, db, nkeys, 0, end_bit, s));
     NULPA_CUDA(cudaGetLastError());
     dfree(tmp);
     uint64_t* sorted = db.Current();
     uint64_t* other = db.Alternate();
     size_t tb2 = 0;
-    cub::DeviceSelect::Unique(nullptr, tb2, sorted, other, d_num, nkeys, s);
+    NULPA_CUDA(cub::DeviceSelect::Unique(nullptr, tb2, sorted, other, d_num, nkeys, s));
     tmp = dmalloc(tb2);
-    cub::DeviceSelect::Unique(tmp, tb2, sorted, other, d_num, nkeys, s);
+    NULPA_CUDA(cub::DeviceSelect::Unique(tmp, tb2, sorted, other, d_num, nkeys, s));
     NULPA_CUDA(cudaGetLastError());
     dfree(tmp);
     uint64_t nu = 0;

@@ -185,9 +185,9 @@ void finalize_graph(nulpa_graph* g, cudaStream_t s) {
     auto degs = cub::TransformInputIterator<uint32_t, DegreeOf, cub::CountingInputIterator<uint32_t>>(
         cub::CountingInputIterator<uint32_t>(0), DegreeOf{g->offsets});
     size_t tb = 0;
-    cub::DeviceReduce::Max(nullptr, tb, degs, d_max, n, s);
+    NULPA_CUDA(cub::DeviceReduce::Max(nullptr, tb, degs, d_max, n, s));
     void* tmp = dmalloc(tb);
-    cub::DeviceReduce::Max(tmp, tb, degs, d_max, n, s);
+    NULPA_CUDA(cub::DeviceReduce::Max(tmp, tb, degs, d_max, n, s));
     NULPA_CUDA(cudaMemcpyAsync(&maxd, d_max, sizeof maxd, cudaMemcpyDeviceToHost, s));
     NULPA_CUDA(cudaStreamSynchronize(s));
     dfree(tmp);
@@ -198,13 +198,13 @@ void finalize_graph(nulpa_graph* g, cudaStream_t s) {
     auto wd = cub::TransformInputIterator<double, ToDouble, const float*>(g->weights, ToDouble{});
     auto nu = cub::TransformInputIterator<uint32_t, IsUnit, const float*>(g->weights, IsUnit{});
     size_t tb1 = 0, tb2 = 0;
-    cub::DeviceReduce::Sum(nullptr, tb1, wd, d_sum, g->m2, s);
-    cub::DeviceReduce::Sum(nullptr, tb2, nu, d_nonunit, g->m2, s);
+    NULPA_CUDA(cub::DeviceReduce::Sum(nullptr, tb1, wd, d_sum, g->m2, s));
+    NULPA_CUDA(cub::DeviceReduce::Sum(nullptr, tb2, nu, d_nonunit, g->m2, s));
     void* tmp = dmalloc(std::max(tb1, tb2));
-    cub::DeviceReduce::Sum(tmp, tb1, wd, d_sum, g->m2, s);
+    NULPA_CUDA(cub::DeviceReduce::Sum(tmp, tb1, wd, d_sum, g->m2, s));
     NULPA_CUDA(cudaMemcpyAsync(&total, d_sum, sizeof total, cudaMemcpyDeviceToHost, s));
     uint32_t nonunit = 0;
-    cub::DeviceReduce::Sum(tmp, tb2, nu, d_nonunit, g->m2, s);
+    NULPA_CUDA(cub::DeviceReduce::Sum(tmp, tb2, nu, d_nonunit, g->m2, s));
     NULPA_CUDA(cudaMemcpyAsync(&nonunit, d_nonunit, sizeof nonunit, cudaMemcpyDeviceToHost, s));
     NULPA_CUDA(cudaStreamSynchronize(s));
     dfree(tmp);
@@ -243,14 +243,14 @@ void partition_two_way(const uint64_t* off, uint32_t n, uint32_t sw, uint32_t* l
   uint64_t* d_num = dalloc<uint64_t>(1);
   cub::CountingInputIterator<uint32_t> ids(0);
   size_t tb = 0;
-  cub::DeviceSelect::If(nullptr, tb, ids, low, d_num, static_cast<uint64_t>(n),
-                        DegInRange{off, 0, sw - 1ull}, s);
+  NULPA_CUDA(cub::DeviceSelect::If(nullptr, tb, ids, low, d_num, static_cast<uint64_t>(n),
+                        DegInRange{off, 0, sw - 1ull}, s));
   void* tmp = dmalloc(tb);
-  cub::DeviceSelect::If(tmp, tb, ids, low, d_num, static_cast<uint64_t>(n),
-                        DegInRange{off, 0, sw - 1ull}, s);
+  NULPA_CUDA(cub::DeviceSelect::If(tmp, tb, ids, low, d_num, static_cast<uint64_t>(n),
+                        DegInRange{off, 0, sw - 1ull}, s));
   NULPA_CUDA(cudaMemcpyAsync(n_low, d_num, 8, cudaMemcpyDeviceToHost, s));
-  cub::DeviceSelect::If(tmp, tb, ids, high, d_num, static_cast<uint64_t>(n),
-                        DegInRange{off, sw, ~0ull}, s);
+  NULPA_CUDA(cub::DeviceSelect::If(tmp, tb, ids, high, d_num, static_cast<uint64_t>(n),
+                        DegInRange{off, sw, ~0ull}, s));
   NULPA_CUDA(cudaMemcpyAsync(n_high, d_num, 8, cudaMemcpyDeviceToHost, s));
   NULPA_CUDA(cudaStreamSynchronize(s));
   dfree(tmp);
@@ -278,9 +278,9 @@ void scramble_list(uint32_t* list, uint32_t count, cudaStream_t s, int shift = 0
   k_hash_keys<<<256, 256, 0, s>>>(list, count, k0, shift);
   cub::DoubleBuffer<uint32_t> keys(k0, k1), vals(list, v1);
   size_t tb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, count, 0, 32, s);
+  NULPA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, count, 0, 32, s));
   void* tmp = dmalloc(tb);
-  cub::DeviceRadixSort::SortPairs(tmp, tb, keys, vals, count, 0, 32, s);
+  NULPA_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, vals, count, 0, 32, s));
   if (vals.Current() != list)
     NULPA_CUDA(cudaMemcpyAsync(list, vals.Current(), count * 4ull, cudaMemcpyDeviceToDevice, s));
   NULPA_CUDA(cudaStreamSynchronize(s));
@@ -363,12 +363,12 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
     uint32_t* scratch = dalloc<uint32_t>(uint64_t(span) + 1);
     size_t tbytes = 0;
     cub::CountingInputIterator<uint32_t> ids(v_lo);
-    cub::DeviceSelect::If(nullptr, tbytes, ids, scratch, d_num, static_cast<uint64_t>(span),
-                          DegInRange{g->offsets, 1, 1}, s);
+    NULPA_CUDA(cub::DeviceSelect::If(nullptr, tbytes, ids, scratch, d_num, static_cast<uint64_t>(span),
+                          DegInRange{g->offsets, 1, 1}, s));
     void* tmp = dmalloc(tbytes);
     for (int t = 0; t < Plan::kLists; ++t) {
-      cub::DeviceSelect::If(tmp, tbytes, ids, scratch, d_num, static_cast<uint64_t>(span),
-                            DegInRange{g->offsets, bounds[t][0], bounds[t][1]}, s);
+      NULPA_CUDA(cub::DeviceSelect::If(tmp, tbytes, ids, scratch, d_num, static_cast<uint64_t>(span),
+                            DegInRange{g->offsets, bounds[t][0], bounds[t][1]}, s));
       uint64_t cnt = 0;
       NULPA_CUDA(cudaMemcpyAsync(&cnt, d_num, sizeof cnt, cudaMemcpyDeviceToHost, s));
       NULPA_CUDA(cudaStreamSynchronize(s));

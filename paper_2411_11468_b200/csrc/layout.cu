@@ -181,9 +181,9 @@ void permute_csr(const uint64_t* src_off, const uint32_t* src_tgt, const float* 
     auto degs = cub::TransformInputIterator<uint64_t, RowDegree, cub::CountingInputIterator<uint32_t>>(
         cub::CountingInputIterator<uint32_t>(0), RowDegree{src_off, src_row});
     size_t tb = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, tb, degs, dst_off + 1, n, s);
+    NULPA_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, degs, dst_off + 1, n, s));
     void* tmp = dmalloc(tb);
-    cub::DeviceScan::InclusiveSum(tmp, tb, degs, dst_off + 1, n, s);
+    NULPA_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, degs, dst_off + 1, n, s));
     if (m2 && long_prefix)
       k_permute_long_rows<<<148 * 8, 256, 0, s>>>(src_off, src_tgt, src_w, src_row, map,
                                                   dst_off, dst_tgt, dst_w, long_prefix);
@@ -451,22 +451,22 @@ void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g) {
       auto degs = cub::TransformInputIterator<uint64_t, RowDegree, cub::CountingInputIterator<uint32_t>>(
           cub::CountingInputIterator<uint32_t>(0), RowDegree{src_off, g->perm});
       size_t tb = 0;
-      cub::DeviceScan::InclusiveSum(nullptr, tb, degs, g->offsets + 1, n, sb);
+      NULPA_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, degs, g->offsets + 1, n, sb));
       auto is_long = cub::TransformInputIterator<uint32_t, LongRow, cub::CountingInputIterator<uint32_t>>(
           cub::CountingInputIterator<uint32_t>(0), LongRow{src_off});
       size_t tb2 = 0;
       L = dalloc<uint32_t>(uint64_t(n) + 1);
-      cub::DeviceSelect::Flagged(nullptr, tb2, cub::CountingInputIterator<uint32_t>(0), is_long, L,
-                                 range, n, sb);
+      NULPA_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, cub::CountingInputIterator<uint32_t>(0), is_long, L,
+                                 range, n, sb));
       auto dg = cub::TransformInputIterator<uint32_t, DegreeOfRow, cub::CountingInputIterator<uint32_t>>(
           cub::CountingInputIterator<uint32_t>(0), DegreeOfRow{src_off});
       size_t tb3 = 0;
-      cub::DeviceReduce::Max(nullptr, tb3, dg, d_max, n, sb);
+      NULPA_CUDA(cub::DeviceReduce::Max(nullptr, tb3, dg, d_max, n, sb));
       tmp = dmalloc(std::max(tb, std::max(tb2, tb3)));
-      cub::DeviceScan::InclusiveSum(tmp, tb, degs, g->offsets + 1, n, sb);
-      cub::DeviceSelect::Flagged(tmp, tb2, cub::CountingInputIterator<uint32_t>(0), is_long, L,
-                                 range, n, sb);
-      cub::DeviceReduce::Max(tmp, tb3, dg, d_max, n, sb);
+      NULPA_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, degs, g->offsets + 1, n, sb));
+      NULPA_CUDA(cub::DeviceSelect::Flagged(tmp, tb2, cub::CountingInputIterator<uint32_t>(0), is_long, L,
+                                 range, n, sb));
+      NULPA_CUDA(cub::DeviceReduce::Max(tmp, tb3, dg, d_max, n, sb));
       uint32_t nL = 0;
       NULPA_CUDA(cudaMemcpyAsync(&nL, range, 4, cudaMemcpyDeviceToHost, sb));
       NULPA_CUDA(cudaMemcpyAsync(&g->max_degree, d_max, 4, cudaMemcpyDeviceToHost, sb));
@@ -477,9 +477,9 @@ void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g) {
         auto ld = cub::TransformInputIterator<uint64_t, LongDeg, cub::CountingInputIterator<uint32_t>>(
             cub::CountingInputIterator<uint32_t>(0), LongDeg{src_off, L});
         size_t tb4 = 0;
-        cub::DeviceScan::InclusiveSum(nullptr, tb4, ld, LP + 1, nL, sb);
+        NULPA_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb4, ld, LP + 1, nL, sb));
         void* tmp4 = dmalloc(tb4);
-        cub::DeviceScan::InclusiveSum(tmp4, tb4, ld, LP + 1, nL, sb);
+        NULPA_CUDA(cub::DeviceScan::InclusiveSum(tmp4, tb4, ld, LP + 1, nL, sb));
         NULPA_CUDA(cudaStreamSynchronize(sb));
         dfree(tmp4);
       }
@@ -546,9 +546,9 @@ void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g) {
         double* d_sum = dalloc<double>(1);
         auto wd = cub::TransformInputIterator<double, ToDoubleW, const float*>(g->weights, ToDoubleW{});
         size_t tb = 0;
-        cub::DeviceReduce::Sum(nullptr, tb, wd, d_sum, m2, sb);
+        NULPA_CUDA(cub::DeviceReduce::Sum(nullptr, tb, wd, d_sum, m2, sb));
         void* t2 = dmalloc(tb);
-        cub::DeviceReduce::Sum(t2, tb, wd, d_sum, m2, sb);
+        NULPA_CUDA(cub::DeviceReduce::Sum(t2, tb, wd, d_sum, m2, sb));
         NULPA_CUDA(cudaMemcpyAsync(&g->total_2m, d_sum, 8, cudaMemcpyDeviceToHost, sb));
         NULPA_CUDA(cudaStreamSynchronize(sb));
         dfree(t2);
@@ -579,9 +579,9 @@ void build_perm(const uint64_t* off, uint32_t n, uint32_t** perm_out, uint32_t**
     cub::DoubleBuffer<uint8_t> keys(k0, k1);
     cub::DoubleBuffer<uint32_t> vals(ids, perm);
     size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, n, 0, 6, s);
+    NULPA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, n, 0, 6, s));
     void* tmp = dmalloc(tb);
-    cub::DeviceRadixSort::SortPairs(tmp, tb, keys, vals, n, 0, 6, s);
+    NULPA_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, vals, n, 0, 6, s));
     NULPA_CUDA(cudaStreamSynchronize(s));
     dfree(tmp);
     if (vals.Current() != perm) std::swap(ids, perm);
@@ -611,9 +611,9 @@ void relayout_graph(nulpa_graph* g, cudaStream_t s) {
         cub::CountingInputIterator<uint32_t>(0), LongRow{g->offsets});
     uint32_t* d_cnt = dalloc<uint32_t>(1);
     size_t tb = 0;
-    cub::DeviceReduce::Sum(nullptr, tb, is_long, d_cnt, n, s);
+    NULPA_CUDA(cub::DeviceReduce::Sum(nullptr, tb, is_long, d_cnt, n, s));
     void* tmp = dmalloc(tb);
-    cub::DeviceReduce::Sum(tmp, tb, is_long, d_cnt, n, s);
+    NULPA_CUDA(cub::DeviceReduce::Sum(tmp, tb, is_long, d_cnt, n, s));
     NULPA_CUDA(cudaMemcpyAsync(&long_rows, d_cnt, 4, cudaMemcpyDeviceToHost, s));
     NULPA_CUDA(cudaStreamSynchronize(s));
     dfree(tmp);

@@ -269,19 +269,25 @@ void community_stats_device(nulpa_graph* g, const uint32_t* labels, cudaStream_t
     k_sizes<<<std::min<uint32_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(lab, n, size);
     size_t t1 = 0, t2 = 0, t3 = 0;
     cub::CountingInputIterator<uint32_t> ids(0);
-    cub::DeviceSelect::If(nullptr, t1, ids, comm, d_num, n, Present{size}, s);
-    cub::DeviceRadixSort::SortKeys(nullptr, t2, sz, sz_sorted, n, 0, 32, s);
-    cub::DeviceRunLengthEncode::Encode(nullptr, t3, sz_sorted, runs, run_len, d_num, n, s);
+    // Every cub call uses the same 32-bit item-count type: the temp-storage size
+    // queried for one offset type does not cover another.
+    NULPA_CUDA(cub::DeviceSelect::If(nullptr, t1, ids, comm, d_num, n, Present{size}, s));
+    NULPA_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t2, sz, sz_sorted, n, 0, 32, s));
+    NULPA_CUDA(
+        cub::DeviceRunLengthEncode::Encode(nullptr, t3, sz_sorted, runs, run_len, d_num, n, s));
     tmp = dmalloc(std::max(t1, std::max(t2, t3)));
-    cub::DeviceSelect::If(tmp, t1, ids, comm, d_num, n, Present{size}, s);
-    uint64_t k = 0;
-    NULPA_CUDA(cudaMemcpyAsync(&k, d_num, 8, cudaMemcpyDeviceToHost, s));
+    NULPA_CUDA(cub::DeviceSelect::If(tmp, t1, ids, comm, d_num, n, Present{size}, s));
+    uint64_t k64 = 0;
+    NULPA_CUDA(cudaMemcpyAsync(&k64, d_num, 8, cudaMemcpyDeviceToHost, s));
     NULPA_CUDA(cudaStreamSynchronize(s));
+    const uint32_t k = static_cast<uint32_t>(k64);
     if (k) {
-      k_gather_stats<<<std::min<uint64_t>((k + 255) / 256, 148 * 8), 256, 0, s>>>(
+      k_gather_stats<<<std::min<uint32_t>((k + 255) / 256, 148 * 8), 256, 0, s>>>(
           comm, k, size, sigma, big, sz, sg, bg);
-      cub::DeviceRadixSort::SortKeys(tmp, t2, sz, sz_sorted, k, 0, 32, s);
-      cub::DeviceRunLengthEncode::Encode(tmp, t3, sz_sorted, runs, run_len, d_num, k, s);
+      NULPA_CUDA(cudaGetLastError());
+      NULPA_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t2, sz, sz_sorted, k, 0, 32, s));
+      NULPA_CUDA(
+          cub::DeviceRunLengthEncode::Encode(tmp, t3, sz_sorted, runs, run_len, d_num, k, s));
     }
     uint64_t nh = 0;
     if (k) NULPA_CUDA(cudaMemcpyAsync(&nh, d_num, 8, cudaMemcpyDeviceToHost, s));
@@ -323,9 +329,9 @@ uint64_t community_count_device(nulpa_graph* g, const uint32_t* lab, cudaStream_
   auto it = cub::TransformInputIterator<unsigned long long, U8ToU64, const uint8_t*>(present,
                                                                                      U8ToU64{});
   size_t tb = 0;
-  cub::DeviceReduce::Sum(nullptr, tb, it, d_cnt, n, s);
+  NULPA_CUDA(cub::DeviceReduce::Sum(nullptr, tb, it, d_cnt, n, s));
   void* tmp = dmalloc(tb);
-  cub::DeviceReduce::Sum(tmp, tb, it, d_cnt, n, s);
+  NULPA_CUDA(cub::DeviceReduce::Sum(tmp, tb, it, d_cnt, n, s));
   unsigned long long cnt = 0;
   NULPA_CUDA(cudaMemcpyAsync(&cnt, d_cnt, 8, cudaMemcpyDeviceToHost, s));
   NULPA_CUDA(cudaStreamSynchronize(s));
