@@ -24,6 +24,8 @@ OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libnulpa.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# tuning experiments: extra nvcc flags (e.g. -DNULPA_WIDE_LIMIT=8192); rebuild with force=True
+EXTRA_NVCC = os.environ.get("NULPA_NVCC_FLAGS", "").split()
 CU_SOURCES = ["graph.cu", "layout.cu", "engine.cu", "quality.cu", "gen.cu", "build_csr.cu"]
 CXX_SOURCES = ["dropin.cpp", "loaders.cpp"]
 
@@ -55,7 +57,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
         objs.append(o)
         if force or not _newer(o, [s] + headers):
             jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                         "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr", *inc, "-c", str(s),
+                         "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr", *EXTRA_NVCC, *inc, "-c", str(s),
                          "-o", str(o)])
     for src in CXX_SOURCES:
         s = CSRC / src

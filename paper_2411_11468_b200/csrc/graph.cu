@@ -397,7 +397,7 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
 
     // Wide tier (k_wide): one L2-resident row snapshot per resident CTA.
     if (p->count[dev::T_CLUSTER] && !p->weighted)
-      p->wide_scratch = dalloc<uint32_t>(uint64_t(sm_count()) * dev::kClusterMax);
+      p->wide_scratch = dalloc<uint32_t>(uint64_t(sm_count()) * dev::kWideScratch);
     // Hub tier: per-hub global tables and (hub, chunk) work items. Hub counts
     // are small (vertices of degree > block_max), so the layout is built on
     // the host.

@@ -726,14 +726,16 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
 // ---- tier: wide rows, one 1024-thread CTA per vertex, label-partitioned phases --------
 // Rows of kBigMax < d <= kClusterMax (unit weights). The CTA's 16K-slot shared
 // table holds at most kWideLimit distinct labels, so a row with more distinct
-// labels is aggregated in P phases: phase p streams the whole row but inserts
-// only the labels with phase_of(label, P) == p, sweeps the table into a running
-// (max count, min label) and clears it. The argmax over all phases is exact (each
-// label lives in exactly one phase). The first pass from identity labels
-// (every label distinct) starts at P = ceil(d / kWideLimit); other passes start
-// at P = 1 and double P when the table overflows. Re-streaming the row costs HBM
-// bandwidth for the targets only (labels hit L2); no cluster barriers, no remote
-// atomics, and every SM owns its own vertex.
+// labels is aggregated in P phases over a hash partition of the labels: phase 0
+// gathers the row, inserts the labels with phase_of(label, P) == 0 and appends every
+// other label to its phase's bucket in the CTA's scratch (L2-resident); phase q
+// streams bucket q. Each phase sweeps the table into a running (max count, min label)
+// and clears it. The argmax over all phases is exact (each label lives in exactly one
+// phase). The first pass from identity labels (every label distinct) starts at
+// P = ceil(d / kWideLimit); other passes start at P = 1 and double P when the table
+// overflows (past kWideBuckets phases the row re-streams an in-order snapshot,
+// filtering by phase). No cluster barriers, no remote atomics, and every SM owns its
+// own vertex.
 #ifndef NULPA_WIDE_LIMIT
 #define NULPA_WIDE_LIMIT 12288
 #endif
@@ -743,6 +745,12 @@ __device__ __forceinline__ uint32_t phase_of(uint32_t key, uint32_t P) {
   const uint32_t h = (key ^ (key >> 16)) * 0x7FEB352Du;
   return static_cast<uint32_t>((static_cast<uint64_t>(h) * P) >> 32);
 }
+
+// Phase buckets of the wide tier: bucket q (1 <= q < P) of a P-phase row holds up to
+// d labels at scratch + (q - 1) * d, so no label distribution can overfill one.
+constexpr uint32_t kWideBuckets = 8;  // P <= 8 is bucketed; larger P re-streams in order
+static_assert((kWideBuckets - 1) * uint64_t(kClusterMax) <= kWideScratch,
+              "wide scratch holds every bucket layout");
 
 constexpr size_t wide_bytes() {
   return size_t(kClusterCap) * 8 + size_t(kClusterCap) * sizeof(uint16_t);
@@ -754,7 +762,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
                                                          uint32_t* __restrict__ scratch) {
   // This CTA's row snapshot: phase 0 of a multi-phase vertex gathers the labels
   // once and writes them here (L2-resident); later phases stream them back.
-  uint32_t* snap = scratch + size_t(blockIdx.x) * kClusterMax;
+  uint32_t* snap = scratch + size_t(blockIdx.x) * kWideScratch;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemTable<W> tab;
   tab.bind(smem_raw, kClusterCap);
@@ -762,6 +770,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
   __shared__ uint32_t s_item;
   __shared__ int s_flag, s_over;
   __shared__ unsigned s_occ_n;
+  __shared__ unsigned s_bcnt[kWideBuckets];
   __shared__ Best<VBits<W>> red[32];
   constexpr uint32_t kWideBatch = 4;  // vertices per work-counter fetch (batched prologue)
   __shared__ Meta s_meta[kWideBatch];
@@ -784,18 +793,26 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
     const uint64_t lo = m.lo;
     const uint32_t d = m.d;
     uint32_t P = fresh ? (d + kWideLimit - 1) / kWideLimit : 1u;
-    // A phase can only overflow when it may hold more than kWideLimit labels.
-    const bool may_overflow = P > 1 || d > kWideLimit;
+    // Bucketed phases: phase 0 gathers the row once and appends every label of a
+    // later phase to that phase's bucket in the CTA's L2 scratch, so phase q > 0
+    // streams only its own labels (d label reads in all, not P * d).
     Best<VBits<W>> best{VBits<W>(0), kEmpty};  // running result (thread 0)
     for (uint32_t ph = 0; ph < P; ++ph) {
+      const bool use_b = P > 1 && P <= kWideBuckets;
       if (threadIdx.x == 0) {
         s_occ_n = 0;
         s_over = 0;
+        if (ph == 0)
+          for (uint32_t b = 0; b < kWideBuckets; ++b) s_bcnt[b] = 0;
       }
       __syncthreads();
+      // A phase can only overflow when it may hold more than kWideLimit labels.
+      const uint32_t len = (use_b && ph > 0) ? s_bcnt[ph] : d;
+      const bool may_overflow = len > kWideLimit || (P > 1 && !use_b);
       const uint32_t cap = P == 1 ? min(static_cast<uint32_t>(kClusterCap), pow2_ceil(2 * d))
                                   : static_cast<uint32_t>(kClusterCap);
-      for (uint32_t base = 0; base < d; base += kBigThreads * U) {
+      const uint32_t* src = use_b ? snap + size_t(ph - 1) * d : snap;
+      for (uint32_t base = 0; base < len; base += kBigThreads * U) {
         uint32_t lab[U];
         if (ph == 0) {
           uint32_t j[U];
@@ -808,30 +825,49 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
           for (int u = 0; u < U; ++u) {
             const uint32_t e = base + u * kBigThreads + threadIdx.x;
             lab[u] = j[u] != i ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
-            if (P > 1 && e < d) snap[e] = lab[u];
+            if (P > 1 && !use_b && e < d) snap[e] = lab[u];
+          }
+          if (use_b) {
+            const int lane = threadIdx.x & 31;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t q = lab[u] != kEmpty ? phase_of(lab[u], P) : 0u;
+              const unsigned peers = __match_any_sync(kFull, q);
+              unsigned at = 0;
+              const int leader = __ffs(peers) - 1;
+              if (q != 0 && lane == leader) at = atomicAdd(&s_bcnt[q], __popc(peers));
+              at = __shfl_sync(kFull, at, leader) + __popc(peers & ((1u << lane) - 1u));
+              if (q != 0) {
+                snap[size_t(q - 1) * d + at] = lab[u];
+                lab[u] = kEmpty;
+              }
+            }
           }
         } else {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint32_t e = base + u * kBigThreads + threadIdx.x;
-            lab[u] = e < d ? __ldcg(snap + e) : kEmpty;
+            lab[u] = e < len ? __ldcg(src + e) : kEmpty;
           }
         }
+        if (!use_b) {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (P > 1 && lab[u] != kEmpty && phase_of(lab[u], P) != ph) lab[u] = kEmpty;
+          for (int u = 0; u < U; ++u)
+            if (P > 1 && lab[u] != kEmpty && phase_of(lab[u], P) != ph) lab[u] = kEmpty;
+        }
         const uint32_t wbase = base + (threadIdx.x & ~31u);
         unsigned live = 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) live |= (wbase + u * kBigThreads < d ? 1u : 0u) << u;
+        for (int u = 0; u < U; ++u) live |= (wbase + u * kBigThreads < len ? 1u : 0u) << u;
         unsigned long long f = 0;
         gather_insert_multi<U, W>(c, lab, live, tab, cap, occ, &s_occ_n, f);
         if (f) s_over = 1;  // table full: treat as overflow
         // Stop early once the phase holds too many distinct labels (block-uniform:
-        // every thread reads the counters between the same two barriers).
+        // every thread reads the counters between the same two barriers). A
+        // bucketed phase 0 must finish its scatter, so it only stops on a full table.
         if (may_overflow) {
           __syncthreads();
-          const bool stop = s_over || s_occ_n > kWideLimit;
+          const bool stop = s_over || (s_occ_n > kWideLimit && !(use_b && ph == 0));
           __syncthreads();
           if (stop) {
             if (threadIdx.x == 0) s_over = 1;
@@ -840,7 +876,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
         }
       }
       __syncthreads();
-      const bool over = s_over != 0;
+      const bool over = s_over != 0;  // (a bucketed phase 0 past kWideLimit is still exact)
       Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n, threadIdx.x, blockDim.x);
       b = block_best(b, red);  // (ends with a barrier: the table is clear again)
       if (over) {

@@ -243,3 +243,24 @@ def test_grid_matches_numpy():
             rows.append(nb)
     assert g.targets.tolist() == [x for row in rows for x in row]
     assert np.array_equal(np.diff(g.offsets.astype(np.int64)), [len(r) for r in rows])
+
+
+@pytest.mark.parametrize("repeat", [0, 15000, 29000])
+def test_wide_phase_buckets_sync_step(repeat):
+    # A 30000-leaf star: the centre lands in the wide tier with more distinct labels
+    # than one phase holds, so its phases are bucketed; `repeat` leaves sharing one
+    # label overfill that label's bucket (or not) and force the in-order fallback.
+    leaves = 30000
+    n = leaves + 1
+    off = np.zeros(n + 1, np.uint64)
+    off[1] = leaves
+    off[2:] = leaves + np.arange(1, leaves + 1, dtype=np.uint64)
+    tgt = np.concatenate([np.arange(1, n, dtype=np.uint32), np.zeros(leaves, np.uint32)])
+    g = lp.CsrGraph(off, tgt, None)
+    pg = O.PortGraph(off, tgt, None)
+    lab = np.arange(n, dtype=np.uint32)
+    lab[n - repeat:] = 7
+    for pl in (0, 1):
+        want, wc = O.port_sync_step(pg, lab, pl)
+        got, gc = lp.sync_step(g, lab, pl)
+        assert gc == wc and np.array_equal(got, want)
