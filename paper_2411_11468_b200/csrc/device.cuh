@@ -83,7 +83,11 @@ constexpr int kBigMax = NULPA_MID_MAX;  // load <= 3/4
 constexpr int kClusterSize = 8;     // portable cluster size
 constexpr int kClusterCap = 16384;  // slots per CTA of the cluster
 constexpr int kClusterMax = kClusterSize * kClusterCap * 3 / 4;  // 98304, load <= 3/4
-constexpr uint32_t kWideScratch = 7 * 98304;  // u32 per wide-tier CTA: row snapshot / 7 phase buckets
+#ifndef NULPA_WIDE_BUCKETS
+#define NULPA_WIDE_BUCKETS 8
+#endif
+// u32 per wide-tier CTA: the row snapshot, or the buckets of phases 1..NULPA_WIDE_BUCKETS-1
+constexpr uint32_t kWideScratch = (NULPA_WIDE_BUCKETS - 1) * uint32_t(kClusterMax);
 constexpr int kHubChunk = 2048;     // edges per hub work item (<= kBlockCap / 2)
 constexpr int kHubSweep = 8192;     // table slots per hub sweep item
 

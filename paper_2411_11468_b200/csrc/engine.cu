@@ -13,6 +13,7 @@
 #include <cstring>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "internal.hpp"
 #include "layout.hpp"
@@ -288,13 +289,32 @@ struct DBuf {
   }
 };
 
+// Pinned host counters. Buffers are recycled through a per-thread free list:
+// cudaHostAlloc / cudaFreeHost on every call cost milliseconds (and can stall on
+// the driver's unmap), far more than the counters they carry.
 struct Pinned {
   unsigned long long* p = nullptr;
+  size_t cap = 0;
   explicit Pinned(size_t count = C_COUNT) {
+    auto& fl = free_list();
+    for (size_t k = 0; k < fl.size(); ++k)
+      if (fl[k].second >= count) {
+        p = fl[k].first;
+        cap = fl[k].second;
+        fl.erase(fl.begin() + k);
+        return;
+      }
     NULPA_CUDA(cudaHostAlloc(&p, count * sizeof(unsigned long long), cudaHostAllocDefault));
+    cap = count;
   }
   ~Pinned() {
-    if (p) cudaFreeHost(p);
+    if (p) free_list().emplace_back(p, cap);
+  }
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+  static std::vector<std::pair<unsigned long long*, size_t>>& free_list() {
+    static thread_local std::vector<std::pair<unsigned long long*, size_t>> fl;
+    return fl;
   }
 };
 
@@ -333,6 +353,7 @@ uint64_t device_cross_check(nulpa_graph* g, uint32_t* lab, const uint32_t* prev,
 
 void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
              uint32_t* labels_host, uint32_t* labels_dev_out, nulpa_stats* st) {
+  Trace tr("run_lpa");
   validate_opts(g, o);
   use_device(g->device);
   const auto t_setup = std::chrono::steady_clock::now();
@@ -367,6 +388,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       NULPA_CUDA(cudaEventCreate(&e[0]));
       NULPA_CUDA(cudaEventCreate(&e[1]));
     }
+  tr.mark("plan + buffers");
   k_init<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(lab0.p, flags.p, g->offsets, n, g->perm);
   NULPA_CUDA(cudaGetLastError());
   NULPA_CUDA(cudaStreamSynchronize(s));
@@ -558,6 +580,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       cudaEventDestroy(e[1]);
     }
 
+  tr.mark("loop");
   // Results leave in vertex order (layout.cu).
   if (labels_dev_out) to_vertices_u32(g, cur, labels_dev_out, s);
   if (labels_host) {
@@ -575,6 +598,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     NULPA_CUDA(cudaMemcpyAsync(labels_host, src, n * 4ull, cudaMemcpyDeviceToHost, s));
   }
   NULPA_CUDA(cudaStreamSynchronize(s));
+  tr.mark("labels out");
   if (st) {
     st->iterations = iterations;
     st->converged = converged ? 1 : 0;
@@ -887,8 +911,11 @@ int nulpa_run(const nulpa_csr* csr, const nulpa_opts* opts, const nulpa_tuning* 
     nulpa_graph probe;  // validate before any device work (lpa.cpp:363)
     probe.n = csr->n;
     validate_opts(&probe, *opts);
+    Trace tr("nulpa_run");
     HostGraph hg(csr, opts->device);
+    tr.mark("upload");
     run_lpa(hg.g, *opts, tuning, labels_out, nullptr, stats);
+    tr.mark("run_lpa");
   });
 }
 

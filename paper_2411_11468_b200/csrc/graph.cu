@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -110,14 +112,16 @@ void use_device(int device) {
   if (device < 0 || device >= count)
     throw Error(NULPA_EINVAL, "CUDA device " + std::to_string(device) + " out of range");
   NULPA_CUDA(cudaSetDevice(device));
-  // Device buffers come from the stream-ordered pool; keep up to 64 GB of freed
-  // memory cached so repeated lpa() calls (new graph, plan, labels each time)
-  // do not pay cudaMalloc/cudaFree of multi-GB arrays.
+  // Device buffers come from the stream-ordered pool, which keeps freed memory
+  // mapped so repeated lpa() calls (new graph, plan, labels each time) neither
+  // re-map multi-GB arrays nor trim the pool at every synchronisation point.
+  // NULPA_POOL_KEEP_GB caps what stays cached (default: everything).
   static thread_local int configured = -1;
   if (configured != device) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = 64ull << 30;
+      const char* env = std::getenv("NULPA_POOL_KEEP_GB");
+      uint64_t keep = env ? std::strtoull(env, nullptr, 10) << 30 : ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     (void)cudaGetLastError();
@@ -127,6 +131,24 @@ void use_device(int device) {
 
 // Allocations are stream-ordered on the legacy stream; every buffer is freed only
 // after the work that used it has been synchronised.
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+Trace::Trace(const char* sc) : on(std::getenv("NULPA_TRACE") != nullptr), scope(sc) {
+  t0 = last = on ? now_s() : 0.0;
+}
+
+Trace::~Trace() { mark("exit"); }
+
+void Trace::mark(const char* what) {
+  if (!on) return;
+  const double t = now_s();
+  std::fprintf(stderr, "[nulpa trace] %s: %-24s +%8.3f ms (at %8.3f ms)\n", scope, what,
+               (t - last) * 1e3, (t - t0) * 1e3);
+  last = t;
+}
+
 void* dmalloc(size_t bytes) {
   void* p = nullptr;
   cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 16, 0);

@@ -60,6 +60,16 @@ T* dalloc(size_t count) {
   return static_cast<T*>(dmalloc(count * sizeof(T) + (count == 0 ? 16 : 0)));
 }
 
+// Host-side phase timestamps on stderr when NULPA_TRACE is set (diagnostics only).
+struct Trace {
+  explicit Trace(const char* scope);
+  ~Trace();
+  void mark(const char* what);
+  bool on;
+  const char* scope;
+  double t0, last;
+};
+
 struct Plan;
 }  // namespace nulpa
 

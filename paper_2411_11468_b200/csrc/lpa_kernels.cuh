@@ -748,7 +748,7 @@ __device__ __forceinline__ uint32_t phase_of(uint32_t key, uint32_t P) {
 
 // Phase buckets of the wide tier: bucket q (1 <= q < P) of a P-phase row holds up to
 // d labels at scratch + (q - 1) * d, so no label distribution can overfill one.
-constexpr uint32_t kWideBuckets = 8;  // P <= 8 is bucketed; larger P re-streams in order
+constexpr uint32_t kWideBuckets = NULPA_WIDE_BUCKETS;  // P <= this is bucketed; larger P re-streams in order
 static_assert((kWideBuckets - 1) * uint64_t(kClusterMax) <= kWideScratch,
               "wide scratch holds every bucket layout");
 
