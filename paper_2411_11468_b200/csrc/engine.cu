@@ -89,16 +89,27 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   constexpr size_t big_smem = team_bytes<Tab, kBigCap, kBigMax>();
   constexpr size_t cluster_smem = cluster_bytes<Tab>();
   constexpr size_t hub_smem = kHubCap * Tab::kSlotBytes + kHubChunk * sizeof(uint16_t);
-  auto k_wt = k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax>;
-  auto k_b1 = k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax>;
-  auto k_b2 = k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max>;
-  auto k_bg = k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax>;
+  // First pass of a run (labels still mostly distinct): the team tables skip the
+  // in-warp dedupe (see k_team).
+  const bool dd = !c.fresh;
+  auto k_wt = dd ? k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, true>
+                 : k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, false>;
+  auto k_b1 = dd ? k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax, true>
+                 : k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax, false>;
+  auto k_b2 = dd ? k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max, true>
+                 : k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max, false>;
+  auto k_bg = dd ? k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, true>
+                 : k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, false>;
   static bool init = false;
   if (!init) {
-    allow_smem(k_wt, wtab_smem);
-    allow_smem(k_b1, block_smem);
-    allow_smem(k_b2, block2_smem);
-    allow_smem(k_bg, big_smem);
+    allow_smem(k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, true>, wtab_smem);
+    allow_smem(k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, false>, wtab_smem);
+    allow_smem(k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax, true>, block_smem);
+    allow_smem(k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax, false>, block_smem);
+    allow_smem(k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max, true>, block2_smem);
+    allow_smem(k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max, false>, block2_smem);
+    allow_smem(k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, true>, big_smem);
+    allow_smem(k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, false>, big_smem);
     allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
     if constexpr (!WEIGHTED) allow_smem(k_wide<MODE, W>, wide_bytes());
     allow_smem(k_hub_accum<MODE, W, WEIGHTED>, hub_smem);
