@@ -296,7 +296,7 @@ __device__ __forceinline__ void gather_insert(const PassCtx& c, uint32_t lab, W 
 // count adds, one occupancy append), so the rounds' latency chains overlap
 // instead of running back to back. `live` has bit u set when round u holds at
 // least one of the warp's edges (warp-uniform). All 32 lanes call it.
-template <int U, typename W, bool DEDUP = true>
+template <int U, typename W, int DEDUP = 1>
 __device__ __forceinline__ void gather_insert_multi(const PassCtx& c, const uint32_t (&lab)[U],
                                                     unsigned live, SmemTable<W>& tab,
                                                     uint32_t cap, uint16_t* occ, unsigned* occ_n,
@@ -309,7 +309,13 @@ __device__ __forceinline__ void gather_insert_multi(const PassCtx& c, const uint
   bool lead[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    peers[u] = (live >> u & 1u) ? (DEDUP ? __match_any_sync(kFull, lab[u]) : 1u << lane) : 0u;
+    if (!(live >> u & 1u)) {
+      peers[u] = 0u;
+    } else if constexpr (DEDUP == 1) {
+      peers[u] = __match_any_sync(kFull, lab[u]);
+    } else {
+      peers[u] = 1u << lane;
+    }
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     lead[u] = lab[u] != kEmpty && (peers[u] & lt) == 0u && peers[u] != 0u;
@@ -368,7 +374,7 @@ __device__ __forceinline__ void gather_insert_multi(const PassCtx& c, const uint
 
 // Gather edges [e0, e1) of vertex i (U edges per thread in flight) into `tab`.
 // `T` threads cooperate; all of them call it with the same bounds.
-template <int MODE, typename W, bool WEIGHTED, typename Tab, int U = 4, bool DEDUP = true>
+template <int MODE, typename W, bool WEIGHTED, typename Tab, int U = 4, int DEDUP = 1>
 __device__ __forceinline__ void team_gather(const PassCtx& c, uint32_t i, uint64_t lo,
                                             uint32_t e0, uint32_t e1, Tab& tab, uint32_t cap,
                                             uint32_t tid, uint32_t T, uint64_t pol,
@@ -504,7 +510,7 @@ constexpr size_t team_bytes() {
 // every label is distinct and the table's own claim/add handles the few repeats
 // for less (launch_pass picks the variant per pass).
 template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CAP, int MAXD,
-          bool DEDUP = true>
+          int DEDUP = 1>
 __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : (CTA_THREADS == 512 ? 2 : 1))
     k_team(PassCtx c, const uint32_t* __restrict__ list,
                                                       uint32_t count) {
@@ -866,7 +872,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
 #pragma unroll
         for (int u = 0; u < U; ++u) live |= (wbase + u * kBigThreads < len ? 1u : 0u) << u;
         unsigned long long f = 0;
-        gather_insert_multi<U, W, false>(c, lab, live, tab, cap, occ, &s_occ_n, f);
+        gather_insert_multi<U, W, 0>(c, lab, live, tab, cap, occ, &s_occ_n, f);
         if (f) s_over = 1;  // table full: treat as overflow
         // Stop early once the phase holds too many distinct labels (block-uniform:
         // every thread reads the counters between the same two barriers). A
