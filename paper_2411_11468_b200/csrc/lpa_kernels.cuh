@@ -820,7 +820,10 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
       __syncthreads();
       // A phase can only overflow when it may hold more than kWideLimit labels.
       const uint32_t len = (use_b && ph > 0) ? s_bcnt[ph] : d;
-      const bool may_overflow = len > kWideLimit || (P > 1 && !use_b);
+      // Early stop (a per-round block vote) only where a row may hold more distinct
+      // labels than the phase takes and the phase re-streams the whole row. Bucketed
+      // phases run to the end: a full table (rare) still flags s_over and restarts.
+      const bool may_overflow = !use_b && (len > kWideLimit || P > 1);
       const uint32_t cap = P == 1 ? min(static_cast<uint32_t>(kClusterCap), pow2_ceil(2 * d))
                                   : static_cast<uint32_t>(kClusterCap);
       const uint32_t* src = use_b ? snap + size_t(ph - 1) * d : snap;
@@ -874,14 +877,13 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
         unsigned long long f = 0;
         gather_insert_multi<U, W, 0>(c, lab, live, tab, cap, occ, &s_occ_n, f);
         if (f) s_over = 1;  // table full: treat as overflow
-        // Stop early once the phase holds too many distinct labels (block-uniform:
-        // every thread reads the counters between the same two barriers). A
-        // bucketed phase 0 must finish its scatter, so it only stops on a full table.
+        // Stop early once the phase holds too many distinct labels: one barrier
+        // with a block-wide OR (uniform result). Thread 0's read of the occupancy
+        // count may miss appends still in flight; the vote is a heuristic, while
+        // exactness rests on s_over (a failed insert) alone.
         if (may_overflow) {
-          __syncthreads();
-          const bool stop = s_over || (s_occ_n > kWideLimit && !(use_b && ph == 0));
-          __syncthreads();
-          if (stop) {
+          const unsigned occ_now = *static_cast<volatile unsigned*>(&s_occ_n);
+          if (__syncthreads_or(f != 0 || (threadIdx.x == 0 && occ_now > kWideLimit))) {
             if (threadIdx.x == 0) s_over = 1;
             break;
           }
