@@ -474,14 +474,23 @@ __device__ __forceinline__ void team_sync(int id, int nthreads) {
 }
 
 template <int TEAM, typename V>
-__device__ __forceinline__ Best<V> team_best(Best<V> b, Best<V>* red, int team_tid, int bar) {
+__device__ __forceinline__ Best<V> team_best(Best<V> b, Best<V>* red, int team_tid, int bar,
+                                             unsigned* reset = nullptr) {
+  // `reset` (optional): zeroed once every team thread is past its reads of it
+  // (the occupancy count of the sweep that produced b), ordered before return.
   b = warp_best(b);
   if constexpr (TEAM == 32) {
+    if (reset) {
+      __syncwarp();
+      if (team_tid == 0) *reset = 0;
+      __syncwarp();
+    }
     return b;
   } else {
     const int w = team_tid >> 5, lane = team_tid & 31;
     if (lane == 0) red[w] = b;
     team_sync(bar, TEAM);
+    if (reset && team_tid == 0) *reset = 0;
     if (w == 0) {
       Best<V> r = lane < TEAM / 32 ? red[lane] : Best<V>{V(0), kEmpty};
       r = warp_best(r);
@@ -519,7 +528,6 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : (CTA_THR
   using Tab = std::conditional_t<kPacked<WEIGHTED>, SmemTable<W>, Table<false, W>>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Best<VBits<W>> s_red[kTeams][TEAM / 32 > 0 ? TEAM / 32 : 1];
-  __shared__ int s_flag[kTeams];
   __shared__ unsigned s_occ_n[kTeams];
   const int team = threadIdx.x / TEAM, ttid = threadIdx.x % TEAM;
   const int bar = 1 + team;  // named barrier 0 is __syncthreads
@@ -534,6 +542,8 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : (CTA_THR
       team_sync(bar, TEAM);
   };
   for (uint32_t s = ttid; s < CAP; s += TEAM) tab.clear_slot(s);  // once per lifetime
+  if (ttid == 0) s_occ_n[team] = 0;
+  sync();
   const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
   // Teams take kBatch list entries at a time: the team's first warp fetches the
@@ -575,29 +585,28 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : (CTA_THR
       else
         m = s_meta[team][v];
       if (!m.act) continue;  // uniform over the team
-      if (ttid == 0) s_occ_n[team] = 0;
       const uint32_t cap = table_cap<CAP>(m.d);
-      sync();
+      // Two team barriers per vertex: after the gather, and inside team_best
+      // (which also re-arms the occupancy count for the next vertex; the sweep
+      // has cleared the table by then).
       team_gather<MODE, W, WEIGHTED, Tab, kTeamU, DEDUP>(c, m.i, m.lo, 0, m.d, tab, cap, ttid, TEAM, pol, occ,
                                      &s_occ_n[team], fails);
       sync();
       Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n[team], ttid, TEAM);
-      b = team_best<TEAM>(b, s_red[team], ttid, bar);
-      int changed = 0;
+      b = team_best<TEAM>(b, s_red[team], ttid, bar, &s_occ_n[team]);
+      // Every thread holds b and m.cur, so every thread knows the move (the
+      // rule of apply_move_cur); thread 0 writes it.
+      const bool changed = b.k != kEmpty && (c.pick_less ? b.k < m.cur : b.k != m.cur);
       if (ttid == 0) {
-        changed = apply_move_cur<MODE>(c, m.i, b.k, m.cur) ? 1 : 0;
-        s_flag[team] = changed;
+        apply_move_cur<MODE>(c, m.i, b.k, m.cur);
         ++n_v;
         n_e += m.d;
         n_dn += changed;
         if (MODE == kAsync && changed && c.wake) n_w += m.d;
       }
-      sync();
-      changed = s_flag[team];
       if (MODE == kAsync && changed && c.wake)
         for (uint32_t e = ttid; e < m.d; e += TEAM)
           wake_vertex(c.flags, ld_stream(c.g.tgt + m.lo + e, pol));
-      sync();
     }
     if constexpr (TEAM > 32) sync();  // s_meta is rewritten by the next batch
   }
