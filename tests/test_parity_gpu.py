@@ -264,3 +264,16 @@ def test_wide_phase_buckets_sync_step(repeat):
         want, wc = O.port_sync_step(pg, lab, pl)
         got, gc = lp.sync_step(g, lab, pl)
         assert gc == wc and np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("kind,size", [("rmat", 13), ("web", 20000)])
+def test_sync_trajectory_table_first_pass(kind, size):
+    # Without the table-free identity pass, the Synchronous first pass runs every table
+    # tier from all-distinct labels (the team kernels' no-dedupe variant, the wide
+    # tier's phase buckets): still bit-exact.
+    dg, g = _device_graph(kind, size)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    want, ws = O.port_lpa(pg, exec_mode=2)
+    r = dg.lpa(lp.LpaConfig(exec=lp.ExecMode.Synchronous), lp.Tuning(identity_first=False))
+    assert np.array_equal(r.labels, want)
+    assert r.stats.delta_n_per_iter == ws["delta_n"]
