@@ -760,6 +760,9 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
 #ifndef NULPA_WIDE_LIMIT
 #define NULPA_WIDE_LIMIT 12288
 #endif
+#ifndef NULPA_WIDE_U
+#define NULPA_WIDE_U 4
+#endif
 constexpr uint32_t kWideLimit = NULPA_WIDE_LIMIT;  // distinct labels per phase (load <= 3/4)
 
 __device__ __forceinline__ uint32_t phase_of(uint32_t key, uint32_t P) {
@@ -798,7 +801,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
   for (uint32_t x = threadIdx.x; x < kClusterCap; x += blockDim.x) tab.clear_slot(x);  // once
   const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
-  constexpr int U = 4;
+  constexpr int U = NULPA_WIDE_U;  // gather rounds in flight per thread
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(c.work, kWideBatch);
     __syncthreads();
