@@ -181,7 +181,7 @@ def bench_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / len(timed), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": f"{desc} (bounded CPU sample of the {args.workload} "
                                    f"workload)", "n": g.order(), "m2": m2,
                        "iterations": timed[-1][1]["iterations"], "modularity": q},
