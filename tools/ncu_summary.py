@@ -29,9 +29,24 @@ def launches(path):
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "lts__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
            "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
-           "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
+           "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+           "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+           "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 STALLS = ["long_scoreboard", "short_scoreboard", "wait", "branch_resolving", "barrier",
           "mio_throttle", "lg_throttle", "membar", "no_instruction", "math_pipe_throttle"]
+
+
+def num(d, k):
+    try:
+        return float(d[k].replace(",", ""))
+    except (KeyError, ValueError):
+        return float("nan")
+
+
+def ratio(d, a, b):
+    den = num(d, b)
+    return num(d, a) / den if den else float("nan")
 
 
 def full(path):
@@ -42,7 +57,8 @@ def full(path):
     h, units, data = rows[0], rows[1], rows[2:]
     print(f"\n== ncu --set full ({path.split('/')[-1]})")
     print("kernel | ms | DRAM rd GB | DRAM wr GB | DRAM %peak | L2 hit % | warps active % | "
-          "issue active % | warp-inst (G) | top stalls (cycles per issue)")
+          "issue active % | warp-inst (G) | ld sectors/req | smem bank conflicts (G) | "
+          "top stalls (cycles per issue)")
     for r in data:
         d = dict(zip(h, r))
         u = dict(zip(h, units))
@@ -59,6 +75,8 @@ def full(path):
               f"{float(d['sm__warps_active.avg.pct_of_peak_sustained_active']):.1f} | "
               f"{float(d['smsp__issue_active.avg.pct_of_peak_sustained_active']):.1f} | "
               f"{float(d['smsp__inst_executed.sum']) / 1e9:.2f} | "
+              f"{ratio(d, 'l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum', 'l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum'):.2f} | "
+              f"{num(d, 'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum') / 1e9:.2f} | "
               + " ".join(f"{s}={v:.1f}" for v, s in st))
 
 
