@@ -9,6 +9,7 @@
 // synchronisation. elapsed_seconds covers the loop only (lpa.cpp:269,311),
 // measured with CUDA events.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -44,6 +45,15 @@ template <typename K>
 void allow_smem(K kernel, size_t bytes) {
   NULPA_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(bytes)));
+}
+
+// True once per device for each `done` mask (function attributes are set per device:
+// a process that runs on device 1 after device 0 must set them again).
+inline bool first_on_device(std::atomic<uint64_t>& done) {
+  int dev = 0;
+  NULPA_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  return (done.fetch_or(bit) & bit) == 0;
 }
 
 // Grid for a grid-stride kernel: enough CTAs for `work` items at `per_block`
@@ -101,8 +111,8 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
                  : k_team<MODE, W, WEIGHTED, 256, 256, kBlock2Cap, kBlock2Max, 0>;
   auto k_bg = dd ? k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, kDedupLater>
                  : k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, 0>;
-  static bool init = false;
-  if (!init) {
+  static std::atomic<uint64_t> init{0};
+  if (first_on_device(init)) {
     allow_smem(k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, kDedupLater>, wtab_smem);
     allow_smem(k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, 0>, wtab_smem);
     allow_smem(k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax, kDedupLater>, block_smem);
@@ -114,7 +124,6 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
     if constexpr (!WEIGHTED) allow_smem(k_wide<MODE, W>, wide_bytes());
     allow_smem(k_hub_accum<MODE, W, WEIGHTED>, hub_smem);
-    init = true;
   }
   int launches = 0;
   auto tier = [&](int t) {
@@ -192,7 +201,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
       k_wide<MODE, W><<<resident_grid(k_wide<MODE, W>, kBigThreads, wide_bytes(),
                                       p.count[T_CLUSTER], 1, sms),
                         kBigThreads, wide_bytes(), s>>>(c, p.list[T_CLUSTER], p.count[T_CLUSTER],
-                                                        c.fresh, p.wide_scratch);
+                                                        c.fresh, p.wide_scratch, p.wide_stride);
     prof.end(T_CLUSTER, s);
     ++launches;
   }
@@ -257,11 +266,8 @@ int long_rows_first_pass(const Plan& p, PassCtx c, unsigned long long* ctr, int 
 template <typename W, bool WEIGHTED>
 void launch_sequential(const PassCtx& c, void* gtab, cudaStream_t s) {
   constexpr size_t smem = kHubCap * Table<kPacked<WEIGHTED>, W>::kSlotBytes;
-  static bool init = false;
-  if (!init) {
-    allow_smem(k_sequential<W, WEIGHTED>, smem);
-    init = true;
-  }
+  static std::atomic<uint64_t> init{0};
+  if (first_on_device(init)) allow_smem(k_sequential<W, WEIGHTED>, smem);
   k_sequential<W, WEIGHTED><<<1, kBlockThreads, smem, s>>>(c, gtab);
   NULPA_CUDA(cudaGetLastError());
 }

@@ -417,9 +417,16 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
       for (int t = dev::T_THREAD; t <= dev::T_BLOCK; ++t) scramble_list(p->list[t], p->count[t], s, 5);
     }
 
-    // Wide tier (k_wide): one L2-resident row snapshot per resident CTA.
-    if (p->count[dev::T_CLUSTER] && !p->weighted)
-      p->wide_scratch = dalloc<uint32_t>(uint64_t(sm_count()) * dev::kWideScratch);
+    // Wide tier (k_wide): per resident CTA, room for the buckets of phases
+    // 1..kWideBuckets-1 of its longest possible row (or one in-order snapshot).
+    if (p->count[dev::T_CLUSTER] && !p->weighted) {
+      // (a non-empty wide tier means max_degree > kBigMax; anything else is stale)
+      const uint32_t dmax = g->max_degree > uint32_t(dev::kBigMax)
+                                ? std::min<uint32_t>(g->max_degree, dev::kClusterMax)
+                                : uint32_t(dev::kClusterMax);
+      p->wide_stride = (NULPA_WIDE_BUCKETS - 1) * dmax;
+      p->wide_scratch = dalloc<uint32_t>(uint64_t(sm_count()) * p->wide_stride);
+    }
     // Hub tier: per-hub global tables and (hub, chunk) work items. Hub counts
     // are small (vertices of degree > block_max), so the layout is built on
     // the host.

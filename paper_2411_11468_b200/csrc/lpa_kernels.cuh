@@ -783,10 +783,11 @@ constexpr size_t wide_bytes() {
 template <int MODE, typename W>
 __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32_t* __restrict__ list,
                                                          uint32_t count, int fresh,
-                                                         uint32_t* __restrict__ scratch) {
+                                                         uint32_t* __restrict__ scratch,
+                                                         uint32_t stride) {
   // This CTA's row snapshot: phase 0 of a multi-phase vertex gathers the labels
   // once and writes them here (L2-resident); later phases stream them back.
-  uint32_t* snap = scratch + size_t(blockIdx.x) * kWideScratch;
+  uint32_t* snap = scratch + size_t(blockIdx.x) * stride;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemTable<W> tab;
   tab.bind(smem_raw, kClusterCap);
