@@ -95,11 +95,15 @@ typedef struct nulpa_tuning {
                                  (k_first_pass; a legal schedule, all reads first) */
   uint32_t profile;           /* 1: time each tier with CUDA events (stats.tier_*) */
   uint32_t schedule;          /* ParallelAsync visit order inside each tier:
-                                 0 default (= 3), 1 position order (degree buckets,
+                                 0 default (= 4), 1 position order (degree buckets,
                                  largest first; ascending id inside a bucket), 2 the
                                  tiers up to block_max scrambled in 32-position blocks,
                                  3 only the register tiers (degree <= 32) scrambled in
-                                 32-position blocks, position order above.
+                                 32-position blocks, position order above, 4 as 3, but
+                                 when the thread tier holds at least half of the edges
+                                 (lattice / road-like graphs) each thread walks a
+                                 contiguous chunk of it in order, as the reference's
+                                 workers walk theirs.
                                  Any order is a valid asynchronous schedule;
                                  Synchronous/Sequential results do not depend on it. */
   uint32_t no_identity_first; /* 1: disable the table-free first pass from identity labels */

@@ -72,6 +72,12 @@ unsigned resident_grid(K kernel, int threads, size_t smem, uint64_t work, unsign
   return grid_for(work, per_block, static_cast<unsigned>(per_sm) * sms);
 }
 
+// Shortest chunk a CHUNKED thread-tier walk gives one thread (k_thread).
+#ifndef NULPA_MIN_CHUNK
+#define NULPA_MIN_CHUNK 32
+#endif
+constexpr unsigned kMinChunk = NULPA_MIN_CHUNK;
+
 // Optional per-tier CUDA-event timing (tuning.profile).
 struct Prof {
   bool on = false;
@@ -132,7 +138,13 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   };
   if (p.count[T_THREAD] && (tiers >> T_THREAD & 1u)) {
     tier(T_THREAD);
-    if (p.thread_max <= 8)
+    if (p.thread_max <= 8 && MODE == kAsync && p.chunked_thread)
+      // chunks of >= kMinChunk vertices per thread (a short chunk propagates little)
+      k_thread<MODE, W, WEIGHTED, 8, true>
+          <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, true>, 256, 0, p.count[T_THREAD],
+                           256 * kMinChunk, sms),
+             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+    else if (p.thread_max <= 8)
       k_thread<MODE, W, WEIGHTED, 8>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8>, 256, 0, p.count[T_THREAD], 256, sms),
              256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);

@@ -341,7 +341,7 @@ TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* t) {
   wmax = std::max<uint32_t>(std::min<uint32_t>(wmax, dev::kWarpTabMax), 32u);
   uint32_t bmax = (t && t->block_max_degree) ? t->block_max_degree : uint32_t(dev::kBlockMax);
   bmax = std::max<uint32_t>(std::min<uint32_t>(bmax, dev::kBlockMax), wmax);
-  const uint32_t sched = (t && t->schedule) ? t->schedule : 3u;  // default: see nulpa.h
+  const uint32_t sched = (t && t->schedule) ? t->schedule : 4u;  // default: see nulpa.h
   return {tmax, wmax, bmax, sched};
 }
 
@@ -406,6 +406,28 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
     // Scrambled visit order (ParallelAsync only: any interleaving is a valid
     // asynchronous schedule; Synchronous/Sequential results do not depend on it).
     // Tiers up to degree block_max are scrambled in 32-position blocks.
+    if (tb.schedule == 4 && p->count[dev::T_THREAD]) {
+      // Edges of the thread tier: when they are most of the graph, the tier is walked
+      // in contiguous chunks (k_thread CHUNKED) from an unscrambled list.
+      const uint32_t m = p->count[dev::T_THREAD];
+      auto degs = cub::TransformInputIterator<uint32_t, DegreeOf, const uint32_t*>(
+          p->list[dev::T_THREAD], DegreeOf{g->offsets});
+      unsigned long long* d_sum = dalloc<unsigned long long>(1);
+      size_t tb2 = 0;
+      NULPA_CUDA(cub::DeviceReduce::Sum(nullptr, tb2, degs, d_sum, m, s));
+      void* t2 = dmalloc(tb2);
+      NULPA_CUDA(cub::DeviceReduce::Sum(t2, tb2, degs, d_sum, m, s));
+      unsigned long long e = 0;
+      NULPA_CUDA(cudaMemcpyAsync(&e, d_sum, 8, cudaMemcpyDeviceToHost, s));
+      NULPA_CUDA(cudaStreamSynchronize(s));
+      dfree(t2);
+      dfree(d_sum);
+      p->chunked_thread = 2 * e >= g->m2;
+    }
+    if (tb.schedule == 4) {  // as 3, except a chunk-walked thread tier stays unscrambled
+      for (int t = p->chunked_thread ? dev::T_HALF : dev::T_THREAD; t <= dev::T_WARP; ++t)
+        scramble_list(p->list[t], p->count[t], s, 5);
+    }
     if (tb.schedule == 3) {  // the register tiers (<= 32) scrambled, position order above
       for (int t = dev::T_THREAD; t <= dev::T_WARP; ++t) scramble_list(p->list[t], p->count[t], s, 5);
     }

@@ -126,13 +126,19 @@ constexpr bool kPacked = !WEIGHTED;  // unit weights -> packed 64-bit slots
 
 // ---- tier: thread per vertex ---------------------------------------------------
 
-template <int MODE, typename W, bool WEIGHTED, int DMAX>
+// CHUNKED (ParallelAsync, schedule 4): thread k walks the contiguous list slice
+// [k*L, (k+1)*L) in order, as each of the reference's workers walks its chunk
+// (lpa.cpp:139-165), instead of the grid-stride interleave.
+template <int MODE, typename W, bool WEIGHTED, int DMAX, bool CHUNKED = false>
 __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __restrict__ list,
                                                 uint32_t count) {
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
   const uint64_t pol = policy_evict_first();
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t L = CHUNKED ? (count + stride - 1) / stride : 0u;
+  const uint32_t t_end = CHUNKED ? min(count, (tid + 1) * L) : count;
+  for (uint32_t t = CHUNKED ? tid * L : tid; t < t_end; t += CHUNKED ? 1u : stride) {
     const uint32_t i = __ldg(list + t);
     if (claim_vertex(c, i)) continue;
     const uint64_t lo = __ldg(c.g.off + i);

@@ -19,6 +19,9 @@ struct Plan {
   static constexpr int kLists = dev::T_HUB + 1;
   uint32_t* list[kLists] = {};
   uint32_t count[kLists] = {};
+  // Thread tier walked in contiguous chunks (ParallelAsync): schedule 4, chosen when
+  // the tier carries most of the graph's edges (lattice / road-like inputs).
+  bool chunked_thread = false;
   bool weighted = false;  // hub tables: packed 64-bit words (unit weights) or split
   // Hub tier.
   uint32_t n_hubs = 0, n_items = 0;

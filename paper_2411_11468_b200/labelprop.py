@@ -120,7 +120,7 @@ class Tuning:
     thread_max_degree: int = 0
     warp_max_degree: int = 0
     block_max_degree: int = 0
-    schedule: int = 0  # 0 default (= 3); 1 position order; 2/3 scrambled (see nulpa.h)
+    schedule: int = 0  # 0 default (= 4); 1 position order; 2/3 scrambled; 4 chunk walk (nulpa.h)
     profile: bool = False
     identity_first: bool = True  # table-free first pass from identity labels
     async_first_pass: int = 0  # 1: ParallelAsync pass 0 as the table-free synchronous pass
