@@ -277,3 +277,17 @@ def test_sync_trajectory_table_first_pass(kind, size):
     r = dg.lpa(lp.LpaConfig(exec=lp.ExecMode.Synchronous), lp.Tuning(identity_first=False))
     assert np.array_equal(r.labels, want)
     assert r.stats.delta_n_per_iter == ws["delta_n"]
+
+
+def test_async_lattice_converges():
+    # A lattice is all thread tier: the chunk-walked order (schedule 4) floods labels along
+    # id-contiguous runs as the reference's workers do, and converges; the grid-stride
+    # order drifts by one row per pass and stops unconverged at max_iterations.
+    dg = lp.DeviceGraph.grid(1024, 1024)
+    g = dg.download()
+    r = dg.lpa(lp.LpaConfig())
+    assert r.stats.converged and r.stats.iterations < 20
+    q = lp.modularity(g, r.labels)
+    assert q > 0.75, q
+    r3 = dg.lpa(lp.LpaConfig(), lp.Tuning(schedule=3))
+    assert lp.modularity(g, r3.labels) < q
