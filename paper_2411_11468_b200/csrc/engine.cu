@@ -887,6 +887,11 @@ struct HostGraph {
     const int rc = nulpa_graph_upload(csr, device, &g);
     if (rc != NULPA_OK) throw Error(rc, nulpa_last_error());
   }
+  // lpa(): the run's plan is built while the targets cross PCIe.
+  HostGraph(const nulpa_csr* csr, const nulpa_opts& o, const nulpa_tuning* tuning) {
+    const TierBounds tb = resolve_tiers(o.switch_degree, tuning);
+    g = upload_graph(csr, o.device, &tb, o.precision == 64 ? 8 : 4);
+  }
   ~HostGraph() {
     if (g) nulpa_graph_free(g);
   }
@@ -942,7 +947,7 @@ int nulpa_run(const nulpa_csr* csr, const nulpa_opts* opts, const nulpa_tuning* 
     probe.n = csr->n;
     validate_opts(&probe, *opts);
     Trace tr("nulpa_run");
-    HostGraph hg(csr, opts->device);
+    HostGraph hg(csr, *opts, tuning);
     tr.mark("upload");
     run_lpa(hg.g, *opts, tuning, labels_out, nullptr, stats);
     tr.mark("run_lpa");

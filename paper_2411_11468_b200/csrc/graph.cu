@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -537,6 +538,58 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
 
 using namespace nulpa;
 
+namespace nulpa {
+nulpa_graph* upload_graph(const nulpa_csr* csr, int device, const TierBounds* tb,
+                          int value_bytes) {
+  check_host_csr(csr);
+  use_device(device);
+  auto* g = new nulpa_graph();
+  try {
+    g->device = device;
+    g->n = csr->n;
+    g->m2 = csr->m2;
+    g->owns = true;
+    if (can_upload_pipelined(csr)) {
+      std::function<void()> plan_now;
+      if (tb)
+        plan_now = [&] {
+          cudaStream_t sp = nullptr;
+          NULPA_CUDA(cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking));
+          try {
+            get_plan(g, *tb, value_bytes, sp);
+          } catch (...) {
+            cudaStreamDestroy(sp);
+            throw;
+          }
+          cudaStreamDestroy(sp);
+        };
+      upload_pipelined(csr, g, plan_now);
+      // a weight array dropped as all-unit after the plan was built: plan again later
+      if (g->plan && g->plan->weighted != (g->weights != nullptr)) {
+        delete g->plan;
+        g->plan = nullptr;
+      }
+      return g;
+    }
+    g->offsets = dalloc<uint64_t>(uint64_t(csr->n) + 1);
+    g->targets = dalloc<uint32_t>(csr->m2);
+    NULPA_CUDA(cudaMemcpy(g->offsets, csr->offsets, (uint64_t(csr->n) + 1) * 8,
+                          cudaMemcpyHostToDevice));
+    if (csr->m2)
+      NULPA_CUDA(cudaMemcpy(g->targets, csr->targets, csr->m2 * 4, cudaMemcpyHostToDevice));
+    if (csr->weights && csr->m2) {
+      g->weights = dalloc<float>(csr->m2);
+      NULPA_CUDA(cudaMemcpy(g->weights, csr->weights, csr->m2 * 4, cudaMemcpyHostToDevice));
+    }
+    finalize_graph(g, 0);
+  } catch (...) {
+    nulpa_graph_free(g);
+    throw;
+  }
+  return g;
+}
+}  // namespace nulpa
+
 extern "C" {
 
 const char* nulpa_last_error(void) { return nulpa::last_error().c_str(); }
@@ -555,37 +608,11 @@ int nulpa_device_count(int* count) {
   });
 }
 
+
 int nulpa_graph_upload(const nulpa_csr* csr, int device, nulpa_graph** out) {
   return guarded([&] {
-    check_host_csr(csr);
-    use_device(device);
-    auto* g = new nulpa_graph();
-    try {
-      g->device = device;
-      g->n = csr->n;
-      g->m2 = csr->m2;
-      g->owns = true;
-      if (can_upload_pipelined(csr)) {
-        upload_pipelined(csr, g);
-        *out = g;
-        return;
-      }
-      g->offsets = dalloc<uint64_t>(uint64_t(csr->n) + 1);
-      g->targets = dalloc<uint32_t>(csr->m2);
-      NULPA_CUDA(cudaMemcpy(g->offsets, csr->offsets, (uint64_t(csr->n) + 1) * 8,
-                            cudaMemcpyHostToDevice));
-      if (csr->m2)
-        NULPA_CUDA(cudaMemcpy(g->targets, csr->targets, csr->m2 * 4, cudaMemcpyHostToDevice));
-      if (csr->weights && csr->m2) {
-        g->weights = dalloc<float>(csr->m2);
-        NULPA_CUDA(cudaMemcpy(g->weights, csr->weights, csr->m2 * 4, cudaMemcpyHostToDevice));
-      }
-      finalize_graph(g, 0);
-    } catch (...) {
-      nulpa_graph_free(g);
-      throw;
-    }
-    *out = g;
+    if (!out) throw Error(NULPA_EINVAL, "null argument");
+    *out = upload_graph(csr, device);
   });
 }
 

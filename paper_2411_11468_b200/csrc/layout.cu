@@ -373,7 +373,8 @@ struct ToDoubleW {
 // ~256 MB on one stream while the previous chunk is validated and scattered into
 // position order on another, so the relayout and the structural checks hide behind
 // the PCIe transfer.
-void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g) {
+void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g,
+                      const std::function<void()>& while_streaming) {
   // Entries per staging buffer (NULPA_UPLOAD_CHUNK overrides it: the tests force
   // many small chunks and rows longer than a chunk).
   uint64_t kChunk = 64ull << 20;
@@ -528,6 +529,7 @@ void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g) {
         NULPA_CUDA(cudaEventRecord(freed[b], sb));
         v_a = v_b;
       }
+      if (while_streaming) while_streaming();
     }
     unsigned long long desc = 0;
     NULPA_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, sb));

@@ -80,4 +80,9 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
 
 int sm_count();
 
+// Host CSR -> resident graph (nulpa_graph_upload). With `tb`, the plan for
+// (tb, value_bytes) is built while the targets stream in (nulpa_run).
+nulpa_graph* upload_graph(const nulpa_csr* csr, int device, const TierBounds* tb = nullptr,
+                          int value_bytes = 4);
+
 }  // namespace nulpa
