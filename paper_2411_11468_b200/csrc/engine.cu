@@ -129,7 +129,8 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     allow_smem(k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, 0>, big_smem);
     allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
     if constexpr (!WEIGHTED) allow_smem(k_wide<MODE, W>, wide_bytes());
-    allow_smem(k_hub_accum<MODE, W, WEIGHTED>, hub_smem);
+    allow_smem(k_hub_accum<MODE, W, WEIGHTED, 1>, hub_smem);
+    allow_smem(k_hub_accum<MODE, W, WEIGHTED, 0>, hub_smem);
   }
   int launches = 0;
   auto tier = [&](int t) {
@@ -221,10 +222,13 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     tier(T_HUB);
     const HubCtx h = p.hub_ctx();
     const unsigned gi =
-        resident_grid(k_hub_accum<MODE, W, WEIGHTED>, kBlockThreads, hub_smem, p.n_items, 1, sms);
+        resident_grid(k_hub_accum<MODE, W, WEIGHTED, 1>, kBlockThreads, hub_smem, p.n_items, 1, sms);
     const unsigned gh = grid_for(p.n_hubs, 256, 1024);
     k_hub_select<MODE><<<gh, 256, 0, s>>>(c, h);
-    k_hub_accum<MODE, W, WEIGHTED><<<gi, kBlockThreads, hub_smem, s>>>(c, h);
+    if (c.fresh)  // first pass: labels mostly distinct, no in-warp dedupe (see k_team)
+      k_hub_accum<MODE, W, WEIGHTED, 0><<<gi, kBlockThreads, hub_smem, s>>>(c, h);
+    else
+      k_hub_accum<MODE, W, WEIGHTED, 1><<<gi, kBlockThreads, hub_smem, s>>>(c, h);
     const unsigned gs = grid_for(p.n_sitems, 1, sms * 8);
     k_hub_sweep<W, WEIGHTED><<<gs, kBlockThreads, 0, s>>>(h);
     launches += 3;

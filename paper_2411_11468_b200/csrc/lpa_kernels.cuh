@@ -1048,7 +1048,7 @@ __device__ __forceinline__ void bind_hub_table(Tab& g, const HubCtx& h, uint32_t
 // then flush each distinct label once into the hub's global table; newly
 // claimed global slots are appended to the hub's occupied list (one atomic per
 // warp).
-template <int MODE, typename W, bool WEIGHTED>
+template <int MODE, typename W, bool WEIGHTED, int DEDUP = 1>
 __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h) {
   using Tab = std::conditional_t<kPacked<WEIGHTED>, SmemTable<W>, Table<false, W>>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1073,14 +1073,51 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h
     const uint32_t cap = kHubCap;
     if (threadIdx.x == 0) s_occ_n = 0;
     __syncthreads();
-    team_gather<MODE, W, WEIGHTED>(c, i, lo, e0, e1, tab, cap, threadIdx.x, blockDim.x, pol,
-                                   socc, &s_occ_n, fails);
+    team_gather<MODE, W, WEIGHTED, Tab, kTeamU, DEDUP>(c, i, lo, e0, e1, tab, cap, threadIdx.x,
+                                                      blockDim.x, pol, socc, &s_occ_n, fails);
     __syncthreads();
     Table<kPacked<WEIGHTED>, W> g;  // the hub's global table (swept densely, k_hub_sweep)
     bind_hub_table<Table<kPacked<WEIGHTED>, W>, W, kPacked<WEIGHTED>>(g, h, x);
     const uint32_t gcap = h.tab_cap[x];
     const uint32_t n_occ = s_occ_n;
-    for (uint32_t p = threadIdx.x; p < n_occ; p += blockDim.x) {
+    uint32_t p0 = 0;
+    if constexpr (kPacked<WEIGHTED>) {
+      // Packed (unit-weight) tables: kFlushU claims in flight per thread. Each is a
+      // CAS of (key, count) into the label's first slot, which either claims it or
+      // returns the resident key (then one fire-and-forget add); only a collision
+      // takes the probe walk.
+      constexpr uint32_t kFlushU = 4;
+      const uint32_t mask = gcap - 1;
+      for (; p0 + kFlushU * blockDim.x <= n_occ; p0 += kFlushU * blockDim.x) {
+        uint32_t sl[kFlushU], key[kFlushU], cnt[kFlushU];
+        unsigned long long old[kFlushU];
+#pragma unroll
+        for (uint32_t u = 0; u < kFlushU; ++u) {
+          sl[u] = socc[p0 + u * blockDim.x + threadIdx.x];
+          VBits<W> vb;
+          tab.read(sl[u], key[u], vb);
+          cnt[u] = static_cast<uint32_t>(tab.value(sl[u]));
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < kFlushU; ++u)
+          old[u] = atomicCAS(g.w + (hash_start(key[u], gcap) & mask), kEmptyWord,
+                             (static_cast<unsigned long long>(key[u]) << 32) | cnt[u]);
+#pragma unroll
+        for (uint32_t u = 0; u < kFlushU; ++u) {
+          if (old[u] != kEmptyWord) {
+            if (static_cast<uint32_t>(old[u] >> 32) == key[u]) {
+              atomicAdd(g.w + (hash_start(key[u], gcap) & mask),
+                        static_cast<unsigned long long>(cnt[u]));
+            } else {
+              uint32_t gslot;
+              if (g.add(gcap, c.strategy, key[u], W(cnt[u]), &gslot) == 0) ++fails;
+            }
+          }
+          tab.clear_slot(sl[u]);
+        }
+      }
+    }
+    for (uint32_t p = p0 + threadIdx.x; p < n_occ; p += blockDim.x) {
       const uint32_t sl = socc[p];
       uint32_t k;
       VBits<W> vb;
