@@ -1048,6 +1048,9 @@ __device__ __forceinline__ void bind_hub_table(Tab& g, const HubCtx& h, uint32_t
 // then flush each distinct label once into the hub's global table; newly
 // claimed global slots are appended to the hub's occupied list (one atomic per
 // warp).
+#ifndef NULPA_FLUSH_U
+#define NULPA_FLUSH_U 4
+#endif
 template <int MODE, typename W, bool WEIGHTED, int DEDUP = 1>
 __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h) {
   using Tab = std::conditional_t<kPacked<WEIGHTED>, SmemTable<W>, Table<false, W>>;
@@ -1086,7 +1089,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h
       // CAS of (key, count) into the label's first slot, which either claims it or
       // returns the resident key (then one fire-and-forget add); only a collision
       // takes the probe walk.
-      constexpr uint32_t kFlushU = 4;
+      constexpr uint32_t kFlushU = NULPA_FLUSH_U;
       const uint32_t mask = gcap - 1;
       for (; p0 + kFlushU * blockDim.x <= n_occ; p0 += kFlushU * blockDim.x) {
         uint32_t sl[kFlushU], key[kFlushU], cnt[kFlushU];
