@@ -291,3 +291,69 @@ def test_async_lattice_converges():
     assert q > 0.75, q
     r3 = dg.lpa(lp.LpaConfig(), lp.Tuning(schedule=3))
     assert lp.modularity(g, r3.labels) < q
+
+
+def _hub_graph(seed=11, n=160000, hubs=3, hub_deg=120000, extra=400000):
+    """Hubs above the wide tier (degree > 98304) sharing leaves, plus random edges so the
+    leaves carry a spread of labels: every hub row has many distinct and repeated labels."""
+    rng = np.random.default_rng(seed)
+    u, v = [], []
+    for h in range(hubs):
+        leaves = rng.choice(np.arange(hubs, n), hub_deg, replace=False)
+        u.append(np.full(hub_deg, h, np.uint32))
+        v.append(leaves.astype(np.uint32))
+    a = rng.integers(hubs, n, extra).astype(np.uint32)
+    b = rng.integers(hubs, n, extra).astype(np.uint32)
+    u.append(a)
+    v.append(b)
+    u, v = np.concatenate(u), np.concatenate(v)
+    keep = u != v
+    el = lp.EdgeList(u[keep], v[keep], np.ones(int(keep.sum())), n)
+    g = lp.build_csr(el, True)  # (duplicates merge into weight 2: dropped, unit weights)
+    return lp.CsrGraph(g.offsets, g.targets, None)
+
+
+@pytest.mark.parametrize("labels", ["identity", "random", "few"])
+def test_hub_tier_sync_step_bit_exact(labels):
+    # The hub tier (shared pre-aggregation, the batched CAS-first flush into the global
+    # tables, the dense sweep) against the C restatement, with and without Pick-Less.
+    g = _hub_graph()
+    assert int(np.diff(g.offsets.astype(np.int64)).max()) > 98304
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    n = g.order()
+    rng = np.random.default_rng(5)
+    lab = {"identity": np.arange(n, dtype=np.uint32),
+           "random": rng.integers(0, n, n).astype(np.uint32),
+           "few": (rng.integers(0, 50, n) * 997).astype(np.uint32)}[labels]
+    for pl in (0, 1):
+        want, wc = O.port_sync_step(pg, lab, pl)
+        got, gc = lp.sync_step(g, lab, pl)
+        assert gc == wc and np.array_equal(got, want)
+
+
+def test_hub_tier_sync_trajectory_bit_exact():
+    g = _hub_graph(seed=12)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    want, ws = O.port_lpa(pg, exec_mode=2)
+    for tuning in (None, lp.Tuning(identity_first=False)):
+        r = lp.lpa(g, lp.LpaConfig(exec=lp.ExecMode.Synchronous), tuning)
+        assert np.array_equal(r.labels, want)
+        assert r.stats.delta_n_per_iter == ws["delta_n"]
+
+
+def test_hub_tier_weighted_sync_step_bit_exact():
+    # The same hubs with the merged duplicate weights kept (2.0 where an edge was listed
+    # twice): the split-table (weighted) hub path.
+    g0 = _hub_graph(seed=13)
+    # symmetric weights, w(u,v) = w(v,u): 2.0 on a hashed fifth of the edge pairs
+    u = np.repeat(np.arange(g0.order(), dtype=np.uint64), np.diff(g0.offsets.astype(np.int64)))
+    v = g0.targets.astype(np.uint64)
+    key = np.minimum(u, v) * np.uint64(1000003) + np.maximum(u, v)
+    w = np.where((key * np.uint64(2654435761)) % np.uint64(5) == 0, 2.0, 1.0).astype(np.float32)
+    g = lp.CsrGraph(g0.offsets, g0.targets, w)
+    pg = O.PortGraph(g.offsets, g.targets, g.weights)
+    lab = np.arange(g.order(), dtype=np.uint32)
+    for pl in (0, 1):
+        want, wc = O.port_sync_step(pg, lab, pl)
+        got, gc = lp.sync_step(g, lab, pl)
+        assert gc == wc and np.array_equal(got, want)
