@@ -357,3 +357,26 @@ def test_hub_tier_weighted_sync_step_bit_exact():
         want, wc = O.port_sync_step(pg, lab, pl)
         got, gc = lp.sync_step(g, lab, pl)
         assert gc == wc and np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("leaves", [7000, 30000])
+def test_wide_tier_weighted_sync_step_bit_exact(leaves):
+    # Weighted rows of the wide-tier degrees run the 8-CTA cluster kernel (k_cluster,
+    # the table spread over the cluster's shared memories): a weighted star whose leaves
+    # carry 40 labels with non-integer weights.
+    n = leaves + 1
+    off = np.zeros(n + 1, np.uint64)
+    off[1] = leaves
+    off[2:] = leaves + np.arange(1, leaves + 1, dtype=np.uint64)
+    tgt = np.concatenate([np.arange(1, n, dtype=np.uint32), np.zeros(leaves, np.uint32)])
+    rng = np.random.default_rng(leaves)
+    wl = (rng.integers(1, 8, leaves) * 0.375).astype(np.float32)
+    w = np.concatenate([wl, wl])
+    g = lp.CsrGraph(off, tgt, w)
+    pg = O.PortGraph(off, tgt, w)
+    lab = (rng.integers(0, 40, n) * 13 + 1).astype(np.uint32)
+    lab[0] = 0
+    for pl in (0, 1):
+        want, wc = O.port_sync_step(pg, lab, pl)
+        got, gc = lp.sync_step(g, lab, pl)
+        assert gc == wc and np.array_equal(got, want)
