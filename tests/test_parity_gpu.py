@@ -380,3 +380,13 @@ def test_wide_tier_weighted_sync_step_bit_exact(leaves):
         want, wc = O.port_sync_step(pg, lab, pl)
         got, gc = lp.sync_step(g, lab, pl)
         assert gc == wc and np.array_equal(got, want)
+
+
+def test_sequential_with_hub_rows_bit_exact():
+    # Sequential mode's in-order CTA walk with rows beyond the shared table (its global
+    # table path), on a smaller hub graph.
+    g = _hub_graph(seed=14, n=40000, hubs=2, hub_deg=30000, extra=60000)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    want, ws = O.port_lpa(pg, exec_mode=1)
+    r = lp.lpa(g, lp.LpaConfig(exec=lp.ExecMode.Sequential))
+    assert np.array_equal(r.labels, want) and r.stats.delta_n_per_iter == ws["delta_n"]
