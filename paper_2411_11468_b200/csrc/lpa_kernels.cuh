@@ -1045,9 +1045,8 @@ __device__ __forceinline__ void bind_hub_table(Tab& g, const HubCtx& h, uint32_t
 }
 
 // Accumulate one (hub, chunk) item: pre-aggregate the chunk in shared memory,
-// then flush each distinct label once into the hub's global table; newly
-// claimed global slots are appended to the hub's occupied list (one atomic per
-// warp).
+// then flush each distinct label once into the hub's global table (swept densely
+// afterwards by k_hub_sweep).
 #ifndef NULPA_FLUSH_U
 #define NULPA_FLUSH_U 4
 #endif
