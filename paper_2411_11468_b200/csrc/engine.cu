@@ -12,7 +12,10 @@
 #include <atomic>
 #include <chrono>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -62,12 +65,26 @@ inline bool first_on_device(std::atomic<uint64_t>& done) {
 template <typename K>
 unsigned resident_grid(K kernel, int threads, size_t smem, uint64_t work, unsigned per_block,
                        int sms) {
+  // Occupancy is a property of (kernel, block, smem) on this architecture: query it once
+  // (the query costs microseconds per launch, which small graphs feel).
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t>, int> cache;
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), threads, smem);
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) !=
-          cudaSuccess ||
-      per_sm < 1) {
-    (void)cudaGetLastError();
-    per_sm = 1;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) per_sm = it->second;
+  }
+  if (per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) !=
+            cudaSuccess ||
+        per_sm < 1) {
+      (void)cudaGetLastError();
+      per_sm = 1;
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    cache[key] = per_sm;
   }
   return grid_for(work, per_block, static_cast<unsigned>(per_sm) * sms);
 }
