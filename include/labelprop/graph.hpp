@@ -5,9 +5,10 @@
 // weights f32[m2], total weight 2m as double), so code compiled against either
 // header can hand its graph to nulpa's labelprop::lpa. The constructor and
 // weighted_degree are defined in paper_2411_11468_b200/csrc/dropin.cpp with the
-// reference's validation message (graph.cpp:165-178). load_graph, build_csr and
-// write_edge_list (graph.cpp:18-161,180-325) are restated in loaders.cpp (host
-// parsing) and build_csr.cu (the CSR built on the device, bit-exact).
+// reference's validation message (graph.cpp:165-178). load_graph and
+// write_edge_list (graph.cpp:18-161,180-184,309-325) are implemented in textio.cpp
+// (chunk-parallel parsing of the mapped file, the reference's messages); build_csr
+// (graph.cpp:186-307) in build_csr.cu (the CSR built on the device, bit-exact).
 #pragma once
 
 #include <cstdint>

@@ -268,6 +268,15 @@ int nulpa_graph_from_edge_list(const uint32_t* u, const uint32_t* v, const doubl
                                nulpa_graph** out);
 /* load_graph + build_csr. */
 int nulpa_graph_load(const char* path, int format, int symmetrize, int device, nulpa_graph** out);
+/* labelprop::write_edge_list (graph.hpp:112, graph.cpp:309-325): `u v w` once per
+ * undirected edge (u <= v), same bytes and messages. weights NULL = unit. */
+int nulpa_write_edge_list(const char* path, const nulpa_csr* csr);
+/* labelprop::write_membership (io.hpp:12, io.cpp:9-14): `vertex<TAB>label` lines, the
+ * text formatted on `device` from host labels[n]. */
+int nulpa_write_membership(const char* path, const uint32_t* labels, uint64_t n, int device);
+/* labelprop::read_membership (io.hpp:19, io.cpp:16-56): labels[n] from the TSV; same
+ * checks, messages and error kinds (NULPA_EFORMAT / NULPA_EINVAL). */
+int nulpa_read_membership(const char* path, uint32_t n, uint32_t* labels);
 
 /* ---- pass-level sessions: the partitioned multi-GPU path --------
  * A session runs single passes over the POSITION range [v_begin, v_end) of a

@@ -214,6 +214,9 @@ def ref() -> C.CDLL:
                                             C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             ("ref_modularity_oracle", C.c_int, [vp, vp, C.POINTER(C.c_double)]),
             ("ref_hardware_concurrency", C.c_uint32, []),
+            ("ref_write_edge_list", C.c_int, [vp, C.c_char_p]),
+            ("ref_write_membership", C.c_int, [C.c_char_p, vp, C.c_uint64]),
+            ("ref_read_membership", C.c_int, [C.c_char_p, C.c_uint32, vp]),
         ]:
             f = getattr(L, name)
             f.restype = res
@@ -357,6 +360,65 @@ def ref_load_graph(path, fmt):
     w = np.empty(ne, np.float64)
     ref().ref_load_graph(str(path).encode(), fmt, ne, _p(u), _p(v), _p(w), C.byref(nd))
     return u, v, w, nd.value
+
+
+# The reference's ofstream writers crash once numpy's bundled runtime libraries are in the
+# process (a libstdc++/libgfortran interaction, reproducible with ctypes alone), so they
+# run in a child interpreter that loads only ctypes.
+_WRITER = r"""
+import ctypes as C, sys
+L = C.CDLL(sys.argv[1])
+def load(path, ct):
+    raw = open(path, "rb").read()
+    return (ct * (len(raw) // C.sizeof(ct))).from_buffer_copy(raw)
+L.ref_last_error.restype = C.c_char_p
+if sys.argv[2] == "edges":
+    o, t, w = load(sys.argv[3], C.c_uint64), load(sys.argv[4], C.c_uint32), load(sys.argv[5], C.c_float)
+    L.ref_graph_from_csr.restype = C.c_void_p
+    g = C.c_void_p(L.ref_graph_from_csr(o, t, w, C.c_uint32(len(o) - 1), C.c_uint64(len(t))))
+    rc = L.ref_write_edge_list(g, sys.argv[6].encode())
+else:
+    lab = load(sys.argv[3], C.c_uint32)
+    rc = L.ref_write_membership(sys.argv[4].encode(), lab, C.c_uint64(len(lab)))
+if rc:
+    sys.stderr.write(L.ref_last_error().decode()); sys.exit(3)
+"""
+
+
+def _run_writer(*args):
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, "-c", _WRITER, str(REF_LIB), *map(str, args)],
+                       capture_output=True, text=True)
+    if r.returncode:
+        raise ValueError(r.stderr.strip() or f"reference writer failed ({r.returncode})")
+
+
+def ref_write_edge_list(g: "RefGraph", path):
+    """labelprop_ref::write_edge_list (graph.cpp:309-325)."""
+    import tempfile
+    o, t, w = g.arrays()
+    with tempfile.TemporaryDirectory() as d:
+        files = [f"{d}/{k}.bin" for k in "otw"]
+        for f, a in zip(files, (o, t, w)):
+            a.tofile(f)
+        _run_writer("edges", *files, path)
+
+
+def ref_write_membership(path, labels):
+    """labelprop_ref::write_membership (io.cpp:9-14)."""
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        _u32(labels).tofile(f"{d}/l.bin")
+        _run_writer("membership", f"{d}/l.bin", path)
+
+
+def ref_read_membership(path, n):
+    """labelprop_ref::read_membership (io.cpp:16-56), or ValueError('F:..'/'V:..')."""
+    out = np.zeros(n, np.uint32)
+    if ref().ref_read_membership(str(path).encode(), n, _p(out)) != 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return out
 
 
 def ref_planted_edges(n, communities, p_in, p_out, seed):

@@ -27,6 +27,7 @@
 #include "labelprop/graph.hpp"
 #include "labelprop/hashtable.hpp"
 #include "labelprop/lpa.hpp"
+#include "labelprop/io.hpp"
 #include "labelprop/quality.hpp"
 #include "support/oracles.hpp"  // reference test oracles (tests/support/oracles.hpp)
 
@@ -146,6 +147,42 @@ REF_API int64_t ref_load_graph(const char* path, int format, uint64_t cap, uint3
     g_err = std::string("E:") + e.what();
   }
   return -1;
+}
+
+namespace {
+// Run an I/O call; 0 on success, -1 with "F:"/"V:"/"E:" + message in ref_last_error.
+template <typename F>
+int io_guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const FormatError& e) {
+    g_err = std::string("F:") + e.what();
+  } catch (const ValidationError& e) {
+    g_err = std::string("V:") + e.what();
+  } catch (const std::exception& e) {
+    g_err = std::string("E:") + e.what();
+  }
+  return -1;
+}
+}  // namespace
+
+// write_edge_list(g, path)  graph.cpp:309-325
+REF_API int ref_write_edge_list(void* h, const char* path) {
+  return io_guard([&] { write_edge_list(*static_cast<CsrGraph*>(h), path); });
+}
+
+// write_membership(path, labels)  io.cpp:9-14
+REF_API int ref_write_membership(const char* path, const uint32_t* labels, uint64_t n) {
+  return io_guard([&] { write_membership(path, std::span<const VertexId>(labels, n)); });
+}
+
+// read_membership(path, n)  io.cpp:16-56
+REF_API int ref_read_membership(const char* path, uint32_t n, uint32_t* labels) {
+  return io_guard([&] {
+    auto l = read_membership(path, n);
+    std::copy(l.begin(), l.end(), labels);
+  });
 }
 
 // planted_partition(...)  generators.cpp:45-88, then build_csr(symmetrize)

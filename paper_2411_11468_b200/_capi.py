@@ -125,6 +125,9 @@ _SIGS = {
     "nulpa_graph_from_edge_list": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
                                              C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "nulpa_graph_load": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "nulpa_write_edge_list": (C.c_int, [C.c_char_p, C.POINTER(nulpa_csr)]),
+    "nulpa_write_membership": (C.c_int, [C.c_char_p, C.c_void_p, C.c_uint64, C.c_int]),
+    "nulpa_read_membership": (C.c_int, [C.c_char_p, C.c_uint32, C.c_void_p]),
     "nulpa_session_create": (C.c_int, [C.c_void_p, C.POINTER(nulpa_opts),
                                        C.POINTER(nulpa_tuning), C.c_uint32, C.c_uint32,
                                        C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),

@@ -55,7 +55,7 @@ int device_from_env() {
 
 }  // namespace
 
-// load_graph (graph.cpp:180-184) over nulpa_load_edge_list (loaders.cpp).
+// load_graph (graph.cpp:180-184) over nulpa_load_edge_list (textio.cpp).
 EdgeList load_graph(const std::string& path, FileFormat format) {
   nulpa_edge_list el{};
   const int rc = nulpa_load_edge_list(
@@ -97,23 +97,11 @@ CsrGraph build_csr(const EdgeList& el, bool symmetrize) {
   return CsrGraph(std::move(off), std::move(tgt), std::move(wt));
 }
 
-// write_edge_list (graph.cpp:309-325): host output, same text.
+// write_edge_list (graph.cpp:309-325) over nulpa_write_edge_list (textio.cpp).
 void write_edge_list(const CsrGraph& g, const std::string& path) {
-  std::ofstream out(path);
-  if (!out) throw ValidationError("cannot open output file: " + path);
-  out << "% undirected weighted edge list: u v w (each edge once, u <= v)\n";
-  out << "% vertices " << g.order() << '\n';
-  char buf[64];
-  for (VertexId i = 0; i < g.order(); ++i) {
-    auto nbrs = g.neighbors(i);
-    auto ws = g.edge_weights(i);
-    for (std::size_t p = 0; p < nbrs.size(); ++p) {
-      if (nbrs[p] < i) continue;  // u <= v once; self-loops included
-      auto r = std::to_chars(buf, buf + sizeof buf, ws[p]);
-      out << i << ' ' << nbrs[p] << ' ' << std::string_view(buf, r.ptr - buf) << '\n';
-    }
-  }
-  if (!out) throw ValidationError("failed writing " + path);
+  const nulpa_csr c = view(g);
+  const int rc = nulpa_write_edge_list(path.c_str(), &c);
+  if (rc != NULPA_OK) raise(rc);
 }
 
 CsrGraph::CsrGraph(std::vector<std::uint64_t> offsets, std::vector<VertexId> targets,
@@ -229,51 +217,17 @@ CommunityStats community_stats(const CsrGraph& g, std::span<const VertexId> labe
   return st;
 }
 
-// write_membership / read_membership (io.cpp:9-56): host I/O, the reference's messages.
+// write_membership (io.cpp:9-14): the text is formatted on the device (textout.cu).
 void write_membership(const std::string& path, std::span<const VertexId> labels) {
-  std::ofstream out(path);
-  if (!out) throw ValidationError("cannot open output file: " + path);
-  for (std::size_t i = 0; i < labels.size(); ++i) out << i << '\t' << labels[i] << '\n';
-  if (!out) throw ValidationError("failed writing " + path);
+  const int rc = nulpa_write_membership(path.c_str(), labels.data(), labels.size(), device_from_env());
+  if (rc != NULPA_OK) raise(rc);
 }
 
+// read_membership (io.cpp:16-56): chunk-parallel parse of the mapped file (textio.cpp).
 std::vector<VertexId> read_membership(const std::string& path, std::uint32_t n) {
-  std::ifstream in(path);
-  if (!in) throw ValidationError("cannot open membership file: " + path);
-  std::vector<VertexId> labels(n, 0);
-  std::vector<std::uint8_t> seen(n, 0);
-  std::string line;
-  for (std::size_t lineno = 1; std::getline(in, line); ++lineno) {
-    std::size_t a = 0;
-    auto skip_ws = [&] {
-      while (a < line.size() && std::isspace(static_cast<unsigned char>(line[a]))) ++a;
-    };
-    skip_ws();
-    if (a == line.size() || line[a] == '#' || line[a] == '%') continue;
-    const std::string where = path + ":" + std::to_string(lineno) + ": ";
-    std::uint64_t field[2] = {0, 0};
-    for (auto& f : field) {
-      auto [p, ec] = std::from_chars(line.data() + a, line.data() + line.size(), f);
-      if (ec != std::errc() || p == line.data() + a)
-        throw FormatError(where + "expected 'vertex<TAB>label'");
-      a = static_cast<std::size_t>(p - line.data());
-      skip_ws();
-    }
-    if (a != line.size()) throw FormatError(where + "trailing content after label");
-    const std::uint64_t vertex = field[0], label = field[1];
-    if (vertex >= n)
-      throw ValidationError(where + "vertex " + std::to_string(vertex) + " out of range for n=" +
-                            std::to_string(n));
-    if (label >= n)
-      throw ValidationError(where + "label " + std::to_string(label) + " out of range for n=" +
-                            std::to_string(n));
-    if (seen[vertex])
-      throw ValidationError(where + "vertex " + std::to_string(vertex) + " assigned twice");
-    seen[vertex] = 1;
-    labels[vertex] = static_cast<VertexId>(label);
-  }
-  for (std::uint32_t i = 0; i < n; ++i)
-    if (!seen[i]) throw ValidationError(path + ": no label for vertex " + std::to_string(i));
+  std::vector<VertexId> labels(n);
+  const int rc = nulpa_read_membership(path.c_str(), n, labels.data());
+  if (rc != NULPA_OK) raise(rc);
   return labels;
 }
 

@@ -92,7 +92,6 @@ class LpaResult:
     stats: RunStats
 
 
-@dataclass
 class FileFormat(IntEnum):
     """labelprop::FileFormat (graph.hpp:86)."""
     MatrixMarket = 0
@@ -319,47 +318,26 @@ def delta_modularity(m: float, ki: float, ki_to_c: float, ki_to_d: float, sigma_
     return (ki_to_c - ki_to_d) / m - ki * (ki + sigma_c - sigma_d) / (2.0 * m * m)
 
 
-def write_membership(path, labels) -> None:
-    """labelprop::write_membership (io.cpp:9-14): `vertex<TAB>label` per line."""
-    lab = np.asarray(labels)
-    try:
-        with open(path, "w") as f:
-            f.writelines(f"{i}\t{int(c)}\n" for i, c in enumerate(lab))
-    except OSError:
-        raise ValidationError(f"cannot open output file: {path}") from None
+def write_membership(path, labels, device: int = 0) -> None:
+    """labelprop::write_membership (io.cpp:9-14): `vertex<TAB>label` per line, the text
+    formatted on the device (nulpa_write_membership, textout.cu)."""
+    lab = np.ascontiguousarray(labels, dtype=np.uint32)
+    _capi.check(_capi.lib().nulpa_write_membership(str(path).encode(), _ptr(lab), lab.size,
+                                                   device))
 
 
 def read_membership(path, n: int) -> np.ndarray:
-    """labelprop::read_membership (io.cpp:16-56): same checks and messages."""
-    try:
-        f = open(path)
-    except OSError:
-        raise ValidationError(f"cannot open membership file: {path}") from None
+    """labelprop::read_membership (io.cpp:16-56): same checks and messages
+    (nulpa_read_membership, textio.cpp)."""
     labels = np.zeros(n, np.uint32)
-    seen = np.zeros(n, bool)
-    with f:
-        for lineno, line in enumerate(f, 1):
-            s = line.strip()
-            if not s or s[0] in "#%":
-                continue
-            toks = s.split()
-            if not toks[0].isdigit() or len(toks) < 2 or not toks[1].isdigit():
-                raise FormatError(f"{path}:{lineno}: expected 'vertex<TAB>label'")
-            if len(toks) > 2:
-                raise FormatError(f"{path}:{lineno}: trailing content after label")
-            v, c = int(toks[0]), int(toks[1])
-            if v >= n:
-                raise ValidationError(f"{path}:{lineno}: vertex {v} out of range for n={n}")
-            if c >= n:
-                raise ValidationError(f"{path}:{lineno}: label {c} out of range for n={n}")
-            if seen[v]:
-                raise ValidationError(f"{path}:{lineno}: vertex {v} assigned twice")
-            seen[v] = True
-            labels[v] = c
-    missing = np.flatnonzero(~seen)
-    if missing.size:
-        raise ValidationError(f"{path}: no label for vertex {int(missing[0])}")
+    _capi.check(_capi.lib().nulpa_read_membership(str(path).encode(), n, _ptr(labels)))
     return labels
+
+
+def write_edge_list(g: CsrGraph, path) -> None:
+    """labelprop::write_edge_list (graph.hpp:112, graph.cpp:309-325)."""
+    csr = g.csr_view()
+    _capi.check(_capi.lib().nulpa_write_edge_list(str(path).encode(), C.byref(csr)))
 
 
 def partition_by_degree(g: CsrGraph, switch_degree: int) -> DegreePartition:

@@ -152,3 +152,122 @@ def test_load_graph_file_end_to_end(tmp_path):
     r = dg.lpa(lp.LpaConfig(exec=lp.ExecMode.Synchronous))
     want, _ = O.port_lpa(O.PortGraph(ro, rt, rw), exec_mode=2)
     assert np.array_equal(r.labels, want)
+
+
+# ---- chunk-parallel parsing: fuzzed files, many chunks, against the reference --------
+
+def _fuzz_lines(rng, kind, n_lines):
+    """Mostly valid lines of `kind` ('el', 'mm' or 'mem'), with comments, blanks, CRs and
+    (sometimes) one bad line somewhere."""
+    lines = []
+    for i in range(n_lines):
+        r = rng.random()
+        if r < 0.03:
+            lines.append("% a comment" if kind != "el" or rng.random() < 0.5 else "# c")
+        elif r < 0.05:
+            lines.append("   " if rng.random() < 0.5 else "")
+        elif kind == "el":
+            a, b = rng.integers(0, 500, 2)
+            lines.append(f"{a} {b}" + (f" {rng.integers(1, 9) * 0.25}" if rng.random() < 0.5 else "")
+                         + ("\r" if rng.random() < 0.05 else ""))
+        elif kind == "mm":
+            a, b = rng.integers(1, 301, 2)
+            lines.append(f"{a}\t{b} {rng.integers(1, 9) * 0.5}")
+        else:
+            lines.append(f"{i}\t{rng.integers(0, n_lines)}")
+    bad = {"el": ["0 x", "1 2 3 4", "7 4294967295", "3 4 -1", "% vertices 99999999999", "5"],
+           "mm": ["1 2", "0 3 1", "400 1 1", "1 2 abc", "1 2 0"],
+           "mem": ["x 1", "1 2 3", "1 2x", "99999999 1", "1 99999999"]}[kind]
+    if rng.random() < 0.7:
+        at = int(rng.integers(0, len(lines)))
+        lines[at] = bad[int(rng.integers(0, len(bad)))]
+    return lines
+
+
+def _ours_or_error(fn):
+    try:
+        return "ok", fn()
+    except (lp.FormatError, lp.ValidationError) as e:
+        return ("F:" if type(e) is lp.FormatError else "V:") + str(e), None
+
+
+def _refs_or_error(fn):
+    try:
+        return "ok", fn()
+    except ValueError as e:
+        return str(e), None
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("kind", ["el", "mm"])
+def test_graph_file_chunks_match_reference(tmp_path, monkeypatch, seed, kind):
+    monkeypatch.setenv("NULPA_TEXT_CHUNK_BYTES", str(64 + 97 * seed))  # many small chunks
+    rng = np.random.default_rng(1000 * seed + len(kind))
+    body = _fuzz_lines(rng, kind, 400)
+    if kind == "mm":
+        nnz = int(rng.integers(300, 420))  # sometimes short, sometimes trailing junk
+        text = f"%%MatrixMarket matrix coordinate real general\n% c\n300 300 {nnz}\n"
+    else:
+        text = "% vertices 600\n" if seed % 2 else ""
+    p = tmp_path / f"g.{kind}"
+    p.write_text(text + "\n".join(body) + ("\n" if seed % 3 else ""))
+    fmt = 0 if kind == "mm" else 1
+    got, el = _ours_or_error(lambda: lp.load_graph(p, lp.FileFormat(fmt)))
+    want, ref = _refs_or_error(lambda: O.ref_load_graph(p, fmt))
+    assert got == want
+    if el is not None:
+        u, v, w, nd = ref
+        assert np.array_equal(el.u, u) and np.array_equal(el.v, v) and np.array_equal(el.w, w)
+        assert (el.n_declared if el.n_declared is not None else -1) == nd
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", range(12))
+def test_read_membership_chunks_match_reference(tmp_path, monkeypatch, seed):
+    monkeypatch.setenv("NULPA_TEXT_CHUNK_BYTES", str(48 + 61 * seed))
+    rng = np.random.default_rng(seed)
+    n = 300
+    lines = _fuzz_lines(rng, "mem", n)
+    if seed % 4 == 1:  # a duplicate vertex
+        lines.append(f"{int(rng.integers(0, n))}\t0")
+    if seed % 4 == 2:  # a missing vertex
+        lines = [ln for ln in lines if not ln.startswith(f"{n - 7}\t")]
+    p = tmp_path / "m.tsv"
+    p.write_text("\n".join(lines) + "\n")
+    got, lab = _ours_or_error(lambda: lp.read_membership(p, n))
+    want, ref = _refs_or_error(lambda: O.ref_read_membership(p, n))
+    assert got == want
+    if lab is not None:
+        assert np.array_equal(lab, ref)
+
+
+@needs_ref
+@pytest.mark.parametrize("weighted", [False, True])
+def test_write_edge_list_bytes_match_reference(tmp_path, monkeypatch, weighted):
+    rng = np.random.default_rng(5)
+    n = 3000
+    u, v, w = _random_edges(rng, n, 6 * n, weighted=weighted)
+    ref = O.RefGraph.from_edges(u, v, w, n + 5, True)
+    ro, rt, rw = ref.arrays()
+    O.ref_write_edge_list(ref, tmp_path / "ref.txt")
+    g = lp.CsrGraph(ro, rt, rw)
+    lp.write_edge_list(g, tmp_path / "ours.txt")
+    assert (tmp_path / "ours.txt").read_bytes() == (tmp_path / "ref.txt").read_bytes()
+    with pytest.raises(lp.ValidationError, match="cannot open output file"):
+        lp.write_edge_list(g, tmp_path / "no" / "such" / "dir.txt")
+
+
+@needs_ref
+@pytest.mark.gpu
+def test_write_membership_bytes_match_reference(tmp_path):
+    rng = np.random.default_rng(2)
+    for n in (0, 1, 10, 12345, 3 * (1 << 20) + 17):
+        lab = rng.integers(0, max(n, 1), n).astype(np.uint32)
+        if n > 5:
+            lab[:3] = [0, n - 1, 9]
+        lp.write_membership(tmp_path / "ours.tsv", lab)
+        O.ref_write_membership(tmp_path / "ref.tsv", lab)
+        assert (tmp_path / "ours.tsv").read_bytes() == (tmp_path / "ref.tsv").read_bytes()
+        if n:
+            assert np.array_equal(lp.read_membership(tmp_path / "ours.tsv", n), lab)

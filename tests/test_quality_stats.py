@@ -78,11 +78,19 @@ def test_delta_modularity_matches_q_difference():
     assert abs(lp.modularity(g, moved) - q0 - dq) < 1e-12
 
 
-def test_membership_round_trip_and_errors(tmp_path):
+@pytest.mark.gpu
+def test_membership_round_trip(tmp_path):
     lab = np.array([3, 3, 0, 1], np.uint32)
     p = tmp_path / "m.tsv"
-    lp.write_membership(p, lab)
+    lp.write_membership(p, lab)  # formatted on the device
     assert p.read_text() == "0\t3\n1\t3\n2\t0\n3\t1\n"
+    assert np.array_equal(lp.read_membership(p, 4), lab)
+
+
+def test_membership_read_and_errors(tmp_path):
+    lab = np.array([3, 3, 0, 1], np.uint32)
+    p = tmp_path / "m.tsv"
+    p.write_text("0\t3\n1 3\n# c\n  2\t0  \n3\t1")
     assert np.array_equal(lp.read_membership(p, 4), lab)
     cases = {
         "1\t2\t3\n": (lp.FormatError, "trailing content after label"),
