@@ -17,6 +17,8 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <mutex>
+#include <atomic>
 #include <new>
 #include <span>
 #include <string>
@@ -277,29 +279,59 @@ REF_API int ref_lpa(void* h, double tolerance, int max_iterations, int pl_period
 // template detail::scan_candidate (lpa.hpp:92-111) with a snapshot reader,
 // then the move rule of sync_move (lpa.cpp:87-88). Every vertex with degree
 // >= 1 is examined (no pruning flags). Returns the changed count.
+// Vertices are independent given the snapshot, and each one's table is its own
+// arena region (slot_offset = 2*O_i, hashtable.hpp:41-46), so host threads take
+// 4096-vertex chunks of the ids (the result does not depend on the thread count).
 REF_API int ref_sync_step(void* h, const uint32_t* labels_in, int pick_less, int strategy,
                           int precision_bits, uint32_t* labels_out, uint64_t* changed) {
   return guard([&] {
     const CsrGraph& g = *static_cast<CsrGraph*>(h);
     const uint32_t n = g.order();
-    uint64_t dn = 0;
-    auto run = [&](auto arena) {
-      for (VertexId i = 0; i < n; ++i) {
-        labels_out[i] = labels_in[i];
-        if (g.degree(i) == 0) continue;
-        auto cand = detail::scan_candidate(g, i, arena, static_cast<ProbeStrategy>(strategy),
-                                           false, [&](VertexId j) { return labels_in[j]; });
-        if (!cand) continue;
-        const bool allowed = pick_less ? (*cand < labels_in[i]) : (*cand != labels_in[i]);
-        if (!allowed) continue;
-        labels_out[i] = *cand;
-        ++dn;
-      }
+    std::atomic<uint64_t> dn{0};
+    std::atomic<uint32_t> next{0};
+    std::atomic<bool> failed{false};
+    std::string fail_msg;
+    std::mutex fail_mu;
+    auto run = [&](auto& arena) {
+      auto work = [&] {
+        uint64_t local = 0;
+        try {
+          for (;;) {
+            const uint32_t b = next.fetch_add(4096);
+            if (b >= n || failed.load()) break;
+            const uint32_t e = std::min<uint64_t>(n, uint64_t(b) + 4096);
+            for (VertexId i = b; i < e; ++i) {
+              labels_out[i] = labels_in[i];
+              if (g.degree(i) == 0) continue;
+              auto cand = detail::scan_candidate(g, i, arena, static_cast<ProbeStrategy>(strategy),
+                                                 false, [&](VertexId j) { return labels_in[j]; });
+              if (!cand) continue;
+              const bool allowed = pick_less ? (*cand < labels_in[i]) : (*cand != labels_in[i]);
+              if (!allowed) continue;
+              labels_out[i] = *cand;
+              ++local;
+            }
+          }
+        } catch (const std::exception& ex) {
+          std::lock_guard<std::mutex> lk(fail_mu);
+          if (!failed.exchange(true)) fail_msg = ex.what();
+        }
+        dn += local;
+      };
+      const unsigned t = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+      std::vector<std::thread> pool;
+      for (unsigned k = 1; k < t; ++k) pool.emplace_back(work);
+      work();
+      for (auto& th : pool) th.join();
+      if (failed) throw InternalError(fail_msg);
     };
-    if (precision_bits == 64)
-      run(HashArena<double>::for_graph(g));
-    else
-      run(HashArena<float>::for_graph(g));
+    if (precision_bits == 64) {
+      auto arena = HashArena<double>::for_graph(g);
+      run(arena);
+    } else {
+      auto arena = HashArena<float>::for_graph(g);
+      run(arena);
+    }
     *changed = dn;
   });
 }

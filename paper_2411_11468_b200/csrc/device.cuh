@@ -159,18 +159,47 @@ __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
   return v;
 }
 
-// Async mode reads neighbour labels that other SMs may be writing in place:
-// load through L2 (ld.global.cg) so a stale L1 line is never reused within a
-// pass. Sync mode reads an immutable snapshot through the read-only path.
+// ---- the asynchronous label / flag protocol (lpa.cpp:44-60) --------------------------
+// The reference makes every label and flag access seq_cst so that "a stale read is
+// always re-examined": a vertex j that claims itself (flags[j] = 1) and then reads a
+// neighbour's label, and a neighbour i that stores a new label and then reads flags[j]
+// to wake j, must not BOTH read the old value (store buffering). On the GPU the labels
+// and flags that other SMs read and write during a pass are accessed with relaxed
+// device-scope operations (morally strong in the PTX memory model; they bypass L1, so
+// no stale line is reused), and a fence.sc.gpu separates each claim store from the
+// label loads that depend on it and each label store from its wake loads. Either the
+// claimer's loads see the new label, or the changer's flag load sees the claim and
+// wakes j. One fence per claimed batch and per changed vertex. (The asm statements are
+// volatile, so the compiler keeps them in program order around the fence.)
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+__device__ __forceinline__ uint8_t ld_relaxed(const uint8_t* p) {
+  uint16_t v;
+  asm volatile("ld.relaxed.gpu.global.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return static_cast<uint8_t>(v);
+}
+__device__ __forceinline__ void st_relaxed(uint8_t* p, uint8_t v) {
+  asm volatile("st.relaxed.gpu.global.u8 [%0], %1;" ::"l"(p), "h"(static_cast<uint16_t>(v)));
+}
+__device__ __forceinline__ void fence_sc() { asm volatile("fence.sc.gpu;" ::: "memory"); }
+
+// Async mode reads neighbour labels that other SMs may be writing in place (relaxed,
+// device scope). Sync mode reads an immutable snapshot through the read-only path.
 template <int MODE>
 __device__ __forceinline__ uint32_t load_label(const uint32_t* p) {
   if constexpr (MODE == kAsync)
-    return __ldcg(p);
+    return ld_relaxed(p);
   else
     return __ldg(p);
 }
 
-__device__ __forceinline__ uint8_t load_flag(const uint8_t* p) { return __ldcg(p); }
+__device__ __forceinline__ uint8_t load_flag(const uint8_t* p) { return ld_relaxed(p); }
 
 template <typename W, bool WEIGHTED>
 __device__ __forceinline__ W edge_weight(const Graph& g, uint64_t e) {

@@ -50,13 +50,21 @@ void allow_smem(K kernel, size_t bytes) {
                                   static_cast<int>(bytes)));
 }
 
-// True once per device for each `done` mask (function attributes are set per device:
-// a process that runs on device 1 after device 0 must set them again).
-inline bool first_on_device(std::atomic<uint64_t>& done) {
+// Run `setup` once per device for each `done` mask (function attributes are set per
+// device: a process that runs on device 1 after device 0 must set them again). The
+// bit is set only after `setup` succeeded, under a lock, so a concurrent caller never
+// launches before the attributes are in place and a failed setup is retried.
+template <typename F>
+void once_per_device(std::atomic<uint64_t>& done, F&& setup) {
   int dev = 0;
   NULPA_CUDA(cudaGetDevice(&dev));
   const uint64_t bit = 1ull << (dev & 63);
-  return (done.fetch_or(bit) & bit) == 0;
+  if (done.load(std::memory_order_acquire) & bit) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  setup();
+  done.fetch_or(bit, std::memory_order_release);
 }
 
 // Grid for a grid-stride kernel: enough CTAs for `work` items at `per_block`
@@ -135,7 +143,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   auto k_bg = dd ? k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, kDedupLater>
                  : k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, 0>;
   static std::atomic<uint64_t> init{0};
-  if (first_on_device(init)) {
+  once_per_device(init, [&] {
     allow_smem(k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, kDedupLater>, wtab_smem);
     allow_smem(k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, 0>, wtab_smem);
     allow_smem(k_team<MODE, W, WEIGHTED, 256, 128, kBlockCap, kBlockMax, kDedupLater>, block_smem);
@@ -148,7 +156,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     if constexpr (!WEIGHTED) allow_smem(k_wide<MODE, W>, wide_bytes());
     allow_smem(k_hub_accum<MODE, W, WEIGHTED, 1>, hub_smem);
     allow_smem(k_hub_accum<MODE, W, WEIGHTED, 0>, hub_smem);
-  }
+  });
   int launches = 0;
   auto tier = [&](int t) {
     c.ctr = ctr + t * C_COUNT;
@@ -250,7 +258,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     k_hub_sweep<W, WEIGHTED><<<gs, kBlockThreads, 0, s>>>(h);
     launches += 3;
     if constexpr (sizeof(VBits<W>) == 8) {
-      k_hub_sweep_key_f64<<<gs, kBlockThreads, 0, s>>>(h);
+      k_hub_sweep_key_f64<kPacked<WEIGHTED>><<<gs, kBlockThreads, 0, s>>>(h);
       ++launches;
     }
     k_hub_decide<MODE, W, WEIGHTED><<<gh, 256, 0, s>>>(c, h);
@@ -300,7 +308,7 @@ template <typename W, bool WEIGHTED>
 void launch_sequential(const PassCtx& c, void* gtab, cudaStream_t s) {
   constexpr size_t smem = kHubCap * Table<kPacked<WEIGHTED>, W>::kSlotBytes;
   static std::atomic<uint64_t> init{0};
-  if (first_on_device(init)) allow_smem(k_sequential<W, WEIGHTED>, smem);
+  once_per_device(init, [&] { allow_smem(k_sequential<W, WEIGHTED>, smem); });
   k_sequential<W, WEIGHTED><<<1, kBlockThreads, smem, s>>>(c, gtab);
   NULPA_CUDA(cudaGetLastError());
 }
@@ -407,6 +415,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
   Trace tr("run_lpa");
   validate_opts(g, o);
   use_device(g->device);
+  std::lock_guard<std::recursive_mutex> plan_lock(g->plan_mu);
   const auto t_setup = std::chrono::steady_clock::now();
   Stream stream;
   cudaStream_t s = stream.s;
@@ -677,6 +686,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
 uint64_t run_sync_step(nulpa_graph* g, const uint32_t* lab_in_dev, int pick_less, int strategy,
                        int precision, uint32_t* lab_out_dev) {
   use_device(g->device);
+  std::lock_guard<std::recursive_mutex> plan_lock(g->plan_mu);
   if (strategy < 0 || strategy > 3) throw Error(NULPA_EINVAL, "unknown probe strategy");
   Stream stream;
   cudaStream_t s = stream.s;
@@ -988,7 +998,7 @@ int nulpa_sync_step(const nulpa_csr* csr, const uint32_t* labels_in, int pick_le
                     int precision, uint32_t* labels_out, uint64_t* changed) {
   return guarded([&] {
     check_host_csr(csr);
-    HostGraph hg(csr, 0);
+    HostGraph hg(csr, default_device());
     DevArray<uint32_t> in(csr->n), out(csr->n);
     in.upload(labels_in);
     const uint64_t dn = run_sync_step(hg.g, in.p, pick_less, strategy, precision, out.p);
@@ -1001,7 +1011,7 @@ int nulpa_cross_check(const nulpa_csr* csr, uint32_t* labels, const uint32_t* pr
                       uint8_t* flags, uint64_t* reverted) {
   return guarded([&] {
     check_host_csr(csr);
-    HostGraph hg(csr, 0);
+    HostGraph hg(csr, default_device());
     const uint32_t n = csr->n;
     DevArray<uint32_t> l(n), pv(n);
     DevArray<uint8_t> f(n);
@@ -1022,7 +1032,7 @@ int nulpa_partition_by_degree(const nulpa_csr* csr, uint32_t switch_degree, uint
     // only the offsets are needed.
     if (switch_degree < 2) throw Error(NULPA_EINVAL, "switch-degree must be >= 2");
     check_host_csr(csr);
-    use_device(0);
+    use_device(default_device());
     const uint32_t n = csr->n;
     Stream stream;
     DevArray<uint64_t> off(uint64_t(n) + 1);

@@ -130,6 +130,16 @@ void use_device(int device) {
   }
 }
 
+int default_device() {
+  if (const char* e = std::getenv("NULPA_DEVICE")) return std::atoi(e);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    dev = 0;
+  }
+  return dev;
+}
+
 // Allocations are stream-ordered on the legacy stream; every buffer is freed only
 // after the work that used it has been synchronised.
 static double now_s() {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -50,6 +51,9 @@ int guarded(F&& f) {
 
 // Select a device, failing loudly when none is usable (no CPU fallback).
 void use_device(int device);
+// Device for C-ABI calls that take none: NULPA_DEVICE when set (the C++ drop-in's rule),
+// else the calling thread's current device.
+int default_device();
 
 // Device allocation that throws Error(NULPA_ENOMEM) on failure.
 void* dmalloc(size_t bytes);
@@ -92,6 +96,9 @@ struct nulpa_graph {
   uint32_t* perm = nullptr;  // device
   uint32_t* inv = nullptr;   // device
   nulpa::Plan* plan = nullptr;  // cached tiering (plan.hpp)
+  // Held by every call that uses `plan`: the cached plan (and its hub tables and
+  // wide-tier scratch) is shared state, so runs on one graph handle are serialised.
+  std::recursive_mutex plan_mu;
 };
 
 namespace nulpa {

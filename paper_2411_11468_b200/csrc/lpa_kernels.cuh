@@ -41,11 +41,12 @@ namespace dev {
 template <int MODE>
 __device__ __forceinline__ bool apply_move(const PassCtx& c, uint32_t i, uint32_t cand) {
   if (cand == kEmpty) return false;
-  const uint32_t cur = (MODE == kAsync) ? __ldcg(c.lab_out + i) : __ldg(c.lab_in + i);
+  const uint32_t cur = (MODE == kAsync) ? ld_relaxed(c.lab_out + i) : __ldg(c.lab_in + i);
   const bool allowed = c.pick_less ? (cand < cur) : (cand != cur);
   if (!allowed) return false;
   if constexpr (MODE == kAsync) {
-    __stcg(c.lab_out + i, cand);
+    st_relaxed(c.lab_out + i, cand);
+    if (c.wake) fence_sc();  // the label store before the wake loads (a18)
   } else {
     c.lab_out[i] = cand;
     if (c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
@@ -57,15 +58,23 @@ __device__ __forceinline__ bool apply_move(const PassCtx& c, uint32_t i, uint32_
 // flag already reads 0: hubs are woken by millions of neighbours per pass, and a
 // load of a hot byte is far cheaper than a partial-sector store to it.
 __device__ __forceinline__ void wake_vertex(uint8_t* flags, uint32_t j) {
-  if (load_flag(flags + j)) flags[j] = 0;
+  if (load_flag(flags + j)) st_relaxed(flags + j, uint8_t(0));
 }
 
 // Check-and-set the processed flag (lpa.cpp:143-144). Returns true to skip.
+// The caller fences (claim_fence) before loading the labels the decision depends on.
 __device__ __forceinline__ bool claim_vertex(const PassCtx& c, uint32_t i) {
   if (!c.flags) return false;
   if (load_flag(c.flags + i)) return true;
-  c.flags[i] = 1;
+  st_relaxed(c.flags + i, uint8_t(1));
   return false;
+}
+
+// fence.sc between this thread's claims and the label loads that follow them (a18).
+// Only async passes with pruning can race a claim against a wake.
+template <int MODE>
+__device__ __forceinline__ void claim_fence(const PassCtx& c) {
+  if (MODE == kAsync && c.flags) fence_sc();
 }
 
 // Apply the move rule given the vertex's current label `cur` (read when the
@@ -77,7 +86,8 @@ __device__ __forceinline__ bool apply_move_cur(const PassCtx& c, uint32_t i, uin
   const bool allowed = c.pick_less ? (cand < cur) : (cand != cur);
   if (!allowed) return false;
   if constexpr (MODE == kAsync) {
-    __stcg(c.lab_out + i, cand);
+    st_relaxed(c.lab_out + i, cand);
+    if (c.wake) fence_sc();  // the label store before the wake loads (a18)
   } else {
     c.lab_out[i] = cand;
     if (c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
@@ -105,9 +115,10 @@ __device__ __forceinline__ Meta fetch_meta(const PassCtx& c, const uint32_t* __r
     if (m.act) {
       m.lo = __ldg(c.g.off + m.i);
       m.d = static_cast<uint32_t>(__ldg(c.g.off + m.i + 1) - m.lo);
-      m.cur = (MODE == kAsync) ? __ldcg(c.lab_out + m.i) : __ldg(c.lab_in + m.i);
+      m.cur = (MODE == kAsync) ? ld_relaxed(c.lab_out + m.i) : __ldg(c.lab_in + m.i);
     }
   }
+  claim_fence<MODE>(c);  // (consumers of the batch synchronise with this thread first)
   return m;
 }
 
@@ -141,6 +152,7 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
   for (uint32_t t = CHUNKED ? tid * L : tid; t < t_end; t += CHUNKED ? 1u : stride) {
     const uint32_t i = __ldg(list + t);
     if (claim_vertex(c, i)) continue;
+    claim_fence<MODE>(c);
     const uint64_t lo = __ldg(c.g.off + i);
     const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
     uint32_t nb[DMAX];
@@ -212,6 +224,7 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
   // then kPer vertices per step with the next step's targets loaded ahead.
   for (uint32_t base = gw * 32; base < count; base += nw * 32) {
     const Meta mine = fetch_meta<MODE>(c, list, base + lane, count);
+    __syncwarp();  // every lane's claim (and its fence) before any lane's label loads
     Meta m = shfl_meta(mine, sub);
     uint32_t j = (m.act && gl < m.d) ? ld_stream(c.g.tgt + m.lo + gl, pol) : m.i;
 #pragma unroll 1
@@ -244,6 +257,7 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
         if (MODE == kAsync && ch && c.wake) n_w += m.d;
       }
       ch = __shfl_sync(kFull, ch, sub * G);
+      if (MODE == kAsync && c.wake) __syncwarp();  // the group leader's store + fence first
       if (MODE == kAsync && ch && c.wake && m.act && gl < m.d) wake_vertex(c.flags, j);
       m = mn;
       j = jn;
@@ -581,8 +595,8 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : (CTA_THR
     if (ttid < kBatch) mine = fetch_meta<MODE>(c, list, base + ttid, count);
     if constexpr (TEAM > 32) {
       if (ttid < kBatch) s_meta[team][ttid] = mine;
-      sync();
     }
+    sync();  // the batch's claims (and fences) before the team's label loads
     const uint32_t nb = min(kBatch, count - base);
     for (uint32_t v = 0; v < nb; ++v) {
       Meta m;
@@ -610,9 +624,11 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : (CTA_THR
         n_dn += changed;
         if (MODE == kAsync && changed && c.wake) n_w += m.d;
       }
-      if (MODE == kAsync && changed && c.wake)
+      if (MODE == kAsync && changed && c.wake) {
+        sync();  // thread 0's label store and fence before the team's wake loads
         for (uint32_t e = ttid; e < m.d; e += TEAM)
           wake_vertex(c.flags, ld_stream(c.g.tgt + m.lo + e, pol));
+      }
     }
     if constexpr (TEAM > 32) sync();  // s_meta is rewritten by the next batch
   }
@@ -671,7 +687,10 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
     if (t >= count) break;  // uniform over the cluster; the final sync below keeps rank 0's
                             // shared memory alive until every rank has read s_item
     const uint32_t i = __ldg(list + t);
-    if (rank == 0 && threadIdx.x == 0) s_flag = claim_vertex(c, i) ? 1 : 0;
+    if (rank == 0 && threadIdx.x == 0) {
+      s_flag = claim_vertex(c, i) ? 1 : 0;
+      claim_fence<MODE>(c);
+    }
     const uint64_t lo = __ldg(c.g.off + i);
     const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
     const uint32_t cap = pow2_ceil(d + d / 3 + 1) / kClusterSize;  // per-rank partition
@@ -973,6 +992,7 @@ __global__ void __launch_bounds__(256) k_first_pass(PassCtx c, uint32_t v_lo, ui
     ++n_dn;
     if (MODE == kSync && c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
     if (MODE == kAsync && c.wake) {
+      fence_sc();  // the label store before the wake loads (a18)
       for (uint32_t e = 0; e < d; ++e) wake_vertex(c.flags, __ldg(c.g.tgt + lo + e));
       n_w += d;
     }
@@ -1171,21 +1191,26 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_sweep(HubCtx h) {
   }
 }
 
-// fp64 weighted path only: the smallest key among slots holding the maximum
-// value (dense, like k_hub_sweep); resets the slots.
+// fp64 values only: the smallest key among slots holding the maximum value (dense,
+// like k_hub_sweep); resets the slots. PACKED = unit weights, where the hub table is
+// (key << 32 | count) words; otherwise split key / double arrays.
+template <bool PACKED>
 __global__ void __launch_bounds__(kBlockThreads) k_hub_sweep_key_f64(HubCtx h) {
-  Table<false, double> g;
+  using Tab = Table<PACKED, double>;
   for (uint32_t it = blockIdx.x; it < h.n_sitems; it += gridDim.x) {
     const uint32_t x = h.sitem_hub[it];
     if (!h.active[x]) continue;
     const uint32_t s0 = h.sitem_start[it];
     const uint32_t s1 = min(h.tab_cap[x], s0 + kHubSweep);
-    g.bind_split(static_cast<uint32_t*>(h.tab) + h.tab_off[x],
-                 static_cast<double*>(h.tab_vals) + h.tab_off[x]);
+    Tab g;
+    bind_hub_table<Tab, double, PACKED>(g, h, x);
     const double bestv = __longlong_as_double(static_cast<long long>(h.best[x]));
     for (uint32_t sl = s0 + threadIdx.x; sl < s1; sl += blockDim.x) {
-      if (g.k[sl] == kEmpty) continue;
-      if (g.v[sl] == bestv) atomicMin(h.best_k + x, g.k[sl]);
+      uint32_t k;
+      double v;
+      g.read(sl, k, v);
+      if (k == kEmpty) continue;
+      if (v == bestv) atomicMin(h.best_k + x, k);
       g.clear_slot(sl);
     }
   }
@@ -1289,13 +1314,41 @@ __global__ void __launch_bounds__(kBlockThreads) k_sequential(PassCtx c, void* g
       tab.bind(gtab, cap);
     for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) tab.clear_slot(s);
     __syncthreads();
-    for (uint32_t base = 0; base < d; base += blockDim.x) {
-      const uint32_t e = base + threadIdx.x;
-      const uint32_t j = e < d ? c.g.tgt[lo + e] : i;
-      const bool valid = e < d && j != i;
-      const uint32_t lab = valid ? c.lab_out[j] : kEmpty;
-      const W w = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
-      gather_insert<W, WEIGHTED>(c, lab, w, tab, cap, nullptr, nullptr, fails);
+    if constexpr (WEIGHTED) {
+      // Each label's weights are added in neighbour order, one rounding at a time,
+      // as the reference's plain accumulation does (hashtable.hpp:119-125): warp 0
+      // walks the row in 32-edge chunks; the lowest lane of each label group claims
+      // (or finds) the slot with its own weight, then adds its peers' weights in
+      // ascending lane order. Different labels touch different slots.
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        for (uint32_t base = 0; base < d; base += 32) {
+          const uint32_t e = base + lane;
+          const uint32_t j = e < d ? c.g.tgt[lo + e] : i;
+          const bool valid = e < d && j != i;
+          const uint32_t lab = valid ? c.lab_out[j] : kEmpty;
+          const W w = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
+          const unsigned peers = __match_any_sync(kFull, lab);
+          const bool lead = lab != kEmpty && (__ffs(peers) - 1) == lane;
+          uint32_t slot = 0;
+          if (lead && tab.add(cap, c.strategy, lab, w, &slot) == 0) ++fails;
+          W acc = lead ? tab.value(slot) : W(0);
+          for (int b = 0; b < 32; ++b) {
+            const W wb = __shfl_sync(kFull, w, b);
+            if (lead && b != lane && ((peers >> b) & 1u)) acc += wb;
+          }
+          if (lead) tab.v[slot] = acc;
+          __syncwarp();
+        }
+      }
+    } else {
+      for (uint32_t base = 0; base < d; base += blockDim.x) {
+        const uint32_t e = base + threadIdx.x;
+        const uint32_t j = e < d ? c.g.tgt[lo + e] : i;
+        const bool valid = e < d && j != i;
+        const uint32_t lab = valid ? c.lab_out[j] : kEmpty;
+        gather_insert<W, WEIGHTED>(c, lab, W(1), tab, cap, nullptr, nullptr, fails);
+      }
     }
     __syncthreads();
     Best<VBits<W>> b{VBits<W>(0), kEmpty};

@@ -165,6 +165,7 @@ void check_labels(nulpa_graph* g, const uint32_t* lab, cudaStream_t s) {
 void accumulate_sigma(nulpa_graph* g, const uint32_t* lab, double* sigma, double* big,
                       cudaStream_t s) {
   const uint32_t n = g->n;
+  std::lock_guard<std::recursive_mutex> plan_lock(g->plan_mu);
   // Any tiering covers every row once: reuse the cached plan when there is one.
   Plan* p = g->plan ? g->plan : get_plan(g, resolve_tiers(32, nullptr), 4, s);
   const Graph dg{g->offsets, g->targets, g->weights, n};
@@ -373,7 +374,7 @@ int nulpa_community_stats(const nulpa_csr* csr, const uint32_t* labels, uint64_t
     check_host_csr(csr);
     if (!count || !hist_len) throw Error(NULPA_EINVAL, "null argument");
     nulpa_graph* g = nullptr;
-    int rc = nulpa_graph_upload(csr, 0, &g);
+    int rc = nulpa_graph_upload(csr, default_device(), &g);
     if (rc) throw Error(rc, nulpa_last_error());
     uint32_t* d = nullptr;
     try {
@@ -403,7 +404,7 @@ int nulpa_modularity(const nulpa_csr* csr, const uint32_t* labels, double* q) {
   return guarded([&] {
     check_host_csr(csr);
     nulpa_graph* g = nullptr;
-    int rc = nulpa_graph_upload(csr, 0, &g);
+    int rc = nulpa_graph_upload(csr, default_device(), &g);
     if (rc) throw Error(rc, nulpa_last_error());
     uint32_t* d = nullptr;
     try {
@@ -424,7 +425,7 @@ int nulpa_community_count(const nulpa_csr* csr, const uint32_t* labels, uint64_t
   return guarded([&] {
     check_host_csr(csr);
     nulpa_graph* g = nullptr;
-    int rc = nulpa_graph_upload(csr, 0, &g);
+    int rc = nulpa_graph_upload(csr, default_device(), &g);
     if (rc) throw Error(rc, nulpa_last_error());
     uint32_t* d = nullptr;
     try {

@@ -14,6 +14,7 @@ GOLDEN = ROOT / "tests" / "golden"
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "large: BASELINE-sized parity gates (minutes, host RAM)")
 
 
 @pytest.fixture(scope="session")

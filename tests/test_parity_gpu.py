@@ -149,6 +149,29 @@ def test_sync_trajectory_vs_port(kind, size):
         assert r.stats.cc_reverts == ws["cc_reverts"]
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+def test_sequential_weighted_non_dyadic_bit_exact(precision):
+    # Sequential mode is bit-reproducible in the reference (one thread, plain adds in
+    # neighbour order). With non-dyadic weights the per-label sums depend on the order of
+    # the adds, so k_sequential must add each label's weights in neighbour order too.
+    rng = np.random.default_rng(21)
+    n = 3000
+    u = rng.integers(0, n, 40000).astype(np.uint32)
+    v = (u + rng.integers(1, 40, u.size).astype(np.uint32) * 7) % n
+    hub = rng.integers(0, n, 6000).astype(np.uint32)  # one long row
+    u = np.concatenate([u, np.full(hub.size, 5, np.uint32)]).astype(np.uint32)
+    v = np.concatenate([v, hub]).astype(np.uint32)
+    w = rng.random(u.size) * 3 + 0.1
+    el = lp.EdgeList(u, v, w, n)
+    g = lp.build_csr(el, True)
+    pg = O.PortGraph(g.offsets, g.targets, g.weights)
+    for pl in (0, 4):
+        want, ws = O.port_lpa(pg, exec_mode=1, pl_period=pl, precision=precision)
+        r = lp.lpa(g, lp.LpaConfig(exec=lp.ExecMode.Sequential, pl_period=pl,
+                                   precision=lp.ValuePrecision(precision)))
+        assert np.array_equal(r.labels, want) and r.stats.delta_n_per_iter == ws["delta_n"]
+
+
 def test_sequential_vs_port_small_rmat():
     dg, g = _device_graph("rmat", 10)
     pg = O.PortGraph(g.offsets, g.targets, None)
@@ -313,8 +336,9 @@ def _hub_graph(seed=11, n=160000, hubs=3, hub_deg=120000, extra=400000):
     return lp.CsrGraph(g.offsets, g.targets, None)
 
 
+@pytest.mark.parametrize("precision", [32, 64])
 @pytest.mark.parametrize("labels", ["identity", "random", "few"])
-def test_hub_tier_sync_step_bit_exact(labels):
+def test_hub_tier_sync_step_bit_exact(labels, precision):
     # The hub tier (shared pre-aggregation, the batched CAS-first flush into the global
     # tables, the dense sweep) against the C restatement, with and without Pick-Less.
     g = _hub_graph()
@@ -326,8 +350,8 @@ def test_hub_tier_sync_step_bit_exact(labels):
            "random": rng.integers(0, n, n).astype(np.uint32),
            "few": (rng.integers(0, 50, n) * 997).astype(np.uint32)}[labels]
     for pl in (0, 1):
-        want, wc = O.port_sync_step(pg, lab, pl)
-        got, gc = lp.sync_step(g, lab, pl)
+        want, wc = O.port_sync_step(pg, lab, pl, precision=precision)
+        got, gc = lp.sync_step(g, lab, pl, precision=lp.ValuePrecision(precision))
         assert gc == wc and np.array_equal(got, want)
 
 
