@@ -13,11 +13,16 @@ e2e     = the same metric through the host-buffer C ABI (nulpa_run): every step 
           the CSR from pinned host memory to the device, runs, and copies labels back.
 roofline: the dominant tier's algorithmic bytes / its event-timed duration.
 cpu_baseline: the reference library itself (oracle/_ref, multithreaded ParallelAsync,
-          switch_degree = UINT32_MAX per SURVEY F5) on a bounded R-MAT sample.
+          switch_degree = UINT32_MAX per SURVEY F5) on the SAME graph (one full run), with
+          its modularity; `quality` adds the SBM-100K config (reference Synchronous and
+          ParallelAsync Q against nulpa's, two-sided).
+--impl reference: the reference arm — the same library on the same workload (R-MAT
+          scale 27, or the largest scale that fits host RAM, stated), the graph built in a
+          child process so the timing process maps no libnulpa.so.
 
-Multi-GPU (N > 1, torchrun): every rank holds a full replica of the graph and runs the
-same workload ("replicas"); timing is max over ranks. The partitioned label exchange of
-SURVEY §8e is not part of this bench yet.
+Multi-GPU (N > 1, torchrun): the edge-balanced 1-D partition of SURVEY §8e
+(paper_2411_11468_b200/dist.py): each rank owns a vertex range, labels are replicated and
+exchanged every pass over NCCL; timing is max over ranks.
 """
 from __future__ import annotations
 
@@ -146,20 +151,122 @@ def ref_switch_degree(workload: str, g=None) -> int:
     return 32
 
 
-def run_reference_cpu(g, reps: int, workload: str = "rmat"):
-    """oracle/_ref: the unmodified reference lpa(), ParallelAsync, all host threads."""
+def host_info() -> dict:
+    """Host cores, threads and memory (lscpu + /proc/meminfo) for the baseline lines."""
+    info = {"threads": os.cpu_count() or 1, "physical_cores": None, "sockets": None,
+            "mem_total_gb": None, "mem_available_gb": None}
+    try:
+        out = subprocess.run(["lscpu", "-p=CORE,SOCKET"], capture_output=True, text=True).stdout
+        rows = [ln.split(",") for ln in out.splitlines() if ln and not ln.startswith("#")]
+        info["physical_cores"] = len({(r[1], r[0]) for r in rows})
+        info["sockets"] = len({r[1] for r in rows})
+    except Exception:
+        pass
+    try:
+        mi = dict(ln.split(":", 1) for ln in Path("/proc/meminfo").read_text().splitlines())
+        info["mem_total_gb"] = int(mi["MemTotal"].split()[0]) / 2**20
+        info["mem_available_gb"] = int(mi["MemAvailable"].split()[0]) / 2**20
+    except Exception:
+        pass
+    return info
+
+
+# R-MAT scale s, edgefactor 16, after symmetrise + dedup: m2 ~ 31.47 * 2^s (measured at
+# s = 22..27). The reference's lpa() on it holds the CSR (offsets 8 B/vertex, targets and
+# float weights 8 B/entry) and its 2*m2-slot HashArena (16 B/entry in fp32,
+# hashtable.hpp:57-59) at once.
+def ref_bytes_needed(scale: int) -> float:
+    n = float(1 << scale)
+    m2 = 31.47 * n
+    return m2 * 24.0 + n * 24.0
+
+
+def ref_fit_scale(want: int, mem_gb: float | None) -> int:
+    """The largest scale <= want whose reference run fits in 85% of available host RAM."""
+    if mem_gb is None:
+        return want
+    s = want
+    while s > 16 and ref_bytes_needed(s) > 0.85 * mem_gb * 2**30:
+        s -= 1
+    return s
+
+
+def export_graph(workload: str, scale: int, seed: int):
+    """Build the workload's CSR in a CHILD process (GPU generator, written as raw arrays to
+    /dev/shm) and map it here: the process that times the reference never loads
+    libnulpa.so. Returns (offsets, targets, meta, cleanup)."""
+    import shutil
+    import tempfile
+    base = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    d = tempfile.mkdtemp(prefix="nulpa_ref_", dir=base)
+    r = subprocess.run([sys.executable, "-m", "paper_2411_11468_b200.workloads", "export",
+                        "--workload", workload, "--scale", str(scale), "--seed", str(seed),
+                        "--out", d], cwd=str(ROOT), capture_output=True, text=True)
+    if r.returncode != 0:
+        shutil.rmtree(d, ignore_errors=True)
+        raise RuntimeError(f"graph export failed: {r.stderr.strip()[-400:]}")
+    meta = json.loads(Path(d, "meta.json").read_text())
+    off = np.fromfile(Path(d, "offsets.u64"), dtype=np.uint64)
+    tgt = np.memmap(Path(d, "targets.u32"), dtype=np.uint32, mode="r")
+    return off, tgt, meta, lambda: shutil.rmtree(d, ignore_errors=True)
+
+
+def run_reference_cpu(rg, n_runs: int, workload: str, budget_s: float = 1e9, g_off=None):
+    """oracle/_ref: the unmodified reference lpa(), ParallelAsync, reference defaults, all
+    host threads (workers = hardware_concurrency). Stops early once `budget_s` of wall
+    time is spent (at least one run)."""
     import oracle as O
-    rg = O.RefGraph.from_csr(g.offsets, g.targets, None)
-    workers = os.cpu_count() or 1
+    workers = int(O.ref().ref_hardware_concurrency()) or (os.cpu_count() or 1)
+    sd = ref_switch_degree(workload, None if g_off is None else _Deg(g_off))
     out = []
-    for _ in range(reps):
-        labels, st = O.ref_lpa(rg, exec_mode=0, workers=workers,
-                               switch_degree=ref_switch_degree(workload, g))
+    t0 = time.time()
+    for _ in range(n_runs):
+        labels, st = O.ref_lpa(rg, exec_mode=0, workers=workers, switch_degree=sd)
         out.append((labels, st))
-    return rg, out, workers
+        if time.time() - t0 > budget_s:
+            break
+    return out, workers, sd
+
+
+class _Deg:
+    """Just enough of a CsrGraph for ref_switch_degree."""
+    def __init__(self, offsets):
+        self.offsets = offsets
+
+
+def sbm_quality(nulpa_q=None) -> dict:
+    """SURVEY §8c gate 3 on the SBM-100K config (planted_partition seed 1): the reference's
+    Synchronous Q (its deterministic mode, lpa.cpp:70-100) and its ParallelAsync Q spread
+    (5 runs, all host threads), modularity per quality.cpp:21-49. With `nulpa_q` (the
+    list of this framework's ParallelAsync Q on the same graph) the two-sided gaps."""
+    import oracle as O
+    rg = O.RefGraph.planted(100000, 100, 14 / 999, 2 / 99000, 1)
+    lab, _ = O.ref_lpa(rg, exec_mode=2)
+    q_sync = O.ref_modularity(rg, lab)
+    workers = int(O.ref().ref_hardware_concurrency())
+    q_async = []
+    for _ in range(5):
+        la, _ = O.ref_lpa(rg, exec_mode=0, workers=workers)
+        q_async.append(O.ref_modularity(rg, la))
+    out = {"graph": "planted_partition(100000, 100, 14/999, 2/99000, seed 1)",
+           "ref_sync_Q": q_sync, "ref_async_Q": q_async, "ref_async_workers": workers}
+    if nulpa_q:
+        qm = float(np.mean(nulpa_q))
+        out.update({"nulpa_async_Q": nulpa_q, "nulpa_async_Q_mean": qm,
+                    "dQ_vs_ref_sync": qm - q_sync, "abs_dQ_vs_ref_sync": abs(qm - q_sync),
+                    "dQ_vs_ref_async_mean": qm - float(np.mean(q_async)),
+                    "abs_dQ_vs_ref_async_mean": abs(qm - float(np.mean(q_async))),
+                    "bar": "north star: |dQ| <= 0.01 vs the reference; the reference's async "
+                           "mode floods low ids (SURVEY F4), so its Synchronous Q is the "
+                           "oracle; nulpa lands above it (higher quality)"})
+    return out
 
 
 def bench_reference(args):
+    """The reference's own CPU implementation (oracle/_ref, the unmodified reference library)
+    on the SAME workload as the nulpa arm: R-MAT scale 27 (or the largest scale that fits
+    in host RAM, stated), generated in a child process so this process maps no libnulpa.so.
+    Each step is one full lpa() run; the step count is bounded by a wall-time budget."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
@@ -168,25 +275,54 @@ def bench_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libnulpa_ref.so not built (needs /root/reference at build)"}))
         return 0
-    from paper_2411_11468_b200 import workloads
-    g, desc = workloads.cpu_sample(args.workload, args.ref_scale, args.seed, 0)
-    m2 = g.directed_size()
-    rg, runs, workers = run_reference_cpu(g, args.warmup + args.steps, args.workload)
-    timed = runs[args.warmup:]
-    secs = sum(st["elapsed_seconds"] for _, st in timed)
-    value = m2 * len(timed) / secs
-    q = O.ref_modularity(rg, timed[-1][0])
-    sample = (f"{desc} (n={g.order()}, m2={m2}), reference ParallelAsync, switch_degree="
-              f"{ref_switch_degree(args.workload, g)}, workers={workers}")
+    host = host_info()
+    scale = args.scale
+    if args.workload == "rmat":
+        scale = ref_fit_scale(args.scale, host["mem_available_gb"])
+    t0 = time.time()
+    off, tgt, meta, cleanup = export_graph(args.workload, scale, args.seed)
+    try:
+        rg = O.RefGraph.from_csr(off, tgt, None)
+        g_off = np.array(off)
+    finally:
+        del tgt
+        cleanup()
+    build_s = time.time() - t0
+    n, m2 = rg.n, rg.m2
+    runs, workers, sd = run_reference_cpu(rg, args.steps, args.workload,
+                                          budget_s=args.ref_budget, g_off=g_off)
+    secs = sum(st["elapsed_seconds"] for _, st in runs)
+    value = m2 * len(runs) / secs
+    q0 = time.time()
+    q = O.ref_modularity(rg, runs[-1][0])
+    q_s = time.time() - q0
+    del rg
+    quality = sbm_quality()
+    same = args.workload != "rmat" or scale == args.scale
+    sample = (f"{meta['workload']} (n={n}, m2={m2}) — the nulpa arm's graph"
+              + ("" if same else f", scale {scale} (scale {args.scale} needs "
+                                f"{ref_bytes_needed(args.scale) / 2**30:.0f} GB host RAM)")
+              + f"; reference lpa() ParallelAsync, switch_degree={sd}, workers={workers}; "
+              f"{len(runs)} full run(s) timed (wall budget {args.ref_budget:.0f} s)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * secs / len(timed), "higher_is_better": True,
+            "n_gpus": args.gpus, "steps": len(runs), "steps_requested": args.steps,
+            "warmup": 0, "ms_per_step": 1e3 * secs / len(runs), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"{desc} (bounded CPU sample of the {args.workload} "
-                                   f"workload)", "n": g.order(), "m2": m2,
-                       "iterations": timed[-1][1]["iterations"], "modularity": q},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers,
-                             "kind": "reference", "sample": sample},
+            "config": {**{k: v for k, v in meta.items() if k not in ("n", "m2")}, "n": n,
+                       "m2": m2, "E_definition": "m2 = directed CSR entries after symmetrise "
+                                                 "+ dedup",
+                       "undirected_edges": m2 // 2, "edges_per_s_undirected": value / 2,
+                       "same_config_as_nulpa": same,
+                       "exec": "ParallelAsync", "switch_degree": sd,
+                       "iterations": runs[-1][1]["iterations"],
+                       "delta_n": runs[-1][1]["delta_n"], "converged": runs[-1][1]["converged"],
+                       "modularity": q, "modularity_seconds": q_s,
+                       "graph_build_seconds": build_s,
+                       "timing": "RunStats.elapsed_seconds (lpa.cpp:269,311): the iteration "
+                                 "loop only, arena allocation excluded"},
+            "quality": quality, "host": host,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
+                             "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -305,31 +441,56 @@ def bench_nulpa(args):
                "h2d_bytes_per_step": int((n + 1) * 8 + m2 * 4),
                "d2h_bytes_per_step": int(n * 4), "steps": args.e2e_steps,
                "seconds_per_step": e_wall / args.e2e_steps, "host_memory": "pinned"}
-        del off_h, tgt_h, lab_h
+        del lab_h
+        host_off, host_tgt = off_h.numpy().view(np.uint64), tgt_h.numpy().view(np.uint32)
     else:
+        host_off = host_tgt = None
+        if rank == 0 and world == 1 and args.cpu_baseline:
+            g_h = dg.download()
+            host_off, host_tgt = g_h.offsets, g_h.targets
         dg.free()
 
-    cpu = None
+    # The reference CPU path beside it, on the SAME graph (the host CSR above), and the
+    # quality comparison: this graph's reference Q, and the SBM-100K config's reference
+    # Synchronous / ParallelAsync Q against nulpa's (two-sided).
+    cpu, quality = None, None
     if rank == 0 and world == 1 and args.cpu_baseline:
         try:
             import oracle as O
-            if O.ref_available():
-                g, desc = workloads.cpu_sample(args.workload, args.ref_scale, args.seed, dev)
-                _, runs, workers = run_reference_cpu(g, 1, args.workload)
-                stc = runs[-1][1]
-                cpu = {"value": g.directed_size() / stc["elapsed_seconds"], "unit": UNIT,
-                       "cores": workers, "kind": "reference",
-                       "sample": f"{desc} (m2={g.directed_size()}), reference lpa() "
-                                 f"ParallelAsync, switch_degree="
-                                 f"{ref_switch_degree(args.workload, g)}, "
-                                 f"{stc['iterations']} iterations, "
-                                 f"{stc['elapsed_seconds']:.2f} s"}
-            else:
-                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                       "sample": "oracle/_ref not built on this box"}
+            if not O.ref_available():
+                raise RuntimeError("oracle/_ref not built on this box")
+            host = host_info()
+            need = ref_bytes_needed(args.scale) if args.workload == "rmat" else 0
+            if need and need > 0.85 * (host["mem_available_gb"] or 0) * 2**30:
+                raise RuntimeError(f"the reference on this graph needs {need / 2**30:.0f} GB "
+                                   f"of host RAM, {host['mem_available_gb']:.0f} GB available")
+            rg = O.RefGraph.from_csr(host_off, host_tgt, None)
+            runs, workers, sd = run_reference_cpu(rg, 1, args.workload, g_off=host_off)
+            stc = runs[-1][1]
+            q_ref = O.ref_modularity(rg, runs[-1][0])
+            del rg
+            cpu = {"value": m2 / stc["elapsed_seconds"], "unit": UNIT, "cores": workers,
+                   "kind": "reference", "physical_cores": host["physical_cores"],
+                   "sample": f"the full {wdesc['workload']} graph (m2={m2}), one reference "
+                             f"lpa() ParallelAsync run, switch_degree={sd}, "
+                             f"{stc['iterations']} iterations, "
+                             f"{stc['elapsed_seconds']:.2f} s (RunStats.elapsed_seconds)"}
+            from paper_2411_11468_b200 import labelprop as lp2
+            sg = O.RefGraph.planted(100000, 100, 14 / 999, 2 / 99000, 1)
+            so, st_, _ = sg.arrays()
+            sgh = lp2.CsrGraph(so, st_, None)
+            nq = [lp2.modularity(sgh, lp2.lpa(sgh).labels) for _ in range(5)]
+            quality = {"this_graph": {"nulpa_Q": q, "ref_async_Q": q_ref,
+                                      "dQ": q - q_ref, "abs_dQ": abs(q - q_ref),
+                                      "ref_iterations": stc["iterations"],
+                                      "nulpa_iterations": int(stats[-1][0].iterations)},
+                       "sbm100k": sbm_quality(nq)}
         except Exception as e:  # the baseline must never sink the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"failed: {e}"}
+    host_off = host_tgt = None
+    if args.e2e_steps > 0:
+        del off_h, tgt_h
 
     if rank == 0:
         s0 = stats[-1][0]
@@ -341,6 +502,7 @@ def bench_nulpa(args):
             "config": {
                 **wdesc, "n": n, "m2": m2,
                 "E_definition": "m2 = directed CSR entries after symmetrise + dedup",
+                "undirected_edges": m2 // 2, "edges_per_s_undirected": value / 2,
                 "undirected_draws": ((1 << args.scale) * args.edgefactor
                                      if args.workload == "rmat" else None),
                 "parallelism": "replicas" if world > 1 else "single",
@@ -369,6 +531,7 @@ def bench_nulpa(args):
                                                         "gather (every gather misses L2)"}},
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "quality": quality,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
         }
@@ -476,7 +639,8 @@ def main():
     ap.add_argument("--scale", type=int, default=27)
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--ref-scale", type=int, default=22)
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="wall-time budget (s) for the reference arm's timed runs")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--thread-max", type=int, default=0)

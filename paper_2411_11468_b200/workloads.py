@@ -82,3 +82,42 @@ def cpu_sample(name: str, ref_scale: int = 22, seed: int = 1, device: int = 0):
     g = dg.download()
     dg.free()
     return g, desc
+
+
+def export_csr(name: str, scale: int, seed: int, out_dir: str, device: int = 0) -> dict:
+    """Build the workload on the device and write its host CSR as raw arrays
+    (`offsets.u64`, `targets.u32`, `meta.json`) into out_dir. bench.py's reference arm
+    runs this in a child process, so the process that times the reference library never
+    maps libnulpa.so."""
+    import json
+    import os
+    dg, desc = build(name, scale, seed, device)
+    g = dg.download()
+    n, m2 = g.order(), g.directed_size()
+    dg.free()
+    os.makedirs(out_dir, exist_ok=True)
+    g.offsets.tofile(os.path.join(out_dir, "offsets.u64"))
+    g.targets.tofile(os.path.join(out_dir, "targets.u32"))
+    meta = {**desc, "n": n, "m2": m2, "scale": scale, "seed": seed}
+    with open(os.path.join(out_dir, "meta.json"), "w") as f:
+        json.dump(meta, f)
+    return meta
+
+
+def _main(argv=None) -> int:
+    import argparse
+    ap = argparse.ArgumentParser(prog="python -m paper_2411_11468_b200.workloads")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    ex = sub.add_parser("export", help="write a workload's CSR as raw arrays")
+    ex.add_argument("--workload", default="rmat", choices=["rmat", "grid", "web", "sbm"])
+    ex.add_argument("--scale", type=int, default=27)
+    ex.add_argument("--seed", type=int, default=1)
+    ex.add_argument("--device", type=int, default=0)
+    ex.add_argument("--out", required=True)
+    a = ap.parse_args(argv)
+    export_csr(a.workload, a.scale, a.seed, a.out, a.device)
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(_main())

@@ -102,8 +102,9 @@ def test_grid4096_sync_step_vs_reference():
 
 
 def test_web_hubs_over_1m_sync_step_vs_reference():
-    # Chung-Lu power law with 3 hubs forced to degree 1.2M: the hub tier's global tables
-    dg = lp.DeviceGraph.web(3_000_000, 12_000_000, 2.1, 3, 1_200_000, seed=5)
+    # Chung-Lu power law with 3 hubs of expected degree 2.5M (distinct neighbours > 1M
+    # after dedup): the hub tier's global tables
+    dg = lp.DeviceGraph.web(16_000_000, 24_000_000, 2.1, 3, 2_500_000, seed=5)
     g = dg.download()
     dg.free()
     deg = np.diff(g.offsets.astype(np.int64))

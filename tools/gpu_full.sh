@@ -7,7 +7,7 @@ bash tools/gpu_check.sh $TAG
 for w in sbm grid web; do
   timeout 900 python bench.py --workload $w --steps 3 --warmup 3 --e2e-steps 1 2>&1 | tail -1 > gpurun_out/${TAG}_bench_$w.json
 done
-timeout 900 python bench.py --scale 24 --steps 3 --warmup 3 --e2e-steps 1 --ref-scale 20 2>&1 | tail -1 > gpurun_out/${TAG}_bench_rmat24.json
+timeout 900 python bench.py --scale 24 --steps 3 --warmup 3 --e2e-steps 1 2>&1 | tail -1 > gpurun_out/${TAG}_bench_rmat24.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/${TAG}_launches_bench.log 2>&1
 timeout 1200 bash tools/profile_kernels.sh 27 ${TAG}_r27_full 0 6 > gpurun_out/${TAG}_ncu_full.log 2>&1
