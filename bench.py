@@ -221,7 +221,10 @@ def run_reference_cpu(rg, n_runs: int, workload: str, budget_s: float = 1e9, g_o
     out = []
     t0 = time.time()
     for _ in range(n_runs):
+        t1 = time.time()
         labels, st = O.ref_lpa(rg, exec_mode=0, workers=workers, switch_degree=sd)
+        _log(f"reference lpa(): {st['iterations']} iterations, elapsed {st['elapsed_seconds']:.2f} s, "
+             f"wall {time.time() - t1:.1f} s")
         out.append((labels, st))
         if time.time() - t0 > budget_s:
             break
@@ -262,6 +265,11 @@ def sbm_quality(nulpa_q=None) -> dict:
     return out
 
 
+def _log(msg: str) -> None:
+    sys.stderr.write(f"[bench {time.strftime('%H:%M:%S')}] {msg}\n")
+    sys.stderr.flush()
+
+
 def bench_reference(args):
     """The reference's own CPU implementation (oracle/_ref, the unmodified reference library)
     on the SAME workload as the nulpa arm: R-MAT scale 27 (or the largest scale that fits
@@ -280,7 +288,9 @@ def bench_reference(args):
     if args.workload == "rmat":
         scale = ref_fit_scale(args.scale, host["mem_available_gb"])
     t0 = time.time()
+    _log(f"reference arm: exporting {args.workload} scale {scale} (host {host})")
     off, tgt, meta, cleanup = export_graph(args.workload, scale, args.seed)
+    _log(f"exported n={meta['n']} m2={meta['m2']} in {time.time() - t0:.1f} s")
     try:
         rg = O.RefGraph.from_csr(off, tgt, None)
         g_off = np.array(off)
@@ -288,14 +298,18 @@ def bench_reference(args):
         del tgt
         cleanup()
     build_s = time.time() - t0
+    _log(f"reference CsrGraph built ({build_s:.1f} s)")
     n, m2 = rg.n, rg.m2
     runs, workers, sd = run_reference_cpu(rg, args.steps, args.workload,
                                           budget_s=args.ref_budget, g_off=g_off)
+    _log(f"{len(runs)} reference run(s): " + ", ".join(
+        f"{st['elapsed_seconds']:.2f} s" for _, st in runs))
     secs = sum(st["elapsed_seconds"] for _, st in runs)
     value = m2 * len(runs) / secs
     q0 = time.time()
     q = O.ref_modularity(rg, runs[-1][0])
     q_s = time.time() - q0
+    _log(f"reference modularity {q:.6g} ({q_s:.1f} s)")
     del rg
     quality = sbm_quality()
     same = args.workload != "rmat" or scale == args.scale
@@ -543,9 +557,10 @@ def bench_nulpa(args):
 
 
 def bench_partitioned(args):
-    """N > 1: the graph is split edge-balanced over the ranks; every pass each
-    rank processes its own range, then labels are all-gathered and wake flags MIN-reduced
-    over NCCL (paper_2411_11468_b200/dist.py). Total work is fixed: strong scaling."""
+    """N > 1: the graph is split edge-balanced over the ranks; each rank keeps
+    only its rows on the device (nulpa_graph_slice) and every pass exchanges changed
+    labels (or the padded owned ranges) and wake flags over NCCL
+    (paper_2411_11468_b200/dist.py). Total work is fixed: strong scaling."""
     import torch
     import torch.distributed as dist
     rank, world, local = dist_env()
@@ -562,7 +577,8 @@ def bench_partitioned(args):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2411_11468_b200 import _capi
     from paper_2411_11468_b200 import labelprop as lp
-    from paper_2411_11468_b200.dist import DeviceRangeEngine, Exchange, run_partitioned
+    from paper_2411_11468_b200.dist import (DeviceRangeEngine, Exchange, partitioned_modularity,
+                                            run_partitioned)
 
     def dmax(x: float) -> float:
         t = torch.tensor([x], dtype=torch.float64, device="cpu" if gloo else f"cuda:{local}")
@@ -577,10 +593,24 @@ def bench_partitioned(args):
     b = (C.c_uint32 * (world + 1))()
     _capi.check(_capi.lib().nulpa_graph_edge_ranges(dg._h, world, b))
     bounds = list(b)
+    lo, hi = bounds[rank], bounds[rank + 1]
     cfg = lp.LpaConfig()
     tuning = lp.Tuning(thread_max_degree=args.thread_max, warp_max_degree=args.warp_max,
                        block_max_degree=args.block_max)
-    eng = DeviceRangeEngine(dg, cfg, bounds[rank], bounds[rank + 1], tuning)
+    # this rank's rows only: the full graph (generated on every rank) is freed
+    eng = DeviceRangeEngine(dg, cfg, lo, hi, tuning, own_rows_only=True)
+    slice_m2 = eng.graph.m2
+    # host copy of this rank's slice (pinned) for the end-to-end leg
+    off_h = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+    tgt_h = torch.empty(max(1, slice_m2), dtype=torch.int32, pin_memory=True)
+    _capi.check(_capi.lib().nulpa_graph_download_raw(eng.graph._h, off_h.data_ptr(),
+                                                     tgt_h.data_ptr(), None))
+    perm_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    inv_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    simple = C.c_int()
+    _capi.check(_capi.lib().nulpa_graph_download_layout(eng.graph._h, perm_h.data_ptr(),
+                                                        inv_h.data_ptr(), C.byref(simple)))
+    dg.free()
     ex = Exchange(bounds, staged=gloo)
     for _ in range(args.warmup):
         run_partitioned(eng, cfg, rank, world, ex, n)
@@ -597,12 +627,50 @@ def bench_partitioned(args):
         torch.cuda.synchronize()
         dist.barrier()
     secs = dmax(ev0.elapsed_time(ev1) * 1e-3)
-    pass_ms = dmax(sum(sum(s.pass_ms) for s in stats))
-    exch_ms = dmax(sum(sum(s.exchange_ms) for s in stats))
-    vl = eng.vertex_labels() if rank == 0 else None
-    q = dg.modularity_device(vl.data_ptr()) if rank == 0 else None
-    comms = dg.community_count_device(vl.data_ptr()) if rank == 0 else None
-    launches = int(sum(s.kernel_launches for s in stats))
+    pass_s = sum(sum(st.pass_ms) for st in stats) * 1e-3
+    pass_s_max = dmax(pass_s)
+    local_bytes = sum(st.local_bytes for st in stats)
+    # roofline: this rank's algorithmic bytes over its pass time; the slowest rank
+    achieved = dmax(local_bytes / max(pass_s, 1e-9) / 1e9)
+    peak, peak_src = hbm_peak()
+    q = partitioned_modularity(eng, staged=gloo)
+    launches = int(sum(st.kernel_launches for st in stats))
+
+    # e2e: every step uploads this rank's rows from pinned host memory (offsets + owned
+    # targets, position order), runs the partitioned lpa(), and reads its labels back
+    e2e = None
+    if args.e2e_steps > 0:
+        eng.free()
+        lab_h = torch.empty(max(1, hi - lo), dtype=torch.int32, pin_memory=True)
+        e_times = []
+        for k in range(args.e2e_steps + 1):  # the first step is untimed (pool warm-up)
+            dist.barrier()
+            torch.cuda.synchronize()
+            w0 = time.time()
+            c2 = _capi.nulpa_csr()
+            c2.n, c2.m2 = n, slice_m2
+            c2.offsets, c2.targets, c2.weights = off_h.data_ptr(), tgt_h.data_ptr(), None
+            h = C.c_void_p()
+            # the host slice is already in position order: upload it with its layout
+            _capi.check(_capi.lib().nulpa_graph_upload_positioned(
+                C.byref(c2), perm_h.data_ptr(), inv_h.data_ptr(), simple.value, local,
+                C.byref(h)))
+            g2 = lp.DeviceGraph(h.value, local)
+            e2 = DeviceRangeEngine(g2, cfg, lo, hi, tuning)
+            run_partitioned(e2, cfg, rank, world, ex, n)
+            lab_h.copy_(e2.labels[lo:hi])
+            torch.cuda.synchronize()
+            e2.free()
+            g2.free()
+            if k:
+                e_times.append(time.time() - w0)
+        e_wall = dmax(sum(e_times))
+        e2e = {"value": args.e2e_steps * m2 / e_wall, "unit": UNIT,
+               "h2d_bytes_per_step": int((n + 1) * 8 + slice_m2 * 4 + 2 * n * 4),
+               "d2h_bytes_per_step": int((hi - lo) * 4), "steps": args.e2e_steps,
+               "seconds_per_step": e_wall / args.e2e_steps, "host_memory": "pinned",
+               "per_rank": "its own rows (offsets + targets of its range, position order) "
+                           "and the position layout up, its labels down"}
     if rank == 0:
         s0 = stats[-1]
         line = {
@@ -610,17 +678,28 @@ def bench_partitioned(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic",
-            "config": {**wdesc, "n": n, "m2": m2,
-                       "parallelism": f"edge-balanced 1-D partition x{world}, replicated labels, "
-                                      "NCCL all-gather-v + MIN-reduce of wake flags per pass",
+            "config": {**wdesc, "n": n, "m2": m2, "undirected_edges": m2 // 2,
+                       "parallelism": f"edge-balanced 1-D partition x{world}: each rank holds "
+                                      "its rows only; replicated labels; per pass one counter "
+                                      "all-gather, a changed-only (or padded full-range) label "
+                                      "all-gather and a MIN reduce-scatter of wake flags (NCCL)",
                        "bounds": bounds, "exec": "ParallelAsync (Jacobi across ranks)",
                        "iterations": s0.iterations, "delta_n": s0.delta_n_per_iter,
-                       "converged": s0.converged, "modularity": q, "communities": comms,
-                       "pass_ms_per_step_max_rank": pass_ms / args.steps,
-                       "exchange_ms_per_step_max_rank": exch_ms / args.steps,
-                       "generate_seconds": gen_s,
+                       "converged": s0.converged, "modularity": q,
+                       "exchange_modes": s0.exchange_modes,
+                       "exchange_bytes_per_step_rank0": sum(s0.exchange_bytes),
+                       "pass_ms_per_step_max_rank": 1e3 * pass_s_max / args.steps,
+                       "generate_seconds": gen_s, "slice_m2_rank0": slice_m2,
                        "l2": "inputs (>= 17 GB) far exceed the 126 MB L2; no flush needed"},
-            "roofline": None, "e2e": None, "cpu_baseline": None, "clocks": clk.summary(),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "whole pass, per rank",
+                         "peak_source": peak_src,
+                         "note": "slowest rank's SURVEY §8d algorithmic bytes over its pass time"},
+            "e2e": e2e,
+            "cpu_baseline": None,
+            "cpu_baseline_note": "the reference CPU baseline is reported by the N=1 line (rank 0, "
+                                 "N=1 only per the bench contract)",
+            "clocks": clk.summary(),
             "gpu_launches": launches,
         }
         print(json.dumps(line))

@@ -310,6 +310,40 @@ int nulpa_session_init(nulpa_session* s);
  * resets every flag before the next pass, see engine.cu run_lpa). */
 int nulpa_session_pass(nulpa_session* s, int pick_less, int wake, nulpa_pass_info* info);
 int nulpa_session_free(nulpa_session* s);
+/* Run the session's kernels on `stream` (a cudaStream_t, e.g. the caller's collective
+ * stream) instead of its own, so caller work on that stream needs no host sync. */
+int nulpa_session_set_stream(nulpa_session* s, void* stream);
+/* Changed-only label exchange: after a pass, write the (position, label) pairs of the
+ * range's labels that changed in it to out_dev[2*cap], padded with 0xFFFFFFFF pairs
+ * (cap >= the pass's changed count); apply_changes writes all-gathered pairs into this
+ * rank's replica (0xFFFFFFFF pairs skipped). Both run on `stream` (a cudaStream_t;
+ * NULL = the legacy default stream). */
+int nulpa_session_pack_changes(nulpa_session* s, uint32_t* out_dev, uint32_t cap, void* stream);
+int nulpa_session_apply_changes(nulpa_session* s, const uint32_t* in_dev, uint64_t pairs,
+                                void* stream);
+/* One rank's graph of a 1-D partition: the rows [v_begin, v_end) of the position order
+ * (global position ids as targets), every other row empty, the layout of `g` kept. */
+int nulpa_graph_slice(nulpa_graph* g, uint32_t v_begin, uint32_t v_end, nulpa_graph** out);
+/* The resident arrays as stored (position order under the degree-bucket layout), no
+ * conversion: a slice saved this way re-uploads with NULPA_LAYOUT_IDENTITY as the same
+ * position-order rows. NULL arrays are skipped. */
+int nulpa_graph_download_raw(const nulpa_graph* g, uint64_t* offsets, uint32_t* targets,
+                             float* weights);
+/* The position layout of a resident graph: perm[p] = vertex id at position p, inv[v] =
+ * position of vertex v (n entries each), and whether every input row was strictly
+ * ascending. Fails on an identity-layout graph. */
+int nulpa_graph_download_layout(const nulpa_graph* g, uint32_t* perm, uint32_t* inv,
+                                int* rows_simple);
+/* Upload a host CSR that is ALREADY in position order (e.g. one rank's slice saved with
+ * nulpa_graph_download_raw) together with its layout; no relayout, no plan. */
+int nulpa_graph_upload_positioned(const nulpa_csr* csr, const uint32_t* perm,
+                                  const uint32_t* inv, int rows_simple, int device,
+                                  nulpa_graph** out);
+/* sigma_c (intra-community stored weight) and Sigma_c (summed weighted degree) over the
+ * rows `g` holds, quality.cpp:29-40, into device arrays of n doubles indexed by label;
+ * labels are in POSITION order. Summed over a partition's slices they are the graph's. */
+int nulpa_community_sums_graph(nulpa_graph* g, const uint32_t* labels_pos_dev, double* sigma_dev,
+                               double* big_dev);
 
 #ifdef __cplusplus
 }

@@ -125,6 +125,16 @@ _SIGS = {
     "nulpa_graph_from_edge_list": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
                                              C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "nulpa_graph_load": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "nulpa_session_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "nulpa_session_pack_changes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p]),
+    "nulpa_session_apply_changes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "nulpa_graph_slice": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "nulpa_graph_download_raw": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "nulpa_graph_download_layout": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.POINTER(C.c_int)]),
+    "nulpa_graph_upload_positioned": (C.c_int, [C.POINTER(nulpa_csr), C.c_void_p, C.c_void_p,
+                                                C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "nulpa_community_sums_graph": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "nulpa_write_edge_list": (C.c_int, [C.c_char_p, C.POINTER(nulpa_csr)]),
     "nulpa_write_membership": (C.c_int, [C.c_char_p, C.c_void_p, C.c_uint64, C.c_int]),
     "nulpa_read_membership": (C.c_int, [C.c_char_p, C.c_uint32, C.c_void_p]),

@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # tuning experiments: extra nvcc flags (e.g. -DNULPA_WIDE_LIMIT=8192); rebuild with force=True
 EXTRA_NVCC = os.environ.get("NULPA_NVCC_FLAGS", "").split()
-CU_SOURCES = ["graph.cu", "layout.cu", "engine.cu", "quality.cu", "gen.cu", "build_csr.cu", "textout.cu"]
+CU_SOURCES = ["graph.cu", "layout.cu", "engine.cu", "quality.cu", "gen.cu", "build_csr.cu", "textout.cu", "partition.cu"]
 CXX_SOURCES = ["dropin.cpp", "textio.cpp"]
 
 

@@ -209,6 +209,51 @@ __device__ __forceinline__ W edge_weight(const Graph& g, uint64_t e) {
     return W(1);
 }
 
+// ---- TMA bulk copies (cp.async.bulk, 1-D) with an mbarrier --------------------------
+// Row slices of the adjacency are staged into shared memory by the copy engine: one
+// thread arms the stage's mbarrier with the byte count and issues the bulk copy; every
+// consumer waits on the barrier's phase parity. The copy needs 16-byte alignment of
+// both addresses and of the size, so a slice is widened to whole 4-entry groups.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+// Make barrier initialisation visible to the async (copy-engine) proxy.
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// Arm `bar` for `bytes` and start the bulk copy global -> shared (evict-first in L2: the
+// targets stream once per pass).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+// Complete the barrier's phase without a copy (an empty stage).
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // ---- (value, key) argmax, ties to the smaller key (ht_better, hashtable.hpp:163-169) ----
 // Candidate values travel as order-preserving u32 bits (integer counts, or the
 // bits of non-negative fp32 sums); fp64 sums travel as doubles.

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -117,6 +118,32 @@ struct Prof {
   }
 };
 
+// Wide-tier variant (NULPA_WIDE_MODE, read once): 0 = plain coalesced target loads,
+// rounds in program order (default); 1 = label prefetch one round ahead; 2 = TMA-staged
+// targets + label prefetch. Measured at R-MAT 27: 29.5 / 30.7 / 40.4 ms of
+// wide tier per run, identical results, so the plain kernel is the default.
+inline int wide_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("NULPA_WIDE_MODE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
+template <int MODE, typename W>
+void launch_wide(const Plan& p, const PassCtx& c, cudaStream_t s, int sms) {
+  const uint32_t cnt = p.count[T_CLUSTER];
+  auto go = [&](auto kernel, size_t smem) {
+    kernel<<<resident_grid(kernel, kBigThreads, smem, cnt, 1, sms), kBigThreads, smem, s>>>(
+        c, p.list[T_CLUSTER], cnt, c.fresh, p.wide_scratch, p.wide_stride, p.m2);
+  };
+  switch (wide_mode()) {
+    case 0: go(k_wide<MODE, W, false, false>, wide_bytes(false)); break;
+    case 1: go(k_wide<MODE, W, false, true>, wide_bytes(false)); break;
+    default: go(k_wide<MODE, W, true, true>, wide_bytes(true));
+  }
+}
+
 // One pass over every tier (SURVEY §3.1 "new B200 stack"). `ctr` holds one
 // C_COUNT block per tier. Returns the number of kernels launched.
 template <int MODE, typename W, bool WEIGHTED>
@@ -153,7 +180,11 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     allow_smem(k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, kDedupLater>, big_smem);
     allow_smem(k_team<MODE, W, WEIGHTED, kMidThreads, kMidThreads, kBigCap, kBigMax, 0>, big_smem);
     allow_smem(k_cluster<MODE, W, WEIGHTED>, cluster_smem);
-    if constexpr (!WEIGHTED) allow_smem(k_wide<MODE, W>, wide_bytes());
+    if constexpr (!WEIGHTED) {
+      allow_smem(k_wide<MODE, W, true, true>, wide_bytes(true));
+      allow_smem(k_wide<MODE, W, false, true>, wide_bytes(false));
+      allow_smem(k_wide<MODE, W, false, false>, wide_bytes(false));
+    }
     allow_smem(k_hub_accum<MODE, W, WEIGHTED, 1>, hub_smem);
     allow_smem(k_hub_accum<MODE, W, WEIGHTED, 0>, hub_smem);
   });
@@ -236,10 +267,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
       k_cluster<MODE, W, WEIGHTED><<<gc, kBigThreads, cluster_smem, s>>>(c, p.list[T_CLUSTER],
                                                                         p.count[T_CLUSTER]);
     else
-      k_wide<MODE, W><<<resident_grid(k_wide<MODE, W>, kBigThreads, wide_bytes(),
-                                      p.count[T_CLUSTER], 1, sms),
-                        kBigThreads, wide_bytes(), s>>>(c, p.list[T_CLUSTER], p.count[T_CLUSTER],
-                                                        c.fresh, p.wide_scratch, p.wide_stride);
+      launch_wide<MODE, W>(p, c, s, sms);
     prof.end(T_CLUSTER, s);
     ++launches;
   }
@@ -774,11 +802,14 @@ struct nulpa_session {
   uint32_t* labels = nullptr;  // caller device array [n] (replicated)
   uint8_t* flags = nullptr;    // caller device array [n]
   nulpa::DBuf<uint32_t> staging, changed;
+  nulpa::DBuf<uint32_t> snapshot;  // labels[lo, hi) at the start of the last pass
   nulpa::DBuf<unsigned long long> ctr;
   nulpa::DBuf<unsigned int> work{2};
   nulpa::Pinned hc{nulpa::dev::kTiers * nulpa::dev::C_COUNT};
   nulpa::Stream stream;
   int sms = 148, vbytes = 4;
+  cudaStream_t ext = nullptr;   // caller's stream (nulpa_session_set_stream; may be the
+  bool has_ext = false;         // legacy default stream 0), else `stream`
   bool fresh = false;           // labels are the identity (after nulpa_session_init)
   bool identity_first = false;  // graph allows the table-free first pass
   ~nulpa_session() { delete plan; }
@@ -789,6 +820,42 @@ namespace {
 __global__ void k_copy_range(const uint32_t* src, uint32_t* dst, uint32_t lo, uint32_t hi) {
   for (uint32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x)
     dst[i] = src[i];
+}
+
+// Changed-only exchange: (position, label) pairs of the range's changed labels,
+// compacted with one atomic per warp, then padded with kEmpty pairs up to `cap`.
+__global__ void k_pack_changes(const uint32_t* lab, const uint32_t* snap, uint32_t lo, uint32_t hi,
+                               uint32_t* out, uint32_t cap, unsigned* count) {
+  const uint32_t span = hi - lo, bound = (span + 31u) & ~31u;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < bound; t += gridDim.x * blockDim.x) {
+    const bool ch = t < span && lab[lo + t] != snap[t];
+    const unsigned m = __ballot_sync(dev::kFull, ch);
+    if (!m) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned b = 0;
+    if (lane == leader) b = atomicAdd(count, static_cast<unsigned>(__popc(m)));
+    b = __shfl_sync(dev::kFull, b, leader) + __popc(m & ((1u << lane) - 1u));
+    if (ch && b < cap) {
+      out[2ull * b] = lo + t;
+      out[2ull * b + 1] = lab[lo + t];
+    }
+  }
+}
+
+__global__ void k_pad_changes(uint32_t* out, uint32_t cap, const unsigned* count) {
+  const uint32_t first = min(*count, cap);
+  for (uint32_t k = first + blockIdx.x * blockDim.x + threadIdx.x; k < cap; k += gridDim.x * blockDim.x) {
+    out[2ull * k] = dev::kEmpty;
+    out[2ull * k + 1] = dev::kEmpty;
+  }
+}
+
+__global__ void k_apply_changes(uint32_t* lab, const uint32_t* in, uint64_t pairs) {
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < pairs;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t p = in[2 * k];
+    if (p != dev::kEmpty) lab[p] = in[2 * k + 1];
+  }
 }
 
 __global__ void k_edge_bounds(const uint64_t* off, uint32_t n, uint32_t parts, uint32_t* bounds) {
@@ -819,7 +886,7 @@ __global__ void k_edge_bounds(const uint64_t* off, uint32_t n, uint32_t parts, u
 void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* info) {
   using namespace dev;
   nulpa_graph* g = ss->g;
-  cudaStream_t s = ss->stream.s;
+  cudaStream_t s = ss->has_ext ? ss->ext : ss->stream.s;
   constexpr int kCtr = kTiers * C_COUNT;
   NULPA_CUDA(cudaMemsetAsync(ss->ctr.p, 0, kCtr * sizeof(unsigned long long), s));
   PassCtx c;
@@ -840,6 +907,10 @@ void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* i
   cudaEvent_t e0, e1;
   NULPA_CUDA(cudaEventCreate(&e0));
   NULPA_CUDA(cudaEventCreate(&e1));
+  // the range's labels before the pass (nulpa_session_pack_changes diffs against it)
+  if (ss->hi > ss->lo)
+    NULPA_CUDA(cudaMemcpyAsync(ss->snapshot.p, ss->labels + ss->lo, (ss->hi - ss->lo) * 4ull,
+                               cudaMemcpyDeviceToDevice, s));
   NULPA_CUDA(cudaEventRecord(e0, s));
   uint64_t launches = 0;
   const bool first =
@@ -1087,6 +1158,7 @@ int nulpa_session_create(nulpa_graph* g, const nulpa_opts* opts, const nulpa_tun
       ss->plan = build_plan(g, resolve_tiers(opts->switch_degree, tuning), ss->vbytes,
                             ss->stream.s, v_begin, v_end);
       ss->ctr = DBuf<unsigned long long>(dev::kTiers * dev::C_COUNT);
+      ss->snapshot = DBuf<uint32_t>(uint64_t(v_end - v_begin) + 1);
       if (opts->exec == NULPA_EXEC_SYNCHRONOUS) {
         ss->staging = DBuf<uint32_t>(g->n);
         ss->changed = DBuf<uint32_t>(uint64_t(v_end - v_begin) + 1);
@@ -1103,10 +1175,11 @@ int nulpa_session_init(nulpa_session* ss) {
   return guarded([&] {
     if (!ss) throw Error(NULPA_EINVAL, "null session");
     use_device(ss->g->device);
-    k_init<<<grid_for(ss->g->n, 256, ss->sms * 8), 256, 0, ss->stream.s>>>(
+    cudaStream_t st = ss->has_ext ? ss->ext : ss->stream.s;
+    k_init<<<grid_for(ss->g->n, 256, ss->sms * 8), 256, 0, st>>>(
         ss->labels, ss->flags, ss->g->offsets, ss->g->n, ss->g->perm);
     NULPA_CUDA(cudaGetLastError());
-    NULPA_CUDA(cudaStreamSynchronize(ss->stream.s));
+    NULPA_CUDA(cudaStreamSynchronize(st));
     ss->fresh = true;
   });
 }
@@ -1116,6 +1189,42 @@ int nulpa_session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_in
     if (!ss) throw Error(NULPA_EINVAL, "null session");
     use_device(ss->g->device);
     session_pass(ss, pick_less, wake, info);
+  });
+}
+
+int nulpa_session_set_stream(nulpa_session* ss, void* stream) {
+  return guarded([&] {
+    if (!ss) throw Error(NULPA_EINVAL, "null session");
+    ss->ext = static_cast<cudaStream_t>(stream);
+    ss->has_ext = true;
+  });
+}
+
+int nulpa_session_pack_changes(nulpa_session* ss, uint32_t* out_dev, uint32_t cap, void* stream) {
+  return guarded([&] {
+    if (!ss || (cap && !out_dev)) throw Error(NULPA_EINVAL, "null argument");
+    use_device(ss->g->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned* cnt = ss->work.p + 1;
+    NULPA_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned), st));
+    const uint32_t span = ss->hi - ss->lo;
+    if (span)
+      k_pack_changes<<<grid_for(span, 256, ss->sms * 8), 256, 0, st>>>(
+          ss->labels, ss->snapshot.p, ss->lo, ss->hi, out_dev, cap, cnt);
+    if (cap) k_pad_changes<<<grid_for(cap, 256, ss->sms * 4), 256, 0, st>>>(out_dev, cap, cnt);
+    NULPA_CUDA(cudaGetLastError());
+  });
+}
+
+int nulpa_session_apply_changes(nulpa_session* ss, const uint32_t* in_dev, uint64_t pairs,
+                                void* stream) {
+  return guarded([&] {
+    if (!ss || (pairs && !in_dev)) throw Error(NULPA_EINVAL, "null argument");
+    use_device(ss->g->device);
+    if (pairs)
+      k_apply_changes<<<grid_for(pairs, 256, ss->sms * 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+          ss->labels, in_dev, pairs);
+    NULPA_CUDA(cudaGetLastError());
   });
 }
 

@@ -379,6 +379,7 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
     p->value_bytes = value_bytes;
     p->v_lo = v_lo;
     p->v_hi = v_hi;
+    p->m2 = g->m2;
     const uint32_t span = v_hi - v_lo;
     p->weighted = g->weights != nullptr;
     const uint64_t tm = tb.thread_max;

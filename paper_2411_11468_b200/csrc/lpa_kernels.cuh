@@ -785,9 +785,6 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
 #ifndef NULPA_WIDE_LIMIT
 #define NULPA_WIDE_LIMIT 12288
 #endif
-#ifndef NULPA_WIDE_U
-#define NULPA_WIDE_U 4
-#endif
 constexpr uint32_t kWideLimit = NULPA_WIDE_LIMIT;  // distinct labels per phase (load <= 3/4)
 
 __device__ __forceinline__ uint32_t phase_of(uint32_t key, uint32_t P) {
@@ -801,33 +798,74 @@ constexpr uint32_t kWideBuckets = NULPA_WIDE_BUCKETS;  // P <= this is bucketed;
 static_assert((kWideBuckets - 1) * uint64_t(kClusterMax) <= kWideScratch,
               "wide scratch holds every bucket layout");
 
-constexpr size_t wide_bytes() {
+constexpr size_t wide_table_bytes() {
   return size_t(kClusterCap) * 8 + size_t(kClusterCap) * sizeof(uint16_t);
 }
+#ifndef NULPA_WIDE_U
+#define NULPA_WIDE_U 4
+#endif
+constexpr uint32_t kWideChunk = kBigThreads * NULPA_WIDE_U;  // row entries per gather round
+constexpr uint32_t kWideStage = kWideChunk + 8;  // one TMA stage (widened to 16-byte groups)
+// STAGED kernels add two TMA stages of row targets after the table.
+constexpr size_t wide_bytes(bool staged = false) {
+  return wide_table_bytes() + (staged ? 2 * size_t(kWideStage) * sizeof(uint32_t) : 0);
+}
 
-template <int MODE, typename W>
+// STAGED: phase 0 streams the row's targets into shared memory with TMA bulk copies,
+// two chunks ahead of the label gather (mbarrier per stage). PREFETCH: the labels of
+// round r + 1 are gathered before round r is inserted, so the dependent label loads are
+// in flight while the table atomics of the previous round run.
+template <int MODE, typename W, bool STAGED = true, bool PREFETCH = true>
 __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32_t* __restrict__ list,
                                                          uint32_t count, int fresh,
                                                          uint32_t* __restrict__ scratch,
-                                                         uint32_t stride) {
-  // This CTA's row snapshot: phase 0 of a multi-phase vertex gathers the labels
-  // once and writes them here (L2-resident); later phases stream them back.
+                                                         uint32_t stride, uint64_t m2) {
+  // This CTA's row snapshot / phase buckets (L2-resident): phase 0 of a multi-phase
+  // vertex writes the labels of later phases here; those phases stream them back.
   uint32_t* snap = scratch + size_t(blockIdx.x) * stride;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemTable<W> tab;
   tab.bind(smem_raw, kClusterCap);
   uint16_t* occ = reinterpret_cast<uint16_t*>(smem_raw + size_t(kClusterCap) * 8);
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw + wide_table_bytes());
   __shared__ uint32_t s_item;
   __shared__ int s_flag, s_over;
   __shared__ unsigned s_occ_n;
   __shared__ unsigned s_bcnt[kWideBuckets];
   __shared__ Best<VBits<W>> red[32];
+  __shared__ __align__(8) uint64_t s_bar[2];
   constexpr uint32_t kWideBatch = 4;  // vertices per work-counter fetch (batched prologue)
   __shared__ Meta s_meta[kWideBatch];
   for (uint32_t x = threadIdx.x; x < kClusterCap; x += blockDim.x) tab.clear_slot(x);  // once
+  if (STAGED && threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_init_fence();
+  }
   const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0, fails = 0;
   constexpr int U = NULPA_WIDE_U;  // gather rounds in flight per thread
+  constexpr uint32_t CH = kWideChunk;
+  uint32_t par = 0;  // phase parity of each TMA stage (bit b), identical in every thread
+  // The 16-byte-group window [a0, a1) of chunk k of the row at `lo` (degree d) that a
+  // bulk copy can move; entries past m2 & ~3 (the array's last partial group) are read
+  // from global memory instead.
+  auto window = [&](uint64_t lo, uint32_t d, uint32_t k, uint64_t& a0, uint64_t& a1) {
+    const uint64_t g0 = lo + uint64_t(k) * CH;
+    const uint64_t g1 = lo + min(uint64_t(d), uint64_t(k + 1) * CH);
+    a0 = g0 & ~3ull;
+    a1 = min((g1 + 3) & ~3ull, m2 & ~3ull);
+  };
+  auto issue = [&](uint64_t lo, uint32_t d, uint32_t k) {  // thread 0 only
+    uint64_t a0, a1;
+    window(lo, d, k, a0, a1);
+    uint64_t* bar = &s_bar[k & 1];
+    if (a1 > a0)
+      tma_load_1d(stage + (k & 1) * kWideStage, c.g.tgt + a0, static_cast<uint32_t>(a1 - a0) * 4u,
+                  bar, pol);
+    else
+      mbar_arrive(bar);
+  };
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(c.work, kWideBatch);
     __syncthreads();
@@ -858,6 +896,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
       __syncthreads();
       // A phase can only overflow when it may hold more than kWideLimit labels.
       const uint32_t len = (use_b && ph > 0) ? s_bcnt[ph] : d;
+      const uint32_t nch = (len + CH - 1) / CH;
       // Early stop (a per-round block vote) only where a row may hold more distinct
       // labels than the phase takes and the phase re-streams the whole row. Bucketed
       // phases run to the end: a full table (rare) still flags s_over and restarts.
@@ -865,36 +904,41 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
       const uint32_t cap = P == 1 ? min(static_cast<uint32_t>(kClusterCap), pow2_ceil(2 * d))
                                   : static_cast<uint32_t>(kClusterCap);
       const uint32_t* src = use_b ? snap + size_t(ph - 1) * d : snap;
-      for (uint32_t base = 0; base < len; base += kBigThreads * U) {
-        uint32_t lab[U];
-        if (ph == 0) {
+      const bool from_row = ph == 0;  // phase 0 gathers targets -> labels; later phases stream labels
+      if (STAGED && from_row && threadIdx.x == 0 && nch > 0) {
+        issue(lo, d, 0);
+        if (nch > 1) issue(lo, d, 1);
+      }
+      // Gather round k into lab[] (issues the loads; the values are consumed later).
+      auto gather = [&](uint32_t k, uint32_t (&lab)[U]) {
+        const uint32_t base = k * CH;
+        if (from_row) {
           uint32_t j[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t e = base + u * kBigThreads + threadIdx.x;
-            j[u] = e < d ? ld_stream(c.g.tgt + lo + e, pol) : i;
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t e = base + u * kBigThreads + threadIdx.x;
-            lab[u] = j[u] != i ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
-            if (P > 1 && !use_b && e < d) snap[e] = lab[u];
-          }
-          if (use_b) {
-            const int lane = threadIdx.x & 31;
+          if constexpr (STAGED) {
+            const uint32_t b = k & 1;
+            mbar_wait(&s_bar[b], (par >> b) & 1u);
+            par ^= 1u << b;
+            uint64_t a0, a1;
+            window(lo, d, k, a0, a1);
+            const uint32_t* buf = stage + b * kWideStage;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              const uint32_t q = lab[u] != kEmpty ? phase_of(lab[u], P) : 0u;
-              const unsigned peers = __match_any_sync(kFull, q);
-              unsigned at = 0;
-              const int leader = __ffs(peers) - 1;
-              if (q != 0 && lane == leader) at = atomicAdd(&s_bcnt[q], __popc(peers));
-              at = __shfl_sync(kFull, at, leader) + __popc(peers & ((1u << lane) - 1u));
-              if (q != 0) {
-                snap[size_t(q - 1) * d + at] = lab[u];
-                lab[u] = kEmpty;
-              }
+              const uint32_t e = base + u * kBigThreads + threadIdx.x;
+              const uint64_t gi = lo + e;
+              j[u] = e < d ? (gi < a1 ? buf[gi - a0] : ld_stream(c.g.tgt + gi, pol)) : i;
             }
+          } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t e = base + u * kBigThreads + threadIdx.x;
+              j[u] = e < d ? ld_stream(c.g.tgt + lo + e, pol) : i;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) lab[u] = j[u] != i ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+          if constexpr (STAGED) {
+            __syncthreads();  // every thread has read stage k & 1: refill it with chunk k + 2
+            if (threadIdx.x == 0 && k + 2 < nch) issue(lo, d, k + 2);
           }
         } else {
 #pragma unroll
@@ -903,17 +947,47 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
             lab[u] = e < len ? __ldcg(src + e) : kEmpty;
           }
         }
+      };
+      uint32_t cur[U], nxt[U];
+      if (nch > 0) gather(0, cur);
+      uint32_t k = 0;
+      for (; k < nch; ++k) {
+        if (PREFETCH && k + 1 < nch) gather(k + 1, nxt);
+        const uint32_t base = k * CH;
+        if (from_row) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t e = base + u * kBigThreads + threadIdx.x;
+            if (P > 1 && !use_b && e < d) snap[e] = cur[u];
+          }
+          if (use_b) {
+            const int lane = threadIdx.x & 31;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t q = cur[u] != kEmpty ? phase_of(cur[u], P) : 0u;
+              const unsigned peers = __match_any_sync(kFull, q);
+              unsigned at = 0;
+              const int leader = __ffs(peers) - 1;
+              if (q != 0 && lane == leader) at = atomicAdd(&s_bcnt[q], __popc(peers));
+              at = __shfl_sync(kFull, at, leader) + __popc(peers & ((1u << lane) - 1u));
+              if (q != 0) {
+                snap[size_t(q - 1) * d + at] = cur[u];
+                cur[u] = kEmpty;
+              }
+            }
+          }
+        }
         if (!use_b) {
 #pragma unroll
           for (int u = 0; u < U; ++u)
-            if (P > 1 && lab[u] != kEmpty && phase_of(lab[u], P) != ph) lab[u] = kEmpty;
+            if (P > 1 && cur[u] != kEmpty && phase_of(cur[u], P) != ph) cur[u] = kEmpty;
         }
         const uint32_t wbase = base + (threadIdx.x & ~31u);
         unsigned live = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) live |= (wbase + u * kBigThreads < len ? 1u : 0u) << u;
         unsigned long long f = 0;
-        gather_insert_multi<U, W, 0>(c, lab, live, tab, cap, occ, &s_occ_n, f);
+        gather_insert_multi<U, W, 0>(c, cur, live, tab, cap, occ, &s_occ_n, f);
         if (f) s_over = 1;  // table full: treat as overflow
         // Stop early once the phase holds too many distinct labels: one barrier
         // with a block-wide OR (uniform result). Thread 0's read of the occupancy
@@ -925,6 +999,21 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
             if (threadIdx.x == 0) s_over = 1;
             break;
           }
+        }
+        if (k + 1 < nch) {
+          if constexpr (!PREFETCH) gather(k + 1, nxt);
+#pragma unroll
+          for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+        }
+      }
+      if (STAGED && from_row) {
+        // an early stop leaves issued chunks unconsumed: complete their phases so every
+        // stage's parity stays in step (chunks k+1 .. min(nch-1, g+2) for the last
+        // gathered round g = k + PREFETCH)
+        const uint32_t g = PREFETCH ? min(k + 1, nch - 1) : k;
+        for (uint32_t q = g + 1; q < nch && q <= g + 2; ++q) {
+          mbar_wait(&s_bar[q & 1], (par >> (q & 1)) & 1u);
+          par ^= 1u << (q & 1);
         }
       }
       __syncthreads();

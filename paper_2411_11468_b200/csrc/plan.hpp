@@ -13,6 +13,7 @@ struct Plan {
   uint32_t* wide_scratch = nullptr;  // [SMs x wide_stride] row snapshots / phase buckets of the wide tier
   uint32_t wide_stride = 0;          // u32 per CTA: (NULPA_WIDE_BUCKETS - 1) x the tier's max degree
   uint32_t v_lo = 0, v_hi = 0;  // vertex range the tiers cover
+  uint64_t m2 = 0;              // the graph's target count (TMA windows stay inside it)
   int value_bytes = 4;  // hashtable value width the hub tables were sized for
   // Tier vertex lists (ascending id unless scrambled), indexed by dev::Tier;
   // list[T_HUB] holds the hubs.

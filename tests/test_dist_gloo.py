@@ -40,6 +40,7 @@ class PortRangeEngine:
     def pass_(self, pick_less, wake=True):
         lab = self.labels.numpy().view(np.uint32)
         flg = self.flags.numpy()
+        self.snap = lab[self.lo:self.hi].copy()
         cand, _ = O.port_sync_step(self.pg, lab, pick_less)  # from the frozen snapshot
         own = np.zeros(self.n, bool)
         own[self.lo:self.hi] = True
@@ -51,6 +52,21 @@ class PortRangeEngine:
             flg[self.tgt[self.off[v]:self.off[v + 1]]] = 0
         return {"changed": int(changed.size), "processed_vertices": int(processed.sum()),
                 "processed_edges": 0, "wake_edges": 0, "device_ms": 0.0, "kernel_launches": 0}
+
+    def pack_changes(self, out, cap):
+        """nulpa_session_pack_changes: (position, label) pairs, 0xFFFFFFFF-padded."""
+        lab = self.labels.numpy().view(np.uint32)
+        pos = np.flatnonzero(lab[self.lo:self.hi] != self.snap) + self.lo
+        assert pos.size <= cap
+        o = out.numpy().view(np.uint32)
+        o[:] = 0xFFFFFFFF
+        o[0:2 * pos.size:2] = pos
+        o[1:2 * pos.size:2] = lab[pos]
+
+    def apply_changes(self, packets, pairs):
+        p = packets.numpy().view(np.uint32)[:2 * pairs].reshape(-1, 2)
+        p = p[p[:, 0] != 0xFFFFFFFF]
+        self.labels.numpy().view(np.uint32)[p[:, 0]] = p[:, 1]
 
     def sync(self):
         pass
@@ -64,7 +80,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, cfg_kw, out):
+def _worker(rank, world, port, name, cfg_kw, out, changed_only=True):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     d = load_golden(name)
@@ -72,16 +88,21 @@ def _worker(rank, world, port, name, cfg_kw, out):
     bounds = edge_balanced_bounds(off, world)
     eng = PortRangeEngine(off, tgt, bounds[rank], bounds[rank + 1])
     cfg = LpaConfig(exec=ExecMode.Synchronous, **cfg_kw)
-    st = run_partitioned(eng, cfg, rank, world, Exchange(bounds, staged=True), eng.n)
+    ex = Exchange(bounds, staged=True, changed_only=changed_only)
+    st = run_partitioned(eng, cfg, rank, world, ex, eng.n)
     out[rank] = (eng.labels.numpy().view(np.uint32).copy(), st.delta_n_per_iter, st.converged,
-                 st.pl_iterations)
+                 st.pl_iterations, st.exchange_modes)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["sbm10k_seed101", "random05", "kat_ring_of_cliques"])
-@pytest.mark.parametrize("cfg_kw", [{"pl_period": 4}, {"pl_period": 0}, {"pl_period": 1,
-                                                                        "prune": False}])
-def test_partitioned_sync_equals_single_process(name, cfg_kw):
+CASES = [(name, cfg_kw, True)
+         for name in ["sbm10k_seed101", "random05", "kat_ring_of_cliques"]
+         for cfg_kw in [{"pl_period": 4}, {"pl_period": 0}, {"pl_period": 1, "prune": False}]]
+CASES.append(("sbm10k_seed101", {"pl_period": 4}, False))  # full-range all-gathers only
+
+
+@pytest.mark.parametrize("name,cfg_kw,changed_only", CASES)
+def test_partitioned_sync_equals_single_process(name, cfg_kw, changed_only):
     world = 2
     d = load_golden(name)
     pg = O.PortGraph(d["offsets"], d["targets"], None)
@@ -89,12 +110,17 @@ def test_partitioned_sync_equals_single_process(name, cfg_kw):
                           prune=cfg_kw.get("prune", True))
     manager = mp.Manager()
     out = manager.dict()
-    mp.spawn(_worker, args=(world, _free_port(), name, cfg_kw, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), name, cfg_kw, out, changed_only), nprocs=world,
+             join=True)
     for r in range(world):
-        labels, dn, conv, pli = out[r]
+        labels, dn, conv, pli, modes = out[r]
         assert np.array_equal(labels, want), (name, cfg_kw, r)
         assert dn == ws["delta_n"] and conv == ws["converged"]
         assert pli == ws["pl_iterations"]
+        if not changed_only:
+            assert set(modes) == {"full"}
+        elif name == "sbm10k_seed101":
+            assert "changed-only" in modes and "full" in modes
 
 
 def test_edge_balanced_bounds():
@@ -112,22 +138,32 @@ def test_edge_balanced_bounds():
 # ---- the same driver over the real CUDA session (2 processes sharing one GPU) ------------
 
 
-def _gpu_worker(rank, world, port, scale, out):
+def _gpu_worker(rank, world, port, scale, out, exec_mode="sync", graph="rmat"):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     from paper_2411_11468_b200 import _capi
     from paper_2411_11468_b200 import labelprop as lp
     from paper_2411_11468_b200.dist import DeviceRangeEngine
     import ctypes as C
-    dg = lp.DeviceGraph.rmat(scale, 16, 5)
+    from paper_2411_11468_b200.dist import partitioned_modularity
+    if graph == "rmat":
+        dg = lp.DeviceGraph.rmat(scale, 16, 5)
+    else:
+        import oracle as O
+        off, tgt, _ = O.RefGraph.planted(100000, 100, 14 / 999, 2 / 99000, 1).arrays()
+        dg = lp.DeviceGraph.upload(lp.CsrGraph(off, tgt, None))
     b = (C.c_uint32 * (world + 1))()
     _capi.check(_capi.lib().nulpa_graph_edge_ranges(dg._h, world, b))
     bounds = list(b)
-    cfg = LpaConfig(exec=ExecMode.Synchronous)
-    eng = DeviceRangeEngine(dg, cfg, bounds[rank], bounds[rank + 1])
-    st = run_partitioned(eng, cfg, rank, world, Exchange(bounds, staged=True), dg.n)
+    cfg = LpaConfig(exec=ExecMode.Synchronous if exec_mode == "sync" else ExecMode.ParallelAsync)
+    # each rank keeps only its own rows (nulpa_graph_slice); the full graph is freed
+    eng = DeviceRangeEngine(dg, cfg, bounds[rank], bounds[rank + 1], own_rows_only=True)
+    slice_m2 = eng.graph.m2
+    dg.free()
+    st = run_partitioned(eng, cfg, rank, world, Exchange(bounds, staged=True), eng.n)
+    q = partitioned_modularity(eng, staged=True)
     out[rank] = (eng.vertex_labels().cpu().numpy().view(np.uint32).copy(), st.delta_n_per_iter,
-                 bounds)
+                 bounds, q, slice_m2, st.exchange_modes, st.converged)
     eng.free()
     dist.destroy_process_group()
 
@@ -142,8 +178,35 @@ def test_partitioned_cuda_sessions_equal_single_gpu_sync():
     manager = mp.Manager()
     out = manager.dict()
     mp.spawn(_gpu_worker, args=(world, _free_port(), scale, out), nprocs=world, join=True)
+    g = lp.DeviceGraph.rmat(scale, 16, 5)
+    m2 = g.m2
+    q_want = lp.modularity(g.download(), want.labels)
+    g.free()
     for r in range(world):
-        labels, dn, bounds = out[r]
+        labels, dn, bounds, q, slice_m2, modes, _ = out[r]
         assert 0 < bounds[1] < bounds[2]
         assert np.array_equal(labels, want.labels)
         assert dn == want.stats.delta_n_per_iter
+        assert abs(q - q_want) < 1e-9  # the slices' community sums, all-reduced
+        assert 0 < slice_m2 < m2       # each rank holds only its own rows
+    assert out[0][4] + out[1][4] == m2
+
+
+@pytest.mark.gpu
+def test_partitioned_async_sbm_quality():
+    # partitioned ParallelAsync (Jacobi across ranks, async inside) on the SBM-100K config:
+    # converges, and its modularity meets the north star's bar against the reference's
+    # Synchronous Q (SURVEY §8c gate 3)
+    import oracle as O
+    if not O.ref_available():
+        pytest.skip("needs oracle/_ref")
+    rg = O.RefGraph.planted(100000, 100, 14 / 999, 2 / 99000, 1)
+    lab, _ = O.ref_lpa(rg, exec_mode=2)
+    q_sync = O.ref_modularity(rg, lab)
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_gpu_worker, args=(2, _free_port(), 0, out, "async", "sbm"), nprocs=2, join=True)
+    labels, dn, bounds, q, slice_m2, modes, conv = out[0]
+    assert conv
+    assert abs(q - O.ref_modularity(rg, labels)) < 1e-9
+    assert q >= q_sync - 0.01, (q, q_sync)
