@@ -343,6 +343,37 @@ def bench_reference(args):
     return 0
 
 
+def dropin_e2e(off, tgt, n: int, m2: int, steps: int) -> dict:
+    """Time build/nulpa_dropin_e2e (tools/cpp/dropin_e2e.cpp) on this graph: the reference
+    caller's view — labelprop::lpa(const CsrGraph&, const LpaConfig&) with std::vector
+    storage, every call uploading the graph and returning the labels."""
+    import shutil
+    import tempfile
+    exe = ROOT / "build" / "nulpa_dropin_e2e"
+    if not exe.exists():
+        return {"value": None, "note": f"{exe} not built"}
+    d = tempfile.mkdtemp(prefix="nulpa_dropin_", dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    try:
+        np.asarray(off).tofile(os.path.join(d, "offsets.u64"))
+        np.asarray(tgt).tofile(os.path.join(d, "targets.u32"))
+        r = subprocess.run([str(exe), d, str(steps)], capture_output=True, text=True)
+        if r.returncode != 0:
+            return {"value": None, "note": f"failed: {r.stderr.strip()[-300:]}"}
+        res = json.loads(r.stdout.strip().splitlines()[-1])
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    return {"value": m2 / res["seconds_per_step"], "unit": UNIT,
+            "h2d_bytes_per_step": int((n + 1) * 8 + m2 * 4),
+            "d2h_bytes_per_step": int(n * 4), "steps": steps,
+            "seconds_per_step": res["seconds_per_step"],
+            "loop_seconds_per_step": res["loop_seconds_per_step"],
+            "host_memory": "pageable (std::vector in labelprop::CsrGraph), weights array of "
+                           "1.0f present on the host: unit chunks are detected on the host and "
+                           "not transferred",
+            "api": "labelprop::lpa(const CsrGraph&, const LpaConfig&) (lpa.hpp:84), "
+                   "build/nulpa_dropin_e2e"}
+
+
 def bench_nulpa(args):
     rank, world, local = dist_env()
     dev = local
@@ -502,6 +533,11 @@ def bench_nulpa(args):
         except Exception as e:  # the baseline must never sink the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"failed: {e}"}
+    # e2e through the C++ drop-in itself: labelprop::lpa(CsrGraph) on std::vector storage
+    # (pageable host memory, an explicit all-ones weight array), in a child process
+    dropin = None
+    if rank == 0 and world == 1 and args.dropin_steps > 0 and host_off is not None:
+        dropin = dropin_e2e(host_off, host_tgt, n, m2, args.dropin_steps)
     host_off = host_tgt = None
     if args.e2e_steps > 0:
         del off_h, tgt_h
@@ -544,6 +580,7 @@ def bench_nulpa(args):
                                              "assumes": "32 B sector per neighbour-label "
                                                         "gather (every gather misses L2)"}},
             "e2e": e2e,
+            "e2e_dropin": dropin,
             "cpu_baseline": cpu,
             "quality": quality,
             "clocks": clk.summary(),
@@ -722,6 +759,8 @@ def main():
                     help="wall-time budget (s) for the reference arm's timed runs")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--dropin-steps", type=int, default=2,
+                    help="timed calls of the C++ drop-in e2e leg (0 = skip)")
     ap.add_argument("--thread-max", type=int, default=0)
     ap.add_argument("--warp-max", type=int, default=0)
     ap.add_argument("--block-max", type=int, default=0)

@@ -107,6 +107,9 @@ typedef struct nulpa_tuning {
                                  Any order is a valid asynchronous schedule;
                                  Synchronous/Sequential results do not depend on it. */
   uint32_t no_identity_first; /* 1: disable the table-free first pass from identity labels */
+  uint32_t unbatched;         /* 1: read the counters back after every pass instead of
+                                 enqueueing passes in batches behind the device-side
+                                 convergence guard (same results) */
 } nulpa_tuning;
 
 #define NULPA_TIERS 10 /* 0 thread, 1 half-warp, 2 warp, 3/4/5 32/128/256-thread teams with

@@ -34,7 +34,8 @@ class nulpa_tuning(C.Structure):
     _fields_ = [("thread_max_degree", C.c_uint32), ("warp_max_degree", C.c_uint32),
                 ("block_max_degree", C.c_uint32), ("hub_chunk", C.c_uint32),
                 ("async_first_pass", C.c_uint32), ("profile", C.c_uint32),
-                ("schedule", C.c_uint32), ("no_identity_first", C.c_uint32)]
+                ("schedule", C.c_uint32), ("no_identity_first", C.c_uint32),
+                ("unbatched", C.c_uint32)]
 
 NULPA_TIERS = 10
 TIER_NAMES = ["thread", "half_warp", "warp", "team32", "team128", "team256", "cta512",

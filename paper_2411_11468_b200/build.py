@@ -91,6 +91,21 @@ def build_cpp_tests() -> Path:
     return out
 
 
+def build_tools() -> Path:
+    """tools/cpp/dropin_e2e.cpp -> build/nulpa_dropin_e2e (bench.py's drop-in e2e leg)."""
+    out = ROOT / "build" / "nulpa_dropin_e2e"
+    src = ROOT / "tools" / "cpp" / "dropin_e2e.cpp"
+    if not src.exists():
+        return out
+    deps = [src, LIB] + list((ROOT / "include").rglob("*.h*"))
+    if not _newer(out, deps):
+        out.parent.mkdir(parents=True, exist_ok=True)
+        _run(["g++", "-std=c++20", "-O2", "-I", str(ROOT / "include"), str(src), "-o", str(out),
+              "-L", str(PKG), "-lnulpa", f"-Wl,-rpath,{PKG}",
+              "-Wl,-rpath,$ORIGIN/../paper_2411_11468_b200"])
+    return out
+
+
 def build_checkers() -> None:
     """Test infrastructure only: oracle/liboracle.so and, where the reference
     sources exist, oracle/_ref/libnulpa_ref.so."""
@@ -104,6 +119,7 @@ def main() -> None:
     build_library(force=force)
     build_checkers()
     build_cpp_tests()
+    build_tools()
     print(LIB)
 
 

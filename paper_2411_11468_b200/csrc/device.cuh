@@ -113,6 +113,9 @@ struct PassCtx {
   const uint32_t* vid = nullptr;  // position -> vertex id (layout.cu); nullptr = identity
   const uint32_t* pos = nullptr;  // vertex id -> position; nullptr = identity
   int fresh = 0;                  // labels are still the identity (first pass of a run)
+  // Pass guard (batched runs, engine.cu): set on the device once the run has converged;
+  // every pass kernel enqueued after that returns at once. nullptr = unguarded.
+  const unsigned* stop = nullptr;
 };
 
 // Vertex id stored at position p (label values are vertex ids).
@@ -141,7 +144,13 @@ struct HubCtx {
   uint32_t n_hubs;
   uint32_t n_items;
   uint32_t n_sitems;
+  const unsigned* stop = nullptr;  // pass guard (PassCtx::stop)
 };
+
+// True once a batched run has converged: the kernel has nothing to do (uniform).
+__device__ __forceinline__ bool stopped(const unsigned* stop) {
+  return stop != nullptr && __ldcg(stop) != 0u;
+}
 
 // ---- memory access helpers -------------------------------------------------
 
@@ -337,6 +346,13 @@ __device__ __forceinline__ void probe_advance(int strategy, uint32_t& idx, uint3
   }
 }
 
+// Unit-weight tables count in u32, exactly. The reference's fp32 values (ValuePrecision
+// Bits32) add 1.0f per occurrence, and an fp32 sum of ones stops growing at 2^24
+// (16777216 + 1 rounds back to 16777216, ties to even), so a label repeated more than
+// 2^24 times in one row compares as 2^24 there. The argmax sees the count the reference
+// would: min(count, 2^24). (Integer counts compare like the bits of their float values.)
+__device__ __forceinline__ uint32_t fp32_count(uint32_t count) { return min(count, 16777216u); }
+
 // Insert results: 0 = failed (table full), 1 = counted into an existing key,
 // 2 = claimed a new slot. The slot index is returned through *slot.
 template <bool PACKED, typename W>
@@ -392,7 +408,7 @@ struct Table<true, W> {
     if constexpr (sizeof(W) == 8)
       v = static_cast<double>(static_cast<uint32_t>(x));
     else
-      v = static_cast<uint32_t>(x);  // integer counts compare like their float bits
+      v = fp32_count(static_cast<uint32_t>(x));
   }
   __device__ __forceinline__ W value(uint32_t s) const {
     return static_cast<W>(static_cast<uint32_t>(w[s]));
@@ -489,7 +505,7 @@ struct SmemTable {
     if constexpr (sizeof(W) == 8)
       v = static_cast<double>(static_cast<uint32_t>(x));
     else
-      v = static_cast<uint32_t>(x);
+      v = fp32_count(static_cast<uint32_t>(x));
   }
   __device__ __forceinline__ W value(uint32_t s) const {
     uint32_t v;

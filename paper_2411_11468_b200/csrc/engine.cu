@@ -40,6 +40,17 @@ __global__ void k_init(uint32_t* lab, uint8_t* flags, const uint64_t* off, uint3
   }
 }
 
+// Batched runs: after pass `iter`, sum the tiers' label changes and, on a non-Pick-Less
+// pass with dN / n < tolerance (lpa.cpp:306), stop the run: *stop = iter + 1, and every
+// pass kernel enqueued behind it returns at once (PassCtx::stop).
+__global__ void k_decide(const unsigned long long* ctr, uint32_t n, double tolerance, int pick_less,
+                         int iter, unsigned* stop) {
+  if (threadIdx.x != 0 || *stop) return;
+  unsigned long long dn = 0;
+  for (int t = 0; t < kTiers; ++t) dn += ctr[t * C_COUNT + C_DN];
+  if (!pick_less && static_cast<double>(dn) / n < tolerance) *stop = static_cast<unsigned>(iter + 1);
+}
+
 inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap) {
   const uint64_t b = (work + per_block - 1) / per_block;
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(b, cap)));
@@ -122,12 +133,53 @@ struct Prof {
 // rounds in program order (default); 1 = label prefetch one round ahead; 2 = TMA-staged
 // targets + label prefetch. Measured at R-MAT 27: 29.5 / 30.7 / 40.4 ms of
 // wide tier per run, identical results, so the plain kernel is the default.
+// Thread tier: two list entries per thread iteration (NULPA_THREAD_PAIR, read once; 1 by
+// default) — one claim fence for both, both rows' loads in flight together.
+inline bool thread_pair() {
+  static const bool m = [] {
+    const char* e = std::getenv("NULPA_THREAD_PAIR");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return m;
+}
+
+// Passes enqueued per host read-back in batched runs (NULPA_BATCH_PASSES, read once).
+inline int batch_passes() {
+  static const int m = [] {
+    const char* e = std::getenv("NULPA_BATCH_PASSES");
+    return e ? std::max(1, std::atoi(e)) : 4;
+  }();
+  return m;
+}
+
 inline int wide_mode() {
   static const int m = [] {
     const char* e = std::getenv("NULPA_WIDE_MODE");
     return e ? std::atoi(e) : 0;
   }();
   return m;
+}
+
+// Steps of a k_group batch whose loads are issued together (NULPA_GROUP_STEPS, read once:
+// 8 by default; 1 = one step at a time).
+inline int group_steps() {
+  static const int m = [] {
+    const char* e = std::getenv("NULPA_GROUP_STEPS");
+    return e ? std::atoi(e) : 8;
+  }();
+  return m;
+}
+
+template <int MODE, typename W, bool WEIGHTED, int G>
+void launch_group(const PassCtx& c, const uint32_t* list, uint32_t count, cudaStream_t s, int sms) {
+  auto go = [&](auto kernel) {
+    kernel<<<resident_grid(kernel, 256, 0, count, 256, sms), 256, 0, s>>>(c, list, count);
+  };
+  switch (group_steps()) {
+    case 1: go(k_group<MODE, W, WEIGHTED, G, 1>); break;
+    case 4: go(k_group<MODE, W, WEIGHTED, G, 4>); break;
+    default: go(k_group<MODE, W, WEIGHTED, G, 8>);
+  }
 }
 
 template <int MODE, typename W>
@@ -201,6 +253,10 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, true>, 256, 0, p.count[T_THREAD],
                            256 * kMinChunk, sms),
              256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+    else if (p.thread_max <= 8 && thread_pair())
+      k_thread<MODE, W, WEIGHTED, 8, false, 2>
+          <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, false, 2>, 256, 0, p.count[T_THREAD], 512, sms),
+             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
     else if (p.thread_max <= 8)
       k_thread<MODE, W, WEIGHTED, 8>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8>, 256, 0, p.count[T_THREAD], 256, sms),
@@ -214,17 +270,13 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   }
   if (p.count[T_HALF] && (tiers >> T_HALF & 1u)) {
     tier(T_HALF);
-    k_group<MODE, W, WEIGHTED, 16>
-        <<<resident_grid(k_group<MODE, W, WEIGHTED, 16>, 256, 0, p.count[T_HALF], 256, sms), 256,
-           0, s>>>(c, p.list[T_HALF], p.count[T_HALF]);
+    launch_group<MODE, W, WEIGHTED, 16>(c, p.list[T_HALF], p.count[T_HALF], s, sms);
     prof.end(T_HALF, s);
     ++launches;
   }
   if (p.count[T_WARP] && (tiers >> T_WARP & 1u)) {
     tier(T_WARP);
-    k_group<MODE, W, WEIGHTED, 32>
-        <<<resident_grid(k_group<MODE, W, WEIGHTED, 32>, 256, 0, p.count[T_WARP], 256, sms), 256,
-           0, s>>>(c, p.list[T_WARP], p.count[T_WARP]);
+    launch_group<MODE, W, WEIGHTED, 32>(c, p.list[T_WARP], p.count[T_WARP], s, sms);
     prof.end(T_WARP, s);
     ++launches;
   }
@@ -273,7 +325,8 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   }
   if (p.n_hubs && (tiers >> T_HUB & 1u)) {
     tier(T_HUB);
-    const HubCtx h = p.hub_ctx();
+    HubCtx h = p.hub_ctx();
+    h.stop = c.stop;
     const unsigned gi =
         resident_grid(k_hub_accum<MODE, W, WEIGHTED, 1>, kBlockThreads, hub_smem, p.n_items, 1, sms);
     const unsigned gh = grid_for(p.n_hubs, 256, 1024);
@@ -455,10 +508,21 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
   DBuf<uint32_t> lab0(n), lab1, prev, changed;
   DBuf<uint8_t> flags(n);
   constexpr int kCtr = kTiers * C_COUNT;
-  DBuf<unsigned long long> ctr(kCtr);
+  // Passes are enqueued kBatch at a time behind a device-side pass guard (k_decide) and
+  // their counters read back once per batch, so a small graph's run is not one host
+  // round trip per pass. Cross-check (a host-driven fixpoint) and Sequential mode keep
+  // one read-back per pass.
+  const bool batched = o.cc_period == 0 && o.exec != NULPA_EXEC_SEQUENTIAL &&
+                       !(tuning && tuning->unbatched);
+  const int kBatch = batched ? std::max(1, std::min(o.max_iterations, batch_passes())) : 1;
+  const int blocks = batched ? o.max_iterations : 1;  // one counter block per pass
+  DBuf<unsigned long long> ctr(size_t(kCtr) * blocks);
   DBuf<unsigned int> work(2);  // cluster-tier work counter
-  unsigned long long* ctr_other = ctr.p + T_OTHER * C_COUNT;
-  Pinned hc(kCtr);
+  DBuf<unsigned int> stop(1);
+  Pinned hc(size_t(kCtr) * blocks + 1);
+  unsigned long long* hstop = hc.p + size_t(kCtr) * blocks;
+  NULPA_CUDA(cudaMemsetAsync(ctr.p, 0, size_t(kCtr) * blocks * sizeof(unsigned long long), s));
+  NULPA_CUDA(cudaMemsetAsync(stop.p, 0, sizeof(unsigned), s));
   if (o.exec == NULPA_EXEC_SYNCHRONOUS) {
     lab1 = DBuf<uint32_t>(n);
     changed = DBuf<uint32_t>(n);
@@ -469,13 +533,17 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     const uint64_t cap = pow2_ceil(2 * std::max<uint32_t>(g->max_degree, 1));
     if (cap > static_cast<uint64_t>(kHubCap)) seq_tab = DBuf<unsigned char>(cap * (4 + 8));
   }
-  Prof prof;
-  prof.on = tuning && tuning->profile;
-  if (prof.on)
-    for (auto& e : prof.ev) {
-      NULPA_CUDA(cudaEventCreate(&e[0]));
-      NULPA_CUDA(cudaEventCreate(&e[1]));
-    }
+  // per-tier CUDA events, one set per pass of a batch
+  std::vector<Prof> profs(kBatch);
+  const bool prof_on = tuning && tuning->profile;
+  for (Prof& pf : profs) {
+    pf.on = prof_on;
+    if (prof_on)
+      for (auto& e : pf.ev) {
+        NULPA_CUDA(cudaEventCreate(&e[0]));
+        NULPA_CUDA(cudaEventCreate(&e[1]));
+      }
+  }
   tr.mark("plan + buffers");
   k_init<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(lab0.p, flags.p, g->offsets, n, g->perm);
   NULPA_CUDA(cudaGetLastError());
@@ -503,13 +571,52 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
   uint32_t* cur = lab0.p;
   uint32_t* nxt = lab1.p;
 
+  // Host bookkeeping of one finished pass from its counter block (returns dN).
+  auto absorb = [&](const unsigned long long* blk, Prof& pf, bool pl, uint64_t reverted) {
+    uint64_t raw_dn = 0;
+    for (int t = 0; t < kTiers; ++t) {
+      const unsigned long long* k = blk + t * C_COUNT;
+      if (k[C_FAIL])
+        throw Error(NULPA_EINTERNAL, "hashtable insertion failed (capacity invariant violated)");
+      raw_dn += k[C_DN];
+      tot_v += k[C_PROC_V];
+      tot_e += k[C_PROC_E];
+      tot_w += k[C_WAKE_E];
+      tier_edges[t] += k[C_PROC_E];
+      // SURVEY §8d per tier: flag sweep over the tier's list (1 B), row bounds
+      // + own label of processed vertices (12 B), target + neighbour label
+      // (+ weight) per scanned edge, label write per change, wake store per
+      // neighbour of a changed vertex.
+      const double list_len = t < Plan::kLists ? p->count[t] : 0.0;
+      tier_bytes[t] += list_len + 12.0 * k[C_PROC_V] + edge_bytes * k[C_PROC_E] +
+                       4.0 * k[C_DN] + double(k[C_WAKE_E]);
+      if (pf.used[t]) {
+        ++tier_passes[t];
+        if (pf.on) {
+          float tms = 0.f;
+          NULPA_CUDA(cudaEventElapsedTime(&tms, pf.ev[t][0], pf.ev[t][1]));
+          tier_ms[t] += tms;
+        }
+      }
+    }
+    const uint64_t dn = raw_dn - reverted;
+    cc_reverts += reverted;
+    if (st && st->delta_n) st->delta_n[iterations] = dn;
+    ++iterations;
+    if (pl) ++pl_iterations;
+    return dn;
+  };
+
   for (int iter = 0; iter < o.max_iterations; ++iter) {
     const bool pick_less = o.pl_period > 0 && iter % o.pl_period == 0;
     const bool check = o.cc_period > 0 && iter % o.cc_period == 0;
     if (check) NULPA_CUDA(cudaMemcpyAsync(prev.p, cur, n * 4ull, cudaMemcpyDeviceToDevice, s));
     const bool was_pl = iter > 0 && o.pl_period > 0 && (iter - 1) % o.pl_period == 0;
     if (!o.prune || (was_pl && !pick_less)) NULPA_CUDA(cudaMemsetAsync(flags.p, 0, n, s));
-    NULPA_CUDA(cudaMemsetAsync(ctr.p, 0, kCtr * sizeof(unsigned long long), s));
+    unsigned long long* ctr_it = ctr.p + size_t(kCtr) * (batched ? iter : 0);
+    unsigned long long* ctr_other = ctr_it + T_OTHER * C_COUNT;
+    if (!batched) NULPA_CUDA(cudaMemsetAsync(ctr_it, 0, kCtr * sizeof(unsigned long long), s));
+    Prof& prof = profs[iter % kBatch];
     for (bool& u : prof.used) u = false;
 
     // Neighbour wake-ups are dead stores when the next pass resets every flag
@@ -525,7 +632,8 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     PassCtx c;
     c.g = dg;
     c.flags = flags.p;
-    c.ctr = ctr.p;
+    c.ctr = ctr_it;
+    c.stop = batched ? stop.p : nullptr;
     c.pick_less = pick_less ? 1 : 0;
     c.strategy = o.strategy;
     c.changed = nullptr;
@@ -545,7 +653,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       // Labels are still the identity: the table-free first pass (k_first_pass).
       c.lab_in = cur;
       c.lab_out = o.exec == NULPA_EXEC_SYNCHRONOUS ? nxt : cur;
-      c.ctr = ctr.p + T_THREAD * C_COUNT;
+      c.ctr = ctr_it + T_THREAD * C_COUNT;
       c.changed = (o.exec == NULPA_EXEC_SYNCHRONOUS && wake) ? changed.p : nullptr;
       if (o.exec == NULPA_EXEC_SYNCHRONOUS)
         NULPA_CUDA(cudaMemcpyAsync(nxt, cur, n * 4ull, cudaMemcpyDeviceToDevice, s));
@@ -560,7 +668,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       if (o.exec == NULPA_EXEC_SYNCHRONOUS) {
         if (wake) {
           k_wake_list<<<grid_for(n, kBlockThreads / 32, sms * 8), kBlockThreads, 0, s>>>(
-              dg, flags.p, changed.p, ctr_other + C_NCHANGED, ctr_other);
+              dg, flags.p, changed.p, ctr_other + C_NCHANGED, ctr_other, c.stop);
           ++launches;
         }
         std::swap(cur, nxt);
@@ -572,11 +680,11 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       c.lab_out = cur;
       const int ft = tuning->async_first_pass == 2 ? T_BLOCK2
                      : tuning->async_first_pass == 3 ? T_CLUSTER : T_HUB;
-      launches += long_rows_first_pass(*p, c, ctr.p, vbytes, s, sms, prof, ft);
+      launches += long_rows_first_pass(*p, c, ctr_it, vbytes, s, sms, prof, ft);
     } else if (o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
       c.lab_in = cur;
       c.lab_out = cur;
-      launches += dispatch_pass<kAsync>(*p, c, ctr.p, vbytes, s, sms, prof);
+      launches += dispatch_pass<kAsync>(*p, c, ctr_it, vbytes, s, sms, prof);
     } else if (o.exec == NULPA_EXEC_SYNCHRONOUS) {
       // sync_move (lpa.cpp:70-100): frozen snapshot `cur`, staged writes to `nxt`,
       // wake-ups after the joint application.
@@ -584,11 +692,11 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       c.lab_in = cur;
       c.lab_out = nxt;
       c.changed = wake ? changed.p : nullptr;
-      launches += dispatch_pass<kSync>(*p, c, ctr.p, vbytes, s, sms, prof);
+      launches += dispatch_pass<kSync>(*p, c, ctr_it, vbytes, s, sms, prof);
       if (wake) {
         prof.begin(T_OTHER, s);
         k_wake_list<<<grid_for(n, kBlockThreads / 32, sms * 8), kBlockThreads, 0, s>>>(
-            dg, flags.p, changed.p, ctr_other + C_NCHANGED, ctr_other);
+            dg, flags.p, changed.p, ctr_other + C_NCHANGED, ctr_other, c.stop);
         prof.end(T_OTHER, s);
         ++launches;
         NULPA_CUDA(cudaGetLastError());
@@ -613,44 +721,40 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       prof.end(T_OTHER, s);
       ++launches;
     }
-    uint64_t reverted = 0;
-    if (check)
-      reverted = device_cross_check(g, cur, prev.p, flags.p, ctr_other + C_AUX, hc.p + T_OTHER * C_COUNT + C_AUX,
-                                    s, sms, &launches);
-    NULPA_CUDA(cudaMemcpyAsync(hc.p, ctr.p, kCtr * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, s));
-    NULPA_CUDA(cudaStreamSynchronize(s));
-    uint64_t raw_dn = 0;
-    for (int t = 0; t < kTiers; ++t) {
-      const unsigned long long* k = hc.p + t * C_COUNT;
-      if (k[C_FAIL])
-        throw Error(NULPA_EINTERNAL, "hashtable insertion failed (capacity invariant violated)");
-      raw_dn += k[C_DN];
-      tot_v += k[C_PROC_V];
-      tot_e += k[C_PROC_E];
-      tot_w += k[C_WAKE_E];
-      tier_edges[t] += k[C_PROC_E];
-      // SURVEY §8d per tier: flag sweep over the tier's list (1 B), row bounds
-      // + own label of processed vertices (12 B), target + neighbour label
-      // (+ weight) per scanned edge, label write per change, wake store per
-      // neighbour of a changed vertex.
-      const double list_len = t < Plan::kLists ? p->count[t] : 0.0;
-      tier_bytes[t] += list_len + 12.0 * k[C_PROC_V] + edge_bytes * k[C_PROC_E] +
-                       4.0 * k[C_DN] + double(k[C_WAKE_E]);
-      if (prof.used[t]) {
-        ++tier_passes[t];
-        if (prof.on) {
-          float tms = 0.f;
-          NULPA_CUDA(cudaEventElapsedTime(&tms, prof.ev[t][0], prof.ev[t][1]));
-          tier_ms[t] += tms;
+    if (batched) {
+      k_decide<<<1, 32, 0, s>>>(ctr_it, n, o.tolerance, pick_less ? 1 : 0, iter, stop.p);
+      ++launches;
+      NULPA_CUDA(cudaGetLastError());
+      // read back once per batch: the guard and the batch's counter blocks
+      const int first = iterations;
+      if ((iter + 1) % kBatch == 0 || iter + 1 == o.max_iterations) {
+        NULPA_CUDA(cudaMemcpyAsync(hc.p + size_t(kCtr) * first, ctr.p + size_t(kCtr) * first,
+                                   size_t(kCtr) * (iter + 1 - first) * sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, s));
+        NULPA_CUDA(cudaMemcpyAsync(hstop, stop.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+        *hstop = 0;
+        NULPA_CUDA(cudaStreamSynchronize(s));
+        const unsigned sv = static_cast<unsigned>(*hstop & 0xFFFFFFFFull);
+        const int last = sv ? static_cast<int>(sv) : iter + 1;  // passes that ran
+        for (int it = first; it < last; ++it) {
+          const bool pl = o.pl_period > 0 && it % o.pl_period == 0;
+          absorb(hc.p + size_t(kCtr) * it, profs[it % kBatch], pl, 0);
+        }
+        if (sv) {
+          converged = true;
+          break;
         }
       }
+      continue;
     }
-    const uint64_t dn = raw_dn - reverted;
-    cc_reverts += reverted;
-    if (st && st->delta_n) st->delta_n[iterations] = dn;
-    ++iterations;
-    if (pick_less) ++pl_iterations;
+    uint64_t reverted = 0;
+    if (check)
+      reverted = device_cross_check(g, cur, prev.p, flags.p, ctr_other + C_AUX,
+                                    hc.p + T_OTHER * C_COUNT + C_AUX, s, sms, &launches);
+    NULPA_CUDA(cudaMemcpyAsync(hc.p, ctr_it, kCtr * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s));
+    NULPA_CUDA(cudaStreamSynchronize(s));
+    const uint64_t dn = absorb(hc.p, prof, pick_less, reverted);
     if (!pick_less && static_cast<double>(dn) / n < o.tolerance) {
       converged = true;
       break;
@@ -662,11 +766,12 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
   NULPA_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
-  if (prof.on)
-    for (auto& e : prof.ev) {
-      cudaEventDestroy(e[0]);
-      cudaEventDestroy(e[1]);
-    }
+  for (Prof& pf : profs)
+    if (pf.on)
+      for (auto& e : pf.ev) {
+        cudaEventDestroy(e[0]);
+        cudaEventDestroy(e[1]);
+      }
 
   tr.mark("loop");
   // Results leave in vertex order (layout.cu).

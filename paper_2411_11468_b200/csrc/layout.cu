@@ -25,6 +25,10 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
 
 #include "internal.hpp"
 #include "layout.hpp"
@@ -358,6 +362,82 @@ int default_layout() { return g_default_layout.load(); }
 void build_perm(const uint64_t* off, uint32_t n, uint32_t** perm_out, uint32_t** inv_out,
                 cudaStream_t s);
 
+namespace {
+
+// ---- pageable host sources (the C++ drop-in's std::vector storage) ------------------
+// cudaMemcpyAsync from pageable memory is staged by the driver through a small pinned
+// buffer at a fraction of the link rate. Pageable chunks are instead copied by all host
+// threads into a pinned ring (two buffers per array, kept across calls) and sent from
+// there, the copy of chunk k+1 overlapping the DMA of chunk k. A chunk whose weights are
+// all 1.0f is not sent at all (filled on the device): unit-weight graphs that arrive with
+// an explicit weight array, as every labelprop::CsrGraph does, cost no weight traffic.
+
+bool is_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+struct PinnedRing {
+  std::mutex mu;
+  void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t cap = 0;  // bytes per buffer
+  void* get(int k, size_t bytes) {  // (called with mu held)
+    if (bytes > cap) {
+      for (void*& b : buf)
+        if (b) {
+          cudaFreeHost(b);
+          b = nullptr;
+        }
+      cap = bytes;
+    }
+    if (!buf[k]) NULPA_CUDA(cudaHostAlloc(&buf[k], cap, cudaHostAllocDefault));
+    return buf[k];
+  }
+};
+PinnedRing& pinned_ring() {
+  static PinnedRing r;
+  return r;
+}
+
+unsigned copy_threads() {
+  const unsigned h = std::thread::hardware_concurrency();
+  return std::max(1u, std::min(h ? h : 1u, 32u));
+}
+
+// dst[0, count) = src[0, count) on all host threads; returns true when every element
+// equals `unit` (checked only when check_unit).
+template <typename T>
+bool parallel_copy(T* dst, const T* src, uint64_t count, bool check_unit, T unit) {
+  const unsigned t = static_cast<unsigned>(std::min<uint64_t>(copy_threads(), count / 65536 + 1));
+  std::atomic<bool> all_unit{true};
+  auto work = [&](unsigned k) {
+    const uint64_t a = count * k / t, b = count * (k + 1) / t;
+    if (dst) std::memcpy(dst + a, src + a, (b - a) * sizeof(T));
+    if (check_unit) {
+      bool u = true;
+      for (uint64_t i = a; i < b && u; ++i) u = src[i] == unit;
+      if (!u) all_unit = false;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned k = 1; k < t; ++k) pool.emplace_back(work, k);
+  work(0);
+  for (auto& th : pool) th.join();
+  return all_unit.load();
+}
+
+__global__ void k_fill_f32(float* p, uint64_t count, float v) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+}  // namespace
+
 bool can_upload_pipelined(const nulpa_csr* csr) {
   return default_layout() == NULPA_LAYOUT_DEGREE_BUCKETS && csr->n >= 2 && csr->m2 > 0;
 }
@@ -486,6 +566,17 @@ void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g,
       }
       // Chunk loop: H2D of chunk k on sa overlaps the scatter of chunk k-1 on sb.
       const uint64_t* ho = csr->offsets;
+      const bool pageable = is_pageable(csr->targets) || (weighted && is_pageable(csr->weights));
+      std::unique_lock<std::mutex> ring_lock(pinned_ring().mu, std::defer_lock);
+      cudaEvent_t sent[2] = {};
+      if (pageable) {
+        ring_lock.lock();
+        for (auto& e : sent) NULPA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      auto destroy_sent = [&] {
+        for (auto& e : sent)
+          if (e) cudaEventDestroy(e);
+      };
       uint32_t v_a = 0;
       for (int k = 0; v_a < n; ++k) {
         const int b = k & 1;
@@ -508,7 +599,26 @@ void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g,
           if (weighted) wstage[b] = dalloc<float>(stage_cap[b]);
         }
         if (k >= 2) NULPA_CUDA(cudaStreamWaitEvent(sa, freed[b], 0));
-        if (cnt) {
+        if (cnt && pageable) {
+          // pinned ring: wait until buffer b's previous DMA has left, refill it on the
+          // host threads, send it
+          if (k >= 2) NULPA_CUDA(cudaEventSynchronize(sent[b]));
+          uint32_t* pt = static_cast<uint32_t*>(pinned_ring().get(2 * b, kChunk * 4 > cnt * 4 ? kChunk * 4 : cnt * 4));
+          parallel_copy<uint32_t>(pt, csr->targets + ho[v_a], cnt, false, 0u);
+          NULPA_CUDA(cudaMemcpyAsync(stage[b], pt, cnt * 4, cudaMemcpyHostToDevice, sa));
+          if (weighted) {
+            const bool unit = parallel_copy<float>(nullptr, csr->weights + ho[v_a], cnt, true, 1.0f);
+            if (unit) {
+              k_fill_f32<<<blocks_for(cnt), 256, 0, sa>>>(wstage[b], cnt, 1.0f);
+              NULPA_CUDA(cudaGetLastError());
+            } else {
+              float* pw = static_cast<float*>(pinned_ring().get(2 * b + 1, kChunk * 4 > cnt * 4 ? kChunk * 4 : cnt * 4));
+              parallel_copy<float>(pw, csr->weights + ho[v_a], cnt, false, 0.0f);
+              NULPA_CUDA(cudaMemcpyAsync(wstage[b], pw, cnt * 4, cudaMemcpyHostToDevice, sa));
+            }
+          }
+          NULPA_CUDA(cudaEventRecord(sent[b], sa));
+        } else if (cnt) {
           NULPA_CUDA(cudaMemcpyAsync(stage[b], csr->targets + ho[v_a], cnt * 4,
                                      cudaMemcpyHostToDevice, sa));
           if (weighted)
@@ -530,6 +640,10 @@ void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g,
         v_a = v_b;
       }
       if (while_streaming) while_streaming();
+      if (pageable) {
+        NULPA_CUDA(cudaStreamSynchronize(sa));  // the ring is reusable once sa has drained
+        destroy_sent();
+      }
     }
     unsigned long long desc = 0;
     NULPA_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, sb));

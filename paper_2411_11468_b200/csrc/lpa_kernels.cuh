@@ -140,51 +140,76 @@ constexpr bool kPacked = !WEIGHTED;  // unit weights -> packed 64-bit slots
 // CHUNKED (ParallelAsync, schedule 4): thread k walks the contiguous list slice
 // [k*L, (k+1)*L) in order, as each of the reference's workers walks its chunk
 // (lpa.cpp:139-165), instead of the grid-stride interleave.
-template <int MODE, typename W, bool WEIGHTED, int DMAX, bool CHUNKED = false>
+// V: list entries a thread takes per iteration (grid-stride walk only): their claims
+// share one fence and their row, target and label loads are issued together.
+template <int MODE, typename W, bool WEIGHTED, int DMAX, bool CHUNKED = false, int V = 1>
 __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __restrict__ list,
                                                 uint32_t count) {
+  static_assert(!CHUNKED || V == 1, "a chunk walk takes its entries one at a time");
+  if (stopped(c.stop)) return;
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
   const uint64_t pol = policy_evict_first();
   const uint32_t stride = gridDim.x * blockDim.x;
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t L = CHUNKED ? (count + stride - 1) / stride : 0u;
   const uint32_t t_end = CHUNKED ? min(count, (tid + 1) * L) : count;
-  for (uint32_t t = CHUNKED ? tid * L : tid; t < t_end; t += CHUNKED ? 1u : stride) {
-    const uint32_t i = __ldg(list + t);
-    if (claim_vertex(c, i)) continue;
+  const uint32_t step = CHUNKED ? 1u : stride;
+  for (uint32_t t = CHUNKED ? tid * L : tid; t < t_end; t += step * V) {
+    uint32_t iv[V], d[V];
+    uint64_t lo[V];
+    bool act[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const uint32_t tv = t + v * step;
+      act[v] = tv < t_end;
+      iv[v] = act[v] ? __ldg(list + tv) : 0u;
+      if (act[v]) act[v] = !claim_vertex(c, iv[v]);
+    }
     claim_fence<MODE>(c);
-    const uint64_t lo = __ldg(c.g.off + i);
-    const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
-    uint32_t nb[DMAX];
-    uint32_t lab[DMAX];
-    W wt[DMAX];
 #pragma unroll
-    for (int k = 0; k < DMAX; ++k) nb[k] = (k < d) ? ld_stream(c.g.tgt + lo + k, pol) : i;
-#pragma unroll
-    for (int k = 0; k < DMAX; ++k) {
-      const bool valid = k < d && nb[k] != i;  // self-loops skipped (lpa.hpp:102)
-      lab[k] = valid ? load_label<MODE>(c.lab_in + nb[k]) : kEmpty;
-      wt[k] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + k) : W(0);
+    for (int v = 0; v < V; ++v) {
+      lo[v] = act[v] ? __ldg(c.g.off + iv[v]) : 0ull;
+      d[v] = act[v] ? static_cast<uint32_t>(__ldg(c.g.off + iv[v] + 1) - lo[v]) : 0u;
     }
-    // Per-label total in neighbour order (bit-identical to the reference's
-    // sequential accumulation, even for non-integer weights), then argmax.
-    Best<VBits<W>> b{VBits<W>(0), kEmpty};
+    uint32_t nb[V][DMAX];
+    uint32_t lab[V][DMAX];
+    W wt[V][DMAX];
 #pragma unroll
-    for (int k = 0; k < DMAX; ++k) {
-      W s = W(0);
-#pragma unroll
-      for (int m = 0; m < DMAX; ++m) s += (lab[m] == lab[k]) ? wt[m] : W(0);
-      best_merge(b, to_vbits<W>(s), lab[k]);
-    }
-    ++n_v;
-    n_e += d;
-    if (!apply_move<MODE>(c, i, b.k)) continue;
-    ++n_dn;
-    if (MODE == kAsync && c.wake) {
+    for (int v = 0; v < V; ++v)
 #pragma unroll
       for (int k = 0; k < DMAX; ++k)
-        if (k < d) wake_vertex(c.flags, nb[k]);
-      n_w += d;
+        nb[v][k] = (k < d[v]) ? ld_stream(c.g.tgt + lo[v] + k, pol) : iv[v];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k) {
+        const bool valid = k < d[v] && nb[v][k] != iv[v];  // self-loops skipped (lpa.hpp:102)
+        lab[v][k] = valid ? load_label<MODE>(c.lab_in + nb[v][k]) : kEmpty;
+        wt[v][k] = valid ? edge_weight<W, WEIGHTED>(c.g, lo[v] + k) : W(0);
+      }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (!act[v]) continue;
+      // Per-label total in neighbour order (bit-identical to the reference's
+      // sequential accumulation, even for non-integer weights), then argmax.
+      Best<VBits<W>> b{VBits<W>(0), kEmpty};
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k) {
+        W sum = W(0);
+#pragma unroll
+        for (int m = 0; m < DMAX; ++m) sum += (lab[v][m] == lab[v][k]) ? wt[v][m] : W(0);
+        best_merge(b, to_vbits<W>(sum), lab[v][k]);
+      }
+      ++n_v;
+      n_e += d[v];
+      if (!apply_move<MODE>(c, iv[v], b.k)) continue;
+      ++n_dn;
+      if (MODE == kAsync && c.wake) {
+#pragma unroll
+        for (int k = 0; k < DMAX; ++k)
+          if (k < d[v]) wake_vertex(c.flags, nb[v][k]);
+        n_w += d[v];
+      }
     }
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
@@ -210,58 +235,69 @@ __device__ __forceinline__ Best<V> group_best(Best<V> b, unsigned gmask) {
   }
 }
 
-template <int MODE, typename W, bool WEIGHTED, int G>
+// S steps of a warp's batch are loaded at once: the targets of all S steps, then their
+// labels (S independent loads in flight per lane), then the S steps are decided one
+// after another. The batch prologue (claims, row bounds, current labels of 32 list
+// entries) is shared through shared memory.
+template <int MODE, typename W, bool WEIGHTED, int G, int S = 8>
 __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __restrict__ list,
                                                uint32_t count) {
-  constexpr int kPer = 32 / G;  // vertices per warp step
-  const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;
+  if (stopped(c.stop)) return;
+  constexpr int kPer = 32 / G;           // vertices per warp step
+  constexpr int kSteps = 32 / kPer;      // steps per 32-entry batch
+  static_assert(kSteps % S == 0, "steps per chunk");
+  const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G, wid = threadIdx.x >> 5;
   const unsigned gmask = (G == 32) ? kFull : (((1u << G) - 1u) << (sub * G));
+  __shared__ Meta s_meta[8][32];
   const uint64_t pol = policy_evict_first();
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  // Each warp takes 32 list entries at a time: one batched prologue (fetch_meta),
-  // then kPer vertices per step with the next step's targets loaded ahead.
   for (uint32_t base = gw * 32; base < count; base += nw * 32) {
-    const Meta mine = fetch_meta<MODE>(c, list, base + lane, count);
+    s_meta[wid][lane] = fetch_meta<MODE>(c, list, base + lane, count);
     __syncwarp();  // every lane's claim (and its fence) before any lane's label loads
-    Meta m = shfl_meta(mine, sub);
-    uint32_t j = (m.act && gl < m.d) ? ld_stream(c.g.tgt + m.lo + gl, pol) : m.i;
 #pragma unroll 1
-    for (int step = 0; step < 32 / kPer; ++step) {
-      // prefetch the next step's targets (immutable) before this step's label reads
-      Meta mn{};
-      uint32_t jn = 0;
-      if (step + 1 < 32 / kPer) {
-        mn = shfl_meta(mine, (step + 1) * kPer + sub);
-        jn = (mn.act && gl < mn.d) ? ld_stream(c.g.tgt + mn.lo + gl, pol) : mn.i;
+    for (int c0 = 0; c0 < kSteps; c0 += S) {
+      uint32_t j[S], lab[S];
+      W w[S];
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        const Meta& m = s_meta[wid][(c0 + k) * kPer + sub];
+        j[k] = (m.act && gl < m.d) ? ld_stream(c.g.tgt + m.lo + gl, pol) : m.i;
       }
-      const bool valid = m.act && gl < m.d && j != m.i;
-      const uint32_t lab = valid ? load_label<MODE>(c.lab_in + j) : kEmpty;
-      const W w = valid ? edge_weight<W, WEIGHTED>(c.g, m.lo + gl) : W(0);
-      const unsigned peers = __match_any_sync(kFull, lab) & gmask;
-      W sm;
-      if constexpr (WEIGHTED)
-        sm = peer_sum(w, peers);
-      else
-        sm = static_cast<W>(__popc(peers));
-      Best<VBits<W>> b{VBits<W>(0), kEmpty};
-      if (lab != kEmpty && (__ffs(peers) - 1) == lane) b = Best<VBits<W>>{to_vbits<W>(sm), lab};
-      b = group_best<VBits<W>, G>(b, gmask);
-      int ch = 0;
-      if (m.act && gl == 0) {
-        ch = apply_move_cur<MODE>(c, m.i, b.k, m.cur) ? 1 : 0;
-        ++n_v;
-        n_e += m.d;
-        n_dn += ch;
-        if (MODE == kAsync && ch && c.wake) n_w += m.d;
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        const Meta& m = s_meta[wid][(c0 + k) * kPer + sub];
+        const bool valid = m.act && gl < m.d && j[k] != m.i;
+        lab[k] = valid ? load_label<MODE>(c.lab_in + j[k]) : kEmpty;
+        w[k] = valid ? edge_weight<W, WEIGHTED>(c.g, m.lo + gl) : W(0);
       }
-      ch = __shfl_sync(kFull, ch, sub * G);
-      if (MODE == kAsync && c.wake) __syncwarp();  // the group leader's store + fence first
-      if (MODE == kAsync && ch && c.wake && m.act && gl < m.d) wake_vertex(c.flags, j);
-      m = mn;
-      j = jn;
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        const Meta m = s_meta[wid][(c0 + k) * kPer + sub];
+        const unsigned peers = __match_any_sync(kFull, lab[k]) & gmask;
+        W sm;
+        if constexpr (WEIGHTED)
+          sm = peer_sum(w[k], peers);
+        else
+          sm = static_cast<W>(__popc(peers));
+        Best<VBits<W>> b{VBits<W>(0), kEmpty};
+        if (lab[k] != kEmpty && (__ffs(peers) - 1) == lane) b = Best<VBits<W>>{to_vbits<W>(sm), lab[k]};
+        b = group_best<VBits<W>, G>(b, gmask);
+        int ch = 0;
+        if (m.act && gl == 0) {
+          ch = apply_move_cur<MODE>(c, m.i, b.k, m.cur) ? 1 : 0;
+          ++n_v;
+          n_e += m.d;
+          n_dn += ch;
+          if (MODE == kAsync && ch && c.wake) n_w += m.d;
+        }
+        ch = __shfl_sync(kFull, ch, sub * G);
+        if (MODE == kAsync && c.wake) __syncwarp();  // the group leader's store + fence first
+        if (MODE == kAsync && ch && c.wake && m.act && gl < m.d) wake_vertex(c.flags, j[k]);
+      }
     }
+    __syncwarp();  // s_meta is rewritten by the next batch
   }
   warp_add_counter(c.ctr, C_PROC_V, n_v);
   warp_add_counter(c.ctr, C_PROC_E, n_e);
@@ -543,6 +579,7 @@ template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CA
 __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : (CTA_THREADS == 512 ? 2 : 1))
     k_team(PassCtx c, const uint32_t* __restrict__ list,
                                                       uint32_t count) {
+  if (stopped(c.stop)) return;
   static_assert(CTA_THREADS % TEAM == 0 && TEAM % 32 == 0, "team shape");
   constexpr int kTeams = CTA_THREADS / TEAM;
   using Tab = std::conditional_t<kPacked<WEIGHTED>, SmemTable<W>, Table<false, W>>;
@@ -659,6 +696,7 @@ constexpr size_t cluster_bytes() {
 template <int MODE, typename W, bool WEIGHTED>
 __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThreads)
     k_cluster(PassCtx c, const uint32_t* __restrict__ list, uint32_t count) {
+  if (stopped(c.stop)) return;
   namespace cg = cooperative_groups;
   static_assert(kClusterSize == 8, "owner_of assumes 8 ranks");
   using Tab = Table<kPacked<WEIGHTED>, W>;
@@ -820,6 +858,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
                                                          uint32_t count, int fresh,
                                                          uint32_t* __restrict__ scratch,
                                                          uint32_t stride, uint64_t m2) {
+  if (stopped(c.stop)) return;
   // This CTA's row snapshot / phase buckets (L2-resident): phase 0 of a multi-phase
   // vertex writes the labels of later phases here; those phases stream them back.
   uint32_t* snap = scratch + size_t(blockIdx.x) * stride;
@@ -1127,6 +1166,7 @@ __global__ void __launch_bounds__(256) k_first_pass_list(PassCtx c, const uint32
 
 template <int MODE>
 __global__ void k_hub_select(PassCtx c, HubCtx h) {
+  if (stopped(c.stop)) return;
   unsigned long long n_v = 0, n_e = 0;
   const uint32_t bound = (h.n_hubs + 31u) & ~31u;
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < bound;
@@ -1161,6 +1201,7 @@ __device__ __forceinline__ void bind_hub_table(Tab& g, const HubCtx& h, uint32_t
 #endif
 template <int MODE, typename W, bool WEIGHTED, int DEDUP = 1>
 __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h) {
+  if (stopped(c.stop)) return;
   using Tab = std::conditional_t<kPacked<WEIGHTED>, SmemTable<W>, Table<false, W>>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned s_occ_n;
@@ -1248,6 +1289,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_accum(PassCtx c, HubCtx h
 // from identity labels fills the tables with ~one label per edge).
 template <typename W, bool WEIGHTED>
 __global__ void __launch_bounds__(kBlockThreads) k_hub_sweep(HubCtx h) {
+  if (stopped(h.stop)) return;
   using Tab = Table<kPacked<WEIGHTED>, W>;
   __shared__ Best<VBits<W>> red[32];
   for (uint32_t it = blockIdx.x; it < h.n_sitems; it += gridDim.x) {
@@ -1285,6 +1327,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_sweep(HubCtx h) {
 // (key << 32 | count) words; otherwise split key / double arrays.
 template <bool PACKED>
 __global__ void __launch_bounds__(kBlockThreads) k_hub_sweep_key_f64(HubCtx h) {
+  if (stopped(h.stop)) return;
   using Tab = Table<PACKED, double>;
   for (uint32_t it = blockIdx.x; it < h.n_sitems; it += gridDim.x) {
     const uint32_t x = h.sitem_hub[it];
@@ -1307,6 +1350,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_sweep_key_f64(HubCtx h) {
 
 template <int MODE, typename W, bool WEIGHTED>
 __global__ void k_hub_decide(PassCtx c, HubCtx h) {
+  if (stopped(c.stop)) return;
   unsigned long long n_dn = 0;
   const uint32_t bound = (h.n_hubs + 31u) & ~31u;
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < bound;
@@ -1332,6 +1376,7 @@ __global__ void k_hub_decide(PassCtx c, HubCtx h) {
 
 // Async wake for changed hubs, one chunk per work item.
 __global__ void __launch_bounds__(kBlockThreads) k_hub_wake(PassCtx c, HubCtx h) {
+  if (stopped(c.stop)) return;
   unsigned long long n_w = 0;
   const uint64_t pol = policy_evict_first();
   for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
@@ -1354,7 +1399,9 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_wake(PassCtx c, HubCtx h)
 __global__ void __launch_bounds__(kBlockThreads) k_wake_list(Graph g, uint8_t* flags,
                                                              const uint32_t* list,
                                                              const unsigned long long* count_p,
-                                                             unsigned long long* ctr) {
+                                                             unsigned long long* ctr,
+                                                             const unsigned* stop = nullptr) {
+  if (stopped(stop)) return;
   const uint32_t count = static_cast<uint32_t>(*count_p);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);

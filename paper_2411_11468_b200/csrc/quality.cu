@@ -26,20 +26,74 @@ __global__ void k_check_labels(const uint32_t* lab, uint32_t n, unsigned long lo
     if (lab[i] >= n) atomicMin(first_bad, static_cast<unsigned long long>(i));
 }
 
-// Rows of degree <= 32: one thread per row.
-__global__ void k_mod_thread(Graph g, const uint32_t* lab, const uint32_t* list, uint32_t count,
-                             double* sigma, double* big) {
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
-    const uint32_t i = list[t];
-    const uint32_t ci = lab[i];
-    double ki = 0.0, si = 0.0;
-    for (uint64_t e = g.off[i]; e < g.off[i + 1]; ++e) {
-      const double w = g.w ? static_cast<double>(g.w[e]) : 1.0;
-      ki += w;
-      if (lab[g.tgt[e]] == ci) si += w;
+// Rows of degree <= 32, 32 list entries per warp, edge-parallel: the lanes scan the
+// degrees of the batch's rows, then walk the batch's edges 32 at a time (lane f of a
+// round takes the f-th edge of the batch, its row found by a 5-step search over the
+// lanes' prefix sums). Targets of consecutive rows are read coalesced, each lane does one
+// label gather per round, and the partial sums are merged per COMMUNITY across the
+// warp (__match_any_sync) before one fp64 atomic pair per community per round.
+__global__ void __launch_bounds__(256) k_mod_rows32(Graph g, const uint32_t* lab,
+                                                    const uint32_t* list, uint32_t count,
+                                                    double* sigma, double* big) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t base = gw * 32; base < count; base += nw * 32) {
+    const uint32_t t = base + lane;
+    uint32_t i = 0, d = 0, ci = kEmpty;
+    uint64_t lo = 0;
+    if (t < count) {
+      i = list[t];
+      lo = g.off[i];
+      d = static_cast<uint32_t>(g.off[i + 1] - lo);
+      ci = lab[i];
     }
-    if (si != 0.0) atomicAdd(sigma + ci, si);
-    if (ki != 0.0) atomicAdd(big + ci, ki);
+    uint32_t pre = d;  // inclusive scan of the degrees
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, pre, o);
+      if (lane >= o) pre += v;
+    }
+    const uint32_t excl = pre - d;
+    const uint32_t total = __shfl_sync(kFull, pre, 31);
+    for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+      const uint32_t f = f0 + lane;
+      int r = 0;  // the last lane whose row starts at or before edge f
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t ex = __shfl_sync(kFull, excl, r + step);
+        if (ex <= f) r += step;
+      }
+      const uint64_t lo_r = __shfl_sync(kFull, lo, r);
+      const uint32_t ci_r = __shfl_sync(kFull, ci, r);
+      const uint32_t ex_r = __shfl_sync(kFull, excl, r);
+      const bool valid = f < total;
+      const uint64_t e = lo_r + (f - ex_r);
+      double w = 0.0, in = 0.0;
+      if (valid) {
+        w = g.w ? static_cast<double>(g.w[e]) : 1.0;
+        if (lab[g.tgt[e]] == ci_r) in = w;
+      }
+      const uint32_t key = valid ? ci_r : kEmpty;
+      const unsigned peers = __match_any_sync(kFull, key);
+      double ks = 0.0, is = 0.0;
+      if (g.w) {
+        for (int b = 0; b < 32; ++b) {  // (uniform loop: every lane shuffles)
+          const double wb = __shfl_sync(kFull, w, b), ib = __shfl_sync(kFull, in, b);
+          if ((peers >> b) & 1u) {
+            ks += wb;
+            is += ib;
+          }
+        }
+      } else {
+        ks = static_cast<double>(__reduce_add_sync(peers, valid ? 1u : 0u));
+        is = static_cast<double>(__reduce_add_sync(peers, in != 0.0 ? 1u : 0u));
+      }
+      if (key != kEmpty && (__ffs(peers) - 1) == lane) {
+        atomicAdd(big + key, ks);
+        if (is != 0.0) atomicAdd(sigma + key, is);
+      }
+    }
   }
 }
 
@@ -170,10 +224,11 @@ void accumulate_sigma(nulpa_graph* g, const uint32_t* lab, double* sigma, double
   Plan* p = g->plan ? g->plan : get_plan(g, resolve_tiers(32, nullptr), 4, s);
   const Graph dg{g->offsets, g->targets, g->weights, n};
   const int sms = sm_count();
-  if (p->count[T_THREAD])
-    k_mod_thread<<<std::min<uint32_t>((p->count[T_THREAD] + 255) / 256, sms * 8), 256, 0, s>>>(
-        dg, lab, p->list[T_THREAD], p->count[T_THREAD], sigma, big);
-  for (int t = T_HALF; t <= T_CLUSTER; ++t)
+  for (int t = T_THREAD; t <= T_WARP; ++t)
+    if (p->count[t])
+      k_mod_rows32<<<std::min<uint32_t>((p->count[t] + 255) / 256, sms * 8), 256, 0, s>>>(
+          dg, lab, p->list[t], p->count[t], sigma, big);
+  for (int t = T_WTAB; t <= T_CLUSTER; ++t)
     if (p->count[t])
       k_mod_warp<<<std::min<uint32_t>((p->count[t] + 7) / 8, sms * 8), 256, 0, s>>>(
           dg, lab, p->list[t], p->count[t], sigma, big);

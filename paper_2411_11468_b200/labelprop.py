@@ -123,6 +123,7 @@ class Tuning:
     profile: bool = False
     identity_first: bool = True  # table-free first pass from identity labels
     async_first_pass: int = 0  # 1: ParallelAsync pass 0 as the table-free synchronous pass
+    batched: bool = True  # passes enqueued in batches behind the device convergence guard
 
     def to_c(self) -> _capi.nulpa_tuning:
         t = _capi.nulpa_tuning()
@@ -133,6 +134,7 @@ class Tuning:
         t.profile = 1 if self.profile else 0
         t.no_identity_first = 0 if self.identity_first else 1
         t.async_first_pass = self.async_first_pass
+        t.unbatched = 0 if self.batched else 1
         return t
 
 

@@ -414,3 +414,33 @@ def test_sequential_with_hub_rows_bit_exact():
     want, ws = O.port_lpa(pg, exec_mode=1)
     r = lp.lpa(g, lp.LpaConfig(exec=lp.ExecMode.Sequential))
     assert np.array_equal(r.labels, want) and r.stats.delta_n_per_iter == ws["delta_n"]
+
+
+@pytest.mark.parametrize("pl_period,max_it", [(4, 20), (0, 20), (1, 3), (4, 1), (2, 6)])
+def test_batched_passes_equal_per_pass_readback(pl_period, max_it):
+    # Passes enqueued in batches behind the device-side convergence guard (k_decide) must
+    # give the same run as one host read-back per pass: labels, dN, iterations,
+    # convergence, pl_iterations; Synchronous against the C restatement too.
+    dg, g = _device_graph("rmat", 13)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    n = g.order()
+    for mode in (lp.ExecMode.Synchronous, lp.ExecMode.ParallelAsync):
+        cfg = lp.LpaConfig(exec=mode, pl_period=pl_period, max_iterations=max_it)
+        a = dg.lpa(cfg, lp.Tuning(batched=True))
+        b = dg.lpa(cfg, lp.Tuning(batched=False))
+        if mode == lp.ExecMode.Synchronous:
+            want, ws = O.port_lpa(pg, exec_mode=2, pl_period=pl_period, max_iterations=max_it)
+            for r in (a, b):
+                assert np.array_equal(r.labels, want)
+                assert r.stats.delta_n_per_iter == ws["delta_n"]
+                assert r.stats.converged == ws["converged"]
+                assert r.stats.pl_iterations == ws["pl_iterations"]
+        # the run_engine stopping rule holds in both (lpa.cpp:306)
+        for r in (a, b):
+            dn = r.stats.delta_n_per_iter
+            assert len(dn) == r.stats.iterations <= max_it
+            pls = [pl_period > 0 and k % pl_period == 0 for k in range(len(dn))]
+            stops = [not pl and d / n < 0.05 for d, pl in zip(dn, pls)]
+            assert not any(stops[:-1])
+            assert r.stats.converged == stops[-1]
+            assert r.stats.pl_iterations == sum(pls)
