@@ -374,6 +374,30 @@ def dropin_e2e(off, tgt, n: int, m2: int, steps: int) -> dict:
                    "build/nulpa_dropin_e2e"}
 
 
+def modularity_roofline(dg, lab, n: int, m2: int, dev: int, peak: float, reps: int = 3) -> dict:
+    """K7 (modularity, quality.cpp:21-49) on the final labels, device-resident: the call
+    relabels to position order, accumulates σ_c / Σ_c per community (k_mod_rows32 /
+    k_mod_warp / k_mod_hub) and folds them (k_mod_fold). Algorithmic bytes per call:
+    m2 * 8 (target + neighbour label) + n * 16 (list entry, row bound, own label, the
+    per-row σ/Σ update) + n * 12 (labels + perm read, position labels written) + n * 32
+    (σ/Σ zeroed, then read by the fold). Timed end to end with CUDA events."""
+    import torch
+    s = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dg.modularity_device(lab.data_ptr())  # warm (allocations)
+    torch.cuda.synchronize(dev)
+    e0.record(s)
+    for _ in range(reps):
+        dg.modularity_device(lab.data_ptr())
+    e1.record(s)
+    torch.cuda.synchronize(dev)
+    sec = e0.elapsed_time(e1) * 1e-3 / reps
+    alg = m2 * 8 + n * (16 + 12 + 32)
+    return {"seconds": sec, "alg_bytes": alg, "achieved": alg / sec / 1e9, "peak": peak,
+            "unit": "GB/s", "frac": alg / sec / 1e9 / peak,
+            "note": "one modularity() call incl. the label range check's 8-byte read-back"}
+
+
 def bench_nulpa(args):
     rank, world, local = dist_env()
     dev = local
@@ -403,6 +427,7 @@ def bench_nulpa(args):
     t0 = time.time()
     dg, wdesc = workloads.build(args.workload, args.scale, args.seed, dev)
     gen_s = time.time() - t0
+    _log(f"graph built: n={dg.n} m2={dg.m2} ({gen_s:.1f} s)")
     n, m2 = dg.n, dg.m2
     cfg = lp.LpaConfig()
     tuning = lp.Tuning(thread_max_degree=args.thread_max, warp_max_degree=args.warp_max,
@@ -431,6 +456,7 @@ def bench_nulpa(args):
             stats.append((st, dn[:st.iterations].tolist()))
         barrier()
         wall = time.time() - w0
+    _log(f"timed region: {args.steps} runs, wall {wall:.2f} s")
     loop_s = sum(s.elapsed_seconds for s, _ in stats)
     loop_s = barrier_max(loop_s)
     wall = barrier_max(wall)
@@ -456,6 +482,8 @@ def bench_nulpa(args):
     last = dg.lpa(cfg, tuning, labels_device_ptr=lab.data_ptr(), want_host=False)
     q = dg.modularity_device(lab.data_ptr())
     comms = dg.community_count_device(lab.data_ptr())
+    k7 = modularity_roofline(dg, lab, n, m2, dev, peak)
+    _log(f"modularity Q={q:.4g}, K7 {k7['seconds'] * 1e3:.1f} ms per call")
     del lab
 
     # e2e through the host-buffer C ABI (pinned host CSR, H2D + run + D2H every step)
@@ -482,6 +510,7 @@ def bench_nulpa(args):
                                               C.byref(st)))
         barrier()
         e_wall = barrier_max(time.time() - e0)
+        _log(f"e2e: {args.e2e_steps} steps, {e_wall:.2f} s")
         e2e = {"value": world * args.e2e_steps * m2 / e_wall, "unit": UNIT,
                "h2d_bytes_per_step": int((n + 1) * 8 + m2 * 4),
                "d2h_bytes_per_step": int(n * 4), "steps": args.e2e_steps,
@@ -512,7 +541,9 @@ def bench_nulpa(args):
             rg = O.RefGraph.from_csr(host_off, host_tgt, None)
             runs, workers, sd = run_reference_cpu(rg, 1, args.workload, g_off=host_off)
             stc = runs[-1][1]
+            q0 = time.time()
             q_ref = O.ref_modularity(rg, runs[-1][0])
+            _log(f"reference modularity {q_ref:.4g} ({time.time() - q0:.1f} s)")
             del rg
             cpu = {"value": m2 / stc["elapsed_seconds"], "unit": UNIT, "cores": workers,
                    "kind": "reference", "physical_cores": host["physical_cores"],
@@ -525,11 +556,13 @@ def bench_nulpa(args):
             so, st_, _ = sg.arrays()
             sgh = lp2.CsrGraph(so, st_, None)
             nq = [lp2.modularity(sgh, lp2.lpa(sgh).labels) for _ in range(5)]
+            q0 = time.time()
             quality = {"this_graph": {"nulpa_Q": q, "ref_async_Q": q_ref,
                                       "dQ": q - q_ref, "abs_dQ": abs(q - q_ref),
                                       "ref_iterations": stc["iterations"],
                                       "nulpa_iterations": int(stats[-1][0].iterations)},
                        "sbm100k": sbm_quality(nq)}
+            _log(f"SBM-100K quality check ({time.time() - q0:.1f} s)")
         except Exception as e:  # the baseline must never sink the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"failed: {e}"}
@@ -537,7 +570,9 @@ def bench_nulpa(args):
     # (pageable host memory, an explicit all-ones weight array), in a child process
     dropin = None
     if rank == 0 and world == 1 and args.dropin_steps > 0 and host_off is not None:
+        q0 = time.time()
         dropin = dropin_e2e(host_off, host_tgt, n, m2, args.dropin_steps)
+        _log(f"drop-in e2e: {args.dropin_steps} steps ({time.time() - q0:.1f} s)")
     host_off = host_tgt = None
     if args.e2e_steps > 0:
         del off_h, tgt_h
@@ -579,6 +614,7 @@ def bench_nulpa(args):
                          "sector_adjusted": {"achieved": sector_gbs, "frac": sector_gbs / peak,
                                              "assumes": "32 B sector per neighbour-label "
                                                         "gather (every gather misses L2)"}},
+            "modularity_k7": k7,
             "e2e": e2e,
             "e2e_dropin": dropin,
             "cpu_baseline": cpu,

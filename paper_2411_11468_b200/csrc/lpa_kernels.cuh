@@ -574,9 +574,12 @@ constexpr size_t team_bytes() {
 // insert. It pays once labels have collapsed; in the first pass of a run almost
 // every label is distinct and the table's own claim/add handles the few repeats
 // for less (launch_pass picks the variant per pass).
+#ifndef NULPA_TEAM_MINB
+#define NULPA_TEAM_MINB 4  // resident 256-thread team CTAs per SM (registers <= 64)
+#endif
 template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CAP, int MAXD,
           int DEDUP = 1>
-__global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? 4 : (CTA_THREADS == 512 ? 2 : 1))
+__global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_MINB : (CTA_THREADS == 512 ? 2 : 1))
     k_team(PassCtx c, const uint32_t* __restrict__ list,
                                                       uint32_t count) {
   if (stopped(c.stop)) return;
