@@ -247,12 +247,17 @@ def sbm_quality(nulpa_q=None) -> dict:
     lab, _ = O.ref_lpa(rg, exec_mode=2)
     q_sync = O.ref_modularity(rg, lab)
     workers = int(O.ref().ref_hardware_concurrency())
+    # all-scalar: this graph has rows of degree >= 32, and the reference's team
+    # path (lpa.cpp:169-230, condition-variable barriers per vertex) stalled for minutes on
+    # the GPU box's 16 host threads (gpurun_out r2i: ref_lpa never returned)
+    sd = ref_switch_degree("sbm", _Deg(rg.arrays()[0]))
     q_async = []
     for _ in range(5):
-        la, _ = O.ref_lpa(rg, exec_mode=0, workers=workers)
+        la, _ = O.ref_lpa(rg, exec_mode=0, workers=workers, switch_degree=sd)
         q_async.append(O.ref_modularity(rg, la))
     out = {"graph": "planted_partition(100000, 100, 14/999, 2/99000, seed 1)",
-           "ref_sync_Q": q_sync, "ref_async_Q": q_async, "ref_async_workers": workers}
+           "ref_sync_Q": q_sync, "ref_async_Q": q_async, "ref_async_workers": workers,
+           "ref_async_switch_degree": sd}
     if nulpa_q:
         qm = float(np.mean(nulpa_q))
         out.update({"nulpa_async_Q": nulpa_q, "nulpa_async_Q_mean": qm,

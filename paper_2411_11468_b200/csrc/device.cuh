@@ -86,6 +86,17 @@ constexpr int kClusterMax = kClusterSize * kClusterCap * 3 / 4;  // 98304, load 
 #ifndef NULPA_WIDE_BUCKETS
 #define NULPA_WIDE_BUCKETS 8
 #endif
+// Wide tier (k_wide): CTA size and shared-table slots. 1024 threads with a 16K-slot table
+// (one CTA per SM), or 512 threads with 8K slots (two independent CTAs per SM).
+#ifndef NULPA_WIDE_THREADS
+#define NULPA_WIDE_THREADS 1024
+#endif
+#ifndef NULPA_WIDE_CAP
+#define NULPA_WIDE_CAP 16384
+#endif
+constexpr int kWideThreads = NULPA_WIDE_THREADS;
+constexpr int kWideCap = NULPA_WIDE_CAP;
+constexpr int kWideCtasPerSm = 1024 / NULPA_WIDE_THREADS;  // resident CTAs per SM (regs <= 64)
 // u32 per wide-tier CTA: the row snapshot, or the buckets of phases 1..NULPA_WIDE_BUCKETS-1
 constexpr uint32_t kWideScratch = (NULPA_WIDE_BUCKETS - 1) * uint32_t(kClusterMax);
 constexpr int kHubChunk = 2048;     // edges per hub work item (<= kBlockCap / 2)
@@ -196,7 +207,11 @@ __device__ __forceinline__ uint8_t ld_relaxed(const uint8_t* p) {
 __device__ __forceinline__ void st_relaxed(uint8_t* p, uint8_t v) {
   asm volatile("st.relaxed.gpu.global.u8 [%0], %1;" ::"l"(p), "h"(static_cast<uint16_t>(v)));
 }
+#ifndef NULPA_NO_FENCE
 __device__ __forceinline__ void fence_sc() { asm volatile("fence.sc.gpu;" ::: "memory"); }
+#else  // (cost measurement only: drops the a18 ordering)
+__device__ __forceinline__ void fence_sc() {}
+#endif
 
 // Async mode reads neighbour labels that other SMs may be writing in place (relaxed,
 // device scope). Sync mode reads an immutable snapshot through the read-only path.

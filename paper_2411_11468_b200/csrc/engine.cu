@@ -133,12 +133,25 @@ struct Prof {
 // rounds in program order (default); 1 = label prefetch one round ahead; 2 = TMA-staged
 // targets + label prefetch. Measured at R-MAT 27: 29.5 / 30.7 / 40.4 ms of
 // wide tier per run, identical results, so the plain kernel is the default.
-// Thread tier: two list entries per thread iteration (NULPA_THREAD_PAIR, read once; 1 by
-// default) — one claim fence for both, both rows' loads in flight together.
+// Thread tier: two list entries per thread iteration (NULPA_THREAD_PAIR, read once; 0 by
+// default) — one claim fence for both, both rows' loads in flight together. Measured at
+// R-MAT 27 on one B200: thread tier 7.6 ms per run with pairs, 5.0 ms without (the
+// 99-register pair kernel runs fewer warps per SM).
 inline bool thread_pair() {
   static const bool m = [] {
     const char* e = std::getenv("NULPA_THREAD_PAIR");
-    return e ? std::atoi(e) != 0 : true;
+    return e ? std::atoi(e) != 0 : false;
+  }();
+  return m;
+}
+
+// Thread tier (degree <= 8) as 8-lane groups (k_group<8>: four rows per warp step, the
+// claims of 32 rows behind one fence per lane) instead of one thread per row
+// (NULPA_THREAD_GROUP, read once; 0 by default).
+inline bool thread_group() {
+  static const bool m = [] {
+    const char* e = std::getenv("NULPA_THREAD_GROUP");
+    return e ? std::atoi(e) != 0 : false;
   }();
   return m;
 }
@@ -161,11 +174,13 @@ inline int wide_mode() {
 }
 
 // Steps of a k_group batch whose loads are issued together (NULPA_GROUP_STEPS, read once:
-// 8 by default; 1 = one step at a time).
+// 1 by default = one step at a time). Loading S steps' labels before any of them decides
+// makes the half-warp / warp tiers read staler labels: measured on one B200, S = 8 took the
+// SBM-100K run from 4 to 6 passes (0.61 -> 1.00 ms) and R-MAT 27 from 105.3 to 106.6 ms.
 inline int group_steps() {
   static const int m = [] {
     const char* e = std::getenv("NULPA_GROUP_STEPS");
-    return e ? std::atoi(e) : 8;
+    return e ? std::atoi(e) : 1;
   }();
   return m;
 }
@@ -186,7 +201,10 @@ template <int MODE, typename W>
 void launch_wide(const Plan& p, const PassCtx& c, cudaStream_t s, int sms) {
   const uint32_t cnt = p.count[T_CLUSTER];
   auto go = [&](auto kernel, size_t smem) {
-    kernel<<<resident_grid(kernel, kBigThreads, smem, cnt, 1, sms), kBigThreads, smem, s>>>(
+    // (the scratch holds kWideCtasPerSm regions per SM: never launch more CTAs than that)
+    const unsigned grid = std::min<unsigned>(resident_grid(kernel, kWideThreads, smem, cnt, 1, sms),
+                                             unsigned(kWideCtasPerSm) * sms);
+    kernel<<<grid, kWideThreads, smem, s>>>(
         c, p.list[T_CLUSTER], cnt, c.fresh, p.wide_scratch, p.wide_stride, p.m2);
   };
   switch (wide_mode()) {
@@ -253,6 +271,8 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, true>, 256, 0, p.count[T_THREAD],
                            256 * kMinChunk, sms),
              256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+    else if (p.thread_max <= 8 && thread_group())
+      launch_group<MODE, W, WEIGHTED, 8>(c, p.list[T_THREAD], p.count[T_THREAD], s, sms);
     else if (p.thread_max <= 8 && thread_pair())
       k_thread<MODE, W, WEIGHTED, 8, false, 2>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, false, 2>, 256, 0, p.count[T_THREAD], 512, sms),

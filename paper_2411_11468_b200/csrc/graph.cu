@@ -193,7 +193,7 @@ void check_host_csr(const nulpa_csr* csr) {
 
 // Reductions over the resident arrays: max degree, 2m, unit-weight detection,
 // structural validation (offsets monotone, targets < n).
-void finalize_graph(nulpa_graph* g, cudaStream_t s) {
+void finalize_graph(nulpa_graph* g, cudaStream_t s, bool relayout) {
   const uint32_t n = g->n;
   unsigned* d_bad = dalloc<unsigned>(1);
   uint32_t* d_max = dalloc<uint32_t>(1);
@@ -268,7 +268,7 @@ void finalize_graph(nulpa_graph* g, cudaStream_t s) {
   dfree(d_nonunit);
   // Position-order residency (layout.cu); rows_simple above refers to the input
   // numbering, in which the in-row order is kept.
-  relayout_graph(g, s);
+  if (relayout) relayout_graph(g, s);
 }
 
 void partition_two_way(const uint64_t* off, uint32_t n, uint32_t sw, uint32_t* low,
@@ -459,7 +459,8 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
                                 ? std::min<uint32_t>(g->max_degree, dev::kClusterMax)
                                 : uint32_t(dev::kClusterMax);
       p->wide_stride = (NULPA_WIDE_BUCKETS - 1) * dmax;
-      p->wide_scratch = dalloc<uint32_t>(uint64_t(sm_count()) * p->wide_stride);
+      // (one region per resident CTA: k_wide's grid is at most kWideCtasPerSm per SM)
+      p->wide_scratch = dalloc<uint32_t>(uint64_t(sm_count()) * dev::kWideCtasPerSm * p->wide_stride);
     }
     // Hub tier: per-hub global tables and (hub, chunk) work items. Hub counts
     // are small (vertices of degree > block_max), so the layout is built on

@@ -104,8 +104,10 @@ struct nulpa_graph {
 namespace nulpa {
 // Validate a host CSR the way CsrGraph's constructor does (graph.cpp:165-172).
 void check_host_csr(const nulpa_csr* csr);
-// Fill max_degree / total_2m of a resident graph (device reductions).
-void finalize_graph(nulpa_graph* g, cudaStream_t s);
+// Fill max_degree / total_2m of a resident graph (device reductions), then move it to the
+// default layout. `relayout = false` for arrays that are already in position order (a
+// rank's row slice, an upload with a given permutation).
+void finalize_graph(nulpa_graph* g, cudaStream_t s, bool relayout = true);
 // partition_by_degree (lpa.cpp:330-336) on the device: ascending-id lists of
 // deg < switch_degree and deg >= switch_degree.
 void partition_two_way(const uint64_t* off, uint32_t n, uint32_t switch_degree, uint32_t* low,

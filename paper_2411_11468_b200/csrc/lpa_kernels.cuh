@@ -38,7 +38,8 @@ namespace dev {
 
 // Apply the move rule for vertex i (lpa.cpp:157-164 / :87-90). Returns true if
 // the label changed. Called by exactly one thread per vertex.
-template <int MODE>
+// FENCE = false: the caller issues the fence itself (once for several label stores).
+template <int MODE, bool FENCE = true>
 __device__ __forceinline__ bool apply_move(const PassCtx& c, uint32_t i, uint32_t cand) {
   if (cand == kEmpty) return false;
   const uint32_t cur = (MODE == kAsync) ? ld_relaxed(c.lab_out + i) : __ldg(c.lab_in + i);
@@ -46,7 +47,7 @@ __device__ __forceinline__ bool apply_move(const PassCtx& c, uint32_t i, uint32_
   if (!allowed) return false;
   if constexpr (MODE == kAsync) {
     st_relaxed(c.lab_out + i, cand);
-    if (c.wake) fence_sc();  // the label store before the wake loads (a18)
+    if (FENCE && c.wake) fence_sc();  // the label store before the wake loads (a18)
   } else {
     c.lab_out[i] = cand;
     if (c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
@@ -187,8 +188,11 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
         lab[v][k] = valid ? load_label<MODE>(c.lab_in + nb[v][k]) : kEmpty;
         wt[v][k] = valid ? edge_weight<W, WEIGHTED>(c.g, lo[v] + k) : W(0);
       }
+    // The V rows' label stores share one fence before their wake loads (a18).
+    bool chg[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
+      chg[v] = false;
       if (!act[v]) continue;
       // Per-label total in neighbour order (bit-identical to the reference's
       // sequential accumulation, even for non-integer weights), then argmax.
@@ -202,9 +206,17 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
       }
       ++n_v;
       n_e += d[v];
-      if (!apply_move<MODE>(c, iv[v], b.k)) continue;
-      ++n_dn;
-      if (MODE == kAsync && c.wake) {
+      chg[v] = apply_move<MODE, false>(c, iv[v], b.k);
+      n_dn += chg[v];
+    }
+    if (MODE == kAsync && c.wake) {
+      bool any = false;
+#pragma unroll
+      for (int v = 0; v < V; ++v) any |= chg[v];
+      if (any) fence_sc();
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (!chg[v]) continue;
 #pragma unroll
         for (int k = 0; k < DMAX; ++k)
           if (k < d[v]) wake_vertex(c.flags, nb[v][k]);
@@ -378,7 +390,9 @@ __device__ __forceinline__ void gather_insert_multi(const PassCtx& c, const uint
     idx[u] = hash_start(lab[u], cap);
   }
 #pragma unroll
-  for (int u = 0; u < U; ++u) cur[u] = lead[u] ? tab.ld_key(idx[u] & mask) : 0u;
+  for (int u = 0; u < U; ++u) {
+    cur[u] = lead[u] ? tab.ld_key(idx[u] & mask) : 0u;
+  }
   int r[U];
   uint32_t slot[U];
 #pragma unroll
@@ -649,8 +663,8 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_M
       // Two team barriers per vertex: after the gather, and inside team_best
       // (which also re-arms the occupancy count for the next vertex; the sweep
       // has cleared the table by then).
-      team_gather<MODE, W, WEIGHTED, Tab, kTeamU, DEDUP>(c, m.i, m.lo, 0, m.d, tab, cap, ttid, TEAM, pol, occ,
-                                     &s_occ_n[team], fails);
+      team_gather<MODE, W, WEIGHTED, Tab, kTeamU, DEDUP>(c, m.i, m.lo, 0, m.d, tab, cap, ttid, TEAM,
+                                                           pol, occ, &s_occ_n[team], fails);
       sync();
       Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n[team], ttid, TEAM);
       b = team_best<TEAM>(b, s_red[team], ttid, bar, &s_occ_n[team]);
@@ -824,7 +838,7 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
 // filtering by phase). No cluster barriers, no remote atomics, and every SM owns its
 // own vertex.
 #ifndef NULPA_WIDE_LIMIT
-#define NULPA_WIDE_LIMIT 12288
+#define NULPA_WIDE_LIMIT (NULPA_WIDE_CAP / 4 * 3)
 #endif
 constexpr uint32_t kWideLimit = NULPA_WIDE_LIMIT;  // distinct labels per phase (load <= 3/4)
 
@@ -840,12 +854,12 @@ static_assert((kWideBuckets - 1) * uint64_t(kClusterMax) <= kWideScratch,
               "wide scratch holds every bucket layout");
 
 constexpr size_t wide_table_bytes() {
-  return size_t(kClusterCap) * 8 + size_t(kClusterCap) * sizeof(uint16_t);
+  return size_t(kWideCap) * 8 + size_t(kWideCap) * sizeof(uint16_t);
 }
 #ifndef NULPA_WIDE_U
 #define NULPA_WIDE_U 4
 #endif
-constexpr uint32_t kWideChunk = kBigThreads * NULPA_WIDE_U;  // row entries per gather round
+constexpr uint32_t kWideChunk = kWideThreads * NULPA_WIDE_U;  // row entries per gather round
 constexpr uint32_t kWideStage = kWideChunk + 8;  // one TMA stage (widened to 16-byte groups)
 // STAGED kernels add two TMA stages of row targets after the table.
 constexpr size_t wide_bytes(bool staged = false) {
@@ -857,7 +871,7 @@ constexpr size_t wide_bytes(bool staged = false) {
 // round r + 1 are gathered before round r is inserted, so the dependent label loads are
 // in flight while the table atomics of the previous round run.
 template <int MODE, typename W, bool STAGED = true, bool PREFETCH = true>
-__global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32_t* __restrict__ list,
+__global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c, const uint32_t* __restrict__ list,
                                                          uint32_t count, int fresh,
                                                          uint32_t* __restrict__ scratch,
                                                          uint32_t stride, uint64_t m2) {
@@ -867,8 +881,8 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
   uint32_t* snap = scratch + size_t(blockIdx.x) * stride;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemTable<W> tab;
-  tab.bind(smem_raw, kClusterCap);
-  uint16_t* occ = reinterpret_cast<uint16_t*>(smem_raw + size_t(kClusterCap) * 8);
+  tab.bind(smem_raw, kWideCap);
+  uint16_t* occ = reinterpret_cast<uint16_t*>(smem_raw + size_t(kWideCap) * 8);
   uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw + wide_table_bytes());
   __shared__ uint32_t s_item;
   __shared__ int s_flag, s_over;
@@ -878,7 +892,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
   __shared__ __align__(8) uint64_t s_bar[2];
   constexpr uint32_t kWideBatch = 4;  // vertices per work-counter fetch (batched prologue)
   __shared__ Meta s_meta[kWideBatch];
-  for (uint32_t x = threadIdx.x; x < kClusterCap; x += blockDim.x) tab.clear_slot(x);  // once
+  for (uint32_t x = threadIdx.x; x < kWideCap; x += blockDim.x) tab.clear_slot(x);  // once
   if (STAGED && threadIdx.x == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
@@ -943,8 +957,8 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
       // labels than the phase takes and the phase re-streams the whole row. Bucketed
       // phases run to the end: a full table (rare) still flags s_over and restarts.
       const bool may_overflow = !use_b && (len > kWideLimit || P > 1);
-      const uint32_t cap = P == 1 ? min(static_cast<uint32_t>(kClusterCap), pow2_ceil(2 * d))
-                                  : static_cast<uint32_t>(kClusterCap);
+      const uint32_t cap = P == 1 ? min(static_cast<uint32_t>(kWideCap), pow2_ceil(2 * d))
+                                  : static_cast<uint32_t>(kWideCap);
       const uint32_t* src = use_b ? snap + size_t(ph - 1) * d : snap;
       const bool from_row = ph == 0;  // phase 0 gathers targets -> labels; later phases stream labels
       if (STAGED && from_row && threadIdx.x == 0 && nch > 0) {
@@ -965,14 +979,14 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
             const uint32_t* buf = stage + b * kWideStage;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              const uint32_t e = base + u * kBigThreads + threadIdx.x;
+              const uint32_t e = base + u * kWideThreads + threadIdx.x;
               const uint64_t gi = lo + e;
               j[u] = e < d ? (gi < a1 ? buf[gi - a0] : ld_stream(c.g.tgt + gi, pol)) : i;
             }
           } else {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              const uint32_t e = base + u * kBigThreads + threadIdx.x;
+              const uint32_t e = base + u * kWideThreads + threadIdx.x;
               j[u] = e < d ? ld_stream(c.g.tgt + lo + e, pol) : i;
             }
           }
@@ -985,7 +999,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
         } else {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const uint32_t e = base + u * kBigThreads + threadIdx.x;
+            const uint32_t e = base + u * kWideThreads + threadIdx.x;
             lab[u] = e < len ? __ldcg(src + e) : kEmpty;
           }
         }
@@ -999,7 +1013,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
         if (from_row) {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const uint32_t e = base + u * kBigThreads + threadIdx.x;
+            const uint32_t e = base + u * kWideThreads + threadIdx.x;
             if (P > 1 && !use_b && e < d) snap[e] = cur[u];
           }
           if (use_b) {
@@ -1027,7 +1041,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_wide(PassCtx c, const uint32
         const uint32_t wbase = base + (threadIdx.x & ~31u);
         unsigned live = 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) live |= (wbase + u * kBigThreads < len ? 1u : 0u) << u;
+        for (int u = 0; u < U; ++u) live |= (wbase + u * kWideThreads < len ? 1u : 0u) << u;
         unsigned long long f = 0;
         gather_insert_multi<U, W, 0>(c, cur, live, tab, cap, occ, &s_occ_n, f);
         if (f) s_over = 1;  // table full: treat as overflow

@@ -72,7 +72,7 @@ nulpa_graph* slice_graph(const nulpa_graph* g, uint32_t lo, uint32_t hi) {
       NULPA_CUDA(cudaMemcpy(s->perm, g->perm, g->n * 4ull, cudaMemcpyDeviceToDevice));
       NULPA_CUDA(cudaMemcpy(s->inv, g->inv, g->n * 4ull, cudaMemcpyDeviceToDevice));
     }
-    finalize_graph(s, 0);
+    finalize_graph(s, 0, /*relayout=*/false);  // already in position order
     s->rows_simple = g->rows_simple;
     s->total_2m = g->total_2m;  // the whole graph's 2m (modularity's normaliser)
   } catch (...) {
@@ -154,7 +154,7 @@ int nulpa_graph_upload_positioned(const nulpa_csr* csr, const uint32_t* perm,
       NULPA_CUDA(cudaMemcpy(g->perm, perm, csr->n * 4ull, cudaMemcpyHostToDevice));
       NULPA_CUDA(cudaMemcpy(g->inv, inv, csr->n * 4ull, cudaMemcpyHostToDevice));
       g->layout = NULPA_LAYOUT_DEGREE_BUCKETS;
-      finalize_graph(g, 0);
+      finalize_graph(g, 0, /*relayout=*/false);  // positioned by the caller
       g->rows_simple = rows_simple != 0;
     } catch (...) {
       nulpa_graph_free(g);

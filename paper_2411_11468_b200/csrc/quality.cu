@@ -97,6 +97,34 @@ __global__ void __launch_bounds__(256) k_mod_rows32(Graph g, const uint32_t* lab
   }
 }
 
+// k_i and the intra-community weight of edges [e, end) step STRIDE of a row whose vertex
+// has label ci: four targets, then their four labels, are in flight per thread (the label
+// gathers are random reads; one at a time left the kernel latency-bound). Sums are fp64.
+template <int STRIDE>
+__device__ __forceinline__ void accumulate_row_slice(const Graph& g, const uint32_t* lab,
+                                                     uint32_t ci, uint64_t e, uint64_t end,
+                                                     double& ki, double& si) {
+  constexpr int U = 4;
+  for (; e + (U - 1) * STRIDE < end; e += U * STRIDE) {
+    uint32_t j[U], l[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) j[u] = __ldg(g.tgt + e + u * STRIDE);
+#pragma unroll
+    for (int u = 0; u < U; ++u) l[u] = __ldg(lab + j[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double w = g.w ? static_cast<double>(__ldg(g.w + e + u * STRIDE)) : 1.0;
+      ki += w;
+      if (l[u] == ci) si += w;
+    }
+  }
+  for (; e < end; e += STRIDE) {
+    const double w = g.w ? static_cast<double>(__ldg(g.w + e)) : 1.0;
+    ki += w;
+    if (__ldg(lab + __ldg(g.tgt + e)) == ci) si += w;
+  }
+}
+
 // Larger rows: one warp per row.
 __global__ void k_mod_warp(Graph g, const uint32_t* lab, const uint32_t* list, uint32_t count,
                            double* sigma, double* big) {
@@ -107,11 +135,7 @@ __global__ void k_mod_warp(Graph g, const uint32_t* lab, const uint32_t* list, u
     const uint32_t i = list[t];
     const uint32_t ci = lab[i];
     double ki = 0.0, si = 0.0;
-    for (uint64_t e = g.off[i] + lane; e < g.off[i + 1]; e += 32) {
-      const double w = g.w ? static_cast<double>(g.w[e]) : 1.0;
-      ki += w;
-      if (lab[g.tgt[e]] == ci) si += w;
-    }
+    accumulate_row_slice<32>(g, lab, ci, g.off[i] + lane, g.off[i + 1], ki, si);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       ki += __shfl_xor_sync(kFull, ki, o);
@@ -136,11 +160,7 @@ __global__ void k_mod_hub(Graph g, const uint32_t* lab, HubCtx h, double* sigma,
     const uint64_t e0 = h.item_start[it];
     const uint64_t e1 = min(d, e0 + static_cast<uint64_t>(kHubChunk));
     double ki = 0.0, si = 0.0;
-    for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      const double w = g.w ? static_cast<double>(g.w[lo + e]) : 1.0;
-      ki += w;
-      if (lab[g.tgt[lo + e]] == ci) si += w;
-    }
+    accumulate_row_slice<256>(g, lab, ci, lo + e0 + threadIdx.x, lo + e1, ki, si);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       ki += __shfl_xor_sync(kFull, ki, o);

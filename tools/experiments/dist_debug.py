@@ -62,3 +62,33 @@ for own in (False, True):
           "mismatch", int((lab != want.labels).sum()))
     for e in engs:
         e.free()
+
+# ---- pass-0 detail: per-rank changes and the slice's rows against the full graph's
+full = dg.download()
+for r in range(P):
+    lo, hi = bounds[r], bounds[r + 1]
+    ea = DeviceRangeEngine(dg, cfg, lo, hi, own_rows_only=False)
+    eb = DeviceRangeEngine(dg, cfg, lo, hi, own_rows_only=True)
+    so = np.empty(dg.n + 1, np.uint64)
+    st = np.empty(max(1, eb.graph.m2), np.uint32)
+    _capi.check(_capi.lib().nulpa_graph_download_raw(eb.graph._h, so.ctypes.data, st.ctypes.data, None))
+    fo = np.empty(dg.n + 1, np.uint64)
+    ft = np.empty(dg.m2, np.uint32)
+    _capi.check(_capi.lib().nulpa_graph_download_raw(dg._h, fo.ctypes.data, ft.ctypes.data, None))
+    rows_ok = all(np.array_equal(ft[fo[v]:fo[v + 1]], st[so[v]:so[v + 1]]) for v in range(lo, hi))
+    print(f"rank {r} [{lo},{hi}) slice m2={eb.graph.m2} rows equal: {rows_ok}; "
+          f"slice max_degree/rows_simple via pass:")
+    for e in (ea, eb):
+        e.init()
+        info = e.pass_(True, True)
+        torch.cuda.synchronize()
+        print("   ", "slice" if e is eb else "full ", info)
+    la = ea.labels.cpu().numpy().view(np.uint32)
+    lb = eb.labels.cpu().numpy().view(np.uint32)
+    diff = np.nonzero(la != lb)[0]
+    print("    differing positions:", diff[:10], len(diff))
+    for p in diff[:3]:
+        print("     pos", p, "full", la[p], "slice", lb[p], "deg", int(fo[p + 1] - fo[p]),
+              "row", ft[fo[p]:fo[p + 1]][:8])
+    ea.free()
+    eb.free()
