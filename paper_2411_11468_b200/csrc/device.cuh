@@ -83,16 +83,20 @@ constexpr int kBigMax = NULPA_MID_MAX;  // load <= 3/4
 constexpr int kClusterSize = 8;     // portable cluster size
 constexpr int kClusterCap = 16384;  // slots per CTA of the cluster
 constexpr int kClusterMax = kClusterSize * kClusterCap * 3 / 4;  // 98304, load <= 3/4
+// Wide tier (k_wide): CTA size and shared-table slots. 512 threads with an 8K-slot table
+// (two independent CTAs per SM, up to 6144 labels per phase, up to 16 bucketed phases);
+// measured at R-MAT 27 on one B200: wide tier 29.9 -> 27.0 ms per run against one
+// 1024-thread CTA per SM with 16K slots (-DNULPA_WIDE_THREADS=1024 -DNULPA_WIDE_CAP=16384
+// -DNULPA_WIDE_BUCKETS=8): while one CTA sits in a barrier or its argmax sweep, the
+// other's label gathers keep the SM's loads in flight.
 #ifndef NULPA_WIDE_BUCKETS
-#define NULPA_WIDE_BUCKETS 8
+#define NULPA_WIDE_BUCKETS 16
 #endif
-// Wide tier (k_wide): CTA size and shared-table slots. 1024 threads with a 16K-slot table
-// (one CTA per SM), or 512 threads with 8K slots (two independent CTAs per SM).
 #ifndef NULPA_WIDE_THREADS
-#define NULPA_WIDE_THREADS 1024
+#define NULPA_WIDE_THREADS 512
 #endif
 #ifndef NULPA_WIDE_CAP
-#define NULPA_WIDE_CAP 16384
+#define NULPA_WIDE_CAP 8192
 #endif
 constexpr int kWideThreads = NULPA_WIDE_THREADS;
 constexpr int kWideCap = NULPA_WIDE_CAP;

@@ -145,17 +145,6 @@ inline bool thread_pair() {
   return m;
 }
 
-// Thread tier (degree <= 8) as 8-lane groups (k_group<8>: four rows per warp step, the
-// claims of 32 rows behind one fence per lane) instead of one thread per row
-// (NULPA_THREAD_GROUP, read once; 0 by default).
-inline bool thread_group() {
-  static const bool m = [] {
-    const char* e = std::getenv("NULPA_THREAD_GROUP");
-    return e ? std::atoi(e) != 0 : false;
-  }();
-  return m;
-}
-
 // Passes enqueued per host read-back in batched runs (NULPA_BATCH_PASSES, read once).
 inline int batch_passes() {
   static const int m = [] {
@@ -188,7 +177,11 @@ inline int group_steps() {
 template <int MODE, typename W, bool WEIGHTED, int G>
 void launch_group(const PassCtx& c, const uint32_t* list, uint32_t count, cudaStream_t s, int sms) {
   auto go = [&](auto kernel) {
-    kernel<<<resident_grid(kernel, 256, 0, count, 256, sms), 256, 0, s>>>(c, list, count);
+    // entries per warp batch: 32, or fewer when the tier does not fill every resident warp
+    const uint32_t warps = resident_grid(kernel, 256, 0, ~0u >> 1, 256, sms) * 8u;
+    uint32_t bsz = 32;
+    while (bsz > 8 && uint64_t(count) < uint64_t(warps) * bsz) bsz >>= 1;
+    kernel<<<resident_grid(kernel, 256, 0, count, 8 * bsz, sms), 256, 0, s>>>(c, list, count, bsz);
   };
   switch (group_steps()) {
     case 1: go(k_group<MODE, W, WEIGHTED, G, 1>); break;
@@ -205,7 +198,7 @@ void launch_wide(const Plan& p, const PassCtx& c, cudaStream_t s, int sms) {
     const unsigned grid = std::min<unsigned>(resident_grid(kernel, kWideThreads, smem, cnt, 1, sms),
                                              unsigned(kWideCtasPerSm) * sms);
     kernel<<<grid, kWideThreads, smem, s>>>(
-        c, p.list[T_CLUSTER], cnt, c.fresh, p.wide_scratch, p.wide_stride, p.m2);
+        c, p.list[T_CLUSTER], cnt, c.fresh, p.wide_scratch, p.wide_stride, p.m2, p.wide_hint);
   };
   switch (wide_mode()) {
     case 0: go(k_wide<MODE, W, false, false>, wide_bytes(false)); break;
@@ -271,8 +264,6 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, true>, 256, 0, p.count[T_THREAD],
                            256 * kMinChunk, sms),
              256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
-    else if (p.thread_max <= 8 && thread_group())
-      launch_group<MODE, W, WEIGHTED, 8>(c, p.list[T_THREAD], p.count[T_THREAD], s, sms);
     else if (p.thread_max <= 8 && thread_pair())
       k_thread<MODE, W, WEIGHTED, 8, false, 2>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, false, 2>, 256, 0, p.count[T_THREAD], 512, sms),

@@ -338,6 +338,7 @@ Plan::~Plan() {
   dfree(item_hub);
   dfree(item_start);
   dfree(wide_scratch);
+  dfree(wide_hint);
 }
 
 TierBounds resolve_tiers(uint32_t switch_degree, const nulpa_tuning* t) {
@@ -461,6 +462,8 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
       p->wide_stride = (NULPA_WIDE_BUCKETS - 1) * dmax;
       // (one region per resident CTA: k_wide's grid is at most kWideCtasPerSm per SM)
       p->wide_scratch = dalloc<uint32_t>(uint64_t(sm_count()) * dev::kWideCtasPerSm * p->wide_stride);
+      p->wide_hint = dalloc<uint32_t>(p->count[dev::T_CLUSTER]);
+      NULPA_CUDA(cudaMemsetAsync(p->wide_hint, 0, p->count[dev::T_CLUSTER] * 4ull, s));
     }
     // Hub tier: per-hub global tables and (hub, chunk) work items. Hub counts
     // are small (vertices of degree > block_max), so the layout is built on

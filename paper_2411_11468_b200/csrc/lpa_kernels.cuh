@@ -62,6 +62,65 @@ __device__ __forceinline__ void wake_vertex(uint8_t* flags, uint32_t j) {
   if (load_flag(flags + j)) st_relaxed(flags + j, uint8_t(0));
 }
 
+// Wake the neighbours in entries [e0, e1) of the row at `lo`, thread `tid` of `T`: U
+// targets, then their U flags, are in flight before any store. (The flag accesses are
+// volatile asm, so a plain loop of wake_vertex would wait out one target load and one flag
+// load per neighbour.)
+template <int U = 4, typename Off>
+__device__ __forceinline__ void wake_row(uint8_t* flags, const uint32_t* __restrict__ tgt, Off lo,
+                                         uint32_t e0, uint32_t e1, uint32_t tid, uint32_t T,
+                                         uint64_t pol) {
+  for (uint32_t b = e0 + tid; b < e1; b += T * U) {
+    uint32_t j[U];
+    uint8_t f[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) j[u] = b + u * T < e1 ? ld_stream(tgt + lo + b + u * T, pol) : kEmpty;
+#pragma unroll
+    for (int u = 0; u < U; ++u) f[u] = j[u] != kEmpty ? load_flag(flags + j[u]) : uint8_t(0);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (f[u]) st_relaxed(flags + j[u], uint8_t(0));
+  }
+}
+
+// Wake the neighbours of every row of a warp's batch whose bit is set in `chg` (lane k
+// holds row k's `lo` and `d`): the rows' entries are walked as one stream, 32 * U at a
+// time (lane f takes the f-th entry, its row found by a search over the lanes' prefix
+// sums), so short rows do not leave lanes idle. All 32 lanes call it.
+template <int U = 4>
+__device__ __forceinline__ void warp_wake_rows(uint8_t* flags, const uint32_t* __restrict__ tgt,
+                                               uint64_t lo, uint32_t d, unsigned chg, uint64_t pol) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t dm = (chg >> lane & 1u) ? d : 0u;
+  uint32_t pre = dm;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t x = __shfl_up_sync(kFull, pre, o);
+    if (lane >= o) pre += x;
+  }
+  const uint32_t excl = pre - dm, total = __shfl_sync(kFull, pre, 31);
+  for (uint32_t f0 = 0; f0 < total; f0 += 32 * U) {
+    uint32_t j[U];
+    uint8_t fl[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t f = f0 + u * 32 + lane;
+      int r = 0;  // the last lane whose rows start at or before entry f
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1)
+        if (__shfl_sync(kFull, excl, r + st) <= f) r += st;
+      const uint64_t lo_r = __shfl_sync(kFull, lo, r);
+      const uint32_t ex_r = __shfl_sync(kFull, excl, r);
+      j[u] = f < total ? ld_stream(tgt + lo_r + (f - ex_r), pol) : kEmpty;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) fl[u] = j[u] != kEmpty ? load_flag(flags + j[u]) : uint8_t(0);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (fl[u]) st_relaxed(flags + j[u], uint8_t(0));
+  }
+}
+
 // Check-and-set the processed flag (lpa.cpp:143-144). Returns true to skip.
 // The caller fences (claim_fence) before loading the labels the decision depends on.
 __device__ __forceinline__ bool claim_vertex(const PassCtx& c, uint32_t i) {
@@ -80,7 +139,7 @@ __device__ __forceinline__ void claim_fence(const PassCtx& c) {
 
 // Apply the move rule given the vertex's current label `cur` (read when the
 // vertex was claimed: only this vertex's own thread ever writes it).
-template <int MODE>
+template <int MODE, bool FENCE = true>
 __device__ __forceinline__ bool apply_move_cur(const PassCtx& c, uint32_t i, uint32_t cand,
                                                uint32_t cur) {
   if (cand == kEmpty) return false;
@@ -88,7 +147,7 @@ __device__ __forceinline__ bool apply_move_cur(const PassCtx& c, uint32_t i, uin
   if (!allowed) return false;
   if constexpr (MODE == kAsync) {
     st_relaxed(c.lab_out + i, cand);
-    if (c.wake) fence_sc();  // the label store before the wake loads (a18)
+    if (FENCE && c.wake) fence_sc();  // the label store before the wake loads (a18)
   } else {
     c.lab_out[i] = cand;
     if (c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
@@ -217,9 +276,12 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         if (!chg[v]) continue;
+        uint8_t f[DMAX];  // every flag load in flight before the first store
+#pragma unroll
+        for (int k = 0; k < DMAX; ++k) f[k] = k < d[v] ? load_flag(c.flags + nb[v][k]) : uint8_t(0);
 #pragma unroll
         for (int k = 0; k < DMAX; ++k)
-          if (k < d[v]) wake_vertex(c.flags, nb[v][k]);
+          if (f[k]) st_relaxed(c.flags + nb[v][k], uint8_t(0));
         n_w += d[v];
       }
     }
@@ -251,13 +313,16 @@ __device__ __forceinline__ Best<V> group_best(Best<V> b, unsigned gmask) {
 // labels (S independent loads in flight per lane), then the S steps are decided one
 // after another. The batch prologue (claims, row bounds, current labels of 32 list
 // entries) is shared through shared memory.
+// `bsz` (8, 16 or 32) list entries per warp batch: 32 on large tiers; small graphs use
+// shorter batches so that more warps share the tier (a warp walks its batch's steps one
+// after another, each step a target and a label load latency).
 template <int MODE, typename W, bool WEIGHTED, int G, int S = 8>
 __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __restrict__ list,
-                                               uint32_t count) {
+                                               uint32_t count, uint32_t bsz = 32) {
   if (stopped(c.stop)) return;
   constexpr int kPer = 32 / G;           // vertices per warp step
-  constexpr int kSteps = 32 / kPer;      // steps per 32-entry batch
-  static_assert(kSteps % S == 0, "steps per chunk");
+  const int kSteps = static_cast<int>(bsz) / kPer;  // steps per batch
+  static_assert((32 / kPer) % S == 0, "steps per chunk (S > 1 runs 32-entry batches)");
   const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G, wid = threadIdx.x >> 5;
   const unsigned gmask = (G == 32) ? kFull : (((1u << G) - 1u) << (sub * G));
   __shared__ Meta s_meta[8][32];
@@ -265,9 +330,14 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t base = gw * 32; base < count; base += nw * 32) {
-    s_meta[wid][lane] = fetch_meta<MODE>(c, list, base + lane, count);
+  if (S > 1) bsz = 32;
+  for (uint32_t base = gw * bsz; base < count; base += nw * bsz) {
+    s_meta[wid][lane] = fetch_meta<MODE>(c, list, base + lane, min(count, base + bsz));
     __syncwarp();  // every lane's claim (and its fence) before any lane's label loads
+    // Async wake-ups are deferred to the end of the batch: every lane that stored a label
+    // fences once, then the warp wakes the changed rows' neighbours as one stream.
+    unsigned chg_bits = 0;
+    bool stored = false;
 #pragma unroll 1
     for (int c0 = 0; c0 < kSteps; c0 += S) {
       uint32_t j[S], lab[S];
@@ -296,18 +366,28 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
         Best<VBits<W>> b{VBits<W>(0), kEmpty};
         if (lab[k] != kEmpty && (__ffs(peers) - 1) == lane) b = Best<VBits<W>>{to_vbits<W>(sm), lab[k]};
         b = group_best<VBits<W>, G>(b, gmask);
-        int ch = 0;
+        bool ch = false;
         if (m.act && gl == 0) {
-          ch = apply_move_cur<MODE>(c, m.i, b.k, m.cur) ? 1 : 0;
+          ch = apply_move_cur<MODE, false>(c, m.i, b.k, m.cur);
+          stored |= ch;
           ++n_v;
           n_e += m.d;
           n_dn += ch;
           if (MODE == kAsync && ch && c.wake) n_w += m.d;
         }
-        ch = __shfl_sync(kFull, ch, sub * G);
-        if (MODE == kAsync && c.wake) __syncwarp();  // the group leader's store + fence first
-        if (MODE == kAsync && ch && c.wake && m.act && gl < m.d) wake_vertex(c.flags, j[k]);
+        if (MODE == kAsync) {
+          const unsigned bl = __ballot_sync(kFull, ch);
+#pragma unroll
+          for (int q = 0; q < kPer; ++q)
+            if (bl >> (q * G) & 1u) chg_bits |= 1u << ((c0 + k) * kPer + q);
+        }
       }
+    }
+    if (MODE == kAsync && c.wake && chg_bits) {
+      if (stored) fence_sc();  // this lane's label stores before any wake load (a18)
+      __syncwarp();
+      const Meta& me = s_meta[wid][lane];
+      warp_wake_rows<4>(c.flags, c.g.tgt, me.lo, me.d, chg_bits, pol);
     }
     __syncwarp();  // s_meta is rewritten by the next batch
   }
@@ -579,6 +659,28 @@ constexpr int kTeamU = NULPA_TEAM_U;  // gather rounds in flight per team thread
 template <int TEAM>
 constexpr uint32_t kTeamBatch = TEAM <= 32 ? 32u : (TEAM <= 128 ? 16u : 4u);
 
+#ifndef NULPA_TEAM_PREFETCH
+#define NULPA_TEAM_PREFETCH 0
+#endif
+constexpr bool kTeamPrefetch = NULPA_TEAM_PREFETCH != 0;
+
+// First gather round of the row in `m` (edges [0, T * U)): targets into j, labels into lab.
+template <int MODE, int U>
+__device__ __forceinline__ void round_load(const PassCtx& c, const Meta& m, uint32_t base,
+                                           uint32_t tid, uint32_t T, uint64_t pol, uint32_t (&j)[U],
+                                           uint32_t (&lab)[U]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t e = base + u * T + tid;
+    j[u] = e < m.d ? ld_stream(c.g.tgt + m.lo + e, pol) : m.i;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t e = base + u * T + tid;
+    lab[u] = (e < m.d && j[u] != m.i) ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+  }
+}
+
 template <typename Tab, int CAP, int MAXD>
 constexpr size_t team_bytes() {
   return size_t(CAP) * Tab::kSlotBytes + size_t(MAXD) * sizeof(uint16_t);
@@ -652,6 +754,29 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_M
     }
     sync();  // the batch's claims (and fences) before the team's label loads
     const uint32_t nb = min(kBatch, count - base);
+    // Cross-vertex prefetch (unit weights): the first gather round of the batch's next
+    // active vertex is loaded while this one is finished — its targets are requested
+    // before this vertex's table inserts, its labels before this vertex's argmax, move
+    // and wake-ups — so a team waits on roughly one memory latency per vertex instead
+    // of two. (The early reads are a legal asynchronous schedule: the vertex was
+    // claimed, and fenced, before any of them.)
+    constexpr bool kPF = kPacked<WEIGHTED> && kTeamPrefetch;
+    constexpr uint32_t kRound = uint32_t(TEAM) * kTeamU;  // row entries of one gather round
+    unsigned act_mask = 0;
+    if constexpr (kPF && TEAM == 32) act_mask = __ballot_sync(kFull, mine.act);
+    auto next_active = [&](uint32_t v) -> uint32_t {  // first active entry after v, or nb
+      if constexpr (TEAM == 32) {
+        const unsigned rest = v >= 31 ? 0u : (act_mask & (~0u << (v + 1)));
+        return rest ? min(nb, static_cast<uint32_t>(__ffs(rest) - 1)) : nb;
+      } else {
+        uint32_t k = v + 1;
+        while (k < nb && !s_meta[team][k].act) ++k;
+        return k;
+      }
+    };
+    uint32_t pf_j[kTeamU], pf_l[kTeamU];
+    uint32_t pf_v = nb;  // entry whose first round is in pf_l (nb = none)
+    unsigned chg_bits = 0;  // entries of the batch whose label changed
     for (uint32_t v = 0; v < nb; ++v) {
       Meta m;
       if constexpr (TEAM == 32)
@@ -663,8 +788,50 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_M
       // Two team barriers per vertex: after the gather, and inside team_best
       // (which also re-arms the occupancy count for the next vertex; the sweep
       // has cleared the table by then).
-      team_gather<MODE, W, WEIGHTED, Tab, kTeamU, DEDUP>(c, m.i, m.lo, 0, m.d, tab, cap, ttid, TEAM,
-                                                           pol, occ, &s_occ_n[team], fails);
+      if constexpr (kPF) {
+        uint32_t lab0[kTeamU];
+        if (pf_v == v) {
+#pragma unroll
+          for (int u = 0; u < kTeamU; ++u) lab0[u] = pf_l[u];
+        } else {
+          round_load<MODE>(c, m, 0, ttid, TEAM, pol, pf_j, lab0);
+        }
+        // the next vertex's first-round targets, in flight during this vertex's inserts
+        pf_v = next_active(v);
+        Meta mn{};
+        if (pf_v < nb) {
+          if constexpr (TEAM == 32)
+            mn = shfl_meta(mine, pf_v);
+          else
+            mn = s_meta[team][pf_v];
+#pragma unroll
+          for (int u = 0; u < kTeamU; ++u) {
+            const uint32_t e = u * TEAM + ttid;
+            pf_j[u] = e < mn.d ? ld_stream(c.g.tgt + mn.lo + e, pol) : mn.i;
+          }
+        }
+        {
+          const uint32_t wb = ttid & ~31u;
+          unsigned live = 0;
+#pragma unroll
+          for (int u = 0; u < kTeamU; ++u) live |= (wb + u * TEAM < m.d ? 1u : 0u) << u;
+          gather_insert_multi<kTeamU, W, DEDUP>(c, lab0, live, tab, cap, occ, &s_occ_n[team], fails);
+        }
+        if (m.d > kRound)
+          team_gather<MODE, W, WEIGHTED, Tab, kTeamU, DEDUP>(c, m.i, m.lo, kRound, m.d, tab, cap, ttid,
+                                                               TEAM, pol, occ, &s_occ_n[team], fails);
+        // the next vertex's first-round labels, in flight during this vertex's argmax
+        if (pf_v < nb) {
+#pragma unroll
+          for (int u = 0; u < kTeamU; ++u) {
+            const uint32_t e = u * TEAM + ttid;
+            pf_l[u] = (e < mn.d && pf_j[u] != mn.i) ? load_label<MODE>(c.lab_in + pf_j[u]) : kEmpty;
+          }
+        }
+      } else {
+        team_gather<MODE, W, WEIGHTED, Tab, kTeamU, DEDUP>(c, m.i, m.lo, 0, m.d, tab, cap, ttid, TEAM,
+                                                             pol, occ, &s_occ_n[team], fails);
+      }
       sync();
       Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n[team], ttid, TEAM);
       b = team_best<TEAM>(b, s_red[team], ttid, bar, &s_occ_n[team]);
@@ -672,16 +839,26 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_M
       // rule of apply_move_cur); thread 0 writes it.
       const bool changed = b.k != kEmpty && (c.pick_less ? b.k < m.cur : b.k != m.cur);
       if (ttid == 0) {
-        apply_move_cur<MODE>(c, m.i, b.k, m.cur);
+        apply_move_cur<MODE, false>(c, m.i, b.k, m.cur);
         ++n_v;
         n_e += m.d;
         n_dn += changed;
         if (MODE == kAsync && changed && c.wake) n_w += m.d;
       }
-      if (MODE == kAsync && changed && c.wake) {
-        sync();  // thread 0's label store and fence before the team's wake loads
-        for (uint32_t e = ttid; e < m.d; e += TEAM)
-          wake_vertex(c.flags, ld_stream(c.g.tgt + m.lo + e, pol));
+      if (MODE == kAsync && changed) chg_bits |= 1u << v;
+    }
+    // Async wake-ups of the batch's changed rows, deferred to here: thread 0 fences its
+    // label stores once (a18), then the team wakes the rows' neighbours.
+    if (MODE == kAsync && c.wake && chg_bits) {
+      if (ttid == 0) fence_sc();
+      sync();
+      if constexpr (TEAM == 32) {
+        warp_wake_rows<4>(c.flags, c.g.tgt, mine.lo, mine.d, chg_bits, pol);
+      } else {
+        for (unsigned bits = chg_bits; bits; bits &= bits - 1) {
+          const Meta& mw = s_meta[team][__ffs(bits) - 1];
+          wake_row<4>(c.flags, c.g.tgt, mw.lo, 0u, mw.d, ttid, TEAM, pol);
+        }
       }
     }
     if constexpr (TEAM > 32) sync();  // s_meta is rewritten by the next batch
@@ -813,8 +990,7 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
     }
     cl.sync();                                                   // (E) decision visible
     if (MODE == kAsync && c.wake && *cl.map_shared_rank(&s_changed, 0))
-      for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
-        wake_vertex(c.flags, ld_stream(c.g.tgt + lo + e, pol));
+      wake_row<4>(c.flags, c.g.tgt, lo, e0, e1, threadIdx.x, blockDim.x, pol);
   }
   cl.sync();
   warp_add_counter(c.ctr, C_PROC_V, n_v);
@@ -874,7 +1050,8 @@ template <int MODE, typename W, bool STAGED = true, bool PREFETCH = true>
 __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c, const uint32_t* __restrict__ list,
                                                          uint32_t count, int fresh,
                                                          uint32_t* __restrict__ scratch,
-                                                         uint32_t stride, uint64_t m2) {
+                                                         uint32_t stride, uint64_t m2,
+                                                         uint32_t* __restrict__ hint) {
   if (stopped(c.stop)) return;
   // This CTA's row snapshot / phase buckets (L2-resident): phase 0 of a multi-phase
   // vertex writes the labels of later phases here; those phases stream them back.
@@ -936,7 +1113,14 @@ __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c
     const uint32_t i = m.i;
     const uint64_t lo = m.lo;
     const uint32_t d = m.d;
-    uint32_t P = fresh ? (d + kWideLimit - 1) / kWideLimit : 1u;
+    // Phases: from identity labels every label is distinct, P = ceil(d / limit). Later
+    // passes start from the distinct-label count the row held in its previous pass (labels
+    // only merge as a run goes on), so neither the per-round overflow vote nor a restart is
+    // needed unless the row is near the limit (or has no history: P = 1 with the vote).
+    const uint32_t h = fresh ? 0u : hint[t0 + vb];
+    uint32_t P = fresh ? (d + kWideLimit - 1) / kWideLimit : max(1u, (h + kWideLimit - 1) / kWideLimit);
+    const bool known = !fresh && h != 0u && h <= kWideLimit / 2;  // far below the limit: no vote
+    uint32_t distinct = 0;  // (thread 0) labels aggregated over the phases of this row
     // Bucketed phases: phase 0 gathers the row once and appends every label of a
     // later phase to that phase's bucket in the CTA's L2 scratch, so phase q > 0
     // streams only its own labels (d label reads in all, not P * d).
@@ -956,7 +1140,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c
       // Early stop (a per-round block vote) only where a row may hold more distinct
       // labels than the phase takes and the phase re-streams the whole row. Bucketed
       // phases run to the end: a full table (rare) still flags s_over and restarts.
-      const bool may_overflow = !use_b && (len > kWideLimit || P > 1);
+      const bool may_overflow = !use_b && !known && (len > kWideLimit || P > 1);
       const uint32_t cap = P == 1 ? min(static_cast<uint32_t>(kWideCap), pow2_ceil(2 * d))
                                   : static_cast<uint32_t>(kWideCap);
       const uint32_t* src = use_b ? snap + size_t(ph - 1) * d : snap;
@@ -1074,6 +1258,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c
       }
       __syncthreads();
       const bool over = s_over != 0;  // (a bucketed phase 0 past kWideLimit is still exact)
+      if (threadIdx.x == 0) distinct += s_occ_n;
       Best<VBits<W>> b = occ_argmax_reset<W>(tab, occ, s_occ_n, threadIdx.x, blockDim.x);
       b = block_best(b, red);  // (ends with a barrier: the table is clear again)
       if (over) {
@@ -1081,11 +1266,13 @@ __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c
         P = max(2 * P, (d + kWideLimit - 1) / kWideLimit);
         ph = static_cast<uint32_t>(-1);
         best = Best<VBits<W>>{VBits<W>(0), kEmpty};
+        distinct = 0;
         continue;
       }
       if (threadIdx.x == 0) best_merge(best, b.v, b.k);
     }
     if (threadIdx.x == 0) {
+      hint[t0 + vb] = max(distinct, 1u);
       s_flag = apply_move_cur<MODE>(c, i, best.k, m.cur) ? 1 : 0;
       ++n_v;
       n_e += d;
@@ -1093,9 +1280,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c
       if (MODE == kAsync && s_flag && c.wake) n_w += d;
     }
     __syncthreads();
-    if (MODE == kAsync && c.wake && s_flag)
-      for (uint32_t e = threadIdx.x; e < d; e += blockDim.x)
-        wake_vertex(c.flags, ld_stream(c.g.tgt + lo + e, pol));
+    if (MODE == kAsync && c.wake && s_flag) wake_row<4>(c.flags, c.g.tgt, lo, 0u, d, threadIdx.x, blockDim.x, pol);
     __syncthreads();
     }
   }
@@ -1138,7 +1323,7 @@ __global__ void __launch_bounds__(256) k_first_pass(PassCtx c, uint32_t v_lo, ui
     if (MODE == kSync && c.changed) c.changed[atomicAdd(c.changed_n, 1ull)] = i;
     if (MODE == kAsync && c.wake) {
       fence_sc();  // the label store before the wake loads (a18)
-      for (uint32_t e = 0; e < d; ++e) wake_vertex(c.flags, __ldg(c.g.tgt + lo + e));
+      wake_row<4>(c.flags, c.g.tgt, lo, 0u, d, 0u, 1u, policy_evict_first());
       n_w += d;
     }
   }
@@ -1404,8 +1589,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_hub_wake(PassCtx c, HubCtx h)
     const uint32_t d = static_cast<uint32_t>(c.g.off[i + 1] - lo);
     const uint32_t e0 = h.item_start[it];
     const uint32_t e1 = min(d, e0 + kHubChunk);
-    for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
-      wake_vertex(c.flags, ld_stream(c.g.tgt + lo + e, pol));
+    wake_row<4>(c.flags, c.g.tgt, lo, e0, e1, threadIdx.x, blockDim.x, pol);
     if (threadIdx.x == 0) n_w += e1 - e0;
   }
   warp_add_counter(c.ctr, C_WAKE_E, n_w);
@@ -1426,7 +1610,7 @@ __global__ void __launch_bounds__(kBlockThreads) k_wake_list(Graph g, uint8_t* f
   for (uint32_t t = gw; t < count; t += nw) {
     const uint32_t i = list[t];
     const uint64_t lo = g.off[i], hi = g.off[i + 1];
-    for (uint64_t e = lo + lane; e < hi; e += 32) wake_vertex(flags, __ldg(g.tgt + e));
+    wake_row<4>(flags, g.tgt, lo, 0u, static_cast<uint32_t>(hi - lo), lane, 32u, policy_evict_first());
     if (lane == 0) n_w += hi - lo;
   }
   warp_add_counter(ctr, C_WAKE_E, n_w);
@@ -1587,7 +1771,7 @@ __global__ void k_cc_apply(Graph g, uint32_t* lab, const uint32_t* prev, const u
       m &= m - 1;
       const uint32_t v = base + b;
       const uint64_t lo = g.off[v], hi = g.off[v + 1];
-      for (uint64_t e = lo + lane; e < hi; e += 32) wake_vertex(flags, g.tgt[e]);
+      wake_row<4>(flags, g.tgt, lo, 0u, static_cast<uint32_t>(hi - lo), lane, 32u, policy_evict_first());
     }
   }
   warp_add_counter(reverted, 0, nrev);
