@@ -131,6 +131,10 @@ struct PassCtx {
   // Pass guard (batched runs, engine.cu): set on the device once the run has converged;
   // every pass kernel enqueued after that returns at once. nullptr = unguarded.
   const unsigned* stop = nullptr;
+  // Positions [0, ro_end) hold labels no thread writes during this launch (async mode): in
+  // position order they are the vertices of the higher-degree tiers, which run in later
+  // launches. Their gathers take the L1-cached read-only path (graph.cu: tier_ro_bounds).
+  uint32_t ro_end = 0;
 };
 
 // Vertex id stored at position p (label values are vertex ids).
@@ -228,6 +232,18 @@ __device__ __forceinline__ uint32_t load_label(const uint32_t* p) {
 }
 
 __device__ __forceinline__ uint8_t load_flag(const uint8_t* p) { return ld_relaxed(p); }
+
+// Neighbour label at position j: labels that cannot change during this launch (j < ro_end:
+// a later tier's vertices) come through the read-only, L1-cached path — the hottest
+// labels of a power-law graph, shared by every warp on the SM — the rest by the relaxed
+// device-scope load of the async protocol.
+template <int MODE, typename Ctx>
+__device__ __forceinline__ uint32_t gather_label(const Ctx& c, uint32_t j) {
+  if constexpr (MODE == kAsync)
+    return j < c.ro_end ? __ldg(c.lab_in + j) : ld_relaxed(c.lab_in + j);
+  else
+    return __ldg(c.lab_in + j);
+}
 
 template <typename W, bool WEIGHTED>
 __device__ __forceinline__ W edge_weight(const Graph& g, uint64_t e) {

@@ -145,6 +145,62 @@ inline bool thread_pair() {
   return m;
 }
 
+// L2 persistence for the hot prefix of the label array (NULPA_L2_PERSIST = MB, read once;
+// 0 = off). In position order the highest-degree vertices come first, so the first few
+// tens of MB of labels take most of the neighbour-label gathers; a persisting access
+// window keeps them resident while the adjacency streams past.
+inline size_t l2_persist_bytes() {
+  static const size_t m = [] {
+    const char* e = std::getenv("NULPA_L2_PERSIST");
+    return e ? static_cast<size_t>(std::atof(e) * (1 << 20)) : size_t(0);
+  }();
+  return m;
+}
+
+struct L2Window {
+  cudaStream_t s = nullptr;
+  bool on = false;
+  L2Window(cudaStream_t st, const void* base, uint32_t n) : s(st) {
+    size_t want = std::min<size_t>(l2_persist_bytes(), size_t(n) * 4);
+    if (want == 0) return;
+    int dev = 0, max_persist = 0, max_window = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    want = std::min<size_t>(want, std::min<size_t>(max_persist, max_window));
+    if (want == 0) return;
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return;
+    }
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    a.accessPolicyWindow.num_bytes = want;
+    a.accessPolicyWindow.hitRatio = 1.0f;
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    on = cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a) == cudaSuccess;
+    if (!on) (void)cudaGetLastError();
+  }
+  ~L2Window() {
+    if (!on) return;
+    cudaStreamAttrValue a{};
+    a.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &a);
+    cudaCtxResetPersistingL2Cache();
+    (void)cudaGetLastError();
+  }
+};
+
+// Read-only label prefixes (PassCtx::ro_end; NULPA_RO=0 turns them off, read once).
+inline bool ro_labels() {
+  static const bool m = [] {
+    const char* e = std::getenv("NULPA_RO");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return m;
+}
+
 // Passes enqueued per host read-back in batched runs (NULPA_BATCH_PASSES, read once).
 inline int batch_passes() {
   static const int m = [] {
@@ -180,7 +236,7 @@ void launch_group(const PassCtx& c, const uint32_t* list, uint32_t count, cudaSt
     // entries per warp batch: 32, or fewer when the tier does not fill every resident warp
     const uint32_t warps = resident_grid(kernel, 256, 0, ~0u >> 1, 256, sms) * 8u;
     uint32_t bsz = 32;
-    while (bsz > 8 && uint64_t(count) < uint64_t(warps) * bsz) bsz >>= 1;
+    while (bsz > 2 && uint64_t(count) < uint64_t(warps) * bsz) bsz >>= 1;
     kernel<<<resident_grid(kernel, 256, 0, count, 8 * bsz, sms), 256, 0, s>>>(c, list, count, bsz);
   };
   switch (group_steps()) {
@@ -252,8 +308,20 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     allow_smem(k_hub_accum<MODE, W, WEIGHTED, 0>, hub_smem);
   });
   int launches = 0;
+  // A team kernel's launch: entries per team batch shrink (from kTeamBatch) until every
+  // resident team has one, then the grid covers the tier.
+  auto team_launch = [&](auto kernel, int threads, int teams, uint32_t max_batch, size_t smem,
+                         const uint32_t* list, uint32_t count, bool counter) {
+    const uint64_t resident = uint64_t(resident_grid(kernel, threads, smem, ~0u >> 1, 1, sms)) * teams;
+    uint32_t bsz = max_batch;
+    while (bsz > 1 && uint64_t(count) < resident * bsz) bsz >>= 1;
+    if (counter) NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
+    kernel<<<resident_grid(kernel, threads, smem, count, teams * bsz, sms), threads, smem, s>>>(
+        c, list, count, bsz);
+  };
   auto tier = [&](int t) {
     c.ctr = ctr + t * C_COUNT;
+    c.ro_end = (t < Plan::kLists && ro_labels()) ? p.ro_end[t] : 0u;
     prof.begin(t, s);
   };
   if (p.count[T_THREAD] && (tiers >> T_THREAD & 1u)) {
@@ -293,31 +361,26 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   }
   if (p.count[T_WTAB] && (tiers >> T_WTAB & 1u)) {
     tier(T_WTAB);
-    k_wt<<<resident_grid(k_wt, 256, wtab_smem, p.count[T_WTAB], 256, sms), 256, wtab_smem, s>>>(
-        c, p.list[T_WTAB], p.count[T_WTAB]);
+    team_launch(k_wt, 256, 8, kTeamBatch<32>, wtab_smem, p.list[T_WTAB], p.count[T_WTAB], false);
     prof.end(T_WTAB, s);
     ++launches;
   }
   if (p.count[T_BLOCK] && (tiers >> T_BLOCK & 1u)) {
     tier(T_BLOCK);
-    k_b1<<<resident_grid(k_b1, 256, block_smem, p.count[T_BLOCK], 2 * kTeamBatch<128>, sms), 256, block_smem, s>>>(
-        c, p.list[T_BLOCK], p.count[T_BLOCK]);
+    team_launch(k_b1, 256, 2, kTeamBatch<128>, block_smem, p.list[T_BLOCK], p.count[T_BLOCK], false);
     prof.end(T_BLOCK, s);
     ++launches;
   }
   if (p.count[T_BLOCK2] && (tiers >> T_BLOCK2 & 1u)) {
     tier(T_BLOCK2);
-    NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
-    k_b2<<<resident_grid(k_b2, 256, block2_smem, p.count[T_BLOCK2], kTeamBatch<256>, sms), 256, block2_smem,
-           s>>>(c, p.list[T_BLOCK2], p.count[T_BLOCK2]);
+    team_launch(k_b2, 256, 1, kTeamBatch<256>, block2_smem, p.list[T_BLOCK2], p.count[T_BLOCK2], true);
     prof.end(T_BLOCK2, s);
     ++launches;
   }
   if (p.count[T_BIG] && (tiers >> T_BIG & 1u)) {
     tier(T_BIG);
-    NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
-    k_bg<<<resident_grid(k_bg, kMidThreads, big_smem, p.count[T_BIG], kTeamBatch<kMidThreads>, sms), kMidThreads,
-           big_smem, s>>>(c, p.list[T_BIG], p.count[T_BIG]);
+    team_launch(k_bg, kMidThreads, 1, kTeamBatch<kMidThreads>, big_smem, p.list[T_BIG], p.count[T_BIG],
+                true);
     prof.end(T_BIG, s);
     ++launches;
   }
@@ -556,6 +619,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       }
   }
   tr.mark("plan + buffers");
+  L2Window l2win(s, lab0.p, n);
   k_init<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(lab0.p, flags.p, g->offsets, n, g->perm);
   NULPA_CUDA(cudaGetLastError());
   NULPA_CUDA(cudaStreamSynchronize(s));

@@ -290,6 +290,25 @@ void partition_two_way(const uint64_t* off, uint32_t n, uint32_t sw, uint32_t* l
   dfree(d_num);
 }
 
+// ro_end per tier: the first position whose degree bucket (ceil(log2 deg), the layout's
+// key) is at most bmax[t]. Position order is by bucket, descending, so every earlier
+// position holds a vertex of a higher-degree tier.
+__global__ void k_ro_bounds(const uint64_t* off, uint32_t n, const int* bmax, int k, uint32_t* out) {
+  const int t = threadIdx.x;
+  if (t >= k) return;
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    const uint64_t d = off[mid + 1] - off[mid];
+    const int b = d == 0 ? -1 : (d == 1 ? 0 : 64 - __clzll(d - 1));
+    if (b <= bmax[t])
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  out[t] = lo;
+}
+
 __global__ void k_hash_keys(const uint32_t* ids, uint32_t count, uint32_t* keys, int shift) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
     uint32_t x = (ids[t] >> shift) * 0x9E3779B1u;
@@ -452,6 +471,24 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
       for (int t = dev::T_THREAD; t <= dev::T_BLOCK; ++t) scramble_list(p->list[t], p->count[t], s, 5);
     }
 
+    // Read-only label prefixes (PassCtx::ro_end), position layout and whole-graph plans.
+    if (g->perm && v_lo == 0 && v_hi == g->n && g->n > 0) {
+      int bm[Plan::kLists];
+      for (int t = 0; t < Plan::kLists; ++t) {
+        const uint64_t hi = bounds[t][1];
+        bm[t] = hi <= 1 ? 0 : (hi >= (1ull << 40) ? 64 : 64 - __builtin_clzll(hi - 1));
+      }
+      int* d_bm = dalloc<int>(Plan::kLists);
+      uint32_t* d_out = dalloc<uint32_t>(Plan::kLists);
+      NULPA_CUDA(cudaMemcpyAsync(d_bm, bm, sizeof bm, cudaMemcpyHostToDevice, s));
+      k_ro_bounds<<<1, 32, 0, s>>>(g->offsets, g->n, d_bm, Plan::kLists, d_out);
+      NULPA_CUDA(cudaGetLastError());
+      NULPA_CUDA(cudaMemcpyAsync(p->ro_end, d_out, Plan::kLists * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      NULPA_CUDA(cudaStreamSynchronize(s));
+      dfree(d_bm);
+      dfree(d_out);
+      p->ro_end[dev::T_HUB] = g->n;  // hub accumulation writes no label
+    }
     // Wide tier (k_wide): per resident CTA, room for the buckets of phases
     // 1..kWideBuckets-1 of its longest possible row (or one in-order snapshot).
     if (p->count[dev::T_CLUSTER] && !p->weighted) {

@@ -182,6 +182,47 @@ __device__ __forceinline__ Meta fetch_meta(const PassCtx& c, const uint32_t* __r
   return m;
 }
 
+// fetch_meta for a whole warp (all 32 lanes call it, lane k takes entry t = base + k).
+// When the batch's 32 list entries are 32 consecutive positions (tier lists are position
+// ranges, scrambled at most in 32-position blocks), the row bounds come from ONE
+// coalesced 256-byte read of off[i0 .. i0+31] plus one 8-byte read by lane 31:
+// off[i + 1] is the next lane's off[i] (NULPA_VEC_META; otherwise two loads per lane).
+#ifndef NULPA_VEC_META
+#define NULPA_VEC_META 0
+#endif
+template <int MODE>
+__device__ __forceinline__ Meta fetch_meta_warp(const PassCtx& c, const uint32_t* __restrict__ list,
+                                                uint32_t t, uint32_t count) {
+  if constexpr (!NULPA_VEC_META) {
+    return fetch_meta<MODE>(c, list, t, count);
+  } else {
+    const int lane = threadIdx.x & 31;
+    Meta m{0u, 0u, 0u, 0ull, false};
+    const bool in = t < count;
+    m.i = in ? __ldg(list + t) : 0u;
+    const uint32_t i0 = __shfl_sync(kFull, m.i, 0);
+    const bool run = __all_sync(kFull, !in || m.i == i0 + static_cast<uint32_t>(lane));
+    m.act = in && !claim_vertex(c, m.i);
+    if (run) {
+      const uint64_t o = in ? __ldg(c.g.off + m.i) : 0ull;
+      uint64_t o1 = __shfl_down_sync(kFull, o, 1);
+      if (lane == 31 && in) o1 = __ldg(c.g.off + m.i + 1);
+      // (a lane past `count` has in == false; the last in-range lane below it loads its own)
+      if (in && lane < 31 && t + 1 >= count) o1 = __ldg(c.g.off + m.i + 1);
+      if (m.act) {
+        m.lo = o;
+        m.d = static_cast<uint32_t>(o1 - o);
+      }
+    } else if (m.act) {
+      m.lo = __ldg(c.g.off + m.i);
+      m.d = static_cast<uint32_t>(__ldg(c.g.off + m.i + 1) - m.lo);
+    }
+    if (m.act) m.cur = (MODE == kAsync) ? ld_relaxed(c.lab_out + m.i) : __ldg(c.lab_in + m.i);
+    claim_fence<MODE>(c);
+    return m;
+  }
+}
+
 __device__ __forceinline__ Meta shfl_meta(const Meta& m, int src) {
   Meta r;
   r.i = __shfl_sync(kFull, m.i, src);
@@ -244,7 +285,7 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
 #pragma unroll
       for (int k = 0; k < DMAX; ++k) {
         const bool valid = k < d[v] && nb[v][k] != iv[v];  // self-loops skipped (lpa.hpp:102)
-        lab[v][k] = valid ? load_label<MODE>(c.lab_in + nb[v][k]) : kEmpty;
+        lab[v][k] = valid ? gather_label<MODE>(c, nb[v][k]) : kEmpty;
         wt[v][k] = valid ? edge_weight<W, WEIGHTED>(c.g, lo[v] + k) : W(0);
       }
     // The V rows' label stores share one fence before their wake loads (a18).
@@ -332,7 +373,7 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   if (S > 1) bsz = 32;
   for (uint32_t base = gw * bsz; base < count; base += nw * bsz) {
-    s_meta[wid][lane] = fetch_meta<MODE>(c, list, base + lane, min(count, base + bsz));
+    s_meta[wid][lane] = fetch_meta_warp<MODE>(c, list, base + lane, min(count, base + bsz));
     __syncwarp();  // every lane's claim (and its fence) before any lane's label loads
     // Async wake-ups are deferred to the end of the batch: every lane that stored a label
     // fences once, then the warp wakes the changed rows' neighbours as one stream.
@@ -351,7 +392,7 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
       for (int k = 0; k < S; ++k) {
         const Meta& m = s_meta[wid][(c0 + k) * kPer + sub];
         const bool valid = m.act && gl < m.d && j[k] != m.i;
-        lab[k] = valid ? load_label<MODE>(c.lab_in + j[k]) : kEmpty;
+        lab[k] = valid ? gather_label<MODE>(c, j[k]) : kEmpty;
         w[k] = valid ? edge_weight<W, WEIGHTED>(c.g, m.lo + gl) : W(0);
       }
 #pragma unroll
@@ -542,7 +583,7 @@ __device__ __forceinline__ void team_gather(const PassCtx& c, uint32_t i, uint64
     for (int u = 0; u < U; ++u) {
       const uint32_t e = base + u * T + tid;
       const bool valid = e < e1 && j[u] != i;
-      lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+      lab[u] = valid ? gather_label<MODE>(c, j[u]) : kEmpty;
       w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
     }
     // Skip warp-rounds with no edge at all (warp-uniform test): short rows do not
@@ -677,7 +718,7 @@ __device__ __forceinline__ void round_load(const PassCtx& c, const Meta& m, uint
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint32_t e = base + u * T + tid;
-    lab[u] = (e < m.d && j[u] != m.i) ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+    lab[u] = (e < m.d && j[u] != m.i) ? gather_label<MODE>(c, j[u]) : kEmpty;
   }
 }
 
@@ -696,8 +737,8 @@ constexpr size_t team_bytes() {
 template <int MODE, typename W, bool WEIGHTED, int CTA_THREADS, int TEAM, int CAP, int MAXD,
           int DEDUP = 1>
 __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_MINB : (CTA_THREADS == 512 ? 2 : 1))
-    k_team(PassCtx c, const uint32_t* __restrict__ list,
-                                                      uint32_t count) {
+    k_team(PassCtx c, const uint32_t* __restrict__ list, uint32_t count,
+           uint32_t bsz = kTeamBatch<TEAM>) {
   if (stopped(c.stop)) return;
   static_assert(CTA_THREADS % TEAM == 0 && TEAM % 32 == 0, "team shape");
   constexpr int kTeams = CTA_THREADS / TEAM;
@@ -725,7 +766,11 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_M
   // Teams take kBatch list entries at a time: the team's first warp fetches the
   // batch prologue (claims, row bounds, current labels) for all of them at once.
   // Larger teams own fewer, longer rows per batch (load balance at the tail).
+  // kBatch entries per team batch at most; `bsz` (<= kBatch) at run time: a tier too small
+  // to give every resident team a full batch uses shorter ones (more teams busy, a shorter
+  // per-team chain of vertices).
   constexpr uint32_t kBatch = kTeamBatch<TEAM>;
+  bsz = min(max(bsz, 1u), kBatch);
   __shared__ Meta s_meta[TEAM > 32 ? kTeams : 1][kBatch];
   const uint32_t nteams = gridDim.x * kTeams;
   // Teams of >= 256 threads own long rows: they pull batches from a work
@@ -735,25 +780,29 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_M
   __shared__ uint32_t s_base[kTeams];
   auto next_base = [&](uint32_t cur) -> uint32_t {
     if constexpr (kDynamic) {
-      if (ttid == 0) s_base[team] = atomicAdd(c.work, kBatch);
+      if (ttid == 0) s_base[team] = atomicAdd(c.work, bsz);
       sync();
       const uint32_t b = s_base[team];
       sync();
       return b;
     } else {
-      return cur + nteams * kBatch;
+      return cur + nteams * bsz;
     }
   };
-  uint32_t first = (blockIdx.x * kTeams + team) * kBatch;
+  uint32_t first = (blockIdx.x * kTeams + team) * bsz;
   if constexpr (kDynamic) first = next_base(0);
   for (uint32_t base = first; base < count; base = next_base(base)) {
     Meta mine{};
-    if (ttid < kBatch) mine = fetch_meta<MODE>(c, list, base + ttid, count);
+    const uint32_t lim = min(count, base + bsz);
+    if constexpr (TEAM == 32)
+      mine = fetch_meta_warp<MODE>(c, list, base + ttid, lim);
+    else if (ttid < kBatch)
+      mine = fetch_meta<MODE>(c, list, base + ttid, lim);
     if constexpr (TEAM > 32) {
       if (ttid < kBatch) s_meta[team][ttid] = mine;
     }
     sync();  // the batch's claims (and fences) before the team's label loads
-    const uint32_t nb = min(kBatch, count - base);
+    const uint32_t nb = min(bsz, count - base);
     // Cross-vertex prefetch (unit weights): the first gather round of the batch's next
     // active vertex is loaded while this one is finished — its targets are requested
     // before this vertex's table inserts, its labels before this vertex's argmax, move
@@ -825,7 +874,7 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_M
 #pragma unroll
           for (int u = 0; u < kTeamU; ++u) {
             const uint32_t e = u * TEAM + ttid;
-            pf_l[u] = (e < mn.d && pf_j[u] != mn.i) ? load_label<MODE>(c.lab_in + pf_j[u]) : kEmpty;
+            pf_l[u] = (e < mn.d && pf_j[u] != mn.i) ? gather_label<MODE>(c, pf_j[u]) : kEmpty;
           }
         }
       } else {
@@ -944,7 +993,7 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
       for (int u = 0; u < U; ++u) {
         const uint32_t e = base + u * blockDim.x + threadIdx.x;
         const bool valid = e < e1 && j[u] != i;
-        lab[u] = valid ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+        lab[u] = valid ? gather_label<MODE>(c, j[u]) : kEmpty;
         w[u] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
       }
       const uint32_t wbase = base + (threadIdx.x & ~31u);
@@ -1175,7 +1224,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c
             }
           }
 #pragma unroll
-          for (int u = 0; u < U; ++u) lab[u] = j[u] != i ? load_label<MODE>(c.lab_in + j[u]) : kEmpty;
+          for (int u = 0; u < U; ++u) lab[u] = j[u] != i ? gather_label<MODE>(c, j[u]) : kEmpty;
           if constexpr (STAGED) {
             __syncthreads();  // every thread has read stage k & 1: refill it with chunk k + 2
             if (threadIdx.x == 0 && k + 2 < nch) issue(lo, d, k + 2);

@@ -13,6 +13,10 @@ struct Plan {
   uint32_t* wide_scratch = nullptr;  // [SMs x wide_stride] row snapshots / phase buckets of the wide tier
   uint32_t wide_stride = 0;          // u32 per CTA: (NULPA_WIDE_BUCKETS - 1) x the tier's max degree
   uint32_t* wide_hint = nullptr;     // [count[T_CLUSTER]] distinct labels each row held in its last pass
+  // Per tier: positions [0, ro_end[t]) belong to higher-degree buckets than any vertex of
+  // tier t (position layout, whole-graph plans; 0 otherwise). T_HUB: n (the hub
+  // accumulate kernels write no label).
+  uint32_t ro_end[dev::kTiers] = {};
   uint32_t v_lo = 0, v_hi = 0;  // vertex range the tiers cover
   uint64_t m2 = 0;              // the graph's target count (TMA windows stay inside it)
   int value_bytes = 4;  // hashtable value width the hub tables were sized for
