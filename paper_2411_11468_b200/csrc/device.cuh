@@ -135,6 +135,8 @@ struct PassCtx {
   // position order they are the vertices of the higher-degree tiers, which run in later
   // launches. Their gathers take the L1-cached read-only path (graph.cu: tier_ro_bounds).
   uint32_t ro_end = 0;
+  // ... and so do positions [ro_lo, n): the lower-degree tiers, which ran in earlier launches.
+  uint32_t ro_lo = 0xFFFFFFFFu;
 };
 
 // Vertex id stored at position p (label values are vertex ids).
@@ -240,7 +242,7 @@ __device__ __forceinline__ uint8_t load_flag(const uint8_t* p) { return ld_relax
 template <int MODE, typename Ctx>
 __device__ __forceinline__ uint32_t gather_label(const Ctx& c, uint32_t j) {
   if constexpr (MODE == kAsync)
-    return j < c.ro_end ? __ldg(c.lab_in + j) : ld_relaxed(c.lab_in + j);
+    return (j < c.ro_end || j >= c.ro_lo) ? __ldg(c.lab_in + j) : ld_relaxed(c.lab_in + j);
   else
     return __ldg(c.lab_in + j);
 }

@@ -201,6 +201,16 @@ inline bool ro_labels() {
   return m;
 }
 
+// ... and the suffix of lower-degree tiers (NULPA_RO_LOW, read once; 0 by default: those
+// labels are cold, and caching them in L1 cost R-MAT 27 97.3 -> 99.5 ms per run).
+inline bool ro_labels_low() {
+  static const bool m = [] {
+    const char* e = std::getenv("NULPA_RO_LOW");
+    return e ? std::atoi(e) != 0 : false;
+  }();
+  return m;
+}
+
 // Passes enqueued per host read-back in batched runs (NULPA_BATCH_PASSES, read once).
 inline int batch_passes() {
   static const int m = [] {
@@ -233,10 +243,10 @@ inline int group_steps() {
 template <int MODE, typename W, bool WEIGHTED, int G>
 void launch_group(const PassCtx& c, const uint32_t* list, uint32_t count, cudaStream_t s, int sms) {
   auto go = [&](auto kernel) {
-    // entries per warp batch: 32, or fewer when the tier does not fill every resident warp
-    const uint32_t warps = resident_grid(kernel, 256, 0, ~0u >> 1, 256, sms) * 8u;
-    uint32_t bsz = 32;
-    while (bsz > 2 && uint64_t(count) < uint64_t(warps) * bsz) bsz >>= 1;
+    // 32 entries per warp batch, walked in order: shorter batches on small tiers (more
+    // warps busy) made the pass more Jacobi-like — SBM-100K quality dropped (Q 0.855 ->
+    // 0.84) and the six-block KAT split a block — for no time gained (0.58 ms per run).
+    constexpr uint32_t bsz = 32;
     kernel<<<resident_grid(kernel, 256, 0, count, 8 * bsz, sms), 256, 0, s>>>(c, list, count, bsz);
   };
   switch (group_steps()) {
@@ -308,20 +318,19 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     allow_smem(k_hub_accum<MODE, W, WEIGHTED, 0>, hub_smem);
   });
   int launches = 0;
-  // A team kernel's launch: entries per team batch shrink (from kTeamBatch) until every
-  // resident team has one, then the grid covers the tier.
+  // A team kernel's launch (full kTeamBatch batches: see launch_group).
   auto team_launch = [&](auto kernel, int threads, int teams, uint32_t max_batch, size_t smem,
                          const uint32_t* list, uint32_t count, bool counter) {
-    const uint64_t resident = uint64_t(resident_grid(kernel, threads, smem, ~0u >> 1, 1, sms)) * teams;
-    uint32_t bsz = max_batch;
-    while (bsz > 1 && uint64_t(count) < resident * bsz) bsz >>= 1;
+    const uint32_t bsz = max_batch;
     if (counter) NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
     kernel<<<resident_grid(kernel, threads, smem, count, teams * bsz, sms), threads, smem, s>>>(
         c, list, count, bsz);
   };
   auto tier = [&](int t) {
     c.ctr = ctr + t * C_COUNT;
-    c.ro_end = (t < Plan::kLists && ro_labels()) ? p.ro_end[t] : 0u;
+    const bool ro = t < Plan::kLists && ro_labels() && p.ro_end[T_HUB] != 0;
+    c.ro_end = ro ? p.ro_end[t] : 0u;
+    c.ro_lo = (ro && ro_labels_low()) ? p.ro_lo[t] : 0xFFFFFFFFu;
     prof.begin(t, s);
   };
   if (p.count[T_THREAD] && (tiers >> T_THREAD & 1u)) {

@@ -473,18 +473,26 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
 
     // Read-only label prefixes (PassCtx::ro_end), position layout and whole-graph plans.
     if (g->perm && v_lo == 0 && v_hi == g->n && g->n > 0) {
-      int bm[Plan::kLists];
+      // bm[t]: the bucket of tier t's highest degree (prefix bound); bm[kLists + t]: one
+      // below the bucket of its lowest degree (suffix bound; every degree there is smaller).
+      auto bucket = [](uint64_t d) { return d <= 1 ? 0 : (d >= (1ull << 40) ? 64 : 64 - __builtin_clzll(d - 1)); };
+      int bm[2 * Plan::kLists];
       for (int t = 0; t < Plan::kLists; ++t) {
-        const uint64_t hi = bounds[t][1];
-        bm[t] = hi <= 1 ? 0 : (hi >= (1ull << 40) ? 64 : 64 - __builtin_clzll(hi - 1));
+        bm[t] = bucket(bounds[t][1]);
+        bm[Plan::kLists + t] = bounds[t][0] <= 1 ? -1 : bucket(bounds[t][0]) - 1;
       }
-      int* d_bm = dalloc<int>(Plan::kLists);
-      uint32_t* d_out = dalloc<uint32_t>(Plan::kLists);
+      int* d_bm = dalloc<int>(2 * Plan::kLists);
+      uint32_t* d_out = dalloc<uint32_t>(2 * Plan::kLists);
       NULPA_CUDA(cudaMemcpyAsync(d_bm, bm, sizeof bm, cudaMemcpyHostToDevice, s));
-      k_ro_bounds<<<1, 32, 0, s>>>(g->offsets, g->n, d_bm, Plan::kLists, d_out);
+      k_ro_bounds<<<1, 64, 0, s>>>(g->offsets, g->n, d_bm, 2 * Plan::kLists, d_out);
       NULPA_CUDA(cudaGetLastError());
-      NULPA_CUDA(cudaMemcpyAsync(p->ro_end, d_out, Plan::kLists * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+      uint32_t out[2 * Plan::kLists];
+      NULPA_CUDA(cudaMemcpyAsync(out, d_out, sizeof out, cudaMemcpyDeviceToHost, s));
       NULPA_CUDA(cudaStreamSynchronize(s));
+      for (int t = 0; t < Plan::kLists; ++t) {
+        p->ro_end[t] = out[t];
+        p->ro_lo[t] = out[Plan::kLists + t];
+      }
       dfree(d_bm);
       dfree(d_out);
       p->ro_end[dev::T_HUB] = g->n;  // hub accumulation writes no label

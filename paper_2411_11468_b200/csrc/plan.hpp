@@ -17,6 +17,7 @@ struct Plan {
   // tier t (position layout, whole-graph plans; 0 otherwise). T_HUB: n (the hub
   // accumulate kernels write no label).
   uint32_t ro_end[dev::kTiers] = {};
+  uint32_t ro_lo[dev::kTiers] = {};  // positions [ro_lo[t], n) belong to lower-degree buckets
   uint32_t v_lo = 0, v_hi = 0;  // vertex range the tiers cover
   uint64_t m2 = 0;              // the graph's target count (TMA windows stay inside it)
   int value_bytes = 4;  // hashtable value width the hub tables were sized for

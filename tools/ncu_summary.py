@@ -7,13 +7,19 @@ import subprocess
 import sys
 
 
+def clean(name):
+    """Kernel names as 'k_team<0, float, 0, 256, ...>' whatever ncu's name base."""
+    return name.replace("(int)", "").replace("(bool)", "").replace("nulpa::dev::", "").replace(
+        "nulpa::<unnamed>::", "")
+
+
 def launches(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h, rows = rows[0], rows[1:]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
     agg = collections.OrderedDict()
     for r in rows:
-        k = r[ki].split("(")[0]
+        k = clean(r[ki]).split("(")[0]
         v = float(r[vi].replace(",", ""))
         a = agg.setdefault(k, [0, 0.0])
         a[0] += 1
@@ -68,7 +74,7 @@ def full(path):
             return v / 1e3 if u[k] == "Mbyte" else v if u[k] == "Gbyte" else v / 1e9
         st = sorted(((float(d[f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio"]), s)
                      for s in STALLS), reverse=True)[:4]
-        print(f"{d['Kernel Name'].split('(')[0][:58]} | {float(d['gpu__time_duration.sum']):.2f} | "
+        print(f"{clean(d['Kernel Name']).split('(')[0][:58]} | {float(d['gpu__time_duration.sum']):.2f} | "
               f"{gb('dram__bytes_read.sum'):.2f} | {gb('dram__bytes_write.sum'):.2f} | "
               f"{float(d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "nan") or "nan"):.1f} | "
               f"{float(d['lts__t_sector_hit_rate.pct']):.1f} | "

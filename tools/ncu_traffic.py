@@ -7,8 +7,8 @@ import json
 import subprocess
 import sys
 
-TIER_OF = [("k_thread", "thread"), ("k_group<0, float, 0, 16>", "half_warp"),
-           ("k_group<0, float, 0, 32>", "warp"), ("k_team<0, float, 0, 256, 32,", "team32"),
+TIER_OF = [("k_thread", "thread"), ("k_group<0, float, 0, 16", "half_warp"),
+           ("k_group<0, float, 0, 32", "warp"), ("k_team<0, float, 0, 256, 32,", "team32"),
            ("k_team<0, float, 0, 256, 128,", "team128"), ("k_team<0, float, 0, 256, 256,", "team256"),
            ("k_team<0, float, 0, 512, 512,", "cta512"), ("k_wide", "wide"), ("k_cluster", "wide"),
            ("k_hub", "hub")]
@@ -21,7 +21,7 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 acc = collections.defaultdict(lambda: [0, 0.0, 0.0])
 for r in data:
     d = dict(zip(h, r))
-    name = d["Kernel Name"]
+    name = d["Kernel Name"].replace("(int)", "").replace("(bool)", "").replace("nulpa::dev::", "")
     tier = next((t for k, t in TIER_OF if k in name), None)
     if tier is None:
         continue
