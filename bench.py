@@ -114,7 +114,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-TRAFFIC_JSON = ROOT / "profiles" / "r1s5" / "ncu_traffic_r27.json"
+TRAFFIC_JSON = ROOT / "profiles" / "r2" / "ncu_traffic_r27.json"
 
 
 def ncu_traffic(tier: str, args):

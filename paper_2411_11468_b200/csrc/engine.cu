@@ -211,6 +211,27 @@ inline bool ro_labels_low() {
   return m;
 }
 
+// In-warp label dedupe in the team tables after the first pass (NULPA_DEDUP_LATER, read
+// once; 1 by default).
+inline bool dedup_later() {
+  static const bool m = [] {
+    const char* e = std::getenv("NULPA_DEDUP_LATER");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return m;
+}
+
+// Thread tier with four claims per fence and batch-deferred wake-ups (k_thread_q;
+// NULPA_THREAD_Q, read once; 0 by default). Measured on one B200: R-MAT 27 thread tier
+// 5.00 -> 5.32 ms per run, web-like 5.75 -> 5.42 ms, SBM-100K 0.04 -> 0.07 ms.
+inline bool thread_q() {
+  static const bool m = [] {
+    const char* e = std::getenv("NULPA_THREAD_Q");
+    return e ? std::atoi(e) != 0 : false;
+  }();
+  return m;
+}
+
 // Passes enqueued per host read-back in batched runs (NULPA_BATCH_PASSES, read once).
 inline int batch_passes() {
   static const int m = [] {
@@ -269,6 +290,7 @@ void launch_wide(const Plan& p, const PassCtx& c, cudaStream_t s, int sms) {
   switch (wide_mode()) {
     case 0: go(k_wide<MODE, W, false, false>, wide_bytes(false)); break;
     case 1: go(k_wide<MODE, W, false, true>, wide_bytes(false)); break;
+    case 3: go(k_wide<MODE, W, false, true, true>, wide_bytes(false)); break;
     default: go(k_wide<MODE, W, true, true>, wide_bytes(true));
   }
 }
@@ -288,7 +310,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   constexpr size_t hub_smem = kHubCap * Tab::kSlotBytes + kHubChunk * sizeof(uint16_t);
   // First pass of a run (labels still mostly distinct): the team tables skip the
   // in-warp dedupe (see k_team).
-  const bool dd = !c.fresh;
+  const bool dd = !c.fresh && dedup_later();
   constexpr int kDedupLater = 1;  // (merging only lane 0's label: 0.6 ms slower)
   auto k_wt = dd ? k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, kDedupLater>
                  : k_team<MODE, W, WEIGHTED, 256, 32, kWarpTabCap, kWarpTabMax, 0>;
@@ -312,6 +334,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     if constexpr (!WEIGHTED) {
       allow_smem(k_wide<MODE, W, true, true>, wide_bytes(true));
       allow_smem(k_wide<MODE, W, false, true>, wide_bytes(false));
+      allow_smem(k_wide<MODE, W, false, true, true>, wide_bytes(false));
       allow_smem(k_wide<MODE, W, false, false>, wide_bytes(false));
     }
     allow_smem(k_hub_accum<MODE, W, WEIGHTED, 1>, hub_smem);
@@ -340,6 +363,10 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
       k_thread<MODE, W, WEIGHTED, 8, true>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, true>, 256, 0, p.count[T_THREAD],
                            256 * kMinChunk, sms),
+             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+    else if (p.thread_max <= 8 && thread_q())
+      k_thread_q<MODE, W, WEIGHTED, 8>
+          <<<resident_grid(k_thread_q<MODE, W, WEIGHTED, 8>, 256, 0, p.count[T_THREAD], 256 * 4, sms),
              256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
     else if (p.thread_max <= 8 && thread_pair())
       k_thread<MODE, W, WEIGHTED, 8, false, 2>

@@ -333,6 +333,91 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
   warp_add_counter(c.ctr, C_WAKE_E, n_w);
 }
 
+// Thread per vertex, Q rows per thread iteration with the protocol's fences amortised:
+// the Q claims share one fence, the Q rows are then decided one after another (one row's
+// loads in registers at a time), and their label stores share one fence before the
+// warp wakes every changed row of the iteration as one stream (warp_wake_rows).
+template <int MODE, typename W, bool WEIGHTED, int DMAX, int Q = 4>
+__global__ void __launch_bounds__(256) k_thread_q(PassCtx c, const uint32_t* __restrict__ list,
+                                                  uint32_t count) {
+  if (stopped(c.stop)) return;
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
+  const uint64_t pol = policy_evict_first();
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  // every lane of a warp runs the same number of iterations (warp-wide wake-ups)
+  const uint32_t span = ((count + 31u) & ~31u);
+  for (uint32_t t = tid; t - (tid & 31u) < span; t += stride * Q) {
+    uint32_t iq[Q];
+    bool aq[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const uint32_t tv = t + q * stride;
+      aq[q] = tv < count;
+      iq[q] = aq[q] ? __ldg(list + tv) : 0u;
+      if (aq[q]) aq[q] = !claim_vertex(c, iq[q]);
+    }
+    claim_fence<MODE>(c);
+    bool stored = false;
+    unsigned chg = 0;  // bit q: row q of this thread changed label
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (!aq[q]) continue;
+      const uint32_t i = iq[q];
+      const uint64_t lo = __ldg(c.g.off + i);
+      const uint32_t d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
+      uint32_t nb[DMAX], lab[DMAX];
+      W wt[DMAX];
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k) nb[k] = (k < d) ? ld_stream(c.g.tgt + lo + k, pol) : i;
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k) {
+        const bool valid = k < d && nb[k] != i;  // self-loops skipped (lpa.hpp:102)
+        lab[k] = valid ? gather_label<MODE>(c, nb[k]) : kEmpty;
+        wt[k] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + k) : W(0);
+      }
+      // per-label total in neighbour order (bit-identical sums), then argmax
+      Best<VBits<W>> b{VBits<W>(0), kEmpty};
+#pragma unroll
+      for (int k = 0; k < DMAX; ++k) {
+        W sum = W(0);
+#pragma unroll
+        for (int m = 0; m < DMAX; ++m) sum += (lab[m] == lab[k]) ? wt[m] : W(0);
+        best_merge(b, to_vbits<W>(sum), lab[k]);
+      }
+      ++n_v;
+      n_e += d;
+      if (apply_move<MODE, false>(c, i, b.k)) {
+        ++n_dn;
+        stored = true;
+        chg |= 1u << q;
+        if (MODE == kAsync && c.wake) n_w += d;
+      }
+    }
+    if (MODE == kAsync && c.wake && __any_sync(kFull, chg != 0)) {
+      if (stored) fence_sc();  // this thread's label stores before any wake load (a18)
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const bool mine = chg >> q & 1u;
+        const unsigned rows = __ballot_sync(kFull, mine);
+        if (!rows) continue;
+        uint64_t lo = 0;
+        uint32_t d = 0;
+        if (mine) {
+          lo = __ldg(c.g.off + iq[q]);
+          d = static_cast<uint32_t>(__ldg(c.g.off + iq[q] + 1) - lo);
+        }
+        warp_wake_rows<4>(c.flags, c.g.tgt, lo, d, rows, pol);
+      }
+    }
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+}
+
 // ---- tier: G lanes per vertex, register dedup -------------------------------------
 
 template <typename V, int G>
@@ -1095,7 +1180,9 @@ constexpr size_t wide_bytes(bool staged = false) {
 // two chunks ahead of the label gather (mbarrier per stage). PREFETCH: the labels of
 // round r + 1 are gathered before round r is inserted, so the dependent label loads are
 // in flight while the table atomics of the previous round run.
-template <int MODE, typename W, bool STAGED = true, bool PREFETCH = true>
+// DEEP (with PREFETCH, not STAGED): the targets of round r + 2 are loaded while round r is
+// inserted, so the label gather of round r + 1 never waits on its targets.
+template <int MODE, typename W, bool STAGED = true, bool PREFETCH = true, bool DEEP = false>
 __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c, const uint32_t* __restrict__ list,
                                                          uint32_t count, int fresh,
                                                          uint32_t* __restrict__ scratch,
@@ -1198,10 +1285,23 @@ __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c
         issue(lo, d, 0);
         if (nch > 1) issue(lo, d, 1);
       }
+      uint32_t jq[U];  // DEEP: the targets of the next round to gather
+      auto load_targets = [&](uint32_t k) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t e = k * CH + u * kWideThreads + threadIdx.x;
+          jq[u] = e < d ? ld_stream(c.g.tgt + lo + e, pol) : i;
+        }
+      };
+      if (DEEP && from_row && nch > 0) load_targets(0);
       // Gather round k into lab[] (issues the loads; the values are consumed later).
       auto gather = [&](uint32_t k, uint32_t (&lab)[U]) {
         const uint32_t base = k * CH;
-        if (from_row) {
+        if (DEEP && from_row) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) lab[u] = jq[u] != i ? gather_label<MODE>(c, jq[u]) : kEmpty;
+          if (k + 1 < nch) load_targets(k + 1);
+        } else if (from_row) {
           uint32_t j[U];
           if constexpr (STAGED) {
             const uint32_t b = k & 1;
