@@ -381,11 +381,12 @@ def dropin_e2e(off, tgt, n: int, m2: int, steps: int) -> dict:
 
 def modularity_roofline(dg, lab, n: int, m2: int, dev: int, peak: float, reps: int = 3) -> dict:
     """K7 (modularity, quality.cpp:21-49) on the final labels, device-resident: the call
-    relabels to position order, accumulates σ_c / Σ_c per community (k_mod_rows32 /
-    k_mod_warp / k_mod_hub) and folds them (k_mod_fold). Algorithmic bytes per call:
-    m2 * 8 (target + neighbour label) + n * 16 (list entry, row bound, own label, the
-    per-row σ/Σ update) + n * 12 (labels + perm read, position labels written) + n * 32
-    (σ/Σ zeroed, then read by the fold). Timed end to end with CUDA events."""
+    relabels to position order, accumulates Σ_c per community and the total intra-community
+    weight (k_mod_rows32 / k_mod_warp / k_mod_hub) and folds them (k_mod_fold). Algorithmic
+    bytes per call: m2 * 8 (target + neighbour label) + n * 16 (list entry, row bound, own
+    label) + n * 8 (the row's Σ_c update) + n * 12 (labels + perm read, position labels
+    written) + n * 16 (Σ_c zeroed, then read by the fold). Timed end to end with CUDA
+    events."""
     import torch
     s = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -397,7 +398,7 @@ def modularity_roofline(dg, lab, n: int, m2: int, dev: int, peak: float, reps: i
     e1.record(s)
     torch.cuda.synchronize(dev)
     sec = e0.elapsed_time(e1) * 1e-3 / reps
-    alg = m2 * 8 + n * (16 + 12 + 32)
+    alg = m2 * 8 + n * (16 + 8 + 12 + 16)
     return {"seconds": sec, "alg_bytes": alg, "achieved": alg / sec / 1e9, "peak": peak,
             "unit": "GB/s", "frac": alg / sec / 1e9 / peak,
             "note": "one modularity() call incl. the label range check's 8-byte read-back"}

@@ -22,7 +22,7 @@
 namespace nulpa {
 
 void accumulate_sigma(nulpa_graph* g, const uint32_t* lab, double* sigma, double* big,
-                      cudaStream_t s);
+                      cudaStream_t s, bool scalar = false);
 
 namespace {
 

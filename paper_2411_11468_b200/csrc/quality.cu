@@ -32,10 +32,14 @@ __global__ void k_check_labels(const uint32_t* lab, uint32_t n, unsigned long lo
 // lanes' prefix sums). Targets of consecutive rows are read coalesced, each lane does one
 // label gather per round, and the partial sums are merged per COMMUNITY across the
 // warp (__match_any_sync) before one fp64 atomic pair per community per round.
+// SCALAR: `sigma` is one accumulator (modularity needs only the total intra-community
+// weight, Σ_c σ_c = Σ_i in_i), summed per thread and added once per warp.
+template <bool SCALAR = false>
 __global__ void __launch_bounds__(256) k_mod_rows32(Graph g, const uint32_t* lab,
                                                     const uint32_t* list, uint32_t count,
                                                     double* sigma, double* big) {
   const int lane = threadIdx.x & 31;
+  double in_acc = 0.0;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t base = gw * 32; base < count; base += nw * 32) {
@@ -56,44 +60,65 @@ __global__ void __launch_bounds__(256) k_mod_rows32(Graph g, const uint32_t* lab
     }
     const uint32_t excl = pre - d;
     const uint32_t total = __shfl_sync(kFull, pre, 31);
-    for (uint32_t f0 = 0; f0 < total; f0 += 32) {
-      const uint32_t f = f0 + lane;
-      int r = 0;  // the last lane whose row starts at or before edge f
+    // four 32-entry rounds per step: their targets, then their labels, are in flight
+    // together (one round at a time was two dependent latencies per 32 entries)
+    constexpr int U = 4;
+    for (uint32_t f0 = 0; f0 < total; f0 += 32 * U) {
+      uint32_t ci_u[U], lab_u[U];
+      uint64_t e_u[U];
+      bool valid[U];
 #pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const uint32_t ex = __shfl_sync(kFull, excl, r + step);
-        if (ex <= f) r += step;
-      }
-      const uint64_t lo_r = __shfl_sync(kFull, lo, r);
-      const uint32_t ci_r = __shfl_sync(kFull, ci, r);
-      const uint32_t ex_r = __shfl_sync(kFull, excl, r);
-      const bool valid = f < total;
-      const uint64_t e = lo_r + (f - ex_r);
-      double w = 0.0, in = 0.0;
-      if (valid) {
-        w = g.w ? static_cast<double>(g.w[e]) : 1.0;
-        if (lab[g.tgt[e]] == ci_r) in = w;
-      }
-      const uint32_t key = valid ? ci_r : kEmpty;
-      const unsigned peers = __match_any_sync(kFull, key);
-      double ks = 0.0, is = 0.0;
-      if (g.w) {
-        for (int b = 0; b < 32; ++b) {  // (uniform loop: every lane shuffles)
-          const double wb = __shfl_sync(kFull, w, b), ib = __shfl_sync(kFull, in, b);
-          if ((peers >> b) & 1u) {
-            ks += wb;
-            is += ib;
-          }
+      for (int u = 0; u < U; ++u) {
+        const uint32_t f = f0 + u * 32 + lane;
+        int r = 0;  // the last lane whose row starts at or before edge f
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const uint32_t ex = __shfl_sync(kFull, excl, r + step);
+          if (ex <= f) r += step;
         }
-      } else {
-        ks = static_cast<double>(__reduce_add_sync(peers, valid ? 1u : 0u));
-        is = static_cast<double>(__reduce_add_sync(peers, in != 0.0 ? 1u : 0u));
+        const uint64_t lo_r = __shfl_sync(kFull, lo, r);
+        ci_u[u] = __shfl_sync(kFull, ci, r);
+        const uint32_t ex_r = __shfl_sync(kFull, excl, r);
+        valid[u] = f < total;
+        e_u[u] = lo_r + (f - ex_r);
+        lab_u[u] = valid[u] ? __ldg(g.tgt + e_u[u]) : 0u;  // (the target, for now)
       }
-      if (key != kEmpty && (__ffs(peers) - 1) == lane) {
-        atomicAdd(big + key, ks);
-        if (is != 0.0) atomicAdd(sigma + key, is);
+#pragma unroll
+      for (int u = 0; u < U; ++u) lab_u[u] = valid[u] ? __ldg(lab + lab_u[u]) : kEmpty;
+#pragma unroll 1
+      for (int u = 0; u < U; ++u) {
+        double w = 0.0, in = 0.0;
+        if (valid[u]) {
+          w = g.w ? static_cast<double>(g.w[e_u[u]]) : 1.0;
+          if (lab_u[u] == ci_u[u]) in = w;
+        }
+        const uint32_t key = valid[u] ? ci_u[u] : kEmpty;
+        const unsigned peers = __match_any_sync(kFull, key);
+        double ks = 0.0, is = 0.0;
+        if (g.w) {
+          for (int b2 = 0; b2 < 32; ++b2) {  // (uniform loop: every lane shuffles)
+            const double wb = __shfl_sync(kFull, w, b2), ib = __shfl_sync(kFull, in, b2);
+            if ((peers >> b2) & 1u) {
+              ks += wb;
+              is += ib;
+            }
+          }
+        } else {
+          ks = static_cast<double>(__reduce_add_sync(peers, valid[u] ? 1u : 0u));
+          if (!SCALAR) is = static_cast<double>(__reduce_add_sync(peers, in != 0.0 ? 1u : 0u));
+        }
+        if constexpr (SCALAR) in_acc += in;
+        if (key != kEmpty && (__ffs(peers) - 1) == lane) {
+          atomicAdd(big + key, ks);
+          if (!SCALAR && is != 0.0) atomicAdd(sigma + key, is);
+        }
       }
     }
+  }
+  if constexpr (SCALAR) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) in_acc += __shfl_xor_sync(kFull, in_acc, o);
+    if (lane == 0 && in_acc != 0.0) atomicAdd(sigma, in_acc);
   }
 }
 
@@ -126,9 +151,11 @@ __device__ __forceinline__ void accumulate_row_slice(const Graph& g, const uint3
 }
 
 // Larger rows: one warp per row.
+template <bool SCALAR = false>
 __global__ void k_mod_warp(Graph g, const uint32_t* lab, const uint32_t* list, uint32_t count,
                            double* sigma, double* big) {
   const int lane = threadIdx.x & 31;
+  double in_acc = 0.0;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t t = gw; t < count; t += nw) {
@@ -142,15 +169,62 @@ __global__ void k_mod_warp(Graph g, const uint32_t* lab, const uint32_t* list, u
       si += __shfl_xor_sync(kFull, si, o);
     }
     if (lane == 0) {
-      if (si != 0.0) atomicAdd(sigma + ci, si);
+      if constexpr (SCALAR)
+        in_acc += si;
+      else if (si != 0.0)
+        atomicAdd(sigma + ci, si);
       if (ki != 0.0) atomicAdd(big + ci, ki);
     }
   }
+  if (SCALAR && lane == 0 && in_acc != 0.0) atomicAdd(sigma, in_acc);
+}
+
+// Long rows (> 1024): one CTA per row, so a 10^4..10^5-entry row is not walked by a single
+// warp (a warp-per-row walk left the few longest rows of a power-law graph as the tail).
+template <bool SCALAR = false>
+__global__ void __launch_bounds__(256) k_mod_block(Graph g, const uint32_t* lab,
+                                                   const uint32_t* list, uint32_t count,
+                                                   double* sigma, double* big) {
+  __shared__ double red[2][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double in_acc = 0.0;
+  for (uint32_t t = blockIdx.x; t < count; t += gridDim.x) {
+    const uint32_t i = list[t];
+    const uint32_t ci = lab[i];
+    double ki = 0.0, si = 0.0;
+    accumulate_row_slice<256>(g, lab, ci, g.off[i] + threadIdx.x, g.off[i + 1], ki, si);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ki += __shfl_xor_sync(kFull, ki, o);
+      si += __shfl_xor_sync(kFull, si, o);
+    }
+    if (lane == 0) {
+      red[0][warp] = ki;
+      red[1][warp] = si;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double k = 0.0, sm = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        k += red[0][w];
+        sm += red[1][w];
+      }
+      if constexpr (SCALAR)
+        in_acc += sm;
+      else if (sm != 0.0)
+        atomicAdd(sigma + ci, sm);
+      if (k != 0.0) atomicAdd(big + ci, k);
+    }
+    __syncthreads();
+  }
+  if (SCALAR && threadIdx.x == 0 && in_acc != 0.0) atomicAdd(sigma, in_acc);
 }
 
 // Hub rows: one CTA per (hub, chunk) item.
+template <bool SCALAR = false>
 __global__ void k_mod_hub(Graph g, const uint32_t* lab, HubCtx h, double* sigma, double* big) {
   __shared__ double red[2][32];
+  double in_acc = 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t it = blockIdx.x; it < h.n_items; it += gridDim.x) {
     const uint32_t i = h.hub_v[h.item_hub[it]];
@@ -177,19 +251,26 @@ __global__ void k_mod_hub(Graph g, const uint32_t* lab, HubCtx h, double* sigma,
         k += red[0][w];
         s += red[1][w];
       }
-      if (s != 0.0) atomicAdd(sigma + ci, s);
+      if constexpr (SCALAR)
+        in_acc += s;
+      else if (s != 0.0)
+        atomicAdd(sigma + ci, s);
       if (k != 0.0) atomicAdd(big + ci, k);
     }
     __syncthreads();
   }
+  if (SCALAR && threadIdx.x == 0 && in_acc != 0.0) atomicAdd(sigma, in_acc);
 }
 
+// Q = Σ_c [σ_c / 2m − (Σ_c / 2m)²] (quality.cpp:41-47). SCALAR: `sigma` holds Σ_c σ_c.
+template <bool SCALAR = false>
 __global__ void k_mod_fold(const double* sigma, const double* big, uint32_t n, double two_m,
                            double* q) {
   __shared__ double red[32];
   double acc = 0.0;
+  if (SCALAR && blockIdx.x == 0 && threadIdx.x == 0) acc = *sigma / two_m;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-    const double sg = sigma[c], bg = big[c];
+    const double sg = SCALAR ? 0.0 : sigma[c], bg = big[c];
     if (bg == 0.0 && sg == 0.0) continue;
     const double frac = bg / two_m;
     acc += sg / two_m - frac * frac;
@@ -237,24 +318,31 @@ void check_labels(nulpa_graph* g, const uint32_t* lab, cudaStream_t s) {
 // sigma[c] (intra-community stored weight) and big[c] (summed weighted degree) for
 // every community c, from position-order labels `lab` (quality.cpp:29-40).
 void accumulate_sigma(nulpa_graph* g, const uint32_t* lab, double* sigma, double* big,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool scalar = false) {
   const uint32_t n = g->n;
   std::lock_guard<std::recursive_mutex> plan_lock(g->plan_mu);
   // Any tiering covers every row once: reuse the cached plan when there is one.
   Plan* p = g->plan ? g->plan : get_plan(g, resolve_tiers(32, nullptr), 4, s);
   const Graph dg{g->offsets, g->targets, g->weights, n};
   const int sms = sm_count();
+  auto rows32 = scalar ? k_mod_rows32<true> : k_mod_rows32<false>;
+  auto warp = scalar ? k_mod_warp<true> : k_mod_warp<false>;
+  auto hub = scalar ? k_mod_hub<true> : k_mod_hub<false>;
+  auto block = scalar ? k_mod_block<true> : k_mod_block<false>;
   for (int t = T_THREAD; t <= T_WARP; ++t)
     if (p->count[t])
-      k_mod_rows32<<<std::min<uint32_t>((p->count[t] + 255) / 256, sms * 8), 256, 0, s>>>(
+      rows32<<<std::min<uint32_t>((p->count[t] + 255) / 256, sms * 8), 256, 0, s>>>(
           dg, lab, p->list[t], p->count[t], sigma, big);
-  for (int t = T_WTAB; t <= T_CLUSTER; ++t)
+  for (int t = T_WTAB; t <= T_BLOCK; ++t)  // rows of 33 .. 1024 entries: a warp per row
     if (p->count[t])
-      k_mod_warp<<<std::min<uint32_t>((p->count[t] + 7) / 8, sms * 8), 256, 0, s>>>(
+      warp<<<std::min<uint32_t>((p->count[t] + 7) / 8, sms * 8), 256, 0, s>>>(
           dg, lab, p->list[t], p->count[t], sigma, big);
+  for (int t = T_BLOCK2; t <= T_CLUSTER; ++t)  // longer rows: a CTA per row
+    if (p->count[t])
+      block<<<std::min<uint32_t>(p->count[t], sms * 8), 256, 0, s>>>(dg, lab, p->list[t],
+                                                                      p->count[t], sigma, big);
   if (p->n_items)
-    k_mod_hub<<<std::min<uint32_t>(p->n_items, sms * 4), 256, 0, s>>>(dg, lab, p->hub_ctx(), sigma,
-                                                                      big);
+    hub<<<std::min<uint32_t>(p->n_items, sms * 4), 256, 0, s>>>(dg, lab, p->hub_ctx(), sigma, big);
   NULPA_CUDA(cudaGetLastError());
 }
 
@@ -272,19 +360,20 @@ double modularity_device(nulpa_graph* g, const uint32_t* labels, cudaStream_t s)
     to_positions_u32(g, labels, lab_pos, s);
     lab = lab_pos;
   }
-  double* sigma = dalloc<double>(2ull * n + 1);
-  double* big = sigma + n;
-  double* d_q = sigma + 2ull * n;
-  NULPA_CUDA(cudaMemsetAsync(sigma, 0, (2ull * n + 1) * sizeof(double), s));
-  accumulate_sigma(g, lab, sigma, big, s);
+  // Σ_c per community (n doubles), Σ_c σ_c as one accumulator, Q
+  double* big = dalloc<double>(uint64_t(n) + 2);
+  double* sigma = big + n;
+  double* d_q = big + n + 1;
+  NULPA_CUDA(cudaMemsetAsync(big, 0, (uint64_t(n) + 2) * sizeof(double), s));
+  accumulate_sigma(g, lab, sigma, big, s, /*scalar=*/true);
   const int sms = sm_count();
-  k_mod_fold<<<std::min<uint32_t>((n + 255) / 256, sms * 4), 256, 0, s>>>(sigma, big, n,
-                                                                          g->total_2m, d_q);
+  k_mod_fold<true><<<std::min<uint32_t>((n + 255) / 256, sms * 4), 256, 0, s>>>(sigma, big, n,
+                                                                                g->total_2m, d_q);
   NULPA_CUDA(cudaGetLastError());
   double q = 0.0;
   NULPA_CUDA(cudaMemcpyAsync(&q, d_q, sizeof q, cudaMemcpyDeviceToHost, s));
   NULPA_CUDA(cudaStreamSynchronize(s));
-  dfree(sigma);
+  dfree(big);
   dfree(lab_pos);
   return q;
 }
