@@ -464,15 +464,19 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
     // fences once, then the warp wakes the changed rows' neighbours as one stream.
     unsigned chg_bits = 0;
     bool stored = false;
+    // S == 1: the next step's target is loaded while this step's label is in flight
+    // (targets never change, so this adds no staleness)
+    auto step_target = [&](int st) -> uint32_t {
+      const Meta& m = s_meta[wid][st * kPer + sub];
+      return (m.act && gl < m.d) ? ld_stream(c.g.tgt + m.lo + gl, pol) : m.i;
+    };
+    uint32_t jn = (S == 1 && kSteps > 0) ? step_target(0) : 0u;
 #pragma unroll 1
     for (int c0 = 0; c0 < kSteps; c0 += S) {
       uint32_t j[S], lab[S];
       W w[S];
 #pragma unroll
-      for (int k = 0; k < S; ++k) {
-        const Meta& m = s_meta[wid][(c0 + k) * kPer + sub];
-        j[k] = (m.act && gl < m.d) ? ld_stream(c.g.tgt + m.lo + gl, pol) : m.i;
-      }
+      for (int k = 0; k < S; ++k) j[k] = S == 1 ? jn : step_target(c0 + k);
 #pragma unroll
       for (int k = 0; k < S; ++k) {
         const Meta& m = s_meta[wid][(c0 + k) * kPer + sub];
@@ -480,6 +484,7 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
         lab[k] = valid ? gather_label<MODE>(c, j[k]) : kEmpty;
         w[k] = valid ? edge_weight<W, WEIGHTED>(c.g, m.lo + gl) : W(0);
       }
+      if (S == 1 && c0 + 1 < kSteps) jn = step_target(c0 + 1);
 #pragma unroll
       for (int k = 0; k < S; ++k) {
         const Meta m = s_meta[wid][(c0 + k) * kPer + sub];
@@ -788,7 +793,8 @@ constexpr uint32_t kTeamBatch = TEAM <= 32 ? 32u : (TEAM <= 128 ? 16u : 4u);
 #ifndef NULPA_TEAM_PREFETCH
 #define NULPA_TEAM_PREFETCH 0
 #endif
-constexpr bool kTeamPrefetch = NULPA_TEAM_PREFETCH != 0;
+// 1: the next vertex's first-round targets and labels; 2: its targets only (no staleness)
+constexpr int kTeamPrefetch = NULPA_TEAM_PREFETCH;
 
 // First gather round of the row in `m` (edges [0, T * U)): targets into j, labels into lab.
 template <int MODE, int U>
@@ -894,7 +900,7 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_M
     // and wake-ups — so a team waits on roughly one memory latency per vertex instead
     // of two. (The early reads are a legal asynchronous schedule: the vertex was
     // claimed, and fenced, before any of them.)
-    constexpr bool kPF = kPacked<WEIGHTED> && kTeamPrefetch;
+    constexpr bool kPF = kPacked<WEIGHTED> && kTeamPrefetch != 0;
     constexpr uint32_t kRound = uint32_t(TEAM) * kTeamU;  // row entries of one gather round
     unsigned act_mask = 0;
     if constexpr (kPF && TEAM == 32) act_mask = __ballot_sync(kFull, mine.act);
@@ -924,7 +930,13 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_M
       // has cleared the table by then).
       if constexpr (kPF) {
         uint32_t lab0[kTeamU];
-        if (pf_v == v) {
+        if (pf_v == v && kTeamPrefetch == 2) {
+#pragma unroll
+          for (int u = 0; u < kTeamU; ++u) {
+            const uint32_t e = u * TEAM + ttid;
+            lab0[u] = (e < m.d && pf_j[u] != m.i) ? gather_label<MODE>(c, pf_j[u]) : kEmpty;
+          }
+        } else if (pf_v == v) {
 #pragma unroll
           for (int u = 0; u < kTeamU; ++u) lab0[u] = pf_l[u];
         } else {
@@ -955,7 +967,7 @@ __global__ void __launch_bounds__(CTA_THREADS, CTA_THREADS <= 256 ? NULPA_TEAM_M
           team_gather<MODE, W, WEIGHTED, Tab, kTeamU, DEDUP>(c, m.i, m.lo, kRound, m.d, tab, cap, ttid,
                                                                TEAM, pol, occ, &s_occ_n[team], fails);
         // the next vertex's first-round labels, in flight during this vertex's argmax
-        if (pf_v < nb) {
+        if (kTeamPrefetch == 1 && pf_v < nb) {
 #pragma unroll
           for (int u = 0; u < kTeamU; ++u) {
             const uint32_t e = u * TEAM + ttid;
