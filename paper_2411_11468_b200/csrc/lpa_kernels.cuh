@@ -1162,7 +1162,10 @@ __global__ void __cluster_dims__(kClusterSize, 1, 1) __launch_bounds__(kBigThrea
 #ifndef NULPA_WIDE_LIMIT
 #define NULPA_WIDE_LIMIT (NULPA_WIDE_CAP / 4 * 3)
 #endif
-constexpr uint32_t kWideLimit = NULPA_WIDE_LIMIT;  // distinct labels per phase (load <= 3/4)
+constexpr uint32_t kWideLimit = NULPA_WIDE_LIMIT;
+#ifndef NULPA_WIDE_FRESH_P1
+#define NULPA_WIDE_FRESH_P1 0  // 1: the first pass also starts at one phase (overflow vote on)
+#endif  // distinct labels per phase (load <= 3/4)
 
 __device__ __forceinline__ uint32_t phase_of(uint32_t key, uint32_t P) {
   const uint32_t h = (key ^ (key >> 16)) * 0x7FEB352Du;
@@ -1266,7 +1269,8 @@ __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c
     // only merge as a run goes on), so neither the per-round overflow vote nor a restart is
     // needed unless the row is near the limit (or has no history: P = 1 with the vote).
     const uint32_t h = fresh ? 0u : hint[t0 + vb];
-    uint32_t P = fresh ? (d + kWideLimit - 1) / kWideLimit : max(1u, (h + kWideLimit - 1) / kWideLimit);
+    uint32_t P = (fresh && !NULPA_WIDE_FRESH_P1) ? (d + kWideLimit - 1) / kWideLimit
+                                                 : max(1u, (h + kWideLimit - 1) / kWideLimit);
     const bool known = !fresh && h != 0u && h <= kWideLimit / 2;  // far below the limit: no vote
     uint32_t distinct = 0;  // (thread 0) labels aggregated over the phases of this row
     // Bucketed phases: phase 0 gathers the row once and appends every label of a
