@@ -128,6 +128,8 @@ struct PassCtx {
   const uint32_t* vid = nullptr;  // position -> vertex id (layout.cu); nullptr = identity
   const uint32_t* pos = nullptr;  // vertex id -> position; nullptr = identity
   int fresh = 0;                  // labels are still the identity (first pass of a run)
+  int hints = 0;                  // the wide tier's per-row hints come from this run's
+                                  // previous pass (k_wide; 0: ignore them)
   // Pass guard (batched runs, engine.cu): set on the device once the run has converged;
   // every pass kernel enqueued after that returns at once. nullptr = unguarded.
   const unsigned* stop = nullptr;

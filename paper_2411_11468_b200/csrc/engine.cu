@@ -754,6 +754,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     c.vid = g->perm;
     c.pos = g->inv;
     c.fresh = iter == 0 ? 1 : 0;
+    c.hints = iter > 0 ? 1 : 0;
     // Synchronous only: there the identity first pass is exactly the reference's.
     // (Under ParallelAsync it is a legal schedule too, but it replaces the in-place
     // first pass, whose early label flooding converges R-MAT one pass sooner and
@@ -1028,6 +1029,7 @@ struct nulpa_session {
   bool has_ext = false;         // legacy default stream 0), else `stream`
   bool fresh = false;           // labels are the identity (after nulpa_session_init)
   bool identity_first = false;  // graph allows the table-free first pass
+  uint64_t passes = 0;          // passes since nulpa_session_init
   ~nulpa_session() { delete plan; }
 };
 
@@ -1119,6 +1121,8 @@ void session_pass(nulpa_session* ss, int pick_less, int wake, nulpa_pass_info* i
   c.vid = g->perm;
   c.pos = g->inv;
   c.fresh = ss->fresh ? 1 : 0;
+  c.hints = ss->passes > 0 ? 1 : 0;  // hints written by this session's earlier passes
+  ++ss->passes;
   Prof prof;
   cudaEvent_t e0, e1;
   NULPA_CUDA(cudaEventCreate(&e0));
@@ -1397,6 +1401,7 @@ int nulpa_session_init(nulpa_session* ss) {
     NULPA_CUDA(cudaGetLastError());
     NULPA_CUDA(cudaStreamSynchronize(st));
     ss->fresh = true;
+    ss->passes = 0;
   });
 }
 

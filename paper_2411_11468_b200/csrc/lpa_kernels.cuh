@@ -1268,7 +1268,7 @@ __global__ void __launch_bounds__(kWideThreads, kWideCtasPerSm) k_wide(PassCtx c
     // passes start from the distinct-label count the row held in its previous pass (labels
     // only merge as a run goes on), so neither the per-round overflow vote nor a restart is
     // needed unless the row is near the limit (or has no history: P = 1 with the vote).
-    const uint32_t h = fresh ? 0u : hint[t0 + vb];
+    const uint32_t h = (fresh || !c.hints) ? 0u : hint[t0 + vb];
     uint32_t P = (fresh && !NULPA_WIDE_FRESH_P1) ? (d + kWideLimit - 1) / kWideLimit
                                                  : max(1u, (h + kWideLimit - 1) / kWideLimit);
     const bool known = !fresh && h != 0u && h <= kWideLimit / 2;  // far below the limit: no vote
