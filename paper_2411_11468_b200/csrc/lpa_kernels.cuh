@@ -333,76 +333,6 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
   warp_add_counter(c.ctr, C_WAKE_E, n_w);
 }
 
-// Thread per vertex, chunk-walked by WARPS (ParallelAsync, lattice-like inputs): warp w
-// walks the contiguous list slice [w*Lw, (w+1)*Lw) 32 entries per step, lane k taking entry
-// 32*s + k, so the rows of a step are read coalesced; labels still travel along the chunk
-// step after step (lane 0 of step s + 1 reads lane 31's label of step s, ordered by the
-// __syncwarp between steps), as they do along each thread's chunk in k_thread<CHUNKED>.
-template <int MODE, typename W, bool WEIGHTED, int DMAX>
-__global__ void __launch_bounds__(256) k_thread_wchunk(PassCtx c, const uint32_t* __restrict__ list,
-                                                       uint32_t count) {
-  if (stopped(c.stop)) return;
-  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
-  const uint64_t pol = policy_evict_first();
-  const int lane = threadIdx.x & 31;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t Lw = (((count + nwarps - 1) / nwarps) + 31u) & ~31u;
-  const uint32_t w0 = w * Lw, w1 = min(count, w0 + Lw);
-  for (uint32_t b = w0; b < w1; b += 32) {
-    const uint32_t t = b + lane;
-    bool act = t < w1;
-    const uint32_t i = act ? __ldg(list + t) : 0u;
-    if (act) act = !claim_vertex(c, i);
-    claim_fence<MODE>(c);
-    uint64_t lo = 0;
-    uint32_t d = 0;
-    if (act) {
-      lo = __ldg(c.g.off + i);
-      d = static_cast<uint32_t>(__ldg(c.g.off + i + 1) - lo);
-    }
-    uint32_t nb[DMAX], lab[DMAX];
-    W wt[DMAX];
-#pragma unroll
-    for (int k = 0; k < DMAX; ++k) nb[k] = (k < d) ? ld_stream(c.g.tgt + lo + k, pol) : i;
-#pragma unroll
-    for (int k = 0; k < DMAX; ++k) {
-      const bool valid = k < d && nb[k] != i;  // self-loops skipped (lpa.hpp:102)
-      lab[k] = valid ? gather_label<MODE>(c, nb[k]) : kEmpty;
-      wt[k] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + k) : W(0);
-    }
-    bool chg = false;
-    if (act) {
-      Best<VBits<W>> bst{VBits<W>(0), kEmpty};
-#pragma unroll
-      for (int k = 0; k < DMAX; ++k) {
-        W sum = W(0);
-#pragma unroll
-        for (int m = 0; m < DMAX; ++m) sum += (lab[m] == lab[k]) ? wt[m] : W(0);
-        best_merge(bst, to_vbits<W>(sum), lab[k]);
-      }
-      ++n_v;
-      n_e += d;
-      chg = apply_move<MODE>(c, i, bst.k);  // (store, then the fence before its wake loads)
-      n_dn += chg;
-    }
-    if (MODE == kAsync && c.wake && chg) {
-      uint8_t f[DMAX];
-#pragma unroll
-      for (int k = 0; k < DMAX; ++k) f[k] = k < d ? load_flag(c.flags + nb[k]) : uint8_t(0);
-#pragma unroll
-      for (int k = 0; k < DMAX; ++k)
-        if (f[k]) st_relaxed(c.flags + nb[k], uint8_t(0));
-      n_w += d;
-    }
-    __syncwarp();  // this step's label stores before the next step's label loads
-  }
-  warp_add_counter(c.ctr, C_PROC_V, n_v);
-  warp_add_counter(c.ctr, C_PROC_E, n_e);
-  warp_add_counter(c.ctr, C_DN, n_dn);
-  warp_add_counter(c.ctr, C_WAKE_E, n_w);
-}
-
 // Thread per vertex, Q rows per thread iteration with the protocol's fences amortised:
 // the Q claims share one fence, the Q rows are then decided one after another (one row's
 // loads in registers at a time), and their label stores share one fence before the
