@@ -232,16 +232,6 @@ inline bool thread_q() {
   return m;
 }
 
-// Chunk-walked thread tier by warps (k_thread_wchunk; NULPA_WARP_CHUNKS, read once; 0 by
-// default = k_thread<CHUNKED>, one chunk per thread).
-inline bool warp_chunks() {
-  static const bool m = [] {
-    const char* e = std::getenv("NULPA_WARP_CHUNKS");
-    return e ? std::atoi(e) != 0 : false;
-  }();
-  return m;
-}
-
 // Passes enqueued per host read-back in batched runs (NULPA_BATCH_PASSES, read once).
 inline int batch_passes() {
   static const int m = [] {
@@ -368,12 +358,7 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   };
   if (p.count[T_THREAD] && (tiers >> T_THREAD & 1u)) {
     tier(T_THREAD);
-    if (p.thread_max <= 8 && MODE == kAsync && p.chunked_thread && warp_chunks())
-      k_thread_wchunk<MODE, W, WEIGHTED, 8>
-          <<<resident_grid(k_thread_wchunk<MODE, W, WEIGHTED, 8>, 256, 0, p.count[T_THREAD],
-                           256 * kMinChunk, sms),
-             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
-    else if (p.thread_max <= 8 && MODE == kAsync && p.chunked_thread)
+    if (p.thread_max <= 8 && MODE == kAsync && p.chunked_thread)
       // chunks of >= kMinChunk vertices per thread (a short chunk propagates little)
       k_thread<MODE, W, WEIGHTED, 8, true>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, true>, 256, 0, p.count[T_THREAD],
