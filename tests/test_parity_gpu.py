@@ -444,3 +444,26 @@ def test_batched_passes_equal_per_pass_readback(pl_period, max_it):
             assert not any(stops[:-1])
             assert r.stats.converged == stops[-1]
             assert r.stats.pl_iterations == sum(pls)
+
+
+def test_sync_step_after_run_on_cached_plan():
+    # A ParallelAsync run leaves per-row distinct-label hints in the graph's cached plan
+    # (wide tier, k_wide); a later single sync step with all-distinct random labels must
+    # ignore them (hints are trusted only inside one run) and still be bit-exact and quick.
+    import time
+    torch = pytest.importorskip("torch")
+    dg = lp.DeviceGraph.web(60000, 600000, 2.1, 4, 20000, 3)  # rows above 6144: wide tier
+    g = dg.download()
+    assert int(np.diff(g.offsets.astype(np.int64)).max()) > 6144
+    dg.lpa(lp.LpaConfig(), want_host=False)  # populates the hints (labels collapse)
+    pg = O.PortGraph(g.offsets, g.targets, None)
+    lab = np.random.default_rng(5).permutation(g.order()).astype(np.uint32)
+    want, wc = O.port_sync_step(pg, lab, 0)
+    dev = f"cuda:{dg.device}"
+    lin = torch.from_numpy(lab.view(np.int32)).to(dev)  # vertex order in and out
+    out = torch.empty_like(lin)
+    t0 = time.time()
+    changed = dg.sync_step_device(lin.data_ptr(), out.data_ptr(), False)
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 10.0
+    assert changed == wc and np.array_equal(out.cpu().numpy().view(np.uint32), want)
