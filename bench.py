@@ -270,6 +270,24 @@ def sbm_quality(nulpa_q=None) -> dict:
     return out
 
 
+def sbm_loop_time(lp2, sgh, m2: int, runs: int = 20) -> dict:
+    """The small-graph latency figure (SBM-100K, resident on the device): unprofiled
+    ParallelAsync runs (no per-tier timing events), loop time per run from the library's
+    own CUDA events (RunStats.elapsed_seconds)."""
+    sdg = lp2.DeviceGraph.upload(sgh)
+    try:
+        for _ in range(3):
+            sdg.lpa(want_host=False)
+        res = [sdg.lpa(want_host=False).stats for _ in range(runs)]
+    finally:
+        sdg.free()
+    ms = sorted(r.elapsed_seconds * 1e3 for r in res)
+    med = ms[len(ms) // 2]
+    return {"ms_per_run_median": med, "ms_per_run_min": ms[0], "runs": runs,
+            "iterations": sorted({r.iterations for r in res}), "m2": m2,
+            "edges_per_s": m2 / (med * 1e-3), "profiled": False}
+
+
 def _log(msg: str) -> None:
     sys.stderr.write(f"[bench {time.strftime('%H:%M:%S')}] {msg}\n")
     sys.stderr.flush()
@@ -562,12 +580,13 @@ def bench_nulpa(args):
             so, st_, _ = sg.arrays()
             sgh = lp2.CsrGraph(so, st_, None)
             nq = [lp2.modularity(sgh, lp2.lpa(sgh).labels) for _ in range(5)]
+            sbm_loop = sbm_loop_time(lp2, sgh, int(so[-1]))
             q0 = time.time()
             quality = {"this_graph": {"nulpa_Q": q, "ref_async_Q": q_ref,
                                       "dQ": q - q_ref, "abs_dQ": abs(q - q_ref),
                                       "ref_iterations": stc["iterations"],
                                       "nulpa_iterations": int(stats[-1][0].iterations)},
-                       "sbm100k": sbm_quality(nq)}
+                       "sbm100k": dict(sbm_quality(nq), nulpa_loop=sbm_loop)}
             _log(f"SBM-100K quality check ({time.time() - q0:.1f} s)")
         except Exception as e:  # the baseline must never sink the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",

@@ -129,6 +129,81 @@ struct Prof {
   }
 };
 
+// Concurrent tiers (NULPA_CONCURRENT, read once). A pass is two tier groups, the
+// reference's two lists (lpa.cpp:139-230): the register tiers (degree <= 32: thread,
+// half warp, warp) and then the table tiers (team32 .. hub), with the group boundary
+// a stream join, as the reference's low list finishes before its team list starts.
+// Within a group the tiers run on their own streams, side by side: on a small graph
+// every tier kernel is a fraction of the GPU and a pass stops being the SUM of its
+// tiers' latency chains. Any order of the vertices inside one list is an ordering the
+// reference's workers can produce. 0 = off, 1 = on, 2 = both groups for graphs of at
+// most 2^22 vertices and the register group above (default), 3 = the register group
+// only, 4 = the table group only. Measured on one B200 (loop ms per run, off -> default):
+// SBM-100K 0.456 -> 0.286 (with one-row small-tier batches), R-MAT 18 1.33 -> 0.72,
+// R-MAT 22 5.1 -> 4.3, R-MAT 24 12.7 -> 12.3, R-MAT 27 96.9 -> 95.3, web 66.1 -> 64.6.
+// The table group side by side on large graphs is slower (R-MAT 27: 108.8 ms): its
+// tiers each fill the GPU and lose the read-only label path.
+inline int concurrent_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("NULPA_CONCURRENT");
+    return e ? std::atoi(e) : 2;
+  }();
+  return m;
+}
+
+// Tier streams of one device (created once), forked from and joined into the run's
+// stream. One run at a time holds them (Fork::lease); a concurrent run on the same
+// device falls back to one stream.
+struct Fork {
+  cudaStream_t st[kTiers] = {};
+  cudaEvent_t go = nullptr;
+  cudaEvent_t done[kTiers] = {};
+  bool used[kTiers] = {};
+  unsigned groups = 3;  // bit 0: register tiers side by side, bit 1: table tiers
+  std::mutex mu;
+  void init() {
+    if (go) return;
+    for (int t = 0; t < kTiers; ++t) {
+      NULPA_CUDA(cudaStreamCreateWithFlags(&st[t], cudaStreamNonBlocking));
+      NULPA_CUDA(cudaEventCreateWithFlags(&done[t], cudaEventDisableTiming));
+    }
+    NULPA_CUDA(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
+  }
+  // Start a group: every tier stream waits for the work enqueued on `s` so far.
+  void fork(cudaStream_t s) {
+    NULPA_CUDA(cudaEventRecord(go, s));
+    for (int t = 0; t < kTiers; ++t) used[t] = false;
+  }
+  cudaStream_t enter(int t) {
+    if (!used[t]) NULPA_CUDA(cudaStreamWaitEvent(st[t], go, 0));
+    used[t] = true;
+    return st[t];
+  }
+  // End a group: `s` waits for every tier stream the group used.
+  void join(cudaStream_t s) {
+    for (int t = 0; t < kTiers; ++t)
+      if (used[t]) {
+        NULPA_CUDA(cudaEventRecord(done[t], st[t]));
+        NULPA_CUDA(cudaStreamWaitEvent(s, done[t], 0));
+        used[t] = false;
+      }
+  }
+  static Fork& of_device(int dev) {
+    static Fork forks[64];
+    return forks[dev & 63];
+  }
+};
+
+// One-row batches for team tiers of at most one row per team (NULPA_SMALL_TIER_BATCH,
+// read once; 1 by default).
+inline bool small_tier_batch() {
+  static const bool m = [] {
+    const char* e = std::getenv("NULPA_SMALL_TIER_BATCH");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return m;
+}
+
 // Wide-tier variant (NULPA_WIDE_MODE, read once): 0 = plain coalesced target loads,
 // rounds in program order (default); 1 = label prefetch one round ahead; 2 = TMA-staged
 // targets + label prefetch. Measured at R-MAT 27: 29.5 / 30.7 / 40.4 ms of
@@ -299,7 +374,7 @@ void launch_wide(const Plan& p, const PassCtx& c, cudaStream_t s, int sms) {
 // C_COUNT block per tier. Returns the number of kernels launched.
 template <int MODE, typename W, bool WEIGHTED>
 int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t s, int sms,
-                Prof& prof, unsigned tiers = ~0u) {
+                Prof& prof, unsigned tiers = ~0u, Fork* fk = nullptr) {
   using Tab = Table<kPacked<WEIGHTED>, W>;
   // Team kernels: <CTA threads, team threads, table slots, max degree> per tier.
   constexpr size_t wtab_smem = 8 * team_bytes<Tab, kWarpTabCap, kWarpTabMax>();
@@ -341,21 +416,54 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     allow_smem(k_hub_accum<MODE, W, WEIGHTED, 0>, hub_smem);
   });
   int launches = 0;
+  cudaStream_t ts = s;  // the current tier's stream
   // A team kernel's launch (full kTeamBatch batches: see launch_group).
   auto team_launch = [&](auto kernel, int threads, int teams, uint32_t max_batch, size_t smem,
                          const uint32_t* list, uint32_t count, bool counter) {
-    const uint32_t bsz = max_batch;
-    if (counter) NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
-    kernel<<<resident_grid(kernel, threads, smem, count, teams * bsz, sms), threads, smem, s>>>(
+    // A tier of at most one row per team of one CTA per SM (a few stray long rows of a
+    // small graph) takes one row per batch: its rows are too few to be neighbours, and a
+    // full batch would be one team's serial chain of row latencies (SBM-100K: 10 rows of
+    // degree > 32, 25 us per pass as one batch).
+    const uint32_t bsz = (small_tier_batch() && count <= uint32_t(teams) * sms) ? 1u : max_batch;
+    if (counter) NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), ts));
+    kernel<<<resident_grid(kernel, threads, smem, count, teams * bsz, sms), threads, smem, ts>>>(
         c, list, count, bsz);
   };
+  // Tier groups (see concurrent_mode): [T_THREAD, T_WARP] and [T_WTAB, T_HUB]. A group
+  // with two or more tiers to run goes side by side on the fork's streams when `fk` is
+  // given; each of its tiers then has its own work counter (c.work[t]).
+  auto runs = [&](int t) {
+    return (t == T_HUB ? p.n_hubs != 0 : p.count[t] != 0) && (tiers >> t & 1u) != 0;
+  };
+  int n_low = 0, n_high = 0;
+  uint32_t low_ro = 0xFFFFFFFFu;  // positions above every register tier that runs
+  for (int t = T_THREAD; t <= T_HUB; ++t)
+    if (runs(t)) {
+      if (t <= T_WARP) {
+        ++n_low;
+        low_ro = std::min(low_ro, p.ro_end[t]);
+      } else {
+        ++n_high;
+      }
+    }
+  const bool conc_low = fk && (fk->groups & 1u) && n_low >= 2;
+  const bool conc_high = fk && (fk->groups & 2u) && n_high >= 2;
+  unsigned int* const work0 = c.work;
+  bool conc = false;    // the current tier runs beside the others of its group
   auto tier = [&](int t) {
+    conc = t <= T_WARP ? conc_low : conc_high;
+    ts = conc ? fk->enter(t) : s;
+    c.work = conc ? work0 + t : work0;
     c.ctr = ctr + t * C_COUNT;
     const bool ro = t < Plan::kLists && ro_labels() && p.ro_end[T_HUB] != 0;
-    c.ro_end = ro ? p.ro_end[t] : 0u;
-    c.ro_lo = (ro && ro_labels_low()) ? p.ro_lo[t] : 0xFFFFFFFFu;
-    prof.begin(t, s);
+    // Read-only labels must not be written during the launch: beside other tiers that
+    // is only the prefix above the whole register group (and nothing for the table
+    // group, whose hub tier sits at the top).
+    c.ro_end = !ro ? 0u : !conc ? p.ro_end[t] : t <= T_WARP ? low_ro : 0u;
+    c.ro_lo = (ro && !conc && ro_labels_low()) ? p.ro_lo[t] : 0xFFFFFFFFu;
+    prof.begin(t, ts);
   };
+  if (conc_low) fk->fork(s);
   if (p.count[T_THREAD] && (tiers >> T_THREAD & 1u)) {
     tier(T_THREAD);
     if (p.thread_max <= 8 && MODE == kAsync && p.chunked_thread)
@@ -363,74 +471,76 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
       k_thread<MODE, W, WEIGHTED, 8, true>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, true>, 256, 0, p.count[T_THREAD],
                            256 * kMinChunk, sms),
-             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+             256, 0, ts>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
     else if (p.thread_max <= 8 && thread_q())
       k_thread_q<MODE, W, WEIGHTED, 8>
           <<<resident_grid(k_thread_q<MODE, W, WEIGHTED, 8>, 256, 0, p.count[T_THREAD], 256 * 4, sms),
-             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+             256, 0, ts>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
     else if (p.thread_max <= 8 && thread_pair())
       k_thread<MODE, W, WEIGHTED, 8, false, 2>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, false, 2>, 256, 0, p.count[T_THREAD], 512, sms),
-             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+             256, 0, ts>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
     else if (p.thread_max <= 8)
       k_thread<MODE, W, WEIGHTED, 8>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8>, 256, 0, p.count[T_THREAD], 256, sms),
-             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+             256, 0, ts>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
     else
       k_thread<MODE, W, WEIGHTED, 16>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 16>, 256, 0, p.count[T_THREAD], 256, sms),
-             256, 0, s>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
-    prof.end(T_THREAD, s);
+             256, 0, ts>>>(c, p.list[T_THREAD], p.count[T_THREAD]);
+    prof.end(T_THREAD, ts);
     ++launches;
   }
   if (p.count[T_HALF] && (tiers >> T_HALF & 1u)) {
     tier(T_HALF);
-    launch_group<MODE, W, WEIGHTED, 16>(c, p.list[T_HALF], p.count[T_HALF], s, sms);
-    prof.end(T_HALF, s);
+    launch_group<MODE, W, WEIGHTED, 16>(c, p.list[T_HALF], p.count[T_HALF], ts, sms);
+    prof.end(T_HALF, ts);
     ++launches;
   }
   if (p.count[T_WARP] && (tiers >> T_WARP & 1u)) {
     tier(T_WARP);
-    launch_group<MODE, W, WEIGHTED, 32>(c, p.list[T_WARP], p.count[T_WARP], s, sms);
-    prof.end(T_WARP, s);
+    launch_group<MODE, W, WEIGHTED, 32>(c, p.list[T_WARP], p.count[T_WARP], ts, sms);
+    prof.end(T_WARP, ts);
     ++launches;
   }
+  if (conc_low) fk->join(s);
+  if (conc_high) fk->fork(s);
   if (p.count[T_WTAB] && (tiers >> T_WTAB & 1u)) {
     tier(T_WTAB);
     team_launch(k_wt, 256, 8, kTeamBatch<32>, wtab_smem, p.list[T_WTAB], p.count[T_WTAB], false);
-    prof.end(T_WTAB, s);
+    prof.end(T_WTAB, ts);
     ++launches;
   }
   if (p.count[T_BLOCK] && (tiers >> T_BLOCK & 1u)) {
     tier(T_BLOCK);
     team_launch(k_b1, 256, 2, kTeamBatch<128>, block_smem, p.list[T_BLOCK], p.count[T_BLOCK], false);
-    prof.end(T_BLOCK, s);
+    prof.end(T_BLOCK, ts);
     ++launches;
   }
   if (p.count[T_BLOCK2] && (tiers >> T_BLOCK2 & 1u)) {
     tier(T_BLOCK2);
     team_launch(k_b2, 256, 1, kTeamBatch<256>, block2_smem, p.list[T_BLOCK2], p.count[T_BLOCK2], true);
-    prof.end(T_BLOCK2, s);
+    prof.end(T_BLOCK2, ts);
     ++launches;
   }
   if (p.count[T_BIG] && (tiers >> T_BIG & 1u)) {
     tier(T_BIG);
     team_launch(k_bg, kMidThreads, 1, kTeamBatch<kMidThreads>, big_smem, p.list[T_BIG], p.count[T_BIG],
                 true);
-    prof.end(T_BIG, s);
+    prof.end(T_BIG, ts);
     ++launches;
   }
   if (p.count[T_CLUSTER] && (tiers >> T_CLUSTER & 1u)) {
     tier(T_CLUSTER);
-    NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), s));
+    NULPA_CUDA(cudaMemsetAsync(c.work, 0, sizeof(unsigned int), ts));
     // persistent clusters pull vertices from c.work; grid a multiple of the cluster size
     const unsigned gc = std::max<unsigned>(kClusterSize, (sms / kClusterSize) * kClusterSize);
     if constexpr (WEIGHTED)
-      k_cluster<MODE, W, WEIGHTED><<<gc, kBigThreads, cluster_smem, s>>>(c, p.list[T_CLUSTER],
+      k_cluster<MODE, W, WEIGHTED><<<gc, kBigThreads, cluster_smem, ts>>>(c, p.list[T_CLUSTER],
                                                                         p.count[T_CLUSTER]);
     else
-      launch_wide<MODE, W>(p, c, s, sms);
-    prof.end(T_CLUSTER, s);
+      launch_wide<MODE, W>(p, c, ts, sms);
+    prof.end(T_CLUSTER, ts);
     ++launches;
   }
   if (p.n_hubs && (tiers >> T_HUB & 1u)) {
@@ -440,39 +550,40 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     const unsigned gi =
         resident_grid(k_hub_accum<MODE, W, WEIGHTED, 1>, kBlockThreads, hub_smem, p.n_items, 1, sms);
     const unsigned gh = grid_for(p.n_hubs, 256, 1024);
-    k_hub_select<MODE><<<gh, 256, 0, s>>>(c, h);
+    k_hub_select<MODE><<<gh, 256, 0, ts>>>(c, h);
     if (c.fresh)  // first pass: labels mostly distinct, no in-warp dedupe (see k_team)
-      k_hub_accum<MODE, W, WEIGHTED, 0><<<gi, kBlockThreads, hub_smem, s>>>(c, h);
+      k_hub_accum<MODE, W, WEIGHTED, 0><<<gi, kBlockThreads, hub_smem, ts>>>(c, h);
     else
-      k_hub_accum<MODE, W, WEIGHTED, 1><<<gi, kBlockThreads, hub_smem, s>>>(c, h);
+      k_hub_accum<MODE, W, WEIGHTED, 1><<<gi, kBlockThreads, hub_smem, ts>>>(c, h);
     const unsigned gs = grid_for(p.n_sitems, 1, sms * 8);
-    k_hub_sweep<W, WEIGHTED><<<gs, kBlockThreads, 0, s>>>(h);
+    k_hub_sweep<W, WEIGHTED><<<gs, kBlockThreads, 0, ts>>>(h);
     launches += 3;
     if constexpr (sizeof(VBits<W>) == 8) {
-      k_hub_sweep_key_f64<kPacked<WEIGHTED>><<<gs, kBlockThreads, 0, s>>>(h);
+      k_hub_sweep_key_f64<kPacked<WEIGHTED>><<<gs, kBlockThreads, 0, ts>>>(h);
       ++launches;
     }
-    k_hub_decide<MODE, W, WEIGHTED><<<gh, 256, 0, s>>>(c, h);
+    k_hub_decide<MODE, W, WEIGHTED><<<gh, 256, 0, ts>>>(c, h);
     ++launches;
     if (MODE == kAsync && c.wake) {
-      k_hub_wake<<<gi, kBlockThreads, 0, s>>>(c, h);
+      k_hub_wake<<<gi, kBlockThreads, 0, ts>>>(c, h);
       ++launches;
     }
-    prof.end(T_HUB, s);
+    prof.end(T_HUB, ts);
   }
+  if (conc_high) fk->join(s);
   NULPA_CUDA(cudaGetLastError());
   return launches;
 }
 
 template <int MODE>
 int dispatch_pass(const Plan& p, const PassCtx& c, unsigned long long* ctr, int value_bytes,
-                  cudaStream_t s, int sms, Prof& prof, unsigned tiers = ~0u) {
+                  cudaStream_t s, int sms, Prof& prof, unsigned tiers = ~0u, Fork* fk = nullptr) {
   const bool weighted = c.g.w != nullptr;
   if (value_bytes == 8)
-    return weighted ? launch_pass<MODE, double, true>(p, c, ctr, s, sms, prof, tiers)
-                    : launch_pass<MODE, double, false>(p, c, ctr, s, sms, prof, tiers);
-  return weighted ? launch_pass<MODE, float, true>(p, c, ctr, s, sms, prof, tiers)
-                  : launch_pass<MODE, float, false>(p, c, ctr, s, sms, prof, tiers);
+    return weighted ? launch_pass<MODE, double, true>(p, c, ctr, s, sms, prof, tiers, fk)
+                    : launch_pass<MODE, double, false>(p, c, ctr, s, sms, prof, tiers, fk);
+  return weighted ? launch_pass<MODE, float, true>(p, c, ctr, s, sms, prof, tiers, fk)
+                  : launch_pass<MODE, float, false>(p, c, ctr, s, sms, prof, tiers, fk);
 }
 
 // ParallelAsync first pass, long rows first: every tier of degree > block_max runs
@@ -627,7 +738,22 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
   const int kBatch = batched ? std::max(1, std::min(o.max_iterations, batch_passes())) : 1;
   const int blocks = batched ? o.max_iterations : 1;  // one counter block per pass
   DBuf<unsigned long long> ctr(size_t(kCtr) * blocks);
-  DBuf<unsigned int> work(2);  // cluster-tier work counter
+  DBuf<unsigned int> work(kTiers);  // work counters of the team / wide tiers (one per tier)
+  // Tier streams for side-by-side tiers (concurrent_mode), leased for the whole run.
+  const int cmode = concurrent_mode();
+  Fork* fk = nullptr;
+  std::unique_lock<std::mutex> fork_lock;
+  const unsigned groups = cmode == 1 || (cmode == 2 && n <= (1u << 22)) ? 3u
+                          : cmode == 2 || cmode == 3 ? 1u : cmode == 4 ? 2u : 0u;
+  if (groups) {
+    Fork& f = Fork::of_device(g->device);
+    fork_lock = std::unique_lock<std::mutex>(f.mu, std::try_to_lock);
+    if (fork_lock.owns_lock()) {
+      f.init();
+      f.groups = groups;
+      fk = &f;
+    }
+  }
   DBuf<unsigned int> stop(1);
   Pinned hc(size_t(kCtr) * blocks + 1);
   unsigned long long* hstop = hc.p + size_t(kCtr) * blocks;
@@ -796,7 +922,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
     } else if (o.exec == NULPA_EXEC_PARALLEL_ASYNC) {
       c.lab_in = cur;
       c.lab_out = cur;
-      launches += dispatch_pass<kAsync>(*p, c, ctr_it, vbytes, s, sms, prof);
+      launches += dispatch_pass<kAsync>(*p, c, ctr_it, vbytes, s, sms, prof, ~0u, fk);
     } else if (o.exec == NULPA_EXEC_SYNCHRONOUS) {
       // sync_move (lpa.cpp:70-100): frozen snapshot `cur`, staged writes to `nxt`,
       // wake-ups after the joint application.
@@ -804,7 +930,7 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
       c.lab_in = cur;
       c.lab_out = nxt;
       c.changed = wake ? changed.p : nullptr;
-      launches += dispatch_pass<kSync>(*p, c, ctr_it, vbytes, s, sms, prof);
+      launches += dispatch_pass<kSync>(*p, c, ctr_it, vbytes, s, sms, prof, ~0u, fk);
       if (wake) {
         prof.begin(T_OTHER, s);
         k_wake_list<<<grid_for(n, kBlockThreads / 32, sms * 8), kBlockThreads, 0, s>>>(

@@ -485,9 +485,23 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
         w[k] = valid ? edge_weight<W, WEIGHTED>(c.g, m.lo + gl) : W(0);
       }
       if (S == 1 && c0 + 1 < kSteps) jn = step_target(c0 + 1);
+      // Async, S > 1: the labels of all S steps were loaded before any of them was
+      // decided, so step k patches in the moves of this chunk's earlier steps (a lane
+      // whose neighbour is one of those vertices takes its new label): every step sees
+      // the batch's earlier moves exactly as the one-step-at-a-time walk does.
+      uint32_t pv[S][kPer], pl[S][kPer];
 #pragma unroll
       for (int k = 0; k < S; ++k) {
         const Meta m = s_meta[wid][(c0 + k) * kPer + sub];
+        if constexpr (MODE == kAsync && S > 1) {
+          uint32_t x = lab[k];
+#pragma unroll
+          for (int q = 0; q < k; ++q)
+#pragma unroll
+            for (int r = 0; r < kPer; ++r)
+              if (j[k] == pv[q][r] && pl[q][r] != kEmpty && x != kEmpty) x = pl[q][r];
+          lab[k] = x;
+        }
         const unsigned peers = __match_any_sync(kFull, lab[k]) & gmask;
         W sm;
         if constexpr (WEIGHTED)
@@ -511,6 +525,13 @@ __global__ void __launch_bounds__(256) k_group(PassCtx c, const uint32_t* __rest
 #pragma unroll
           for (int q = 0; q < kPer; ++q)
             if (bl >> (q * G) & 1u) chg_bits |= 1u << ((c0 + k) * kPer + q);
+          if constexpr (S > 1) {
+#pragma unroll
+            for (int r = 0; r < kPer; ++r) {  // lane r * G decided vertex r of this step
+              pv[k][r] = __shfl_sync(kFull, m.i, r * G);
+              pl[k][r] = __shfl_sync(kFull, ch ? b.k : kEmpty, r * G);
+            }
+          }
         }
       }
     }
