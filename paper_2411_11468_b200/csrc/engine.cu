@@ -194,6 +194,16 @@ struct Fork {
   }
 };
 
+// Rows per iteration of the chunk-major walk (NULPA_CHUNK_ROWS, read once): 1 = k_thread's
+// walk (a fence pair per row), 2 / 4 / 8 = k_chunk_walk (one fence pair per group).
+inline int chunk_rows() {
+  static const int m = [] {
+    const char* e = std::getenv("NULPA_CHUNK_ROWS");
+    return e ? std::atoi(e) : 4;
+  }();
+  return m;
+}
+
 // One-row batches for team tiers of at most one row per team (NULPA_SMALL_TIER_BATCH,
 // read once; 1 by default).
 inline bool small_tier_batch() {
@@ -466,7 +476,27 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   if (conc_low) fk->fork(s);
   if (p.count[T_THREAD] && (tiers >> T_THREAD & 1u)) {
     tier(T_THREAD);
-    if (p.thread_max <= 8 && MODE == kAsync && p.chunked_thread)
+    if (p.thread_max <= 8 && MODE == kAsync && p.chunked_thread && p.chunk_L) {
+      // the graph's chunk-major range: one thread per chunk of chunk_L entries
+      const unsigned gc = grid_for((p.count[T_THREAD] + p.chunk_L - 1) / p.chunk_L, 256, ~0u);
+      switch (chunk_rows()) {
+        case 1:
+          k_thread<MODE, W, WEIGHTED, 8, true><<<gc, 256, 0, ts>>>(
+              c, p.list[T_THREAD], p.count[T_THREAD], p.chunk_lo, p.chunk_L);
+          break;
+        case 2:
+          k_chunk_walk<MODE, W, WEIGHTED, 8, 2><<<gc, 256, 0, ts>>>(c, p.count[T_THREAD],
+                                                                     p.chunk_lo, p.chunk_L);
+          break;
+        case 8:
+          k_chunk_walk<MODE, W, WEIGHTED, 8, 8><<<gc, 256, 0, ts>>>(c, p.count[T_THREAD],
+                                                                     p.chunk_lo, p.chunk_L);
+          break;
+        default:
+          k_chunk_walk<MODE, W, WEIGHTED, 8, 4><<<gc, 256, 0, ts>>>(c, p.count[T_THREAD],
+                                                                     p.chunk_lo, p.chunk_L);
+      }
+    } else if (p.thread_max <= 8 && MODE == kAsync && p.chunked_thread)
       // chunks of >= kMinChunk vertices per thread (a short chunk propagates little)
       k_thread<MODE, W, WEIGHTED, 8, true>
           <<<resident_grid(k_thread<MODE, W, WEIGHTED, 8, true>, 256, 0, p.count[T_THREAD],

@@ -455,6 +455,13 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
       dfree(t2);
       dfree(d_sum);
       p->chunked_thread = 2 * e >= g->m2;
+      // The graph stores exactly this tier chunk-major (layout.cu chunk_major): the walk
+      // reads it coalesced.
+      if (p->chunked_thread && g->chunk_n && v_lo == 0 && v_hi == g->n && tb.thread_max == 8 &&
+          m == g->chunk_n) {
+        p->chunk_lo = g->chunk_lo;
+        p->chunk_L = g->chunk_L;
+      }
     }
     if (tb.schedule == 4) {  // as 3, except a chunk-walked thread tier stays unscrambled
       for (int t = p->chunked_thread ? dev::T_HALF : dev::T_THREAD; t <= dev::T_WARP; ++t)
@@ -489,6 +496,11 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
       uint32_t out[2 * Plan::kLists];
       NULPA_CUDA(cudaMemcpyAsync(out, d_out, sizeof out, cudaMemcpyDeviceToHost, s));
       NULPA_CUDA(cudaStreamSynchronize(s));
+      // Inside a chunk-major low range (degrees 1..8, buckets 0..3, not sorted) a bucket
+      // bound below 3 has no position: take the range's edges (fewer read-only labels).
+      if (g->chunk_n)
+        for (int x = 0; x < 2 * Plan::kLists; ++x)
+          if (bm[x] >= 0 && bm[x] < 3) out[x] = x < Plan::kLists ? g->chunk_lo : g->chunk_lo + g->chunk_n;
       for (int t = 0; t < Plan::kLists; ++t) {
         p->ro_end[t] = out[t];
         p->ro_lo[t] = out[Plan::kLists + t];

@@ -95,6 +95,11 @@ struct nulpa_graph {
   int layout = NULPA_LAYOUT_IDENTITY;
   uint32_t* perm = nullptr;  // device
   uint32_t* inv = nullptr;   // device
+  // Chunk-major low range (layout.cu build_perm): positions [chunk_lo, chunk_lo + chunk_n)
+  // hold the rows of degree 1..8 transposed for a chunk walk of chunk_n / chunk_L threads
+  // (entry e = k * chunk_L + r of the range's bucket order sits at column r, row k).
+  // chunk_n = 0: no such range.
+  uint32_t chunk_lo = 0, chunk_n = 0, chunk_L = 0;
   nulpa::Plan* plan = nullptr;  // cached tiering (plan.hpp)
   // Held by every call that uses `plan`: the cached plan (and its hub tables and
   // wide-tier scratch) is shared state, so runs on one graph handle are serialised.

@@ -360,7 +360,7 @@ __global__ void k_offsets_ok(const uint64_t* off, uint32_t n, uint64_t m2, unsig
 int default_layout() { return g_default_layout.load(); }
 
 void build_perm(const uint64_t* off, uint32_t n, uint32_t** perm_out, uint32_t** inv_out,
-                cudaStream_t s);
+                cudaStream_t s, nulpa_graph* g);
 
 namespace {
 
@@ -523,7 +523,7 @@ void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g,
     NULPA_CUDA(cudaStreamSynchronize(sb));
     if (bad) throw Error(NULPA_EINVAL, "inconsistent CSR arrays");
     // Permutation, position-order offsets, the long-row list of the input order.
-    build_perm(src_off, n, &g->perm, &g->inv, sb);
+    build_perm(src_off, n, &g->perm, &g->inv, sb, g);
     g->offsets = dalloc<uint64_t>(uint64_t(n) + 1);
     g->targets = dalloc<uint32_t>(m2);
     if (weighted) g->weights = dalloc<float>(m2);
@@ -682,8 +682,119 @@ void upload_pipelined(const nulpa_csr* csr, nulpa_graph* g,
 
 // perm (position -> vertex) and inv (vertex -> position) of the bucketed order,
 // from the input's offsets.
+int sm_count();
+
+namespace {
+
+// ---- chunk-major low range ----------------------------------------------------------
+// On lattice- and road-like graphs the rows of degree <= 8 carry most of the edges, and
+// ParallelAsync walks them in contiguous chunks, one chunk per thread, as each reference
+// worker walks its slice (lpa.cpp:139-165; k_thread CHUNKED): thread k visits entries
+// k*L .. k*L + L - 1 of the range. In bucket order those entries are L positions apart
+// across the lanes of a warp, so every load of the walk touches 32 sectors. Storing the
+// range chunk-major — entry e = k*L + r at column r, row k — puts lane k's r-th row next
+// to lane k+1's: the walk's row bounds, targets, own labels and flags are read coalesced,
+// and so are its neighbour labels (a lattice neighbour e +- 1 or e +- width sits in the
+// next lane's or the same lane's column). Only positions move; the walk and every result
+// stay as they were.
+// Column r holds the q + (r < rem) chunks that reach it (range size M = q*L + rem), so it
+// starts at r*q + min(r, rem).
+constexpr uint32_t kChunkMaxDeg = 8;
+constexpr uint32_t kChunkThreadsPerSm = 1024;  // the chunk walk's threads (k_thread: 4 x 256 per SM)
+constexpr uint32_t kChunkMin = 32;             // shortest chunk (a short chunk propagates little)
+
+__global__ void k_low_range_stats(const uint64_t* off, uint32_t n, unsigned long long* out) {
+  // out[0]: rows of degree > kChunkMaxDeg, out[1]: rows of degree 1..kChunkMaxDeg, out[2]: their entries
+  unsigned long long hi = 0, lo = 0, e = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint64_t d = off[v + 1] - off[v];
+    hi += d > kChunkMaxDeg;
+    lo += d >= 1 && d <= kChunkMaxDeg;
+    e += (d >= 1 && d <= kChunkMaxDeg) ? d : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    hi += __shfl_xor_sync(0xFFFFFFFFu, hi, o);
+    lo += __shfl_xor_sync(0xFFFFFFFFu, lo, o);
+    e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, hi);
+    atomicAdd(out + 1, lo);
+    atomicAdd(out + 2, e);
+  }
+}
+
+// dst[a + j] = src[a + e(j)]: position a + j of the chunk-major range holds bucket-order
+// entry e(j) = k*L + r (column r, row k); positions outside the range are copied.
+__global__ void k_chunk_transpose(const uint32_t* src, uint32_t* dst, uint32_t n, uint32_t a,
+                                  uint32_t M, uint32_t L) {
+  const uint32_t q = M / L, rem = M % L;
+  const uint64_t wide = uint64_t(rem) * (q + 1);  // positions of the rem taller columns
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    if (p < a || p >= a + M) {
+      dst[p] = src[p];
+      continue;
+    }
+    const uint32_t j = p - a;
+    uint32_t r, k;
+    if (j < wide) {
+      r = j / (q + 1);
+      k = j % (q + 1);
+    } else {
+      const uint32_t jj = static_cast<uint32_t>(j - wide);
+      r = rem + jj / q;
+      k = jj % q;
+    }
+    dst[p] = src[a + k * L + r];
+  }
+}
+
+inline bool chunk_major_enabled() {
+  static const bool m = [] {
+    const char* e = std::getenv("NULPA_CHUNK_MAJOR");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return m;
+}
+
+// Apply the chunk-major order to the low range of a bucket-order `perm` when that range
+// carries at least half of the entries (where the thread tier is walked in chunks,
+// graph.cu build_plan) and is large enough for coalescing to matter.
+void chunk_major(const uint64_t* off, uint32_t n, uint32_t* perm, cudaStream_t s, nulpa_graph* g) {
+  if (!g) return;
+  g->chunk_lo = g->chunk_n = g->chunk_L = 0;
+  if (!chunk_major_enabled() || n < 2) return;
+  unsigned long long* d = dalloc<unsigned long long>(4);
+  NULPA_CUDA(cudaMemsetAsync(d, 0, 3 * sizeof(unsigned long long), s));
+  k_low_range_stats<<<blocks_for(n), 256, 0, s>>>(off, n, d);
+  NULPA_CUDA(cudaGetLastError());
+  NULPA_CUDA(cudaMemcpyAsync(d + 3, off + n, 8, cudaMemcpyDeviceToDevice, s));
+  unsigned long long h[4] = {0, 0, 0, 0};
+  NULPA_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, s));
+  NULPA_CUDA(cudaStreamSynchronize(s));
+  dfree(d);
+  const uint64_t a = h[0], M = h[1], e = h[2], m2 = h[3];
+  const uint64_t T = uint64_t(sm_count()) * kChunkThreadsPerSm;
+  if (M < (1u << 16) || 2 * e < m2) return;
+  // (chunks of at least kChunkMin entries, as the walk's own bound: engine.cu kMinChunk)
+  const uint64_t L = std::max<uint64_t>((M + T - 1) / T, kChunkMin);
+  uint32_t* tmp = dalloc<uint32_t>(n);
+  k_chunk_transpose<<<blocks_for(n), 256, 0, s>>>(perm, tmp, n, static_cast<uint32_t>(a),
+                                                  static_cast<uint32_t>(M), static_cast<uint32_t>(L));
+  NULPA_CUDA(cudaGetLastError());
+  NULPA_CUDA(cudaMemcpyAsync(perm, tmp, uint64_t(n) * 4, cudaMemcpyDeviceToDevice, s));
+  NULPA_CUDA(cudaStreamSynchronize(s));
+  dfree(tmp);
+  g->chunk_lo = static_cast<uint32_t>(a);
+  g->chunk_n = static_cast<uint32_t>(M);
+  g->chunk_L = static_cast<uint32_t>(L);
+}
+
+}  // namespace
+
 void build_perm(const uint64_t* off, uint32_t n, uint32_t** perm_out, uint32_t** inv_out,
-                cudaStream_t s) {
+                cudaStream_t s, nulpa_graph* g) {
   uint8_t* k0 = dalloc<uint8_t>(n);
   uint8_t* k1 = dalloc<uint8_t>(n);
   uint32_t* ids = dalloc<uint32_t>(n);
@@ -705,6 +816,7 @@ void build_perm(const uint64_t* off, uint32_t n, uint32_t** perm_out, uint32_t**
   dfree(k0);
   dfree(k1);
   dfree(ids);
+  chunk_major(off, n, perm, s, g);
   uint32_t* inv = dalloc<uint32_t>(n);
   k_invert<<<blocks_for(n), 256, 0, s>>>(perm, n, inv);
   NULPA_CUDA(cudaGetLastError());
@@ -714,11 +826,12 @@ void build_perm(const uint64_t* off, uint32_t n, uint32_t** perm_out, uint32_t**
 
 void relayout_graph(nulpa_graph* g, cudaStream_t s) {
   g->layout = NULPA_LAYOUT_IDENTITY;
+  g->chunk_lo = g->chunk_n = g->chunk_L = 0;
   if (default_layout() != NULPA_LAYOUT_DEGREE_BUCKETS || g->n < 2) return;
   const uint32_t n = g->n;
   const uint64_t m2 = g->m2;
   uint32_t *perm = nullptr, *inv = nullptr;
-  build_perm(g->offsets, n, &perm, &inv, s);
+  build_perm(g->offsets, n, &perm, &inv, s, g);
   // Rows longer than kLongRow form a prefix of the position order (their
   // buckets come first): copy them edge-balanced.
   uint32_t long_rows = 0;

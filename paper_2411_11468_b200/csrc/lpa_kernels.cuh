@@ -243,16 +243,23 @@ constexpr bool kPacked = !WEIGHTED;  // unit weights -> packed 64-bit slots
 // (lpa.cpp:139-165), instead of the grid-stride interleave.
 // V: list entries a thread takes per iteration (grid-stride walk only): their claims
 // share one fence and their row, target and label loads are issued together.
+// cm_L != 0 (CHUNKED): the tier is the graph's chunk-major range at cm_lo (layout.cu
+// chunk_major) with chunks of cm_L entries: entry r of chunk k sits at column r, row k,
+// i.e. at cm_lo + r*q + min(r, rem) + k for count = q*cm_L + rem, and the grid must
+// cover every chunk.
 template <int MODE, typename W, bool WEIGHTED, int DMAX, bool CHUNKED = false, int V = 1>
 __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __restrict__ list,
-                                                uint32_t count) {
+                                                uint32_t count, uint32_t cm_lo = 0,
+                                                uint32_t cm_L = 0) {
   static_assert(!CHUNKED || V == 1, "a chunk walk takes its entries one at a time");
   if (stopped(c.stop)) return;
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
   const uint64_t pol = policy_evict_first();
   const uint32_t stride = gridDim.x * blockDim.x;
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t L = CHUNKED ? (count + stride - 1) / stride : 0u;
+  const uint32_t L = CHUNKED ? (cm_L ? cm_L : (count + stride - 1) / stride) : 0u;
+  const uint32_t cq = (CHUNKED && cm_L) ? count / cm_L : 0u;
+  const uint32_t crem = (CHUNKED && cm_L) ? count % cm_L : 0u;
   const uint32_t t_end = CHUNKED ? min(count, (tid + 1) * L) : count;
   const uint32_t step = CHUNKED ? 1u : stride;
   for (uint32_t t = CHUNKED ? tid * L : tid; t < t_end; t += step * V) {
@@ -263,7 +270,12 @@ __global__ void __launch_bounds__(256) k_thread(PassCtx c, const uint32_t* __res
     for (int v = 0; v < V; ++v) {
       const uint32_t tv = t + v * step;
       act[v] = tv < t_end;
-      iv[v] = act[v] ? __ldg(list + tv) : 0u;
+      if (CHUNKED && cm_L) {
+        const uint32_t r = tv - tid * L;
+        iv[v] = act[v] ? cm_lo + r * cq + min(r, crem) + tid : 0u;
+      } else {
+        iv[v] = act[v] ? __ldg(list + tv) : 0u;
+      }
       if (act[v]) act[v] = !claim_vertex(c, iv[v]);
     }
     claim_fence<MODE>(c);
@@ -409,6 +421,98 @@ __global__ void __launch_bounds__(256) k_thread_q(PassCtx c, const uint32_t* __r
           d = static_cast<uint32_t>(__ldg(c.g.off + iq[q] + 1) - lo);
         }
         warp_wake_rows<4>(c.flags, c.g.tgt, lo, d, rows, pol);
+      }
+    }
+  }
+  warp_add_counter(c.ctr, C_PROC_V, n_v);
+  warp_add_counter(c.ctr, C_PROC_E, n_e);
+  warp_add_counter(c.ctr, C_DN, n_dn);
+  warp_add_counter(c.ctr, C_WAKE_E, n_w);
+}
+
+// Chunk walk over the graph's chunk-major range (layout.cu chunk_major), Q rows of a
+// thread's chunk per iteration: their claims share one fence, their row bounds are loaded
+// together, the rows are decided one after another in chunk order (each row's loads
+// follow the previous row's label store, so the walk sees its own moves as k_thread's
+// does), and their label stores share one fence before this thread wakes the changed
+// rows' neighbours. Thread k's rows sit at cm_lo + r*q + min(r, rem) + k: every load is
+// coalesced across the warp.
+template <int MODE, typename W, bool WEIGHTED, int DMAX, int Q = 4>
+__global__ void __launch_bounds__(256) k_chunk_walk(PassCtx c, uint32_t count, uint32_t cm_lo,
+                                                    uint32_t cm_L) {
+  if (stopped(c.stop)) return;
+  unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
+  const uint64_t pol = policy_evict_first();
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t cq = count / cm_L, crem = count % cm_L;
+  // entries of this thread's chunk: cm_L for k < cq, crem for k == cq, none above
+  const uint32_t len = k < cq ? cm_L : (k == cq ? crem : 0u);
+  for (uint32_t r0 = 0; r0 < len; r0 += Q) {
+    uint32_t iq[Q];
+    bool aq[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const uint32_t r = r0 + q;
+      aq[q] = r < len;
+      iq[q] = cm_lo + r * cq + min(r, crem) + k;
+      if (aq[q]) aq[q] = !claim_vertex(c, iq[q]);
+    }
+    claim_fence<MODE>(c);
+    uint64_t lq[Q];
+    uint32_t dq[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      lq[q] = aq[q] ? __ldg(c.g.off + iq[q]) : 0ull;
+      dq[q] = aq[q] ? static_cast<uint32_t>(__ldg(c.g.off + iq[q] + 1) - lq[q]) : 0u;
+    }
+    unsigned chg = 0;  // bit q: row q changed label
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (!aq[q]) continue;
+      const uint32_t i = iq[q];
+      const uint64_t lo = lq[q];
+      const uint32_t d = dq[q];
+      uint32_t nb[DMAX], lab[DMAX];
+      W wt[DMAX];
+#pragma unroll
+      for (int e = 0; e < DMAX; ++e) nb[e] = (e < d) ? ld_stream(c.g.tgt + lo + e, pol) : i;
+#pragma unroll
+      for (int e = 0; e < DMAX; ++e) {
+        const bool valid = e < d && nb[e] != i;  // self-loops skipped (lpa.hpp:102)
+        lab[e] = valid ? gather_label<MODE>(c, nb[e]) : kEmpty;
+        wt[e] = valid ? edge_weight<W, WEIGHTED>(c.g, lo + e) : W(0);
+      }
+      // per-label total in neighbour order (bit-identical sums), then argmax
+      Best<VBits<W>> b{VBits<W>(0), kEmpty};
+#pragma unroll
+      for (int e = 0; e < DMAX; ++e) {
+        W sum = W(0);
+#pragma unroll
+        for (int m = 0; m < DMAX; ++m) sum += (lab[m] == lab[e]) ? wt[m] : W(0);
+        best_merge(b, to_vbits<W>(sum), lab[e]);
+      }
+      ++n_v;
+      n_e += d;
+      if (apply_move<MODE, false>(c, i, b.k)) {
+        ++n_dn;
+        chg |= 1u << q;
+        if (MODE == kAsync && c.wake) n_w += d;
+      }
+    }
+    if (MODE == kAsync && c.wake && chg) {
+      fence_sc();  // this thread's label stores before any wake load (a18)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        if (!(chg >> q & 1u)) continue;
+        uint32_t nb[DMAX];
+        uint8_t f[DMAX];  // every flag load in flight before the first store
+#pragma unroll
+        for (int e = 0; e < DMAX; ++e) nb[e] = e < dq[q] ? ld_stream(c.g.tgt + lq[q] + e, pol) : 0u;
+#pragma unroll
+        for (int e = 0; e < DMAX; ++e) f[e] = e < dq[q] ? load_flag(c.flags + nb[e]) : uint8_t(0);
+#pragma unroll
+        for (int e = 0; e < DMAX; ++e)
+          if (f[e]) st_relaxed(c.flags + nb[e], uint8_t(0));
       }
     }
   }

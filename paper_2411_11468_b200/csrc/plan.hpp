@@ -29,6 +29,9 @@ struct Plan {
   // Thread tier walked in contiguous chunks (ParallelAsync): schedule 4, chosen when
   // the tier carries most of the graph's edges (lattice / road-like inputs).
   bool chunked_thread = false;
+  // ... over the graph's chunk-major low range (nulpa_graph::chunk_*): the walk computes
+  // its positions (chunk_lo + column start + chunk index) instead of reading the list.
+  uint32_t chunk_lo = 0, chunk_L = 0;
   bool weighted = false;  // hub tables: packed 64-bit words (unit weights) or split
   // Hub tier.
   uint32_t n_hubs = 0, n_items = 0;
