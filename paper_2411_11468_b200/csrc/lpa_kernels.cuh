@@ -437,9 +437,11 @@ __global__ void __launch_bounds__(256) k_thread_q(PassCtx c, const uint32_t* __r
 // does), and their label stores share one fence before this thread wakes the changed
 // rows' neighbours. Thread k's rows sit at cm_lo + r*q + min(r, rem) + k: every load is
 // coalesced across the warp.
-template <int MODE, typename W, bool WEIGHTED, int DMAX, int Q = 4>
-__global__ void __launch_bounds__(256) k_chunk_walk(PassCtx c, uint32_t count, uint32_t cm_lo,
-                                                    uint32_t cm_L) {
+// PF: the next row's targets are loaded while this row's labels are in flight (targets
+// never change), so a row's chain is one label round trip.
+template <int MODE, typename W, bool WEIGHTED, int DMAX, int Q = 4, bool PF = false>
+__global__ void __launch_bounds__(256, 4) k_chunk_walk(PassCtx c, uint32_t count, uint32_t cm_lo,
+                                                       uint32_t cm_L) {
   if (stopped(c.stop)) return;
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
   const uint64_t pol = policy_evict_first();
@@ -466,16 +468,30 @@ __global__ void __launch_bounds__(256) k_chunk_walk(PassCtx c, uint32_t count, u
       dq[q] = aq[q] ? static_cast<uint32_t>(__ldg(c.g.off + iq[q] + 1) - lq[q]) : 0u;
     }
     unsigned chg = 0;  // bit q: row q changed label
+    uint32_t nn[DMAX];  // PF: the next active row's targets
+    auto row_targets = [&](int q, uint32_t (&dst)[DMAX]) {
+#pragma unroll
+      for (int e = 0; e < DMAX; ++e)
+        dst[e] = (aq[q] && e < dq[q]) ? ld_stream(c.g.tgt + lq[q] + e, pol) : iq[q];
+    };
+    if (PF) row_targets(0, nn);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
+      uint32_t nb[DMAX], lab[DMAX];
+      if constexpr (PF) {
+#pragma unroll
+        for (int e = 0; e < DMAX; ++e) nb[e] = nn[e];
+        if (q + 1 < Q) row_targets(q + 1, nn);  // (before this row's gathers, in flight with them)
+      }
       if (!aq[q]) continue;
       const uint32_t i = iq[q];
       const uint64_t lo = lq[q];
       const uint32_t d = dq[q];
-      uint32_t nb[DMAX], lab[DMAX];
       W wt[DMAX];
+      if constexpr (!PF) {
 #pragma unroll
-      for (int e = 0; e < DMAX; ++e) nb[e] = (e < d) ? ld_stream(c.g.tgt + lo + e, pol) : i;
+        for (int e = 0; e < DMAX; ++e) nb[e] = (e < d) ? ld_stream(c.g.tgt + lo + e, pol) : i;
+      }
 #pragma unroll
       for (int e = 0; e < DMAX; ++e) {
         const bool valid = e < d && nb[e] != i;  // self-loops skipped (lpa.hpp:102)
