@@ -288,6 +288,45 @@ def sbm_loop_time(lp2, sgh, m2: int, runs: int = 20) -> dict:
             "edges_per_s": m2 / (med * 1e-3), "profiled": False}
 
 
+def grid_shape(dev: int, peak: float, runs: int = 5) -> dict:
+    """The lattice shape beside the headline, measured in every default run: the 4096²
+    grid (all thread tier, walked in chunks over the chunk-major range):
+    unprofiled loop time per run, then one profiled run for the thread tier's algorithmic
+    bytes over its event-timed duration."""
+    import torch
+    from paper_2411_11468_b200 import _capi, workloads
+    from paper_2411_11468_b200 import labelprop as lp
+    dg, wdesc = workloads.build("grid", 27, 1, dev)
+    try:
+        cfg = lp.LpaConfig()
+        for _ in range(3):
+            dg.lpa(cfg, want_host=False)
+        res = [dg.lpa(cfg, want_host=False).stats for _ in range(runs)]
+        ms = sorted(r.elapsed_seconds * 1e3 for r in res)
+        med = ms[len(ms) // 2]
+        t = lp.Tuning().to_c()
+        t.profile = 1
+        o = lp._opts(cfg, dev)
+        st = _capi.nulpa_stats()
+        _capi.check(_capi.lib().nulpa_run_graph(dg._h, C.byref(o), C.byref(t), None, None,
+                                                C.byref(st)))
+        th = _capi.TIER_NAMES.index("thread")
+        tms, tby, tp = st.tier_ms[th], st.tier_bytes[th], max(1, st.tier_passes[th])
+        ach = tby / (tms * 1e-3) / 1e9 if tms > 0 else 0.0
+        lab = torch.empty(dg.n, dtype=torch.int32, device=f"cuda:{dev}")
+        dg.lpa(cfg, labels_device_ptr=lab.data_ptr(), want_host=False)
+        q = dg.modularity_device(lab.data_ptr())
+        return {"workload": wdesc["workload"], "n": dg.n, "m2": dg.m2,
+                "ms_per_run_median": med, "ms_per_run_min": ms[0], "runs": runs,
+                "iterations": sorted({r.iterations for r in res}), "modularity": q,
+                "edges_per_s": dg.m2 / (med * 1e-3), "profiled": False,
+                "thread_tier": {"ms_per_launch": tms / tp, "alg_bytes_per_launch": tby / tp,
+                                "achieved_gbs": ach, "peak": peak, "frac": ach / peak,
+                                "kernel": "k_chunk_walk (chunk-major range)"}}
+    finally:
+        dg.free()
+
+
 def _log(msg: str) -> None:
     sys.stderr.write(f"[bench {time.strftime('%H:%M:%S')}] {msg}\n")
     sys.stderr.flush()
@@ -602,6 +641,17 @@ def bench_nulpa(args):
     if args.e2e_steps > 0:
         del off_h, tgt_h
 
+    shapes = None
+    if rank == 0 and world == 1 and args.workload == "rmat" and args.cpu_baseline:
+        try:
+            q0 = time.time()
+            shapes = {"grid4096": grid_shape(dev, peak)}
+            if quality and "sbm100k" in quality:
+                shapes["sbm100k"] = quality["sbm100k"].get("nulpa_loop")
+            _log(f"other shapes ({time.time() - q0:.1f} s)")
+        except Exception as e:  # never sink the headline line
+            shapes = {"failed": str(e)}
+
     if rank == 0:
         s0 = stats[-1][0]
         line = {
@@ -644,6 +694,7 @@ def bench_nulpa(args):
             "e2e_dropin": dropin,
             "cpu_baseline": cpu,
             "quality": quality,
+            "shapes": shapes,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
         }
