@@ -138,7 +138,9 @@ struct Prof {
 // tiers' latency chains. Any order of the vertices inside one list is an ordering the
 // reference's workers can produce. 0 = off, 1 = on, 2 = both groups for graphs of at
 // most 2^22 vertices and the register group above (default), 3 = the register group
-// only, 4 = the table group only. Measured on one B200 (loop ms per run, off -> default):
+// only, 4 = the table group only, 5 = the register group plus the hub accumulation beside
+// the table tiers, 6 = that hub accumulation only (R-MAT 27: 123.7 ms, web 69.2 ms: the
+// resident hub accumulation holds SMs the table tiers need; off). Measured on one B200 (loop ms per run, off -> default):
 // SBM-100K 0.456 -> 0.286 (with one-row small-tier batches), R-MAT 18 1.33 -> 0.72,
 // R-MAT 22 5.1 -> 4.3, R-MAT 24 12.7 -> 12.3, R-MAT 27 96.9 -> 95.3, web 66.1 -> 64.6.
 // The table group side by side on large graphs is slower (R-MAT 27: 108.8 ms): its
@@ -196,12 +198,14 @@ struct Fork {
 
 // Rows per iteration of the chunk-major walk (NULPA_CHUNK_ROWS, read once): 1 = k_thread's
 // walk (a fence pair per row), 2 / 4 / 8 = k_chunk_walk (one fence pair per group), 14 / 18
-// = 4 / 8 rows with the next row's targets prefetched (default 14; 4096² grid per run: 5.67
-// / 4.95 / 4.47 / 4.50 / 4.23 / 4.68 ms for 1 / 2 / 4 / 8 / 14 / 18).
+// = 4 / 8 rows with the next row's targets prefetched, 24 / 28 = the same for ranges of
+// degree <= 4 (4-entry row registers). 0 (default) = 24 where the range's degree is <= 4,
+// else 14. 4096² grid per run: 5.67 / 4.95 / 4.47 / 4.50 / 4.23 / 4.68 / 3.66 / 3.66 ms for
+// 1 / 2 / 4 / 8 / 14 / 18 / 24 / 28.
 inline int chunk_rows() {
   static const int m = [] {
     const char* e = std::getenv("NULPA_CHUNK_ROWS");
-    return e ? std::atoi(e) : 14;
+    return e ? std::atoi(e) : 0;
   }();
   return m;
 }
@@ -481,7 +485,18 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     if (p.thread_max <= 8 && MODE == kAsync && p.chunked_thread && p.chunk_L) {
       // the graph's chunk-major range: one thread per chunk of chunk_L entries
       const unsigned gc = grid_for((p.count[T_THREAD] + p.chunk_L - 1) / p.chunk_L, 256, ~0u);
-      switch (chunk_rows()) {
+      // (default: the degree-<=4 walk where the range allows it, lattices)
+      const int want = chunk_rows() ? chunk_rows() : (p.chunk_dmax <= 4 ? 24 : 14);
+      const int rows = (want >= 20 && p.chunk_dmax > 4) ? 14 : want;
+      switch (rows) {
+        case 24:  // rows of degree <= 4 (lattices): 4-entry registers, 4 rows, prefetched targets
+          k_chunk_walk<MODE, W, WEIGHTED, 4, 4, true><<<gc, 256, 0, ts>>>(
+              c, p.count[T_THREAD], p.chunk_lo, p.chunk_L);
+          break;
+        case 28:  // ... 8 rows
+          k_chunk_walk<MODE, W, WEIGHTED, 4, 8, true><<<gc, 256, 0, ts>>>(
+              c, p.count[T_THREAD], p.chunk_lo, p.chunk_L);
+          break;
         case 1:
           k_thread<MODE, W, WEIGHTED, 8, true><<<gc, 256, 0, ts>>>(
               c, p.list[T_THREAD], p.count[T_THREAD], p.chunk_lo, p.chunk_L);
@@ -545,6 +560,54 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
   }
   if (conc_low) fk->join(s);
   if (conc_high) fk->fork(s);
+  // Hub accumulation beside the table tiers (concurrent_mode 5/6): k_hub_select claims the
+  // hubs and k_hub_accum/sweep fill their tables on the hub stream while team32 .. wide run
+  // on `s`; the hubs' labels are written only after the join (k_hub_decide), so no other
+  // tier sees a hub label change during its launch and every read-only range stays valid.
+  // (The accumulation reads labels the table tiers are writing: an async read of an older
+  // label, re-examined through the hub's flag, which the writer clears, lpa.cpp:161-163.)
+  const bool hub_beside = fk && (fk->groups & 4u) && !conc_high && runs(T_HUB);
+  HubCtx h = p.hub_ctx();
+  h.stop = c.stop;
+  const unsigned gi =
+      p.n_hubs ? resident_grid(k_hub_accum<MODE, W, WEIGHTED, 1>, kBlockThreads, hub_smem, p.n_items, 1, sms) : 1u;
+  const unsigned gh = grid_for(p.n_hubs, 256, 1024);
+  const unsigned gs = grid_for(p.n_sitems, 1, sms * 8);
+  auto hub_gather = [&](const PassCtx& hc, cudaStream_t hs) {
+    int l = 3;
+    k_hub_select<MODE><<<gh, 256, 0, hs>>>(hc, h);
+    if (hc.fresh)  // first pass: labels mostly distinct, no in-warp dedupe (see k_team)
+      k_hub_accum<MODE, W, WEIGHTED, 0><<<gi, kBlockThreads, hub_smem, hs>>>(hc, h);
+    else
+      k_hub_accum<MODE, W, WEIGHTED, 1><<<gi, kBlockThreads, hub_smem, hs>>>(hc, h);
+    k_hub_sweep<W, WEIGHTED><<<gs, kBlockThreads, 0, hs>>>(h);
+    if constexpr (sizeof(VBits<W>) == 8) {
+      k_hub_sweep_key_f64<kPacked<WEIGHTED>><<<gs, kBlockThreads, 0, hs>>>(h);
+      ++l;
+    }
+    return l;
+  };
+  auto hub_finish = [&](const PassCtx& hc, cudaStream_t hs) {
+    int l = 1;
+    k_hub_decide<MODE, W, WEIGHTED><<<gh, 256, 0, hs>>>(hc, h);
+    if (MODE == kAsync && hc.wake) {
+      k_hub_wake<<<gi, kBlockThreads, 0, hs>>>(hc, h);
+      ++l;
+    }
+    return l;
+  };
+  PassCtx chub = c;
+  if (hub_beside) {
+    fk->fork(s);
+    cudaStream_t hs = fk->enter(T_HUB);
+    chub.ctr = ctr + T_HUB * C_COUNT;
+    chub.work = work0;
+    chub.ro_end = (ro_labels() && p.ro_end[T_HUB] != 0) ? p.ro_end[T_HUB] : 0u;
+    chub.ro_lo = 0xFFFFFFFFu;
+    prof.begin(T_HUB, hs);
+    launches += hub_gather(chub, hs);
+    prof.end(T_HUB, hs);
+  }
   if (p.count[T_WTAB] && (tiers >> T_WTAB & 1u)) {
     tier(T_WTAB);
     team_launch(k_wt, 256, 8, kTeamBatch<32>, wtab_smem, p.list[T_WTAB], p.count[T_WTAB], false);
@@ -584,31 +647,15 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
     ++launches;
   }
   if (p.n_hubs && (tiers >> T_HUB & 1u)) {
-    tier(T_HUB);
-    HubCtx h = p.hub_ctx();
-    h.stop = c.stop;
-    const unsigned gi =
-        resident_grid(k_hub_accum<MODE, W, WEIGHTED, 1>, kBlockThreads, hub_smem, p.n_items, 1, sms);
-    const unsigned gh = grid_for(p.n_hubs, 256, 1024);
-    k_hub_select<MODE><<<gh, 256, 0, ts>>>(c, h);
-    if (c.fresh)  // first pass: labels mostly distinct, no in-warp dedupe (see k_team)
-      k_hub_accum<MODE, W, WEIGHTED, 0><<<gi, kBlockThreads, hub_smem, ts>>>(c, h);
-    else
-      k_hub_accum<MODE, W, WEIGHTED, 1><<<gi, kBlockThreads, hub_smem, ts>>>(c, h);
-    const unsigned gs = grid_for(p.n_sitems, 1, sms * 8);
-    k_hub_sweep<W, WEIGHTED><<<gs, kBlockThreads, 0, ts>>>(h);
-    launches += 3;
-    if constexpr (sizeof(VBits<W>) == 8) {
-      k_hub_sweep_key_f64<kPacked<WEIGHTED>><<<gs, kBlockThreads, 0, ts>>>(h);
-      ++launches;
+    if (hub_beside) {
+      fk->join(s);  // the hub tables are complete: decide and wake after the table tiers
+      launches += hub_finish(chub, s);
+    } else {
+      tier(T_HUB);
+      launches += hub_gather(c, ts);
+      launches += hub_finish(c, ts);
+      prof.end(T_HUB, ts);
     }
-    k_hub_decide<MODE, W, WEIGHTED><<<gh, 256, 0, ts>>>(c, h);
-    ++launches;
-    if (MODE == kAsync && c.wake) {
-      k_hub_wake<<<gi, kBlockThreads, 0, ts>>>(c, h);
-      ++launches;
-    }
-    prof.end(T_HUB, ts);
   }
   if (conc_high) fk->join(s);
   NULPA_CUDA(cudaGetLastError());
@@ -784,7 +831,8 @@ void run_lpa(nulpa_graph* g, const nulpa_opts& o, const nulpa_tuning* tuning,
   Fork* fk = nullptr;
   std::unique_lock<std::mutex> fork_lock;
   const unsigned groups = cmode == 1 || (cmode == 2 && n <= (1u << 22)) ? 3u
-                          : cmode == 2 || cmode == 3 ? 1u : cmode == 4 ? 2u : 0u;
+                          : cmode == 2 || cmode == 3 ? 1u : cmode == 4 ? 2u
+                          : cmode == 5 ? 5u : cmode == 6 ? 4u : 0u;
   if (groups) {
     Fork& f = Fork::of_device(g->device);
     fork_lock = std::unique_lock<std::mutex>(f.mu, std::try_to_lock);

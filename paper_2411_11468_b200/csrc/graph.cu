@@ -461,6 +461,7 @@ Plan* build_plan(nulpa_graph* g, const TierBounds& tb, int value_bytes, cudaStre
           m == g->chunk_n) {
         p->chunk_lo = g->chunk_lo;
         p->chunk_L = g->chunk_L;
+        p->chunk_dmax = g->chunk_dmax;
       }
     }
     if (tb.schedule == 4) {  // as 3, except a chunk-walked thread tier stays unscrambled

@@ -100,6 +100,7 @@ struct nulpa_graph {
   // (entry e = k * chunk_L + r of the range's bucket order sits at column r, row k).
   // chunk_n = 0: no such range.
   uint32_t chunk_lo = 0, chunk_n = 0, chunk_L = 0;
+  uint32_t chunk_dmax = 0;  // the range's largest degree (<= 8)
   nulpa::Plan* plan = nullptr;  // cached tiering (plan.hpp)
   // Held by every call that uses `plan`: the cached plan (and its hub tables and
   // wide-tier scratch) is shared state, so runs on one graph handle are serialised.

@@ -704,24 +704,29 @@ constexpr uint32_t kChunkThreadsPerSm = 1024;  // the chunk walk's threads (k_th
 constexpr uint32_t kChunkMin = 32;             // shortest chunk (a short chunk propagates little)
 
 __global__ void k_low_range_stats(const uint64_t* off, uint32_t n, unsigned long long* out) {
-  // out[0]: rows of degree > kChunkMaxDeg, out[1]: rows of degree 1..kChunkMaxDeg, out[2]: their entries
-  unsigned long long hi = 0, lo = 0, e = 0;
+  // out[0]: rows of degree > kChunkMaxDeg, out[1]: rows of degree 1..kChunkMaxDeg, out[2]:
+  // their entries, out[4]: their largest degree
+  unsigned long long hi = 0, lo = 0, e = 0, mx = 0;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     const uint64_t d = off[v + 1] - off[v];
+    const bool low = d >= 1 && d <= kChunkMaxDeg;
     hi += d > kChunkMaxDeg;
-    lo += d >= 1 && d <= kChunkMaxDeg;
-    e += (d >= 1 && d <= kChunkMaxDeg) ? d : 0;
+    lo += low;
+    e += low ? d : 0;
+    mx = low && d > mx ? d : mx;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     hi += __shfl_xor_sync(0xFFFFFFFFu, hi, o);
     lo += __shfl_xor_sync(0xFFFFFFFFu, lo, o);
     e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
+    mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
   }
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(out, hi);
     atomicAdd(out + 1, lo);
     atomicAdd(out + 2, e);
+    atomicMax(out + 4, mx);
   }
 }
 
@@ -763,14 +768,14 @@ inline bool chunk_major_enabled() {
 // graph.cu build_plan) and is large enough for coalescing to matter.
 void chunk_major(const uint64_t* off, uint32_t n, uint32_t* perm, cudaStream_t s, nulpa_graph* g) {
   if (!g) return;
-  g->chunk_lo = g->chunk_n = g->chunk_L = 0;
+  g->chunk_lo = g->chunk_n = g->chunk_L = g->chunk_dmax = 0;
   if (!chunk_major_enabled() || n < 2) return;
-  unsigned long long* d = dalloc<unsigned long long>(4);
-  NULPA_CUDA(cudaMemsetAsync(d, 0, 3 * sizeof(unsigned long long), s));
+  unsigned long long* d = dalloc<unsigned long long>(5);
+  NULPA_CUDA(cudaMemsetAsync(d, 0, 5 * sizeof(unsigned long long), s));
   k_low_range_stats<<<blocks_for(n), 256, 0, s>>>(off, n, d);
   NULPA_CUDA(cudaGetLastError());
   NULPA_CUDA(cudaMemcpyAsync(d + 3, off + n, 8, cudaMemcpyDeviceToDevice, s));
-  unsigned long long h[4] = {0, 0, 0, 0};
+  unsigned long long h[5] = {0, 0, 0, 0, 0};
   NULPA_CUDA(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, s));
   NULPA_CUDA(cudaStreamSynchronize(s));
   dfree(d);
@@ -789,6 +794,7 @@ void chunk_major(const uint64_t* off, uint32_t n, uint32_t* perm, cudaStream_t s
   g->chunk_lo = static_cast<uint32_t>(a);
   g->chunk_n = static_cast<uint32_t>(M);
   g->chunk_L = static_cast<uint32_t>(L);
+  g->chunk_dmax = static_cast<uint32_t>(h[4]);
 }
 
 }  // namespace
@@ -826,7 +832,7 @@ void build_perm(const uint64_t* off, uint32_t n, uint32_t** perm_out, uint32_t**
 
 void relayout_graph(nulpa_graph* g, cudaStream_t s) {
   g->layout = NULPA_LAYOUT_IDENTITY;
-  g->chunk_lo = g->chunk_n = g->chunk_L = 0;
+  g->chunk_lo = g->chunk_n = g->chunk_L = g->chunk_dmax = 0;
   if (default_layout() != NULPA_LAYOUT_DEGREE_BUCKETS || g->n < 2) return;
   const uint32_t n = g->n;
   const uint64_t m2 = g->m2;

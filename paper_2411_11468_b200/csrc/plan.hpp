@@ -31,7 +31,7 @@ struct Plan {
   bool chunked_thread = false;
   // ... over the graph's chunk-major low range (nulpa_graph::chunk_*): the walk computes
   // its positions (chunk_lo + column start + chunk index) instead of reading the list.
-  uint32_t chunk_lo = 0, chunk_L = 0;
+  uint32_t chunk_lo = 0, chunk_L = 0, chunk_dmax = 0;
   bool weighted = false;  // hub tables: packed 64-bit words (unit weights) or split
   // Hub tier.
   uint32_t n_hubs = 0, n_items = 0;

@@ -111,7 +111,8 @@ def test_chunk_major_async_lattice_converges():
     base = _lattice_runs(NULPA_CHUNK_MAJOR=0)
     q0 = np.mean([q for _, _, q in base])
     assert all(c and it < 20 for c, it, _ in base), base
-    for env in ({}, {"NULPA_CHUNK_ROWS": 1}, {"NULPA_CHUNK_ROWS": 4}, {"NULPA_CHUNK_ROWS": 8}):
+    for env in ({}, {"NULPA_CHUNK_ROWS": 1}, {"NULPA_CHUNK_ROWS": 4}, {"NULPA_CHUNK_ROWS": 8},
+                {"NULPA_CHUNK_ROWS": 14}):
         got = _lattice_runs(**env)
         assert all(c and it < 20 for c, it, _ in got), (env, got)
         assert abs(np.mean([q for _, _, q in got]) - q0) <= 0.01, (env, got, base)
