@@ -341,13 +341,15 @@ inline int wide_mode() {
 }
 
 // Steps of a k_group batch whose loads are issued together (NULPA_GROUP_STEPS, read once:
-// 1 by default = one step at a time). Loading S steps' labels before any of them decides
-// makes the half-warp / warp tiers read staler labels: measured on one B200, S = 8 took the
-// SBM-100K run from 4 to 6 passes (0.61 -> 1.00 ms) and R-MAT 27 from 105.3 to 106.6 ms.
+// 2 by default). Loading S steps' labels before any of them decides makes the half-warp /
+// warp tiers read staler labels of the OTHER warps (the batch's own moves are patched in,
+// k_group): measured on one B200, S = 8 took the SBM-100K run from 4 to 6 passes; S = 2
+// keeps 4 passes there (0.282 -> 0.279 ms) and shortens R-MAT 22 4.30 -> 3.95 ms, R-MAT 18
+// 0.730 -> 0.718, R-MAT 27 95.3 -> 95.0 ms against S = 1.
 inline int group_steps() {
   static const int m = [] {
     const char* e = std::getenv("NULPA_GROUP_STEPS");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   return m;
 }
@@ -363,6 +365,7 @@ void launch_group(const PassCtx& c, const uint32_t* list, uint32_t count, cudaSt
   };
   switch (group_steps()) {
     case 1: go(k_group<MODE, W, WEIGHTED, G, 1>); break;
+    case 2: go(k_group<MODE, W, WEIGHTED, G, 2>); break;
     case 4: go(k_group<MODE, W, WEIGHTED, G, 4>); break;
     default: go(k_group<MODE, W, WEIGHTED, G, 8>);
   }

@@ -64,6 +64,7 @@ def serial():
     {"NULPA_CONCURRENT": 1},
     {"NULPA_CONCURRENT": 2},
     {"NULPA_CONCURRENT": 3},
+    {"NULPA_CONCURRENT": 2, "NULPA_GROUP_STEPS": 1},
     {"NULPA_CONCURRENT": 2, "NULPA_GROUP_STEPS": 8},
     {"NULPA_CONCURRENT": 2, "NULPA_SMALL_TIER_BATCH": 0},
 ])

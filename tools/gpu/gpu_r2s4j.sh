@@ -1,5 +1,5 @@
 # Re-verification of the final build (profiles/r2): GPU suite, smoke, default bench, grid bench.
-O=gpurun_out/s4j
+O=gpurun_out/${TAG:-s4j}
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
