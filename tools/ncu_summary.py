@@ -74,7 +74,8 @@ def full(path):
             return v / 1e3 if u[k] == "Mbyte" else v if u[k] == "Gbyte" else v / 1e9
         st = sorted(((float(d[f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio"]), s)
                      for s in STALLS), reverse=True)[:4]
-        scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(
+        scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+                 "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}.get(
             u.get("gpu__time_duration.sum", "msecond"), 1.0)  # -> ms
         print(f"{clean(d['Kernel Name']).split('(')[0][:58]} | {float(d['gpu__time_duration.sum']) * scale:.2f} | "
               f"{gb('dram__bytes_read.sum'):.2f} | {gb('dram__bytes_write.sum'):.2f} | "
