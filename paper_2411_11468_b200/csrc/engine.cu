@@ -500,6 +500,14 @@ int launch_pass(const Plan& p, PassCtx c, unsigned long long* ctr, cudaStream_t 
           k_chunk_walk<MODE, W, WEIGHTED, 4, 8, true><<<gc, 256, 0, ts>>>(
               c, p.count[T_THREAD], p.chunk_lo, p.chunk_L);
           break;
+        case 34:  // degree <= 4, 4 rows, prefetched targets, held to 6 CTAs per SM
+          k_chunk_walk<MODE, W, WEIGHTED, 4, 4, true, 6><<<gc, 256, 0, ts>>>(
+              c, p.count[T_THREAD], p.chunk_lo, p.chunk_L);
+          break;
+        case 32:  // ... 2 rows
+          k_chunk_walk<MODE, W, WEIGHTED, 4, 2, true, 6><<<gc, 256, 0, ts>>>(
+              c, p.count[T_THREAD], p.chunk_lo, p.chunk_L);
+          break;
         case 1:
           k_thread<MODE, W, WEIGHTED, 8, true><<<gc, 256, 0, ts>>>(
               c, p.list[T_THREAD], p.count[T_THREAD], p.chunk_lo, p.chunk_L);

@@ -755,6 +755,15 @@ __global__ void k_chunk_transpose(const uint32_t* src, uint32_t* dst, uint32_t n
   }
 }
 
+// Walk threads per SM the layout is cut for (NULPA_CHUNK_TPS, read once; default 1024).
+inline uint64_t chunk_threads_per_sm() {
+  static const uint64_t m = [] {
+    const char* e = std::getenv("NULPA_CHUNK_TPS");
+    return e ? static_cast<uint64_t>(std::atoi(e)) : uint64_t(kChunkThreadsPerSm);
+  }();
+  return m;
+}
+
 inline bool chunk_major_enabled() {
   static const bool m = [] {
     const char* e = std::getenv("NULPA_CHUNK_MAJOR");
@@ -780,7 +789,7 @@ void chunk_major(const uint64_t* off, uint32_t n, uint32_t* perm, cudaStream_t s
   NULPA_CUDA(cudaStreamSynchronize(s));
   dfree(d);
   const uint64_t a = h[0], M = h[1], e = h[2], m2 = h[3];
-  const uint64_t T = uint64_t(sm_count()) * kChunkThreadsPerSm;
+  const uint64_t T = uint64_t(sm_count()) * chunk_threads_per_sm();
   if (M < (1u << 16) || 2 * e < m2) return;
   // (chunks of at least kChunkMin entries, as the walk's own bound: engine.cu kMinChunk)
   const uint64_t L = std::max<uint64_t>((M + T - 1) / T, kChunkMin);

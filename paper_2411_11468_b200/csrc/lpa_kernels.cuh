@@ -439,9 +439,11 @@ __global__ void __launch_bounds__(256) k_thread_q(PassCtx c, const uint32_t* __r
 // coalesced across the warp.
 // PF: the next row's targets are loaded while this row's labels are in flight (targets
 // never change), so a row's chain is one label round trip.
-template <int MODE, typename W, bool WEIGHTED, int DMAX, int Q = 4, bool PF = false>
-__global__ void __launch_bounds__(256, 4) k_chunk_walk(PassCtx c, uint32_t count, uint32_t cm_lo,
-                                                       uint32_t cm_L) {
+// MINB: resident CTAs of 256 threads per SM the register budget is held to (the layout's
+// walk threads per SM, layout.cu chunk_major: 4 for ranges of degree <= 8, 6 for <= 4).
+template <int MODE, typename W, bool WEIGHTED, int DMAX, int Q = 4, bool PF = false, int MINB = 4>
+__global__ void __launch_bounds__(256, MINB) k_chunk_walk(PassCtx c, uint32_t count, uint32_t cm_lo,
+                                                          uint32_t cm_L) {
   if (stopped(c.stop)) return;
   unsigned long long n_v = 0, n_e = 0, n_dn = 0, n_w = 0;
   const uint64_t pol = policy_evict_first();
