@@ -1,4 +1,4 @@
-O=gpurun_out/s4q
+O=gpurun_out/${TAG:-s4q}
 mkdir -p $O
 timeout 900 python -m pytest tests/test_layout_gpu.py tests/test_dropin_cpp.py tests/test_capi.py -x -q > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
 for v in 0 1; do
