@@ -16,6 +16,8 @@ cpu_baseline: the reference library itself (oracle/_ref, multithreaded ParallelA
           switch_degree = UINT32_MAX per SURVEY F5) on the SAME graph (one full run), with
           its modularity; `quality` adds the SBM-100K config (reference Synchronous and
           ParallelAsync Q against nulpa's, two-sided).
+shapes:   the default line also carries the latency- and coalescing-bound shapes, unprofiled:
+          the 4096² grid (chunk-major thread tier, with its roofline) and SBM-100K.
 --impl reference: the reference arm — the same library on the same workload (R-MAT
           scale 27, or the largest scale that fits host RAM, stated), the graph built in a
           child process so the timing process maps no libnulpa.so.
